@@ -1,0 +1,167 @@
+"""Seeded synthetic inputs for the multishift QR sweep (BASELINE.json ``configs``).
+
+Shared by the oracle tests, the GPU parity tests and bench.py.  This module holds NONE of the
+method's arithmetic (no reflectors, no shifts polynomials): it only draws random numbers.
+
+Recipe:
+  RNG: numpy Generator(PCG64(SeedSequence([2020, cfg, stream]))); 2020 is the paper's test
+       seed.  Streams: 0 upper entries, 1 subdiagonal, 2 shifts, 3 Z0 Gaussian.
+  H:   upper-triangle entries (i <= j) drawn column by column (column-major order), subdiagonal
+       h[j+1, j] drawn in order j = 0..n-2; everything below the subdiagonal is exactly 0.
+  Z0:  identity, or the Q factor of a Householder QR of an n x n N(0,1) matrix (stream 3).
+  shifts: consecutive pairs; real pair = two reals, complex pair = (a+bi, a-bi) adjacent.
+
+Arrays are float64 Fortran-ordered (column-major, ld = n), the layout of the C ABI.
+These inputs stand in for the paper's syn_n / SuiteSparse matrices: a sweep only
+ever sees an upper-Hessenberg matrix, so only its shape and value distribution matter.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+SEED = 2020
+
+
+def rng(cfg: int, stream: int) -> np.random.Generator:
+    return np.random.Generator(np.random.PCG64(np.random.SeedSequence([SEED, cfg, stream])))
+
+
+@dataclass
+class Config:
+    idx: int
+    n: int
+    upper: str            # "u11" = U[-1,1], "n01" = N(0,1)
+    z0: str               # "eye" or "orth"
+    shifts: str           # "mixed" (half real pairs, half conj pairs) or "disk2"
+    nshifts: int
+    window: int | None    # None = library default
+    blocks: int = 1       # number of unreduced diagonal blocks (config 4)
+    name: str = ""
+    gpus: tuple = field(default_factory=lambda: (1,))
+
+
+CONFIGS = {
+    0: Config(0, 256, "u11", "eye", "mixed", 8, 24, name="cfg0_n256_s8_w24"),
+    1: Config(1, 4000, "u11", "orth", "mixed", 100, 151, name="cfg1_n4000_s100_w151"),
+    2: Config(2, 10000, "n01", "eye", "disk2", 256, None, name="cfg2_n10000_s256", gpus=(1, 2, 4, 8)),
+    3: Config(3, 20000, "n01", "orth", "disk2", 512, None, name="cfg3_n20000_s512", gpus=(1, 2, 4, 8)),
+    4: Config(4, 40000, "n01", "eye", "disk2", 512, None, blocks=4, name="cfg4_n40000_4x512",
+              gpus=(8,)),
+}
+
+
+def hessenberg(n: int, upper: str, cfg: int, blocks: int = 1, col_chunk: int = 512) -> np.ndarray:
+    """Random upper-Hessenberg H (Fortran order).  blocks > 1 zeroes h[b*n/blocks, b*n/blocks - 1]."""
+    H = np.zeros((n, n), dtype=np.float64, order="F")
+    g = rng(cfg, 0)
+    for c0 in range(0, n, col_chunk):
+        c1 = min(n, c0 + col_chunk)
+        cnt = (c1 * (c1 + 1) - c0 * (c0 + 1)) // 2
+        if upper == "u11":
+            vals = g.uniform(-1.0, 1.0, cnt)
+        elif upper == "n01":
+            vals = g.standard_normal(cnt)
+        else:
+            raise ValueError(upper)
+        off = 0
+        for j in range(c0, c1):
+            H[: j + 1, j] = vals[off: off + j + 1]
+            off += j + 1
+    sub = rng(cfg, 1).uniform(0.5, 1.5, max(n - 1, 0))
+    idx = np.arange(n - 1)
+    H[idx + 1, idx] = sub
+    if blocks > 1:
+        bs = n // blocks
+        for b in range(1, blocks):
+            H[b * bs, b * bs - 1] = 0.0
+    return H
+
+
+def orthogonal(n: int, cfg: int, device: str = "cpu") -> np.ndarray:
+    """Q factor of a Householder QR of an n x n N(0,1) matrix drawn from stream 3 (Fortran order)."""
+    G = rng(cfg, 3).standard_normal((n, n))
+    if device == "cpu":
+        Q, _ = np.linalg.qr(G)
+        return np.asfortranarray(Q)
+    import torch  # input generation only; not the product path
+    Qt, _ = torch.linalg.qr(torch.from_numpy(G).to(device))
+    return np.asfortranarray(Qt.cpu().numpy())
+
+
+def shifts(kind: str, nshifts: int, cfg: int, stream_offset: int = 0) -> tuple[np.ndarray, np.ndarray]:
+    """Shift set as (re, im) arrays of length nshifts, conjugates adjacent."""
+    g = rng(cfg, 2 + 10 * stream_offset)
+    npairs = nshifts // 2
+    re = np.zeros(nshifts)
+    im = np.zeros(nshifts)
+    if kind == "mixed":
+        nreal = npairs // 2
+        for j in range(npairs):
+            if j < nreal:
+                re[2 * j: 2 * j + 2] = g.uniform(-1.0, 1.0, 2)
+            else:
+                a = g.uniform(-1.0, 1.0)
+                b = g.uniform(0.1, 1.0)
+                re[2 * j: 2 * j + 2] = a
+                im[2 * j], im[2 * j + 1] = b, -b
+    elif kind == "disk2":
+        j = 0
+        while j < npairs:
+            a, b = g.uniform(-2.0, 2.0), g.uniform(0.0, 2.0)
+            if a * a + b * b <= 4.0 and b > 0.0:
+                re[2 * j: 2 * j + 2] = a
+                im[2 * j], im[2 * j + 1] = b, -b
+                j += 1
+    else:
+        raise ValueError(kind)
+    return re, im
+
+
+@dataclass
+class Problem:
+    H: np.ndarray
+    Z: np.ndarray | None
+    ilo: int
+    ihi: int
+    shifts_re: np.ndarray
+    shifts_im: np.ndarray
+    window: int | None
+    blocks: list  # [(ilo, ihi, shift slice start, shift count)]
+
+
+def make(cfg_idx: int, z_device: str = "cpu", n_override: int | None = None) -> Problem:
+    """Materialise BASELINE.json configs[cfg_idx] (optionally at a smaller n for tests)."""
+    c = CONFIGS[cfg_idx]
+    n = n_override or c.n
+    H = hessenberg(n, c.upper, c.idx, blocks=c.blocks)
+    Z = np.asfortranarray(np.eye(n)) if c.z0 == "eye" else orthogonal(n, c.idx, z_device)
+    if c.blocks == 1:
+        re, im = shifts(c.shifts, c.nshifts, c.idx)
+        return Problem(H, Z, 0, n - 1, re, im, c.window, [(0, n - 1, 0, c.nshifts)])
+    bs = n // c.blocks
+    res, ims, blocks = [], [], []
+    for b in range(c.blocks):
+        re, im = shifts(c.shifts, c.nshifts, c.idx, stream_offset=b)
+        res.append(re)
+        ims.append(im)
+        blocks.append((b * bs, b * bs + bs - 1, b * c.nshifts, c.nshifts))
+    return Problem(H, Z, 0, n - 1, np.concatenate(res), np.concatenate(ims), c.window, blocks)
+
+
+def random_case(seed: int, n: int, nshifts: int, ilo: int = 0, ihi: int | None = None,
+                upper: str = "n01", z0: str = "eye", shift_kind: str = "mixed"):
+    """Small random case for property tests: H decoupled at ilo/ihi, Z0 identity or orthogonal."""
+    ihi = n - 1 if ihi is None else ihi
+    H = hessenberg(n, upper, 1000 + seed)
+    if ilo > 0:
+        H[ilo, ilo - 1] = 0.0
+    if ihi < n - 1:
+        H[ihi + 1, ihi] = 0.0
+    if z0 == "eye":
+        Z = np.asfortranarray(np.eye(n))
+    else:
+        Z = orthogonal(n, 1000 + seed)
+    re, im = shifts(shift_kind, nshifts, 1000 + seed)
+    return H, Z, re, im

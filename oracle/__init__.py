@@ -1,0 +1,114 @@
+"""CPU oracle for one multishift QR sweep -- TEST INFRASTRUCTURE ONLY.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s ``cpu_baseline`` /
+``--impl reference`` legs may import this package.  It shares no code with the CUDA product
+path (``paper_2007_03576_b200``): the arithmetic lives in ``oracle/hqr_oracle.c`` (plain C,
+fp64, OpenMP over independent rows/columns only), this module only marshals arguments.
+
+Functions and the passages they follow (PAPER.md line numbers, see hqr_oracle.c):
+  house(x)                 -- 3x3 / 2x2 Householder reflector, P:200 (reading R2 in DESIGN.md)
+  first_column(H, ilo, ..) -- first column of (H - s I)(H - s' I), P:200 (reading R1)
+  sweep(H, Z, ...)         -- nshifts/2 sequential Francis double steps on the full matrix,
+                              P:146-151, P:198-206, P:227-233
+  flops(...)               -- F_alg, the work of applying every reflector directly
+
+Parity pins for every function are in tests/test_oracle.py (none is "parity unpinned").
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "hqr_oracle.c")
+_LIB_PATH = os.path.join(_HERE, "_build", "libhqr_oracle.so")
+_lib = None
+
+
+def build(force: bool = False) -> str:
+    """Compile the oracle with gcc (-O2 -fopenmp, no FMA contraction: reading R10)."""
+    os.makedirs(os.path.dirname(_LIB_PATH), exist_ok=True)
+    if force or not os.path.exists(_LIB_PATH) or os.path.getmtime(_LIB_PATH) < os.path.getmtime(_SRC):
+        cmd = ["gcc", "-O2", "-fopenmp", "-fPIC", "-shared", "-ffp-contract=off", "-std=c11",
+               "-o", _LIB_PATH, _SRC, "-lm"]
+        subprocess.check_call(cmd)
+    return _LIB_PATH
+
+
+def _load():
+    global _lib
+    if _lib is None:
+        build()
+        lib = ctypes.CDLL(_LIB_PATH)
+        dp = ctypes.POINTER(ctypes.c_double)
+        lib.oracle_house.argtypes = [ctypes.c_int, dp, dp, dp, dp]
+        lib.oracle_house.restype = None
+        lib.oracle_first_column.argtypes = [dp, ctypes.c_int64, ctypes.c_int64, ctypes.c_double,
+                                            ctypes.c_double, dp]
+        lib.oracle_first_column.restype = None
+        lib.oracle_sweep.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64,
+                                     ctypes.c_int64, dp, dp, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                     ctypes.c_int]
+        lib.oracle_sweep.restype = ctypes.c_int
+        lib.oracle_flops.argtypes = [ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int,
+                                     ctypes.c_int]
+        lib.oracle_flops.restype = ctypes.c_double
+        _lib = lib
+    return _lib
+
+
+def _dptr(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+
+
+def house(x):
+    """Return (v, tau, beta) with (I - tau v v^T) x = beta e1 (reading R2)."""
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    m = x.shape[0]
+    v = np.zeros(m)
+    tau = ctypes.c_double()
+    beta = ctypes.c_double()
+    _load().oracle_house(m, _dptr(x), _dptr(v), ctypes.byref(tau), ctypes.byref(beta))
+    return v, tau.value, beta.value
+
+
+def first_column(H: np.ndarray, ilo: int, sigma: float, pi: float) -> np.ndarray:
+    H = _as_colmajor(H)
+    x = np.zeros(3)
+    _load().oracle_first_column(_dptr(H), H.shape[0], ilo, sigma, pi, _dptr(x))
+    return x
+
+
+def _as_colmajor(a: np.ndarray) -> np.ndarray:
+    if a.dtype != np.float64 or not a.flags.f_contiguous:
+        raise TypeError("oracle expects float64 Fortran-ordered (column-major) arrays")
+    return a
+
+
+def sweep(H: np.ndarray, Z: np.ndarray | None, ilo: int, ihi: int, shifts_re, shifts_im,
+          order: str = "sequential", bulges: tuple[int, int] | None = None) -> None:
+    """In place: H <- Q^T H Q, Z <- Z Q for one multishift sweep.
+
+    H, Z: n x n float64 Fortran-ordered.  order: "sequential" (the oracle) or "pipelined"
+    (noise-floor measurement only).  bulges=(j0, j1) restricts to shift pairs j0..j1-1.
+    """
+    H = _as_colmajor(H)
+    n = H.shape[0]
+    if Z is not None:
+        Z = _as_colmajor(Z)
+        assert Z.shape == (n, n)
+    sr = np.ascontiguousarray(shifts_re, dtype=np.float64)
+    si = np.ascontiguousarray(shifts_im, dtype=np.float64)
+    ns = sr.shape[0]
+    nb = ns // 2
+    j0, j1 = bulges if bulges is not None else (0, nb)
+    o = {"sequential": 0, "pipelined": 1}[order]
+    _load().oracle_sweep(H.ctypes.data, None if Z is None else Z.ctypes.data, n, ilo, ihi,
+                         _dptr(sr), _dptr(si), ns, o, j0, j1)
+
+
+def flops(n: int, ilo: int, ihi: int, nbulges: int, with_z: bool = True) -> float:
+    return _load().oracle_flops(n, ilo, ihi, nbulges, 1 if with_z else 0)

@@ -1,0 +1,164 @@
+/*
+ * oracle/hqr_oracle.c -- plain, slow CPU oracle for ONE small-bulge multishift QR sweep.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+ * --impl reference legs may load this library.  It shares no code, header, table or helper with
+ * the CUDA product path (paper_2007_03576_b200/csrc); neither includes or links the other.
+ *
+ * What it computes (PAPER.md = /root/reference/PAPER.md, cited as P:<line>):
+ *   One QR iteration is a product of orthogonal similarities H <- Q^T H Q, Z <- Z Q
+ *   (Eq. "H <- Q_k^T ... Q_1^T H Q_1 ... Q_k").  For the multishift sweep the method
+ *   reaches exactly (up to rounding order) the result of nshifts/2 textbook double-implicit-shift
+ *   (Francis) steps, one per shift pair, pair 0 first (P:198-206 the double-shift step, P:206
+ *   implicit-Q theorem, P:227-233 tightly-coupled bulges "chased ... as a single unit").  This
+ *   file writes that plain definition out: every 3x3 (final: 2x2) Householder reflector is applied
+ *   directly to the full matrix H (rows 0..n-1, the "wantt" convention) and to all n rows of Z.
+ *
+ * Readings of the paper (listed in DESIGN.md "Readings"):
+ *   R1 bulge vector: first column of (H - s I)(H - s' I) in real form.
+ *   R2 Householder: beta = -sign(x0)*||x||, sign(0)=+1, tau = (beta-x0)/beta,
+ *      v = [1, x1/(x0-beta), ...]; zero tail => tau = 0, beta = x0 (identity).
+ *   R3 shift pairs: consecutive (2j, 2j+1); sigma = s+s', pi = s*s' (= re*re' - im*im').
+ *   R6 no vigilant deflation during the sweep.  R9 annihilated entries stored as exact 0.0.
+ *
+ * Layout: column-major doubles, leading dimension n (element (i,j) at i + j*n).
+ */
+#include <math.h>
+#include <stddef.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define EL(A, i, j, ld) (A)[(size_t)(i) + (size_t)(j) * (size_t)(ld)]
+
+/* R2: Householder reflector of length m (2 or 3) mapping x to beta*e1 ("generate a 3-by-3
+ * Householder reflector Q1 such that Q1^T v is a multiple of e1").  P = I - tau v v^T. */
+void oracle_house(int m, const double* x, double* v, double* tau, double* beta) {
+  double alpha = x[0];
+  double tail2 = 0.0;
+  for (int i = 1; i < m; ++i) tail2 += x[i] * x[i];
+  v[0] = 1.0;
+  if (tail2 == 0.0) {
+    for (int i = 1; i < m; ++i) v[i] = 0.0;
+    *tau = 0.0;
+    *beta = alpha;
+    return;
+  }
+  double norm = sqrt(alpha * alpha + tail2);
+  double b = (alpha >= 0.0) ? -norm : norm; /* sign(0) = +1 */
+  *tau = (b - alpha) / b;
+  for (int i = 1; i < m; ++i) v[i] = x[i] / (alpha - b);
+  *beta = b;
+}
+
+/* R1: x = (H - s I)(H - s' I) e_ilo restricted to rows ilo..ilo+2, in real arithmetic
+ * ("v = (H - l1 I)(H - l2 I) e1").  sigma = s + s', pi = s s'. */
+void oracle_first_column(const double* H, int64_t n, int64_t ilo, double sigma, double pi,
+                         double* x) {
+  double h00 = EL(H, ilo, ilo, n), h01 = EL(H, ilo, ilo + 1, n);
+  double h10 = EL(H, ilo + 1, ilo, n), h11 = EL(H, ilo + 1, ilo + 1, n);
+  double h21 = EL(H, ilo + 2, ilo + 1, n);
+  x[0] = h00 * (h00 - sigma) + h01 * h10 + pi;
+  x[1] = h10 * (h00 + h11 - sigma);
+  x[2] = h10 * h21;
+}
+
+/* R3: the shift pair of bulge j. */
+static void pair_coeffs(const double* sr, const double* si, int j, double* sigma, double* pi) {
+  *sigma = sr[2 * j] + sr[2 * j + 1];
+  *pi = sr[2 * j] * sr[2 * j + 1] - si[2 * j] * si[2 * j + 1];
+}
+
+/* Apply the reflector of bulge j at position p (acting on rows/cols p+1..p+m) to the full H and Z,
+ * exactly as one step of the textbook chase: compute the vector, apply from the left to
+ * rows p+1..p+m (all columns to the right), store beta / exact zeros in column p, apply from the
+ * right to columns p+1..p+m (all rows above the bulge), and accumulate into Z (all n rows). */
+static void apply_one(double* H, double* Z, int64_t n, int64_t ilo, int64_t ihi, int64_t p,
+                      double sigma, double pi) {
+  int m = (p <= ihi - 3) ? 3 : 2;
+  double x[3], v[3], tau, beta;
+  if (p == ilo - 1) {
+    oracle_first_column(H, n, ilo, sigma, pi, x);
+  } else {
+    for (int i = 0; i < m; ++i) x[i] = EL(H, p + 1 + i, p, n);
+  }
+  oracle_house(m, x, v, &tau, &beta);
+
+  /* left: H(p+1..p+m, c) -= tau v (v^T H(p+1..p+m, c)) for c = first..n-1 */
+  int64_t c0 = (p == ilo - 1) ? ilo : p + 1;
+#pragma omp parallel for schedule(static) if (n - c0 > 2048)
+  for (int64_t c = c0; c < n; ++c) {
+    double w = 0.0;
+    for (int i = 0; i < m; ++i) w += v[i] * EL(H, p + 1 + i, c, n);
+    for (int i = 0; i < m; ++i) EL(H, p + 1 + i, c, n) -= tau * v[i] * w;
+  }
+  if (p >= ilo) { /* R9: annihilated column stored exactly */
+    EL(H, p + 1, p, n) = beta;
+    for (int i = 1; i < m; ++i) EL(H, p + 1 + i, p, n) = 0.0;
+  }
+  /* right: H(r, p+1..p+m) -= tau (H(r, p+1..p+m) v) v^T for r = 0..min(p+m+1, ihi) */
+  int64_t r1 = (p + m + 1 < ihi) ? p + m + 1 : ihi;
+#pragma omp parallel for schedule(static) if (r1 > 2048)
+  for (int64_t r = 0; r <= r1; ++r) {
+    double w = 0.0;
+    for (int i = 0; i < m; ++i) w += EL(H, r, p + 1 + i, n) * v[i];
+    for (int i = 0; i < m; ++i) EL(H, r, p + 1 + i, n) -= tau * w * v[i];
+  }
+  /* Z <- Z P ("Q <- Q Q_1 ... Q_k"), all rows */
+  if (Z) {
+#pragma omp parallel for schedule(static) if (n > 2048)
+    for (int64_t r = 0; r < n; ++r) {
+      double w = 0.0;
+      for (int i = 0; i < m; ++i) w += EL(Z, r, p + 1 + i, n) * v[i];
+      for (int i = 0; i < m; ++i) EL(Z, r, p + 1 + i, n) -= tau * w * v[i];
+    }
+  }
+}
+
+/*
+ * The oracle: one multishift sweep as nshifts/2 sequential Francis double-shift steps (SURVEY §8(c)
+ * algorithm).  order = 0: sequential (bulge 0 sweeps the whole block, then
+ * bulge 1, ...).  order = 1: pipelined (step t: bulge j at p = ilo-1+t-3j, lowest bulge first;
+ * P:228 "chasing them down the diagonal just enough so that the next bulge can be introduced").
+ * Order 1 is used only to measure the rounding noise floor between two valid orders.
+ * Bulges j0 .. j1-1 only (j0 = 0, j1 = nshifts/2 is the whole sweep; a sub-range is the bounded
+ * CPU-baseline sample).  Returns 0.  No argument validation: callers pass valid input.
+ */
+int oracle_sweep(double* H, double* Z, int64_t n, int64_t ilo, int64_t ihi, const double* sr,
+                 const double* si, int nshifts, int order, int j0, int j1) {
+  (void)nshifts;
+  if (order == 0) {
+    for (int j = j0; j < j1; ++j) {
+      double sigma, pi;
+      pair_coeffs(sr, si, j, &sigma, &pi);
+      for (int64_t p = ilo - 1; p <= ihi - 2; ++p) apply_one(H, Z, n, ilo, ihi, p, sigma, pi);
+    }
+  } else {
+    int nb = j1 - j0;
+    int64_t last = (ihi - 2) - (ilo - 1) + 3 * (int64_t)(nb - 1);
+    for (int64_t t = 0; t <= last; ++t) {
+      for (int jj = 0; jj < nb; ++jj) { /* lowest (earliest introduced) first */
+        int64_t p = ilo - 1 + t - 3 * (int64_t)jj;
+        if (p < ilo - 1 || p > ihi - 2) continue;
+        double sigma, pi;
+        pair_coeffs(sr, si, j0 + jj, &sigma, &pi);
+        apply_one(H, Z, n, ilo, ihi, p, sigma, pi);
+      }
+    }
+  }
+  return 0;
+}
+
+/* F_alg: flops of applying every reflector directly, per bulge:
+ * 10*[(n - max(p+1, ilo)) + (min(p+4, ihi)+1) + n] per 3-reflector, 6*[...] for the final one. */
+double oracle_flops(int64_t n, int64_t ilo, int64_t ihi, int nbulges, int with_z) {
+  double f = 0.0;
+  for (int64_t p = ilo - 1; p <= ihi - 2; ++p) {
+    int m = (p <= ihi - 3) ? 3 : 2;
+    int64_t c0 = (p == ilo - 1) ? ilo : p + 1;
+    int64_t r1 = (p + m + 1 < ihi) ? p + m + 1 : ihi;
+    double per = (m == 3) ? 10.0 : 6.0;
+    f += per * ((double)(n - c0) + (double)(r1 + 1) + (with_z ? (double)n : 0.0));
+  }
+  return f * nbulges;
+}

@@ -1,0 +1,117 @@
+// FP64 peak microbenchmark for B200 (sm_100a): DMMA (mma.sync m8n8k4 f64) vs DFMA.
+// Not part of the product: it measures the roofline denominator the bench reports against
+// (MEASURED_PEAKS.json has no fp64 entry). Build: see tools/run_peaks.sh.
+#include <cstdio>
+#include <cstdlib>
+#include <cuda_runtime.h>
+
+#define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { \
+  fprintf(stderr, "CUDA %s at %s:%d\n", cudaGetErrorString(e), __FILE__, __LINE__); exit(1);} } while (0)
+
+template <int NACC>
+__global__ void dmma_loop(double* out, int iters, double seed) {
+  double a = seed + threadIdx.x * 1e-3, b = seed - threadIdx.x * 1e-3;
+  double c[NACC][2];
+#pragma unroll
+  for (int i = 0; i < NACC; ++i) { c[i][0] = 0.0; c[i][1] = 0.0; }
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < NACC; ++i) {
+      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                   : "+d"(c[i][0]), "+d"(c[i][1]) : "d"(a), "d"(b));
+    }
+  }
+  double s = 0;
+#pragma unroll
+  for (int i = 0; i < NACC; ++i) s += c[i][0] + c[i][1];
+  if (s == 12345.678) out[threadIdx.x] = s;  // keep live
+}
+
+template <int NACC>
+__global__ void dfma_loop(double* out, int iters, double seed) {
+  double a = seed + threadIdx.x * 1e-3, b = 1.0 - 1e-9 * threadIdx.x;
+  double c[NACC];
+#pragma unroll
+  for (int i = 0; i < NACC; ++i) c[i] = i;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < NACC; ++i) c[i] = fma(c[i], b, a);
+  }
+  double s = 0;
+#pragma unroll
+  for (int i = 0; i < NACC; ++i) s += c[i];
+  if (s == 12345.678) out[threadIdx.x] = s;
+}
+
+template <typename K>
+static double time_kernel(K kern, int grid, int block, int iters, double* out, int reps) {
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0)); CK(cudaEventCreate(&e1));
+  kern<<<grid, block>>>(out, iters, 0.5);  // warm
+  CK(cudaDeviceSynchronize());
+  float best = 1e30f;
+  for (int r = 0; r < reps; ++r) {
+    CK(cudaEventRecord(e0));
+    kern<<<grid, block>>>(out, iters, 0.5);
+    CK(cudaEventRecord(e1));
+    CK(cudaEventSynchronize(e1));
+    float ms; CK(cudaEventElapsedTime(&ms, e0, e1));
+    if (ms < best) best = ms;
+  }
+  return best;
+}
+
+template <typename K>
+static double sustained(K kern, int grid, int block, int iters, double* out, double seconds, double flop_per_launch) {
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0)); CK(cudaEventCreate(&e1));
+  CK(cudaEventRecord(e0));
+  int launches = 0; float ms = 0;
+  while (true) {
+    for (int i = 0; i < 20; ++i) kern<<<grid, block>>>(out, iters, 0.5);
+    launches += 20;
+    CK(cudaEventRecord(e1)); CK(cudaEventSynchronize(e1));
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    if (ms > seconds * 1e3) break;
+  }
+  return flop_per_launch * launches / (ms * 1e-3) / 1e12;
+}
+
+int main(int argc, char** argv) {
+  int dev = 0; CK(cudaSetDevice(dev));
+  cudaDeviceProp p; CK(cudaGetDeviceProperties(&p, dev));
+  int sms = p.multiProcessorCount;
+  double* out; CK(cudaMalloc(&out, 4096 * sizeof(double)));
+  printf("{\"gpu\": \"%s\", \"sms\": %d, \"smem_optin\": %zu, \"l2\": %d", p.name, sms,
+         (size_t)p.sharedMemPerBlockOptin, p.l2CacheSize);
+  const int iters = 4096;
+  // DMMA: per warp-instruction 8*8*4 FMA = 256 FMA = 512 flop
+  int warps_list[] = {4, 8, 16};
+  double best_dmma = 0;
+  for (int w : warps_list) {
+    int block = 32 * w, grid = sms * 2;
+    double ms = time_kernel(dmma_loop<8>, grid, block, iters, out, 5);
+    double flop = (double)grid * w * iters * 8 * 512.0;
+    double tf = flop / (ms * 1e-3) / 1e12;
+    printf(", \"dmma_w%d_tflops\": %.3f", w, tf);
+    if (tf > best_dmma) best_dmma = tf;
+  }
+  double best_dfma = 0;
+  for (int w : warps_list) {
+    int block = 32 * w, grid = sms * 2;
+    double ms = time_kernel(dfma_loop<16>, grid, block, iters, out, 5);
+    double flop = (double)grid * block * iters * 16 * 2.0;
+    double tf = flop / (ms * 1e-3) / 1e12;
+    printf(", \"dfma_w%d_tflops\": %.3f", w, tf);
+    if (tf > best_dfma) best_dfma = tf;
+  }
+  {
+    int w = 8, block = 256, grid = sms * 2;
+    double flop = (double)grid * w * iters * 8 * 512.0;
+    printf(", \"dmma_sustained_tflops\": %.3f", sustained(dmma_loop<8>, grid, block, iters, out, 4.0, flop));
+    double flop2 = (double)grid * block * iters * 16 * 2.0;
+    printf(", \"dfma_sustained_tflops\": %.3f", sustained(dfma_loop<16>, grid, block, iters, out, 4.0, flop2));
+  }
+  printf(", \"dmma_burst_tflops\": %.3f, \"dfma_burst_tflops\": %.3f}\n", best_dmma, best_dfma);
+  return 0;
+}
