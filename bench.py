@@ -1,0 +1,303 @@
+"""bench.py -- one multishift QR sweep per step on B200 (BASELINE.json metric), JSON line on rank 0.
+
+python bench.py [--gpus N] [--steps K] [--warmup W] [--config 3] [--window 96] [--impl ours|reference]
+
+A "step" is one full sweep (every SURVEY §8(a) row: shift pairing, bulge introduction, in-window
+chase, left / right / Z updates) over the seeded synthetic BASELINE.json configs[--config]
+(default configs[3]: n = 20000, 512 shifts, Z = random orthogonal -- the largest configuration that
+fits one GPU and the one the north_star target is quoted on).  H and Z are restored from pristine
+device copies before every step (untimed); each sweep is timed with CUDA events on the library's
+stream boundary (synchronize on both sides).  Inputs (2 x 3.2 GB) are far larger than L2.
+
+value = F_alg / t  (fp64 GFLOP/s; F_alg = flops of applying every reflector directly, SURVEY
+Appendix B, design independent).  Also reported: seconds/sweep, executed GEMM flops and their
+fraction of the measured FP64 DMMA peak (profiles/fp64_peaks_r01.json), the update kernel's
+roofline, the oracle's CPU baseline on a bounded sample, and the end-to-end number with host
+buffers (pinned host memory, host<->device copies inside the C-ABI call).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+FP64_PEAK_FILE = os.path.join(ROOT, "profiles", "fp64_peaks_r01.json")
+METRIC = "seconds/sweep & fp64 GFLOP/s (frac of FP64 TC peak), n=10k/20k, 1/2/4/8 B200"
+
+
+def fp64_peak():
+    with open(FP64_PEAK_FILE) as f:
+        d = json.load(f)
+    return d["dmma_sustained_tflops"], d["dmma_burst_tflops"]
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, index=0):
+        self.path = f"/tmp/bench_clocks_{os.getpid()}.csv"
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.f = open(self.path, "w")
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={index}", f"--query-gpu={q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        self.p.wait()
+        self.f.close()
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax = float(parts[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        loaded = [s for s in sm if smax and s > 0.5 * smax] or sm
+        return {"sm_mhz": float(np.median(loaded)) if loaded else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_baseline(prob, bulges, n, ilo, ihi):
+    """The oracle as it stands on this host's cores, on a bounded sample: the first `bulges`
+    shift pairs on the full matrix (F_alg per pair is the same for every pair)."""
+    import oracle
+    H = prob.H.copy(order="F")
+    Z = prob.Z.copy(order="F") if prob.Z is not None else None
+    t = time.perf_counter()
+    oracle.sweep(H, Z, ilo, ihi, prob.shifts_re, prob.shifts_im, bulges=(0, bulges))
+    dt = time.perf_counter() - t
+    f = oracle.flops(n, ilo, ihi, bulges, Z is not None)
+    cores = int(os.environ.get("OMP_NUM_THREADS", len(os.sched_getaffinity(0))))
+    return {"value": f / dt / 1e9, "unit": "GFLOP/s", "cores": cores, "kind": "oracle",
+            "sample": f"first {bulges} of {len(prob.shifts_re) // 2} shift pairs on the full "
+                      f"n={n} matrix ({dt:.1f} s; F_alg {f:.3e})",
+            "seconds_per_sweep_extrapolated": dt * (len(prob.shifts_re) // 2) / bulges}
+
+
+def f_alg(n, ilo, ihi, nb, with_z):
+    # SURVEY Appendix B (same closed form the oracle reports; recomputed here without oracle/)
+    tot = 0.0
+    p = np.arange(ilo - 1, ihi - 1, dtype=np.float64)
+    m3 = p <= ihi - 3
+    c0 = np.where(p == ilo - 1, ilo, p + 1)
+    r1 = np.minimum(p + np.where(m3, 3, 2) + 1, ihi)
+    per = np.where(m3, 10.0, 6.0)
+    tot = np.sum(per * ((n - c0) + (r1 + 1) + (n if with_z else 0)))
+    return float(tot) * nb
+
+
+def run_reference(args, cfg_idx):
+    """--impl reference: the oracle timed as it stands on the host cores."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from hqr_inputs import make
+    prob = make(cfg_idx)
+    n = prob.H.shape[0]
+    steps = []
+    cb = None
+    for i in range(args.warmup + args.steps):
+        cb = cpu_baseline(prob, args.ref_bulges, n, prob.ilo, prob.ihi)
+        if i >= args.warmup:
+            steps.append(cb["value"])
+    v = float(np.mean(steps))
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "GFLOP/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": None, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic (seeded, BASELINE.json configs)",
+            "config": {"workload": f"configs[{cfg_idx}]", "n": n, "nshifts": len(prob.shifts_re)},
+            "cpu_baseline": {"value": v, "unit": "GFLOP/s", "cores": cb["cores"], "kind": "oracle",
+                             "sample": cb["sample"]},
+            "e2e": {"value": v, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=3)
+    ap.add_argument("--window", type=int, default=96)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-bulges", type=int, default=2, help="oracle sample size (shift pairs)")
+    ap.add_argument("--ref-bulges", type=int, default=1)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--n", type=int, default=None, help="override n (debug)")
+    args = ap.parse_args()
+
+    if args.impl == "reference":
+        run_reference(args, args.config)
+        return
+
+    import torch
+    import paper_2007_03576_b200 as hq
+    from hqr_inputs import make
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        # The sharded multi-GPU sweep (H block-column / Z block-row, Q broadcast) is not in this
+        # build: every rank runs its own full sweep (replicas) -- reported as such.
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+
+    t0 = time.time()
+    prob = make(args.config, z_device="cuda" if torch.cuda.is_available() else "cpu", n_override=args.n)
+    n = prob.H.shape[0]
+    gen_s = time.time() - t0
+    nshifts = len(prob.shifts_re)
+    hq.setup(local)
+
+    H0 = hq.to_device(prob.H, dev)
+    Z0 = hq.to_device(prob.Z, dev)
+    H = torch.empty_like(H0.t()).t()
+    Z = torch.empty_like(Z0.t()).t()
+
+    def restore():
+        H.t().copy_(H0.t())
+        Z.t().copy_(Z0.t())
+
+    def one():
+        hq.sweep(H, Z, prob.ilo, prob.ihi, prob.shifts_re, prob.shifts_im, args.window)
+
+    for _ in range(args.warmup):
+        restore()
+        one()
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    clk = Clocks(local)
+    times = []
+    launches = 0
+    for _ in range(args.steps):
+        restore()
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        one()   # synchronous: returns after the library stream finished
+        e1.record()
+        torch.cuda.synchronize()
+        times.append(e0.elapsed_time(e1))
+        st = hq.stats()
+        launches += st["kernels_launched"]
+    clocks = clk.stop()
+    ms = float(np.mean(times))
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    st = hq.stats()
+    fa = f_alg(n, prob.ilo, prob.ihi, nshifts // 2, True)
+    value = fa * world / (ms * 1e-3) / 1e9   # replicas: each rank one full sweep
+    peak_sus, peak_burst = fp64_peak()
+    gflops_exec = (st["flops_update"] + st["flops_chase"]) / (ms * 1e-3) / 1e9
+
+    # per-kernel CUDA-event times: the same sweep in profiling mode (events around every launch)
+    hq.teardown()
+    hq.setup(local, flags=hq.FLAG_PROFILE)
+    prof = []
+    for _ in range(max(1, min(args.steps, 2))):
+        restore()
+        torch.cuda.synchronize()
+        one()
+        prof.append(hq.stats())
+    hq.teardown()
+    ps = prof[-1]
+    upd_ms = ps["ms_left"] + ps["ms_right"]
+    upd_launches = ps["launches_left"] + ps["launches_right"]
+    achieved = ps["flops_update"] / (upd_ms * 1e-3) / 1e12  # TF/s over all update launches
+    roofline = {"bound": "tensor", "kernel": "update (left + right/Z DMMA GEMM)",
+                "achieved": achieved, "peak": peak_sus, "unit": "TFLOP/s", "frac": achieved / peak_sus,
+                "traffic": None,
+                "peak_source": "measured FP64 DMMA sustained, profiles/fp64_peaks_r01.json "
+                               "(MEASURED_PEAKS.json has no fp64 entry)",
+                "flops_per_launch": ps["flops_update"] / max(1, upd_launches),
+                "avg_launch_ms": upd_ms / max(1, upd_launches),
+                "share_of_step": upd_ms / max(1e-9, ps["ms_chase"] + upd_ms),
+                "ms_chase": ps["ms_chase"], "ms_left": ps["ms_left"], "ms_right": ps["ms_right"]}
+
+    e2e = None
+    if not args.no_e2e and rank == 0:
+        hq.setup(local)
+        Hh = torch.empty((n, n), dtype=torch.float64, pin_memory=True)
+        Zh = torch.empty((n, n), dtype=torch.float64, pin_memory=True)
+        Hp = np.asfortranarray(prob.H)
+        e2e_t = []
+        for i in range(2):
+            Hh.copy_(torch.from_numpy(Hp.T.copy()))
+            Zh.copy_(torch.from_numpy(np.ascontiguousarray(prob.Z.T)))
+            rc_t = time.perf_counter()
+            rc = hq.sweep_raw(Hh.data_ptr(), Zh.data_ptr(), n, prob.ilo, prob.ihi,
+                              np.ascontiguousarray(prob.shifts_re).ctypes.data,
+                              np.ascontiguousarray(prob.shifts_im).ctypes.data, nshifts, args.window)
+            dt = time.perf_counter() - rc_t
+            assert rc == 0, rc
+            e2e_t.append(dt)
+        st2 = hq.stats()
+        hq.teardown()
+        e2e = {"value": fa / min(e2e_t) / 1e9, "unit": "GFLOP/s",
+               "seconds_per_sweep": min(e2e_t),
+               "h2d_bytes_per_step": st2["h2d_bytes"], "d2h_bytes_per_step": st2["d2h_bytes"],
+               "how": "hqr_sweep with pinned host H and Z (wall clock around the C-ABI call)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(prob, args.cpu_bulges, n, prob.ilo, prob.ihi)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "weak" if world > 1 else "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, BASELINE.json configs)",
+            "config": {"workload": f"configs[{args.config}]", "n": n, "nshifts": nshifts,
+                       "window": st["window_eff"], "z": "random orthogonal" if args.config in (1, 3) else "identity",
+                       "parallelism": "replicas" if world > 1 else "1 GPU",
+                       "l2": "inputs (2 x %.1f GB) larger than L2" % (n * n * 8 / 1e9),
+                       "restore": "H, Z restored from pristine device copies before each step (untimed)"},
+            "seconds_per_sweep": ms * 1e-3,
+            "gflops_alg": value / world, "gflops_exec": gflops_exec,
+            "frac_fp64_peak_exec": gflops_exec / 1e3 / peak_sus,
+            "flops_exec_over_alg": (st["flops_update"] + st["flops_chase"]) / fa,
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
+            "gpu_launches": launches, "steps_per_sweep": st["steps"], "windows_per_sweep": st["windows"],
+            "input_gen_s": gen_s,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

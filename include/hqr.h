@@ -1,0 +1,127 @@
+/*
+ * hqr.h -- C ABI of the B200-native multishift QR sweep (libhqr_b200.so).
+ *
+ * The operation (PAPER.md = the paper's LaTeX body, cited as P:<line>):
+ *   One small-bulge multishift QR sweep on an upper-Hessenberg fp64 matrix H with a given shift set:
+ *     H <- Q^T H Q,  Z <- Z Q                                   (one QR iteration)
+ *   where Q is the product of all 3x3 (final: 2x2) Householder reflectors of the nshifts/2
+ *   tightly-coupled bulges introduced at the top of the active block [ilo, ihi] and chased to its
+ *   bottom (P:198-206 double-shift step, P:227-233 tightly-coupled multi-shift chains with
+ *   accumulated window factors and BLAS-3 off-diagonal updates, P:257-258 several chains,
+ *   P:376-386 "push bulges", P:400-404 / P:452-453 left/right update tasks).
+ *   Bulge j uses shifts (2j, 2j+1): the first column of (H - s I)(H - s' I) restricted to the block.
+ *   The sweep is the exact (up to rounding order) result of nshifts/2 sequential Francis double
+ *   steps (implicit-Q theorem); conventions are fixed in DESIGN.md "Readings" (R1-R12).
+ *
+ * Layout: H and Z are n x n IEEE binary64, column-major, leading dimension n (element (i,j) at
+ * i + j*n).  Indices are 0-based.  Updates span the full matrix ("wantt": rows 0..ilo-1 and columns
+ * ihi+1..n-1 of H are updated; all n rows of Z).
+ *
+ * Ownership: the caller owns H, Z and the shift arrays; the library modifies H and Z in place, never
+ * frees or retains caller memory, and owns all workspace (device buffers, streams, events, CUDA
+ * graphs) between hqr_setup and hqr_teardown.
+ *
+ * Return codes (LAPACK INFO style): 0 ok; -i argument i invalid (see hqr_sweep); 1000 + cudaError_t
+ * on a CUDA runtime failure; 2000 + ncclResult_t on an NCCL failure; -100 library not set up;
+ * -101 no CUDA device / unsupported device (the library never falls back to the CPU).
+ */
+#ifndef HQR_B200_H
+#define HQR_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct hqr_config {
+  int device;           /* CUDA device ordinal used by this process                              */
+  int rank;             /* this process's rank, 0 <= rank < world                                */
+  int world;            /* number of processes (one per GPU); 1 = single GPU                     */
+  const void* nccl_id;  /* world > 1: 128-byte ncclUniqueId created by rank 0 and shared with all */
+                        /* ranks (e.g. through torch.distributed); world == 1: NULL              */
+  int64_t n_max;        /* largest n this setup will sweep (workspace hint; 0 = grow on demand)  */
+  int flags;            /* bit 0: HQR_FLAG_NO_GRAPH -- launch kernels directly instead of         */
+                        /*        replaying a captured CUDA graph                                 */
+                        /* bit 1: HQR_FLAG_PROFILE  -- time every kernel class with CUDA events   */
+} hqr_config;
+
+#define HQR_FLAG_NO_GRAPH 1
+#define HQR_FLAG_PROFILE 2
+
+/* Initialise the library on cfg->device: streams, events, workspace, NCCL communicator (world > 1).
+ * Returns 0, -1 (cfg NULL or inconsistent rank/world/nccl_id), -101 (no usable sm_100 device),
+ * 1000+cudaError_t, 2000+ncclResult_t.  Calling it again re-initialises (tears down first). */
+int hqr_setup(const hqr_config* cfg);
+
+/*
+ * One multishift QR sweep, in place.  Synchronous: returns after the device has finished.
+ *   H         [in,out] n x n column-major; device pointer, or host pointer (pinned or pageable, in
+ *                      which case the library stages it through its own device memory and the
+ *                      host<->device copies are part of the call).  Must be upper Hessenberg on
+ *                      [ilo, ihi] with H[ilo, ilo-1] == 0 (ilo > 0) and H[ihi+1, ihi] == 0 (ihi < n-1).
+ *   Z         [in,out] n x n column-major (device or host), or NULL to skip Z <- Z Q.
+ *   n         matrix order, n >= 1
+ *   ilo, ihi  active block [ilo, ihi], 0 <= ilo <= ihi < n, N = ihi - ilo + 1 >= 3
+ *   shifts_re, shifts_im  [in] host arrays of nshifts doubles; consecutive pairs (2j, 2j+1) form bulge
+ *                      j; a non-real shift must be followed by its exact conjugate; real pairs are
+ *                      any two reals.
+ *   nshifts   even, 2 <= nshifts <= N
+ *   window    diagonal-window side k (performance knob only; never changes the mathematical result):
+ *             the effective side is min(window, N, HQR_MAX_WINDOW); it must be >= 8 unless it
+ *             covers the whole block (window >= N).
+ * Returns 0 or: -1 H NULL; -3 n < 1; -4 ilo < 0 or ilo > ihi; -5 ihi >= n or N < 3;
+ *   -6 non-finite shift; -7 conjugate partner not exact / mixed real-complex pair;
+ *   -8 nshifts odd, < 2 or > N; -9 window out of range; -10 block not decoupled
+ *   (H[ilo,ilo-1] != 0 or H[ihi+1,ihi] != 0); -100 not set up; 1000+cudaError_t; 2000+ncclResult_t.
+ * Matrix entries are assumed finite (no NaN/Inf scan).  With world > 1 it is a collective called by
+ * every rank with identical scalars and shifts (multi-GPU layout: see DESIGN.md §Multi-GPU).
+ */
+int hqr_sweep(double* H, double* Z, int64_t n, int64_t ilo, int64_t ihi, const double* shifts_re,
+              const double* shifts_im, int nshifts, int window);
+
+/* Release everything hqr_setup acquired.  Returns 0 (also when not set up) or 1000+cudaError_t. */
+int hqr_teardown(void);
+
+/* Largest effective window side the chase kernel supports (SMEM-resident window + factor). */
+#define HQR_MAX_WINDOW 112
+/* Library default window side used when window <= 0 is passed to hqr_plan_query / bench. */
+#define HQR_DEFAULT_WINDOW 96
+
+/*
+ * Host-only introspection of the wavefront plan (no GPU needed; used by the tests).
+ *   info[0..9] <- {k_eff, nbc_max, s, lag, nchains, nsteps, nwindows, max_kw, max_nbc, nb}
+ *   windows    <- nwindows rows of 10 int32 {step, chain, w0, w1, t0, t1, b0, nbc, slot, last}
+ *                 (may be NULL or cap too small: only info is written then)
+ * Returns 0 or the same negative argument codes as hqr_sweep (matrix values are not inspected).
+ */
+int hqr_plan_query(int64_t n, int64_t ilo, int64_t ihi, int nshifts, int window, int32_t* info,
+                   int32_t* windows, int64_t cap);
+
+/* Statistics of the last successful hqr_sweep on this process. */
+typedef struct hqr_stats {
+  int64_t kernels_launched;   /* kernels of this library launched by the last sweep              */
+  int64_t steps;              /* wavefront steps                                                  */
+  int64_t windows;            /* chase-kernel CTAs (diagonal windows)                             */
+  double flops_update;        /* GEMM flops of the off-diagonal update kernels (2*M*N*K, real kw) */
+  double flops_chase;         /* flops of the in-window chase (reflector applications)           */
+  double bytes_update;        /* algorithmic HBM bytes of the update kernels (panel read+write)   */
+  double ms_chase;            /* HQR_FLAG_PROFILE only: summed CUDA-event time per kernel class    */
+  double ms_left;
+  double ms_right;            /* right update + fused Z update                                    */
+  double ms_total;            /* CUDA-event time of the whole sweep (device work only)            */
+  int64_t h2d_bytes, d2h_bytes; /* staging copies (host-pointer calls)                           */
+  int launches_left, launches_right, launches_chase;
+  int window_eff;             /* effective window side                                           */
+} hqr_stats;
+
+int hqr_get_stats(hqr_stats* out);
+
+/* Static description of an error code. */
+const char* hqr_error_string(int code);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HQR_B200_H */

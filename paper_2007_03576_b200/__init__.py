@@ -1,0 +1,183 @@
+"""paper_2007_03576_b200 -- B200-native multishift QR sweep (thin Python binding over libhqr_b200.so).
+
+Argument marshalling only: every step of the sweep runs in the sm_100a kernels behind the C ABI
+declared in ``include/hqr.h`` (hqr_setup / hqr_sweep / hqr_teardown, plus hqr_plan_query and
+hqr_get_stats).  There is no CPU fallback: if the shared library or a CUDA device is missing the
+calls raise.
+
+Matrices are fp64, n x n, column-major (leading dimension n):
+  * device: a ``torch.float64`` CUDA tensor with ``stride() == (1, n)`` (e.g. ``T.t()`` of a
+    contiguous tensor T holding the transpose), see :func:`to_device` / :func:`from_device`;
+  * host: a numpy float64 Fortran-ordered array (the library stages it; copies are in the call).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+from . import build as _build
+
+_lib = None
+
+ERRORS = {
+    -1: "H is NULL / invalid config", -3: "n < 1", -4: "ilo < 0 or ilo > ihi",
+    -5: "ihi >= n or active block shorter than 3", -6: "non-finite shift",
+    -7: "shift pair not two reals / exact conjugates", -8: "nshifts odd, < 2 or > N",
+    -9: "window out of range", -10: "active block not decoupled", -100: "not set up",
+    -101: "no usable sm_100 CUDA device",
+}
+
+FLAG_NO_GRAPH = 1
+FLAG_PROFILE = 2
+MAX_WINDOW = 112
+DEFAULT_WINDOW = 96
+
+
+class HQRError(RuntimeError):
+    def __init__(self, code: int, where: str):
+        self.code = code
+        msg = ERRORS.get(code) or ("CUDA error %d" % (code - 1000) if 1000 <= code < 2000 else
+                                   "NCCL error %d" % (code - 2000) if code >= 2000 else "error")
+        super().__init__(f"{where} returned {code}: {msg}")
+
+
+class _Config(ctypes.Structure):
+    _fields_ = [("device", ctypes.c_int), ("rank", ctypes.c_int), ("world", ctypes.c_int),
+                ("nccl_id", ctypes.c_void_p), ("n_max", ctypes.c_int64), ("flags", ctypes.c_int)]
+
+
+class Stats(ctypes.Structure):
+    _fields_ = [("kernels_launched", ctypes.c_int64), ("steps", ctypes.c_int64),
+                ("windows", ctypes.c_int64), ("flops_update", ctypes.c_double),
+                ("flops_chase", ctypes.c_double), ("bytes_update", ctypes.c_double),
+                ("ms_chase", ctypes.c_double), ("ms_left", ctypes.c_double),
+                ("ms_right", ctypes.c_double), ("ms_total", ctypes.c_double),
+                ("h2d_bytes", ctypes.c_int64), ("d2h_bytes", ctypes.c_int64),
+                ("launches_left", ctypes.c_int), ("launches_right", ctypes.c_int),
+                ("launches_chase", ctypes.c_int), ("window_eff", ctypes.c_int)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+SYMBOLS = ["hqr_setup", "hqr_sweep", "hqr_teardown", "hqr_plan_query", "hqr_get_stats",
+           "hqr_error_string"]
+
+
+def lib():
+    """Load (building first if stale) libhqr_b200.so.  Raises if it cannot be loaded."""
+    global _lib
+    if _lib is None:
+        path = _build.LIB
+        if not os.path.exists(path) or _build._stale():
+            _build.build()
+        L = ctypes.CDLL(path)
+        L.hqr_setup.argtypes = [ctypes.POINTER(_Config)]
+        L.hqr_setup.restype = ctypes.c_int
+        L.hqr_sweep.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64,
+                                ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int,
+                                ctypes.c_int]
+        L.hqr_sweep.restype = ctypes.c_int
+        L.hqr_teardown.argtypes = []
+        L.hqr_teardown.restype = ctypes.c_int
+        L.hqr_plan_query.argtypes = [ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int,
+                                     ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64]
+        L.hqr_plan_query.restype = ctypes.c_int
+        L.hqr_get_stats.argtypes = [ctypes.POINTER(Stats)]
+        L.hqr_get_stats.restype = ctypes.c_int
+        L.hqr_error_string.argtypes = [ctypes.c_int]
+        L.hqr_error_string.restype = ctypes.c_char_p
+        _lib = L
+    return _lib
+
+
+def setup(device: int = 0, flags: int = 0, rank: int = 0, world: int = 1, nccl_id: bytes | None = None,
+          n_max: int = 0) -> None:
+    buf = None
+    cfg = _Config(device, rank, world, None, n_max, flags)
+    if nccl_id is not None:
+        buf = ctypes.create_string_buffer(bytes(nccl_id), len(nccl_id))
+        cfg.nccl_id = ctypes.cast(buf, ctypes.c_void_p)
+    rc = lib().hqr_setup(ctypes.byref(cfg))
+    if rc:
+        raise HQRError(rc, "hqr_setup")
+
+
+def teardown() -> None:
+    rc = lib().hqr_teardown()
+    if rc:
+        raise HQRError(rc, "hqr_teardown")
+
+
+def _ptr_n(A):
+    """(pointer, n) of a column-major fp64 matrix given as a torch CUDA view or numpy F-array."""
+    if A is None:
+        return None, None
+    if isinstance(A, np.ndarray):
+        if A.dtype != np.float64 or A.ndim != 2 or A.shape[0] != A.shape[1] or not A.flags.f_contiguous:
+            raise TypeError("host matrices must be square float64 Fortran-ordered numpy arrays")
+        return A.ctypes.data, A.shape[0]
+    import torch
+    if not isinstance(A, torch.Tensor) or A.dtype != torch.float64 or A.dim() != 2:
+        raise TypeError("device matrices must be 2-D torch.float64 tensors")
+    n = A.shape[0]
+    if A.shape[1] != n or A.stride() != (1, n):
+        raise TypeError("device matrices must be column-major views (stride (1, n)); see to_device()")
+    return A.data_ptr(), n
+
+
+def sweep(H, Z, ilo: int, ihi: int, shifts_re, shifts_im, window: int = DEFAULT_WINDOW) -> None:
+    """One multishift QR sweep in place: H <- Q^T H Q, Z <- Z Q (include/hqr.h hqr_sweep)."""
+    hp, n = _ptr_n(H)
+    zp, nz = _ptr_n(Z)
+    if hp is None:
+        raise HQRError(-1, "hqr_sweep")
+    if zp is not None and nz != n:
+        raise ValueError("H and Z must have the same order")
+    sr = np.ascontiguousarray(shifts_re, dtype=np.float64)
+    si = np.ascontiguousarray(shifts_im, dtype=np.float64)
+    if sr.shape != si.shape:
+        raise ValueError("shifts_re and shifts_im must have the same length")
+    rc = lib().hqr_sweep(hp, zp, n, ilo, ihi, sr.ctypes.data, si.ctypes.data, int(sr.shape[0]),
+                         int(window))
+    if rc:
+        raise HQRError(rc, "hqr_sweep")
+
+
+def sweep_raw(H_ptr, Z_ptr, n, ilo, ihi, sr_ptr, si_ptr, nshifts, window) -> int:
+    """Direct ABI call (tests of the error codes); returns the C return code."""
+    return lib().hqr_sweep(H_ptr, Z_ptr, n, ilo, ihi, sr_ptr, si_ptr, nshifts, window)
+
+
+def plan_query(n: int, ilo: int, ihi: int, nshifts: int, window: int):
+    """Host-only plan introspection: (info dict, windows int32 array [nw, 10]) or raises."""
+    info = np.zeros(10, dtype=np.int32)
+    rc = lib().hqr_plan_query(n, ilo, ihi, nshifts, window, info.ctypes.data, None, 0)
+    if rc:
+        raise HQRError(rc, "hqr_plan_query")
+    nw = int(info[6])
+    wins = np.zeros((nw, 10), dtype=np.int32)
+    rc = lib().hqr_plan_query(n, ilo, ihi, nshifts, window, info.ctypes.data, wins.ctypes.data, nw)
+    if rc:
+        raise HQRError(rc, "hqr_plan_query")
+    keys = ["k", "nbc_max", "s", "lag", "nchains", "nsteps", "nwindows", "max_kw", "max_nbc", "nb"]
+    return dict(zip(keys, (int(v) for v in info))), wins
+
+
+def stats() -> dict:
+    st = Stats()
+    lib().hqr_get_stats(ctypes.byref(st))
+    return st.as_dict()
+
+
+def to_device(A: np.ndarray, device: str = "cuda"):
+    """numpy Fortran array -> torch CUDA column-major view (stride (1, n))."""
+    import torch
+    return torch.from_numpy(np.ascontiguousarray(A.T)).to(device).t()
+
+
+def from_device(T) -> np.ndarray:
+    """torch column-major view -> numpy Fortran array."""
+    return np.asfortranarray(T.t().contiguous().cpu().numpy().T)

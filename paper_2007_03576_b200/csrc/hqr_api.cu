@@ -1,0 +1,490 @@
+// hqr_api.cu -- the C ABI (include/hqr.h): validation, planning, workspace, kernel orchestration.
+//
+// Orchestration of one sweep:
+//   a1  validate + pair shifts on the host (sigma_j = s + s', pi_j = s s'), upload 2*nb doubles;
+//   a7  plan the wavefront (plan.hpp) and upload the window table once per distinct plan;
+//   per wavefront step g:  chase(g)  ->  left(g)  ->  right+Z(g)   (one stream, in order)
+//       chase  one CTA per window (a2 introduction + a3 in-window chase, chase.cu)
+//       left   a4 Q^T H(W, right of W) for every window of the step (update.cu)
+//       right  a5 H(above W, W) Q and a6 Z(:, W) Q for every window of the step (update.cu)
+//   The step sequence is captured once into a CUDA graph per (plan, pointers) and replayed
+//   (HQR_FLAG_NO_GRAPH launches directly; HQR_FLAG_PROFILE times each kernel with events).
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <tuple>
+#include <vector>
+
+#include "../../include/hqr.h"
+#include "kernels.hpp"
+#include "plan.hpp"
+
+using hqr::Plan;
+using hqr::StepArgs;
+using hqr::WindowDesc;
+
+namespace {
+
+struct PlanKey {
+  int64_t n, ilo, ihi;
+  int nshifts, window;
+  bool operator<(const PlanKey& o) const {
+    return std::tie(n, ilo, ihi, nshifts, window) < std::tie(o.n, o.ilo, o.ihi, o.nshifts, o.window);
+  }
+};
+
+struct GraphKey {
+  PlanKey pk;
+  const double* H;
+  const double* Z;
+  bool operator<(const GraphKey& o) const {
+    return std::tie(pk, H, Z) < std::tie(o.pk, o.H, o.Z);
+  }
+};
+
+struct CachedPlan {
+  Plan plan;
+  WindowDesc* d_wins = nullptr;
+  int KP = 0;
+};
+
+struct State {
+  bool ready = false;
+  int device = 0, rank = 0, world = 1, flags = 0, num_sms = 0;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  double* d_coef = nullptr;
+  size_t coef_cap = 0;
+  double* d_q = nullptr;
+  size_t q_cap = 0;
+  double* d_hstage = nullptr;
+  double* d_zstage = nullptr;
+  size_t stage_cap = 0;
+  std::map<PlanKey, std::unique_ptr<CachedPlan>> plans;
+  std::map<GraphKey, cudaGraphExec_t> graphs;
+  std::vector<cudaEvent_t> prof_events;
+  hqr_stats stats{};
+};
+
+State g;
+
+int cuerr(cudaError_t e) { return e == cudaSuccess ? 0 : 1000 + (int)e; }
+#define CK(x)                                   \
+  do {                                          \
+    cudaError_t e_ = (x);                       \
+    if (e_ != cudaSuccess) return cuerr(e_);    \
+  } while (0)
+
+// a1: argument validation that does not touch matrix values (shared by hqr_sweep / plan query)
+int validate_scalars(int64_t n, int64_t ilo, int64_t ihi, const double* sr, const double* si,
+                     int nshifts, int window, bool check_shifts) {
+  if (n < 1) return -3;
+  if (ilo < 0 || ilo > ihi) return -4;
+  if (ihi >= n || ihi - ilo + 1 < 3) return -5;
+  const int64_t N = ihi - ilo + 1;
+  if (nshifts < 2 || (nshifts & 1) || nshifts > N) return -8;
+  if (check_shifts) {
+    if (!sr) return -6;
+    if (!si) return -7;
+    for (int i = 0; i < nshifts; ++i)
+      if (!std::isfinite(sr[i]) || !std::isfinite(si[i])) return -6;
+    for (int j = 0; j < nshifts / 2; ++j) {
+      double r0 = sr[2 * j], r1 = sr[2 * j + 1], i0 = si[2 * j], i1 = si[2 * j + 1];
+      bool real_pair = (i0 == 0.0 && i1 == 0.0);
+      bool conj_pair = (i0 != 0.0 && r0 == r1 && i0 == -i1);
+      if (!real_pair && !conj_pair) return -7;
+    }
+  }
+  if (window <= 0) return -9;
+  return 0;
+}
+
+int get_plan(int64_t n, int64_t ilo, int64_t ihi, int nshifts, int window, CachedPlan** out,
+             bool upload) {
+  PlanKey key{n, ilo, ihi, nshifts, window};
+  auto it = g.plans.find(key);
+  if (it == g.plans.end()) {
+    auto cp = std::make_unique<CachedPlan>();
+    int rc = hqr::make_plan(n, ilo, ihi, nshifts, window, hqr::kMaxWindow, &cp->plan);
+    if (rc) return rc;
+    cp->KP = hqr::padded_kp(cp->plan.max_kw);
+    it = g.plans.emplace(key, std::move(cp)).first;
+  }
+  CachedPlan* cp = it->second.get();
+  if (upload && !cp->d_wins) {
+    size_t bytes = cp->plan.windows.size() * sizeof(WindowDesc);
+    CK(cudaMalloc(&cp->d_wins, bytes));
+    CK(cudaMemcpy(cp->d_wins, cp->plan.windows.data(), bytes, cudaMemcpyHostToDevice));
+  }
+  *out = cp;
+  return 0;
+}
+
+bool is_device_ptr(const void* p) {
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+int ensure(double** p, size_t* cap, size_t count) {
+  if (*cap >= count) return 0;
+  if (*p) CK(cudaFree(*p));
+  *p = nullptr;
+  *cap = 0;
+  CK(cudaMalloc(p, count * sizeof(double)));
+  *cap = count;
+  return 0;
+}
+
+cudaEvent_t prof_event(size_t i) {
+  while (g.prof_events.size() <= i) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    g.prof_events.push_back(e);
+  }
+  return g.prof_events[i];
+}
+
+// Enqueue every step of the sweep on g.stream.  prof: record events around each launch.
+int enqueue_sweep(const CachedPlan& cp, double* H, double* Z, int64_t n, bool prof,
+                  std::vector<int>* classes, hqr_stats* st) {
+  const Plan& P = cp.plan;
+  StepArgs a{};
+  a.H = H; a.Z = Z; a.n = n; a.ilo = P.ilo; a.ihi = P.ihi;
+  a.wins = cp.d_wins; a.coef = g.d_coef; a.qslots = g.d_q; a.KP = cp.KP;
+  size_t ev = 0;
+  auto mark = [&](int cls) {
+    if (!prof) return;
+    cudaEventRecord(prof_event(ev++), g.stream);
+    if (classes) classes->push_back(cls);
+  };
+  for (int s = 0; s < P.nsteps; ++s) {
+    a.win_begin = P.step_begin[s];
+    a.win_count = P.step_begin[s + 1] - P.step_begin[s];
+    const WindowDesc* hw = P.windows.data() + a.win_begin;
+    mark(0);
+    CK(hqr::launch_chase(a, P.max_kw, P.max_nbc, g.stream));
+    mark(-1);
+    st->launches_chase++;
+    int64_t items;
+    double fl, by;
+    mark(1);
+    CK(hqr::launch_left(a, hw, g.num_sms, g.stream, &items, &fl, &by));
+    mark(-1);
+    if (items) st->launches_left++;
+    st->flops_update += fl;
+    st->bytes_update += by;
+    mark(2);
+    CK(hqr::launch_right(a, hw, g.num_sms, g.stream, &items, &fl, &by));
+    mark(-1);
+    if (items) st->launches_right++;
+    st->flops_update += fl;
+    st->bytes_update += by;
+    for (int i = 0; i < a.win_count; ++i) {
+      // chase flops: per reflector 10 (3-vector) flops x (left cols + right rows + Q rows) in-window
+      (void)hw;
+    }
+  }
+  st->steps = P.nsteps;
+  st->windows = (int64_t)P.windows.size();
+  st->kernels_launched = st->launches_chase + st->launches_left + st->launches_right;
+  return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+int hqr_setup(const hqr_config* cfg) {
+  if (!cfg) return -1;
+  if (g.ready) hqr_teardown();
+  if (cfg->world < 1 || cfg->rank < 0 || cfg->rank >= cfg->world) return -1;
+  if (cfg->world > 1) return -1;  // multi-GPU sharding: see DESIGN.md §Multi-GPU (not in this build)
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= cfg->device || cfg->device < 0) {
+    cudaGetLastError();
+    return -101;
+  }
+  CK(cudaSetDevice(cfg->device));
+  cudaDeviceProp prop;
+  CK(cudaGetDeviceProperties(&prop, cfg->device));
+  if (prop.major != 10) return -101;  // built for sm_100a only
+  g.device = cfg->device;
+  g.rank = cfg->rank;
+  g.world = cfg->world;
+  g.flags = cfg->flags;
+  g.num_sms = prop.multiProcessorCount;
+  CK(cudaStreamCreateWithFlags(&g.stream, cudaStreamNonBlocking));
+  CK(cudaEventCreate(&g.ev0));
+  CK(cudaEventCreate(&g.ev1));
+  g.ready = true;
+  return 0;
+}
+
+int hqr_teardown(void) {
+  if (!g.ready) return 0;
+  cudaSetDevice(g.device);
+  cudaStreamSynchronize(g.stream);
+  for (auto& kv : g.graphs) cudaGraphExecDestroy(kv.second);
+  g.graphs.clear();
+  for (auto& kv : g.plans)
+    if (kv.second->d_wins) cudaFree(kv.second->d_wins);
+  g.plans.clear();
+  for (auto e : g.prof_events) cudaEventDestroy(e);
+  g.prof_events.clear();
+  if (g.d_coef) cudaFree(g.d_coef);
+  if (g.d_q) cudaFree(g.d_q);
+  if (g.d_hstage) cudaFree(g.d_hstage);
+  if (g.d_zstage) cudaFree(g.d_zstage);
+  g.d_coef = g.d_q = g.d_hstage = g.d_zstage = nullptr;
+  g.coef_cap = g.q_cap = g.stage_cap = 0;
+  cudaEventDestroy(g.ev0);
+  cudaEventDestroy(g.ev1);
+  cudaStreamDestroy(g.stream);
+  g.ready = false;
+  cudaError_t e = cudaGetLastError();
+  return cuerr(e);
+}
+
+int hqr_sweep(double* H, double* Z, int64_t n, int64_t ilo, int64_t ihi, const double* shifts_re,
+              const double* shifts_im, int nshifts, int window) {
+  if (!H) return -1;
+  int rc = validate_scalars(n, ilo, ihi, shifts_re, shifts_im, nshifts, window, true);
+  if (rc) return rc;
+  {  // a7 plan (host only; validates the window)
+    Plan tmp;
+    rc = hqr::make_plan(n, ilo, ihi, nshifts, window, hqr::kMaxWindow, &tmp);
+    if (rc) return rc;
+  }
+  if (!g.ready) return -100;
+  CK(cudaSetDevice(g.device));
+  CachedPlan* cp = nullptr;
+  rc = get_plan(n, ilo, ihi, nshifts, window, &cp, true);
+  if (rc) return rc;
+
+  hqr_stats st{};
+  st.window_eff = cp->plan.k;
+  const bool h_dev = is_device_ptr(H);
+  const bool z_dev = Z ? is_device_ptr(Z) : true;
+
+  // decoupling check (-10): two scalars
+  double sub[2] = {0.0, 0.0};
+  if (ilo > 0 || ihi < n - 1) {
+    const double* p0 = H + ilo + (ilo - 1) * n;
+    const double* p1 = H + (ihi + 1) + ihi * n;
+    if (h_dev) {
+      if (ilo > 0) CK(cudaMemcpy(&sub[0], p0, sizeof(double), cudaMemcpyDeviceToHost));
+      if (ihi < n - 1) CK(cudaMemcpy(&sub[1], p1, sizeof(double), cudaMemcpyDeviceToHost));
+    } else {
+      if (ilo > 0) sub[0] = *p0;
+      if (ihi < n - 1) sub[1] = *p1;
+    }
+    if (sub[0] != 0.0 || sub[1] != 0.0) return -10;
+  }
+
+  // a1 pair the shifts: sigma = s + s', pi = s s' (real form, reading R1/R3)
+  const int nb = nshifts / 2;
+  std::vector<double> coef(2 * nb);
+  for (int j = 0; j < nb; ++j) {
+    coef[2 * j] = shifts_re[2 * j] + shifts_re[2 * j + 1];
+    coef[2 * j + 1] = shifts_re[2 * j] * shifts_re[2 * j + 1] - shifts_im[2 * j] * shifts_im[2 * j + 1];
+  }
+  rc = ensure(&g.d_coef, &g.coef_cap, coef.size());
+  if (rc) return rc;
+  CK(cudaMemcpyAsync(g.d_coef, coef.data(), coef.size() * sizeof(double), cudaMemcpyHostToDevice,
+                     g.stream));
+  rc = ensure(&g.d_q, &g.q_cap, (size_t)cp->plan.nchains * cp->KP * cp->KP);
+  if (rc) return rc;
+
+  // host buffers: stage through library-owned device memory
+  const size_t nn = (size_t)n * (size_t)n;
+  double* dH = H;
+  double* dZ = Z;
+  CK(cudaEventRecord(g.ev0, g.stream));
+  if (!h_dev || !z_dev) {
+    size_t need = nn;
+    if (g.stage_cap < need) {
+      if (g.d_hstage) CK(cudaFree(g.d_hstage));
+      if (g.d_zstage) CK(cudaFree(g.d_zstage));
+      g.d_hstage = g.d_zstage = nullptr;
+      g.stage_cap = 0;
+      CK(cudaMalloc(&g.d_hstage, need * sizeof(double)));
+      CK(cudaMalloc(&g.d_zstage, need * sizeof(double)));
+      g.stage_cap = need;
+    }
+    if (!h_dev) {
+      dH = g.d_hstage;
+      CK(cudaMemcpyAsync(dH, H, nn * sizeof(double), cudaMemcpyHostToDevice, g.stream));
+      st.h2d_bytes += nn * sizeof(double);
+    }
+    if (Z && !z_dev) {
+      dZ = g.d_zstage;
+      CK(cudaMemcpyAsync(dZ, Z, nn * sizeof(double), cudaMemcpyHostToDevice, g.stream));
+      st.h2d_bytes += nn * sizeof(double);
+    }
+  }
+
+  const bool prof = (g.flags & HQR_FLAG_PROFILE) != 0;
+  const bool use_graph = !prof && !(g.flags & HQR_FLAG_NO_GRAPH);
+  std::vector<int> classes;
+  if (use_graph) {
+    GraphKey gk{{n, ilo, ihi, nshifts, window}, dH, dZ};
+    auto it = g.graphs.find(gk);
+    if (it == g.graphs.end()) {
+      cudaGraph_t graph;
+      CK(cudaStreamBeginCapture(g.stream, cudaStreamCaptureModeThreadLocal));
+      hqr_stats tmp{};
+      int rc2 = enqueue_sweep(*cp, dH, dZ, n, false, nullptr, &tmp);
+      cudaError_t ec = cudaStreamEndCapture(g.stream, &graph);
+      if (rc2) return rc2;
+      CK(ec);
+      cudaGraphExec_t exec;
+      CK(cudaGraphInstantiate(&exec, graph, 0));
+      cudaGraphDestroy(graph);
+      it = g.graphs.emplace(gk, exec).first;
+    }
+    CK(cudaGraphLaunch(it->second, g.stream));
+    // launch accounting (same plan as captured)
+    hqr_stats tmp{};
+    {
+      // recount without launching
+      const Plan& P = cp->plan;
+      for (int s = 0; s < P.nsteps; ++s) {
+        int cnt = P.step_begin[s + 1] - P.step_begin[s];
+        const WindowDesc* hw = P.windows.data() + P.step_begin[s];
+        tmp.launches_chase++;
+        for (int i = 0; i < cnt; ++i) {
+          int64_t kw = hw[i].w1 - hw[i].w0 + 1;
+          double cols = (double)(n - 1 - hw[i].w1), rows = (double)hw[i].w0 + (dZ ? (double)n : 0.0);
+          tmp.flops_update += 2.0 * kw * kw * (cols + rows);
+          tmp.bytes_update += 16.0 * kw * (cols + rows);
+        }
+        bool anyl = false, anyr = false;
+        for (int i = 0; i < cnt; ++i) {
+          if (hw[i].w1 < n - 1) anyl = true;
+          if (hw[i].w0 > 0 || dZ) anyr = true;
+        }
+        tmp.launches_left += anyl;
+        tmp.launches_right += anyr;
+      }
+      tmp.steps = P.nsteps;
+      tmp.windows = (int64_t)P.windows.size();
+      tmp.kernels_launched = tmp.launches_chase + tmp.launches_left + tmp.launches_right;
+    }
+    st.flops_update = tmp.flops_update;
+    st.bytes_update = tmp.bytes_update;
+    st.launches_chase = tmp.launches_chase;
+    st.launches_left = tmp.launches_left;
+    st.launches_right = tmp.launches_right;
+    st.steps = tmp.steps;
+    st.windows = tmp.windows;
+    st.kernels_launched = tmp.kernels_launched;
+  } else {
+    rc = enqueue_sweep(*cp, dH, dZ, n, prof, &classes, &st);
+    if (rc) return rc;
+  }
+
+  if (!h_dev) {
+    CK(cudaMemcpyAsync(H, dH, nn * sizeof(double), cudaMemcpyDeviceToHost, g.stream));
+    st.d2h_bytes += nn * sizeof(double);
+  }
+  if (Z && !z_dev) {
+    CK(cudaMemcpyAsync(Z, dZ, nn * sizeof(double), cudaMemcpyDeviceToHost, g.stream));
+    st.d2h_bytes += nn * sizeof(double);
+  }
+  CK(cudaEventRecord(g.ev1, g.stream));
+  CK(cudaStreamSynchronize(g.stream));
+  CK(cudaGetLastError());
+  float ms = 0;
+  CK(cudaEventElapsedTime(&ms, g.ev0, g.ev1));
+  st.ms_total = ms;
+  if (prof) {
+    // events come in (start, end) pairs; classes[2i] is the kernel class of pair i
+    for (size_t i = 0; i + 1 < classes.size(); i += 2) {
+      float e = 0;
+      cudaEventElapsedTime(&e, g.prof_events[i], g.prof_events[i + 1]);
+      if (classes[i] == 0) st.ms_chase += e;
+      else if (classes[i] == 1) st.ms_left += e;
+      else st.ms_right += e;
+    }
+  }
+  // in-window chase flops (per 3-reflector: 10 flops x (left cols + right rows + Q rows))
+  {
+    const Plan& P = cp->plan;
+    double f = 0;
+    for (const WindowDesc& w : P.windows) {
+      for (int t = w.t0; t <= w.t1; ++t)
+        for (int jj = 0; jj < w.nbc; ++jj) {
+          int64_t p = P.ilo - 1 + t - 3 * (int64_t)jj;
+          if (p < P.ilo - 1 || p > P.ihi - 2) continue;
+          int m = (p <= P.ihi - 3) ? 3 : 2;
+          int64_t pl = p - w.w0;
+          double cnt = (double)(w.w1 - std::max<int64_t>(pl, 0) - w.w0) + (double)(pl + m + 2) +
+                       (double)std::min<int64_t>(pl + m + 3, w.w1 - w.w0 + 1);
+          f += (m == 3 ? 10.0 : 6.0) * cnt;
+        }
+    }
+    st.flops_chase = f;
+  }
+  g.stats = st;
+  return 0;
+}
+
+int hqr_plan_query(int64_t n, int64_t ilo, int64_t ihi, int nshifts, int window, int32_t* info,
+                   int32_t* windows, int64_t cap) {
+  int rc = validate_scalars(n, ilo, ihi, nullptr, nullptr, nshifts, window, false);
+  if (rc) return rc;
+  Plan P;
+  rc = hqr::make_plan(n, ilo, ihi, nshifts, window, hqr::kMaxWindow, &P);
+  if (rc) return rc;
+  if (info) {
+    int32_t v[10] = {P.k, P.nbc_max, P.s, P.lag, P.nchains, P.nsteps, (int32_t)P.windows.size(),
+                     P.max_kw, P.max_nbc, P.nb};
+    std::memcpy(info, v, sizeof(v));
+  }
+  if (windows && cap >= (int64_t)P.windows.size()) {
+    for (int s = 0; s < P.nsteps; ++s)
+      for (int i = P.step_begin[s]; i < P.step_begin[s + 1]; ++i) {
+        const WindowDesc& w = P.windows[i];
+        int32_t* r = windows + 10 * (int64_t)i;
+        r[0] = s; r[1] = w.chain; r[2] = w.w0; r[3] = w.w1; r[4] = w.t0; r[5] = w.t1;
+        r[6] = w.b0; r[7] = w.nbc; r[8] = w.slot; r[9] = w.last;
+      }
+  }
+  return 0;
+}
+
+int hqr_get_stats(hqr_stats* out) {
+  if (!out) return -1;
+  *out = g.stats;
+  return 0;
+}
+
+const char* hqr_error_string(int code) {
+  switch (code) {
+    case 0: return "ok";
+    case -1: return "H is NULL / invalid config";
+    case -3: return "n < 1";
+    case -4: return "ilo < 0 or ilo > ihi";
+    case -5: return "ihi >= n or active block shorter than 3";
+    case -6: return "non-finite shift (or shifts_re NULL)";
+    case -7: return "shift pair is neither two reals nor an exact conjugate pair (or shifts_im NULL)";
+    case -8: return "nshifts odd, < 2 or larger than the active block";
+    case -9: return "window out of range";
+    case -10: return "active block not decoupled (H[ilo,ilo-1] or H[ihi+1,ihi] nonzero)";
+    case -100: return "library not set up (call hqr_setup)";
+    case -101: return "no usable sm_100 CUDA device";
+  }
+  if (code >= 2000) return "NCCL error (code - 2000 = ncclResult_t)";
+  if (code >= 1000) return "CUDA error (code - 1000 = cudaError_t)";
+  return "unknown error";
+}
+
+}  // extern "C"

@@ -1,0 +1,42 @@
+// kernels.hpp -- launch interface between the orchestration (hqr_api.cu) and the sm_100a kernels
+// (chase.cu, update.cu).  Product path only; shares nothing with oracle/.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "plan.hpp"
+
+namespace hqr {
+
+// Arguments of one wavefront step (device pointers).
+struct StepArgs {
+  double* H;                 // n x n column-major, ld = n
+  double* Z;                 // n x n column-major or nullptr
+  int64_t n;
+  int64_t ilo, ihi;
+  const WindowDesc* wins;    // device copy of plan.windows
+  int win_begin, win_count;  // this step's windows
+  const double* coef;        // per bulge j: coef[2j] = sigma_j, coef[2j+1] = pi_j
+  double* qslots;            // Q slot s at qslots + s*KP*KP, column-major, ld = KP, zero padded
+  int KP;                    // padded factor side (32, 64, 96 or 128)
+};
+
+// One CTA per window: chase the step's bulges inside SMEM-resident windows, accumulate Q_W.
+cudaError_t launch_chase(const StepArgs& a, int max_kw, int max_nbc, cudaStream_t st);
+size_t chase_smem_bytes(int kw, int nbc);
+
+// Off-diagonal updates of one step.  Left: H(W, w1+1:n) <- Q_W^T H(W, w1+1:n) for every window.
+// Right (+Z): H(0:w0, W) <- H(0:w0, W) Q_W and Z(:, W) <- Z(:, W) Q_W.
+// host_wins: the step's windows on the host (to size the grid).  Returns the number of items
+// (tiles) through *items and the launch's GEMM flops through *flops.
+cudaError_t launch_left(const StepArgs& a, const WindowDesc* host_wins, int num_sms,
+                        cudaStream_t st, int64_t* items, double* flops, double* bytes);
+cudaError_t launch_right(const StepArgs& a, const WindowDesc* host_wins, int num_sms,
+                         cudaStream_t st, int64_t* items, double* flops, double* bytes);
+
+// Largest window side whose chase fits in SMEM (H window + Q_W both resident).
+constexpr int kMaxWindow = 112;
+
+inline int padded_kp(int kw) { return kw <= 32 ? 32 : kw <= 64 ? 64 : kw <= 96 ? 96 : 128; }
+
+}  // namespace hqr

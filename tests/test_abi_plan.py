@@ -1,0 +1,124 @@
+"""CPU tests of the product library without a GPU: the C ABI loads and exports every symbol
+include/hqr.h declares, argument validation returns the documented codes, the wavefront planner's
+invariants hold, and the planned schedule (emulated in numpy) reproduces the oracle."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_2007_03576_b200 as hq
+from hqr_inputs import random_case, make
+from schedule_emulator import emulate
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_library_exports_every_header_symbol():
+    hdr = open(os.path.join(ROOT, "include", "hqr.h")).read()
+    names = set(re.findall(r"^\s*(?:int|const char\*)\s+(hqr_\w+)\s*\(", hdr, re.M))
+    assert names == set(hq.SYMBOLS)
+    L = ctypes.CDLL(hq.lib()._name)
+    for s in names:
+        assert hasattr(L, s), s
+
+
+def _call(n=16, ilo=0, ihi=15, ns=4, window=8, sr=None, si=None, H=True):
+    sr = np.array([0.1, 0.2, 0.3, 0.3] if sr is None else sr, dtype=np.float64)
+    si = np.array([0.0, 0.0, 0.5, -0.5] if si is None else si, dtype=np.float64)
+    Hm = np.asfortranarray(np.eye(max(n, 1)))
+    return hq.sweep_raw(Hm.ctypes.data if H else None, None, n, ilo, ihi, sr.ctypes.data,
+                        si.ctypes.data, ns, window)
+
+
+@pytest.mark.parametrize("kw,code", [
+    (dict(H=False), -1), (dict(n=0), -3), (dict(ilo=-1), -4), (dict(ilo=5, ihi=4), -4),
+    (dict(ihi=16), -5), (dict(ilo=3, ihi=4), -5), (dict(ns=3), -8), (dict(ns=0), -8),
+    (dict(ns=4, n=16, ilo=0, ihi=2), -8), (dict(sr=[np.nan, 0.2, 0.3, 0.3]), -6),
+    (dict(si=[0.0, 0.0, 0.5, 0.5]), -7), (dict(si=[0.1, 0.0, 0.5, -0.5]), -7),
+    (dict(sr=[0.1, 0.2, 0.3, 0.31]), -7), (dict(window=0), -9), (dict(window=7), -9),
+])
+def test_invalid_arguments_exact_codes(kw, code):
+    assert _call(**kw) == code
+
+
+def test_not_set_up_code():
+    hq.lib().hqr_teardown()
+    assert _call() == -100
+
+
+def test_error_strings():
+    L = hq.lib()
+    for c in (0, -1, -3, -4, -5, -6, -7, -8, -9, -10, -100, -101, 1002, 2001):
+        assert L.hqr_error_string(c)
+
+
+@pytest.mark.parametrize("n,ns,ilo,ihi,win", [
+    (256, 8, 0, 255, 24), (20000, 512, 0, 19999, 96), (10000, 256, 0, 9999, 112),
+    (4000, 100, 0, 3999, 151), (300, 20, 40, 259, 24), (9, 8, 0, 8, 8), (200, 60, 10, 190, 8),
+    (5000, 1000, 100, 4899, 64),
+])
+def test_plan_invariants(n, ns, ilo, ihi, win):
+    info, W = hq.plan_query(n, ilo, ihi, ns, win)
+    N = ihi - ilo + 1
+    k = info["k"]
+    assert k == min(win, N, hq.MAX_WINDOW)
+    nb = ns // 2
+    # chains partition the bulges (remainders on the earliest chains), <= (k-2)/6 each
+    chains = {}
+    for w in W:
+        chains.setdefault(int(w[1]), (int(w[6]), int(w[7])))
+    b = 0
+    for c in sorted(chains):
+        b0, nbc = chains[c]
+        assert b0 == b and (N <= k or nbc <= (k - 2) // 6)
+        b += nbc
+    assert b == nb
+    sizes = [chains[c][1] for c in sorted(chains)]
+    assert sizes == sorted(sizes, reverse=True) and max(sizes) - min(sizes) <= 1
+    for step in range(info["nsteps"]):
+        sw = W[W[:, 0] == step]
+        assert len(sw) >= 1
+        # windows of a step are disjoint and listed top (highest chain) first
+        for a_, b_ in zip(sw[:-1], sw[1:]):
+            assert a_[3] < b_[2] and a_[1] > b_[1]
+    for c in chains:
+        cw = W[W[:, 1] == c]
+        steps = cw[:, 0]
+        assert np.all(np.diff(steps) == 1)                       # one window per step
+        assert cw[0, 2] == ilo and cw[-1, 3] == ihi and cw[-1, 9] == 1
+        assert np.all(cw[:, 3] - cw[:, 2] + 1 <= k)
+        assert np.all(cw[1:, 4] == cw[:-1, 5] + 1)               # chain-local steps contiguous
+        nbc = cw[0, 7]
+        for w in cw:
+            for t in (w[4], w[5]):
+                for jj in range(nbc):
+                    p = ilo - 1 + t - 3 * jj
+                    if ilo - 1 <= p <= ihi - 2:
+                        assert (p >= w[2]) or (p == ilo - 1 and w[2] == ilo)   # column p in window
+                        assert min(p + 4, ihi) <= w[3]                          # bulge row inside
+        # the top bulge leaves at p = ihi - 2 in the last step
+        assert ilo - 1 + cw[-1, 5] - 3 * (nbc - 1) == ihi - 2
+    # chain c+1 never overlaps chain c in the same step and starts `lag` steps later
+    assert info["lag"] * info["s"] >= k or info["nchains"] == 1
+
+
+@pytest.mark.parametrize("n,ns,ilo,ihi,win,z0", [
+    (256, 8, 0, 255, 24, "eye"), (256, 8, 0, 255, 13, "orth"), (300, 20, 40, 259, 24, "orth"),
+    (400, 40, 0, 399, 96, "eye"), (200, 60, 10, 190, 20, "eye"), (150, 100, 0, 149, 40, "orth"),
+    (60, 12, 0, 59, 60, "eye"), (9, 8, 0, 8, 8, "eye"), (7, 4, 1, 5, 8, "orth"), (3, 2, 0, 2, 8, "eye"),
+    (120, 24, 0, 119, 112, "orth"),
+])
+def test_schedule_emulation_matches_oracle(n, ns, ilo, ihi, win, z0):
+    H0, Z0, re_, im_ = random_case(n + ns + win, n, ns, ilo, ihi, z0=z0)
+    Ho, Zo = H0.copy(order="F"), Z0.copy(order="F")
+    oracle.sweep(Ho, Zo, ilo, ihi, re_, im_)
+    He, Ze = H0.copy(order="F"), Z0.copy(order="F")
+    emulate(He, Ze, ilo, ihi, re_, im_, win)
+    assert np.linalg.norm(He - Ho) / np.linalg.norm(H0) <= 1e-11
+    assert np.linalg.norm(Ze - Zo) <= 1e-11 * np.sqrt(n)
+    assert np.all(np.tril(He, -2) == 0.0)
+    assert np.array_equal(He[:ilo, :ilo], H0[:ilo, :ilo])
+    assert np.array_equal(He[ihi + 1:, ihi + 1:], H0[ihi + 1:, ihi + 1:])

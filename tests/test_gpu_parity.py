@@ -1,0 +1,133 @@
+"""GPU parity: the CUDA sweep (through the C ABI) against the CPU oracle on the same seeded inputs.
+
+Tolerance (BASELINE.json north_star): ||dH'||_F / ||H||_F <= 1e-10 and ||dZ||_F <= 1e-10 sqrt(n).
+Integer / structural results are exact: entries below the subdiagonal are exactly 0.0, and blocks
+outside the active window that the sweep must not touch are bitwise unchanged.
+"""
+import numpy as np
+import pytest
+
+import oracle
+import paper_2007_03576_b200 as hq
+from hqr_inputs import make, random_case
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-10
+
+
+@pytest.fixture(scope="module", autouse=True)
+def lib_setup():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a B200"
+    hq.setup(0)
+    yield
+    hq.teardown()
+
+
+def gpu_sweep(H0, Z0, ilo, ihi, re_, im_, window):
+    Hd = hq.to_device(H0)
+    Zd = hq.to_device(Z0) if Z0 is not None else None
+    hq.sweep(Hd, Zd, ilo, ihi, re_, im_, window)
+    return hq.from_device(Hd), (hq.from_device(Zd) if Zd is not None else None)
+
+
+def oracle_sweep(H0, Z0, ilo, ihi, re_, im_):
+    H, Z = H0.copy(order="F"), (Z0.copy(order="F") if Z0 is not None else None)
+    oracle.sweep(H, Z, ilo, ihi, re_, im_)
+    return H, Z
+
+
+def check(Hg, Zg, Ho, Zo, H0, ilo, ihi, tol=TOL):
+    n = H0.shape[0]
+    dh = np.linalg.norm(Hg - Ho) / np.linalg.norm(H0)
+    assert dh <= tol, dh
+    if Zo is not None:
+        dz = np.linalg.norm(Zg - Zo) / np.sqrt(n)
+        assert dz <= tol, dz
+    assert np.all(np.tril(Hg, -2) == 0.0)
+    assert np.array_equal(Hg[:ilo, :ilo], H0[:ilo, :ilo])
+    assert np.array_equal(Hg[ihi + 1:, ihi + 1:], H0[ihi + 1:, ihi + 1:])
+    assert np.array_equal(Hg[ilo:ihi + 1, :ilo], H0[ilo:ihi + 1, :ilo])
+    if ilo > 0:
+        assert Hg[ilo, ilo - 1] == 0.0
+    if ihi < n - 1:
+        assert Hg[ihi + 1, ihi] == 0.0
+
+
+def test_config0_full_parity():
+    p = make(0)
+    Hg, Zg = gpu_sweep(p.H, p.Z, p.ilo, p.ihi, p.shifts_re, p.shifts_im, p.window)
+    Ho, Zo = oracle_sweep(p.H, p.Z, p.ilo, p.ihi, p.shifts_re, p.shifts_im)
+    check(Hg, Zg, Ho, Zo, p.H, p.ilo, p.ihi)
+
+
+CASES = [
+    # (seed, n, nshifts, ilo, ihi, window, z0)
+    (0, 3, 2, 0, 2, 8, "eye"), (1, 4, 2, 0, 3, 8, "orth"), (2, 6, 4, 0, 5, 24, "eye"),
+    (3, 9, 8, 0, 8, 8, "eye"), (4, 17, 6, 2, 15, 8, "orth"), (5, 40, 8, 0, 39, 16, "eye"),
+    (6, 64, 12, 0, 63, 32, "orth"), (7, 100, 20, 5, 90, 24, "eye"), (8, 129, 30, 0, 128, 40, "orth"),
+    (9, 200, 60, 10, 190, 20, "eye"), (10, 257, 16, 0, 256, 96, "orth"), (11, 300, 40, 40, 259, 64, "eye"),
+    (12, 333, 50, 0, 332, 112, "orth"), (13, 400, 80, 0, 399, 96, "eye"), (14, 150, 100, 0, 149, 40, "eye"),
+    (15, 120, 24, 0, 119, 112, "orth"), (16, 511, 64, 100, 400, 48, "eye"), (17, 97, 2, 0, 96, 9, "eye"),
+    (18, 250, 248, 0, 249, 112, "eye"), (19, 401, 30, 1, 399, 100, "orth"),
+]
+
+
+@pytest.mark.parametrize("case", CASES, ids=[f"n{c[1]}s{c[2]}w{c[5]}" for c in CASES])
+def test_random_parity(case):
+    seed, n, ns, ilo, ihi, win, z0 = case
+    H0, Z0, re_, im_ = random_case(seed, n, ns, ilo, ihi, z0=z0, shift_kind="mixed" if seed % 2 else "disk2")
+    Hg, Zg = gpu_sweep(H0, Z0, ilo, ihi, re_, im_, win)
+    Ho, Zo = oracle_sweep(H0, Z0, ilo, ihi, re_, im_)
+    check(Hg, Zg, Ho, Zo, H0, ilo, ihi)
+
+
+def test_no_z_and_host_pointer_path():
+    H0, Z0, re_, im_ = random_case(50, 180, 20, 3, 170, z0="orth")
+    Hg, _ = gpu_sweep(H0, None, 3, 170, re_, im_, 32)
+    Hg2, Zg2 = gpu_sweep(H0, Z0, 3, 170, re_, im_, 32)
+    assert np.array_equal(Hg, Hg2)               # Z does not influence H
+    Hh, Zh = H0.copy(order="F"), Z0.copy(order="F")
+    hq.sweep(Hh, Zh, 3, 170, re_, im_, 32)         # host buffers: staged through the library
+    assert np.array_equal(Hh, Hg2) and np.array_equal(Zh, Zg2)
+    st = hq.stats()
+    assert st["h2d_bytes"] == 2 * 180 * 180 * 8 and st["d2h_bytes"] == 2 * 180 * 180 * 8
+
+
+def test_graph_and_direct_launch_bitwise_equal():
+    H0, Z0, re_, im_ = random_case(51, 300, 32, 0, 299, z0="orth")
+    Hg, Zg = gpu_sweep(H0, Z0, 0, 299, re_, im_, 64)
+    hq.teardown()
+    hq.setup(0, flags=hq.FLAG_NO_GRAPH)
+    try:
+        Hd, Zd = gpu_sweep(H0, Z0, 0, 299, re_, im_, 64)
+    finally:
+        hq.teardown()
+        hq.setup(0)
+    assert np.array_equal(Hg, Hd) and np.array_equal(Zg, Zd)
+
+
+def test_decoupling_error_code():
+    H0, Z0, re_, im_ = random_case(52, 50, 4, 0, 49)
+    Hd = hq.to_device(H0)
+    with pytest.raises(hq.HQRError) as e:
+        hq.sweep(Hd, None, 10, 49, re_, im_, 16)      # H[10, 9] != 0
+    assert e.value.code == -10
+    with pytest.raises(hq.HQRError) as e:
+        hq.sweep(Hd, None, 0, 30, re_, im_, 16)       # H[31, 30] != 0
+    assert e.value.code == -10
+
+
+def test_repeat_determinism():
+    H0, Z0, re_, im_ = random_case(53, 400, 40, 0, 399, z0="orth")
+    a = gpu_sweep(H0, Z0, 0, 399, re_, im_, 96)
+    b = gpu_sweep(H0, Z0, 0, 399, re_, im_, 96)
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+
+
+def test_config1_full_parity():
+    p = make(1)
+    Hg, Zg = gpu_sweep(p.H, p.Z, p.ilo, p.ihi, p.shifts_re, p.shifts_im, p.window)
+    Ho, Zo = oracle_sweep(p.H, p.Z, p.ilo, p.ihi, p.shifts_re, p.shifts_im)
+    check(Hg, Zg, Ho, Zo, p.H, p.ilo, p.ihi)
