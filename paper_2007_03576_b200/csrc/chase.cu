@@ -8,15 +8,20 @@
 // (P:198-203): bulge introduction from the first column of (H - s I)(H - s' I), 3x3
 // Householder reflectors chasing the bulge, a final 2x2 reflector at p = ihi - 2.
 //
-// Per step, two phases separated by __syncthreads (DESIGN.md "Chase kernel"):
+// Per step, two phases separated by __syncthreads (DESIGN.md §6):
 //   phase 1  (one warp per bulge) compute the reflector from column p (or the intro vector),
 //            store beta / exact zeros in column p, apply it from the left to rows p+1..p+m,
 //            columns p+1..w1 (lanes across columns);
-//   phase 2  apply every reflector from the right to columns p+1..p+m, rows w0..p+m+1 of the
-//            window and rows 0..p0+3 of Q_W, p0 the chain's deepest bulge (lanes across rows).
+//   phase 2  (same warp; reflector from a SMEM table) apply it from the right to columns p+1..p+m of the window rows
+//            w0..p+m+1 and of Q_W rows 0..p0+3 (p0 = the chain's deepest bulge; deeper rows of
+//            Q_W are still identity rows), lanes across rows.
 // Bulges are 3 apart, so within a phase different bulges touch disjoint rows (phase 1) or
 // disjoint columns (phase 2).  Phase 1 of bulge j writes beta into H[p+1,p] before phase 2 of the
 // bulge above (at p-3) updates that entry -- the sequential order.
+//
+// The kernel is latency-bound (a chain of small dependent reflectors), so it runs 16 warps (one
+// per bulge), keeps every index 32-bit, specialises the common 3-reflector, and computes each
+// reflector with one square root and one division.
 //
 // SMEM layout: column-major H window and Q_W with an odd leading dimension (kw | 1): a warp
 // walking a row (phase 1) or a column (phase 2) hits 32 distinct banks.
@@ -29,62 +34,74 @@ namespace hqr {
 
 namespace {
 
-constexpr int kChaseThreads = 256;
+constexpr int kChaseThreads = 512;
 constexpr int kChaseWarps = kChaseThreads / 32;
 
 // Householder reflector (reading R2): P = I - tau v v^T, v = [1, v1, v2],
 // P x = beta e1 with beta = -sign(x0) ||x||, sign(0) = +1; zero tail -> identity.
-__device__ __forceinline__ void house(int m, double x0, double x1, double x2, double& v1,
-                                      double& v2, double& tau, double& beta) {
-  double tail2 = x1 * x1 + (m == 3 ? x2 * x2 : 0.0);
+// With d = x0 - beta and r = 1 / (d * beta): v_i = x_i / d = x_i * beta * r, tau = -d / beta = -d*d*r.
+__device__ __forceinline__ void house(double x0, double x1, double x2, double& v1, double& v2,
+                                      double& tau, double& beta) {
+  const double tail2 = fma(x1, x1, x2 * x2);
   if (tail2 == 0.0) {
     v1 = 0.0; v2 = 0.0; tau = 0.0; beta = x0;
     return;
   }
-  double nrm = sqrt(x0 * x0 + tail2);
-  double b = (x0 >= 0.0) ? -nrm : nrm;
-  tau = (b - x0) / b;
-  double d = x0 - b;
-  v1 = x1 / d;
-  v2 = (m == 3) ? x2 / d : 0.0;
+  const double nrm = sqrt(fma(x0, x0, tail2));
+  const double b = (x0 >= 0.0) ? -nrm : nrm;
+  const double d = x0 - b;
+  const double r = 1.0 / (d * b);
+  const double br = b * r;
+  v1 = x1 * br;
+  v2 = x2 * br;
+  tau = -d * d * r;
   beta = b;
 }
 
-__global__ void __launch_bounds__(kChaseThreads) chase_kernel(StepArgs a) {
+__global__ void __launch_bounds__(kChaseThreads, 1) chase_kernel(StepArgs a) {
   extern __shared__ double sm[];
   const WindowDesc W = a.wins[a.win_begin + blockIdx.x];
   const int kw = W.w1 - W.w0 + 1;
   const int ldh = kw | 1;
   double* Hs = sm;
-  double* Qs = Hs + (size_t)kw * ldh;
-  double* R = Qs + (size_t)kw * ldh;            // per bulge: v1, v2, tau
-  int* Rp = reinterpret_cast<int*>(R + 3 * W.nbc);  // per bulge: local p (INT_MIN = inactive)
-  int* Rm = Rp + W.nbc;                              // per bulge: m (2 or 3)
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int64_t n = a.n, w0 = W.w0;
-  const int64_t ilo = a.ilo, ihi = a.ihi;
+  double* Qs = Hs + kw * ldh;
+  double* R = Qs + kw * ldh;                          // per bulge: v1, v2, tau
+  int* Rp = reinterpret_cast<int*>(R + 3 * W.nbc);    // per bulge: local p (INT_MIN = skip)
+  int* Rm = Rp + W.nbc;                               // per bulge: m (2 or 3)
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t n = a.n;
+  const int w0 = W.w0;
+  const int ilo = (int)a.ilo, ihi = (int)a.ihi;
 
   // load the window (coalesced along columns), Q_W = I
-  for (int idx = tid; idx < kw * kw; idx += kChaseThreads) {
-    int c = idx / kw, r = idx - c * kw;
-    Hs[r + c * ldh] = a.H[(w0 + r) + (w0 + c) * n];
-    Qs[r + c * ldh] = (r == c) ? 1.0 : 0.0;
+  {
+    const double* g = a.H + (int64_t)w0 * n + w0;
+    for (int c = warp; c < kw; c += kChaseWarps) {
+      const double* gc = g + (int64_t)c * n;
+      for (int r = lane; r < kw; r += 32) {
+        Hs[r + c * ldh] = gc[r];
+        Qs[r + c * ldh] = (r == c) ? 1.0 : 0.0;
+      }
+    }
   }
   __syncthreads();
 
-  const int rmaxH = (int)(ihi - w0);  // last window row inside the active block
+  const int rmaxH = ihi - w0;  // last window row inside the active block
   for (int t = W.t0; t <= W.t1; ++t) {
+    // rows of Q_W below the chain's deepest reflector so far are still identity rows
+    const int rQ = min(ilo - 1 + t - w0 + 3, kw - 1);
     // ---- phase 1: reflectors + left application ------------------------------------------
+    // warp -> bulges jj = warp, warp + 16, ...; the reflector goes to the SMEM table for phase 2
     for (int jj = warp; jj < W.nbc; jj += kChaseWarps) {
-      const int64_t p = ilo - 1 + t - 3 * (int64_t)jj;
+      const int p = ilo - 1 + t - 3 * jj;
       if (p < ilo - 1 || p > ihi - 2) {
         if (lane == 0) Rp[jj] = INT_MIN;
         continue;
       }
-      const int pl = (int)(p - w0);
+      const int pl = p - w0;
       const int m = (p <= ihi - 3) ? 3 : 2;
       double x0, x1, x2;
-      if (p == ilo - 1) {  // bulge introduction; window starts at ilo so local (0,0)
+      if (p == ilo - 1) {  // bulge introduction; the window starts at ilo: local (0,0)
         const int j = W.b0 + jj;
         const double sigma = a.coef[2 * j], pi = a.coef[2 * j + 1];
         const double h00 = Hs[0], h10 = Hs[1], h01 = Hs[ldh], h11 = Hs[1 + ldh], h21 = Hs[2 + ldh];
@@ -92,87 +109,100 @@ __global__ void __launch_bounds__(kChaseThreads) chase_kernel(StepArgs a) {
         x1 = h10 * (h00 + h11 - sigma);
         x2 = h10 * h21;
       } else {
-        const double* col = Hs + (size_t)pl * ldh;
-        x0 = col[pl + 1];
-        x1 = col[pl + 2];
-        x2 = (m == 3) ? col[pl + 3] : 0.0;
+        const double* col = Hs + pl * ldh + pl;
+        x0 = col[1];
+        x1 = col[2];
+        x2 = (m == 3) ? col[3] : 0.0;
       }
       double v1, v2, tau, beta;
-      house(m, x0, x1, x2, v1, v2, tau, beta);
+      house(x0, x1, x2, v1, v2, tau, beta);
       __syncwarp();
       if (lane == 0) {
         if (p >= ilo) {
-          double* col = Hs + (size_t)pl * ldh;
-          col[pl + 1] = beta;
-          col[pl + 2] = 0.0;
-          if (m == 3) col[pl + 3] = 0.0;
+          double* col = Hs + pl * ldh + pl;
+          col[1] = beta;
+          col[2] = 0.0;
+          if (m == 3) col[3] = 0.0;
         }
         R[3 * jj] = v1; R[3 * jj + 1] = v2; R[3 * jj + 2] = tau;
-        Rp[jj] = pl; Rm[jj] = m;
+        Rp[jj] = (tau == 0.0) ? INT_MIN : pl;
+        Rm[jj] = m;
       }
-      if (tau != 0.0) {
-        const int c0 = (p == ilo - 1) ? 0 : pl + 1;
+      if (tau == 0.0) continue;
+      const int c0 = (p == ilo - 1) ? 0 : pl + 1;
+      double* hrow = Hs + (pl + 1);
+      if (m == 3) {
         for (int c = c0 + lane; c < kw; c += 32) {
-          double* hc = Hs + (size_t)c * ldh + (pl + 1);
-          double h0 = hc[0], h1 = hc[1], h2 = (m == 3) ? hc[2] : 0.0;
-          double tw = tau * (h0 + v1 * h1 + v2 * h2);
+          double* hc = hrow + c * ldh;
+          const double h0 = hc[0], h1 = hc[1], h2 = hc[2];
+          const double tw = tau * fma(v2, h2, fma(v1, h1, h0));
           hc[0] = h0 - tw;
-          hc[1] = h1 - tw * v1;
-          if (m == 3) hc[2] = h2 - tw * v2;
+          hc[1] = fma(-tw, v1, h1);
+          hc[2] = fma(-tw, v2, h2);
+        }
+      } else {
+        for (int c = c0 + lane; c < kw; c += 32) {
+          double* hc = hrow + c * ldh;
+          const double h0 = hc[0], h1 = hc[1];
+          const double tw = tau * fma(v1, h1, h0);
+          hc[0] = h0 - tw;
+          hc[1] = fma(-tw, v1, h1);
         }
       }
     }
     __syncthreads();
-    // ---- phase 2: right application to the window and to Q_W --------------------------------
-    // rows of Q_W below the deepest reflector so far (the chain's bulge 0 at p0 = ilo-1+t touches
-    // rows <= p0+3, and positions only grow) are still identity rows: skip them
-    const int rQ0 = (int)(ilo - 1 + t - w0 + 3);
+    // ---- phase 2: right application to the window and to Q_W (same warp, same bulges) ------
     for (int jj = warp; jj < W.nbc; jj += kChaseWarps) {
       const int pl = Rp[jj];
       if (pl == INT_MIN) continue;
-      const double tau = R[3 * jj + 2];
-      if (tau == 0.0) continue;
-      const double v1 = R[3 * jj], v2 = R[3 * jj + 1];
+      const double v1 = R[3 * jj], v2 = R[3 * jj + 1], tau = R[3 * jj + 2];
       const int m = Rm[jj];
-      double* c1 = Hs + (size_t)(pl + 1) * ldh;
       const int rH = min(pl + m + 1, rmaxH);
-      for (int r = lane; r <= rH; r += 32) {
-        double h0 = c1[r], h1 = c1[r + ldh], h2 = (m == 3) ? c1[r + 2 * ldh] : 0.0;
-        double tw = tau * (h0 + v1 * h1 + v2 * h2);
-        c1[r] = h0 - tw;
-        c1[r + ldh] = h1 - tw * v1;
-        if (m == 3) c1[r + 2 * ldh] = h2 - tw * v2;
-      }
-      double* q1 = Qs + (size_t)(pl + 1) * ldh;
-      const int rQ = min(rQ0, kw - 1);
-      for (int r = lane; r <= rQ; r += 32) {
-        double q0 = q1[r], qa = q1[r + ldh], qb = (m == 3) ? q1[r + 2 * ldh] : 0.0;
-        double tw = tau * (q0 + v1 * qa + v2 * qb);
-        q1[r] = q0 - tw;
-        q1[r + ldh] = qa - tw * v1;
-        if (m == 3) q1[r + 2 * ldh] = qb - tw * v2;
+      const int nrows = rH + 1 + rQ + 1;  // window rows 0..rH, then Q_W rows 0..rQ
+      double* c1H = Hs + (pl + 1) * ldh;
+      double* c1Q = Qs + (pl + 1) * ldh;
+      if (m == 3) {
+        for (int i = lane; i < nrows; i += 32) {
+          double* x = (i <= rH) ? c1H + i : c1Q + (i - rH - 1);
+          const double h0 = x[0], h1 = x[ldh], h2 = x[2 * ldh];
+          const double tw = tau * fma(v2, h2, fma(v1, h1, h0));
+          x[0] = h0 - tw;
+          x[ldh] = fma(-tw, v1, h1);
+          x[2 * ldh] = fma(-tw, v2, h2);
+        }
+      } else {
+        for (int i = lane; i < nrows; i += 32) {
+          double* x = (i <= rH) ? c1H + i : c1Q + (i - rH - 1);
+          const double h0 = x[0], h1 = x[ldh];
+          const double tw = tau * fma(v1, h1, h0);
+          x[0] = h0 - tw;
+          x[ldh] = fma(-tw, v1, h1);
+        }
       }
     }
     __syncthreads();
   }
 
-  // write back the window and store Q_W (column-major, ld = KP, zero padded to KP x KP)
-  for (int idx = tid; idx < kw * kw; idx += kChaseThreads) {
-    int c = idx / kw, r = idx - c * kw;
-    a.H[(w0 + r) + (w0 + c) * n] = Hs[r + c * ldh];
+  // write back the window; store Q_W column-major with ld = QLD (= the update kernels' SMEM
+  // layout), zero padded to KP x QLD
+  {
+    double* g = a.H + (int64_t)w0 * n + w0;
+    for (int c = warp; c < kw; c += kChaseWarps) {
+      double* gc = g + (int64_t)c * n;
+      for (int r = lane; r < kw; r += 32) gc[r] = Hs[r + c * ldh];
+    }
   }
-  const int KP = a.KP;
-  double* Q = a.qslots + (size_t)W.slot * KP * KP;
-  for (int idx = tid; idx < KP * KP; idx += kChaseThreads) {
-    int c = idx / KP, r = idx - c * KP;
-    Q[idx] = (r < kw && c < kw) ? Qs[r + c * ldh] : 0.0;
-  }
+  const int KP = a.KP, QLD = a.QLD;
+  double* Q = a.qslots + (size_t)(W.slot + a.slot_offset) * KP * QLD;
+  for (int c = warp; c < KP; c += kChaseWarps)
+    for (int r = lane; r < QLD; r += 32)
+      Q[r + c * QLD] = (r < kw && c < kw) ? Qs[r + c * ldh] : 0.0;
 }
 
 }  // namespace
 
 size_t chase_smem_bytes(int kw, int nbc) {
-  int ldh = kw | 1;
+  const int ldh = kw | 1;
   return (size_t)2 * kw * ldh * sizeof(double) + (size_t)nbc * (3 * sizeof(double) + 2 * sizeof(int));
 }
 

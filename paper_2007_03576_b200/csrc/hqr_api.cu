@@ -46,6 +46,11 @@ struct GraphKey {
   }
 };
 
+struct CachedGraph {
+  cudaGraphExec_t exec;
+  hqr_stats stats;
+};
+
 struct CachedPlan {
   Plan plan;
   WindowDesc* d_wins = nullptr;
@@ -55,8 +60,11 @@ struct CachedPlan {
 struct State {
   bool ready = false;
   int device = 0, rank = 0, world = 1, flags = 0, num_sms = 0;
-  cudaStream_t stream = nullptr;
+  cudaStream_t stream = nullptr;   // stream A: chase -> left -> right (high priority)
+  cudaStream_t zstream = nullptr;  // stream B: Z updates (low priority)
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaEvent_t ev_q[hqr::kQSets] = {}, ev_z[hqr::kQSets] = {};
   double* d_coef = nullptr;
   size_t coef_cap = 0;
   double* d_q = nullptr;
@@ -65,7 +73,7 @@ struct State {
   double* d_zstage = nullptr;
   size_t stage_cap = 0;
   std::map<PlanKey, std::unique_ptr<CachedPlan>> plans;
-  std::map<GraphKey, cudaGraphExec_t> graphs;
+  std::map<GraphKey, CachedGraph> graphs;
   std::vector<cudaEvent_t> prof_events;
   hqr_stats stats{};
 };
@@ -152,45 +160,72 @@ cudaEvent_t prof_event(size_t i) {
   return g.prof_events[i];
 }
 
-// Enqueue every step of the sweep on g.stream.  prof: record events around each launch.
+// Enqueue every step of the sweep.  Stream A (high priority) carries the chain of dependent work
+// chase(g) -> left(g) -> right(g); the Z update, which nothing else reads ("a completely
+// separate subgraph"), runs on stream B (low priority, "min_prio") as soon as chase(g) has
+// produced the step's factors, overlapping the next steps.  kQSets rotating Q slot sets let Z trail
+// the chase by up to kQSets-1 steps.  prof: one stream, events around every launch.
 int enqueue_sweep(const CachedPlan& cp, double* H, double* Z, int64_t n, bool prof,
                   std::vector<int>* classes, hqr_stats* st) {
   const Plan& P = cp.plan;
+  const bool split = (Z != nullptr) && !prof;
+  cudaStream_t A = g.stream, B = split ? g.zstream : g.stream;
   StepArgs a{};
   a.H = H; a.Z = Z; a.n = n; a.ilo = P.ilo; a.ihi = P.ihi;
   a.wins = cp.d_wins; a.coef = g.d_coef; a.qslots = g.d_q; a.KP = cp.KP;
+  a.QLD = hqr::pad_ld(cp.KP);
   size_t ev = 0;
   auto mark = [&](int cls) {
     if (!prof) return;
-    cudaEventRecord(prof_event(ev++), g.stream);
+    cudaEventRecord(prof_event(ev++), A);
     if (classes) classes->push_back(cls);
   };
+  if (split) {
+    CK(cudaEventRecord(g.ev_fork, A));
+    CK(cudaStreamWaitEvent(B, g.ev_fork, 0));
+  }
   for (int s = 0; s < P.nsteps; ++s) {
+    const int set = s % hqr::kQSets;
     a.win_begin = P.step_begin[s];
     a.win_count = P.step_begin[s + 1] - P.step_begin[s];
+    a.slot_offset = set * P.nchains;
     const WindowDesc* hw = P.windows.data() + a.win_begin;
+    if (split && s >= hqr::kQSets) CK(cudaStreamWaitEvent(A, g.ev_z[set], 0));
     mark(0);
-    CK(hqr::launch_chase(a, P.max_kw, P.max_nbc, g.stream));
+    CK(hqr::launch_chase(a, P.max_kw, P.max_nbc, A));
     mark(-1);
     st->launches_chase++;
     int64_t items;
     double fl, by;
+    if (split) {
+      CK(cudaEventRecord(g.ev_q[set], A));
+      CK(cudaStreamWaitEvent(B, g.ev_q[set], 0));
+      StepArgs az = a;
+      az.right_mode = 2;
+      CK(hqr::launch_right(az, hw, g.num_sms, B, &items, &fl, &by));
+      if (items) st->launches_right++;
+      st->flops_update += fl;
+      st->bytes_update += by;
+      CK(cudaEventRecord(g.ev_z[set], B));
+    }
     mark(1);
-    CK(hqr::launch_left(a, hw, g.num_sms, g.stream, &items, &fl, &by));
+    CK(hqr::launch_left(a, hw, g.num_sms, A, &items, &fl, &by));
     mark(-1);
     if (items) st->launches_left++;
     st->flops_update += fl;
     st->bytes_update += by;
     mark(2);
-    CK(hqr::launch_right(a, hw, g.num_sms, g.stream, &items, &fl, &by));
+    StepArgs ar = a;
+    ar.right_mode = split ? 1 : 0;
+    CK(hqr::launch_right(ar, hw, g.num_sms, A, &items, &fl, &by));
     mark(-1);
     if (items) st->launches_right++;
     st->flops_update += fl;
     st->bytes_update += by;
-    for (int i = 0; i < a.win_count; ++i) {
-      // chase flops: per reflector 10 (3-vector) flops x (left cols + right rows + Q rows) in-window
-      (void)hw;
-    }
+  }
+  if (split) {
+    CK(cudaEventRecord(g.ev_join, B));
+    CK(cudaStreamWaitEvent(A, g.ev_join, 0));
   }
   st->steps = P.nsteps;
   st->windows = (int64_t)P.windows.size();
@@ -221,9 +256,18 @@ int hqr_setup(const hqr_config* cfg) {
   g.world = cfg->world;
   g.flags = cfg->flags;
   g.num_sms = prop.multiProcessorCount;
-  CK(cudaStreamCreateWithFlags(&g.stream, cudaStreamNonBlocking));
+  int prio_lo = 0, prio_hi = 0;
+  CK(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+  CK(cudaStreamCreateWithPriority(&g.stream, cudaStreamNonBlocking, prio_hi));
+  CK(cudaStreamCreateWithPriority(&g.zstream, cudaStreamNonBlocking, prio_lo));
   CK(cudaEventCreate(&g.ev0));
   CK(cudaEventCreate(&g.ev1));
+  CK(cudaEventCreateWithFlags(&g.ev_fork, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&g.ev_join, cudaEventDisableTiming));
+  for (int i = 0; i < hqr::kQSets; ++i) {
+    CK(cudaEventCreateWithFlags(&g.ev_q[i], cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&g.ev_z[i], cudaEventDisableTiming));
+  }
   g.ready = true;
   return 0;
 }
@@ -232,7 +276,7 @@ int hqr_teardown(void) {
   if (!g.ready) return 0;
   cudaSetDevice(g.device);
   cudaStreamSynchronize(g.stream);
-  for (auto& kv : g.graphs) cudaGraphExecDestroy(kv.second);
+  for (auto& kv : g.graphs) cudaGraphExecDestroy(kv.second.exec);
   g.graphs.clear();
   for (auto& kv : g.plans)
     if (kv.second->d_wins) cudaFree(kv.second->d_wins);
@@ -247,6 +291,13 @@ int hqr_teardown(void) {
   g.coef_cap = g.q_cap = g.stage_cap = 0;
   cudaEventDestroy(g.ev0);
   cudaEventDestroy(g.ev1);
+  cudaEventDestroy(g.ev_fork);
+  cudaEventDestroy(g.ev_join);
+  for (int i = 0; i < hqr::kQSets; ++i) {
+    cudaEventDestroy(g.ev_q[i]);
+    cudaEventDestroy(g.ev_z[i]);
+  }
+  cudaStreamDestroy(g.zstream);
   cudaStreamDestroy(g.stream);
   g.ready = false;
   cudaError_t e = cudaGetLastError();
@@ -300,7 +351,7 @@ int hqr_sweep(double* H, double* Z, int64_t n, int64_t ilo, int64_t ihi, const d
   if (rc) return rc;
   CK(cudaMemcpyAsync(g.d_coef, coef.data(), coef.size() * sizeof(double), cudaMemcpyHostToDevice,
                      g.stream));
-  rc = ensure(&g.d_q, &g.q_cap, (size_t)cp->plan.nchains * cp->KP * cp->KP);
+  rc = ensure(&g.d_q, &g.q_cap, (size_t)hqr::kQSets * cp->plan.nchains * cp->KP * hqr::pad_ld(cp->KP));
   if (rc) return rc;
 
   // host buffers: stage through library-owned device memory
@@ -340,52 +391,26 @@ int hqr_sweep(double* H, double* Z, int64_t n, int64_t ilo, int64_t ihi, const d
     if (it == g.graphs.end()) {
       cudaGraph_t graph;
       CK(cudaStreamBeginCapture(g.stream, cudaStreamCaptureModeThreadLocal));
-      hqr_stats tmp{};
-      int rc2 = enqueue_sweep(*cp, dH, dZ, n, false, nullptr, &tmp);
+      hqr_stats cap{};
+      int rc2 = enqueue_sweep(*cp, dH, dZ, n, false, nullptr, &cap);
       cudaError_t ec = cudaStreamEndCapture(g.stream, &graph);
       if (rc2) return rc2;
       CK(ec);
       cudaGraphExec_t exec;
       CK(cudaGraphInstantiate(&exec, graph, 0));
       cudaGraphDestroy(graph);
-      it = g.graphs.emplace(gk, exec).first;
+      it = g.graphs.emplace(gk, CachedGraph{exec, cap}).first;
     }
-    CK(cudaGraphLaunch(it->second, g.stream));
-    // launch accounting (same plan as captured)
-    hqr_stats tmp{};
-    {
-      // recount without launching
-      const Plan& P = cp->plan;
-      for (int s = 0; s < P.nsteps; ++s) {
-        int cnt = P.step_begin[s + 1] - P.step_begin[s];
-        const WindowDesc* hw = P.windows.data() + P.step_begin[s];
-        tmp.launches_chase++;
-        for (int i = 0; i < cnt; ++i) {
-          int64_t kw = hw[i].w1 - hw[i].w0 + 1;
-          double cols = (double)(n - 1 - hw[i].w1), rows = (double)hw[i].w0 + (dZ ? (double)n : 0.0);
-          tmp.flops_update += 2.0 * kw * kw * (cols + rows);
-          tmp.bytes_update += 16.0 * kw * (cols + rows);
-        }
-        bool anyl = false, anyr = false;
-        for (int i = 0; i < cnt; ++i) {
-          if (hw[i].w1 < n - 1) anyl = true;
-          if (hw[i].w0 > 0 || dZ) anyr = true;
-        }
-        tmp.launches_left += anyl;
-        tmp.launches_right += anyr;
-      }
-      tmp.steps = P.nsteps;
-      tmp.windows = (int64_t)P.windows.size();
-      tmp.kernels_launched = tmp.launches_chase + tmp.launches_left + tmp.launches_right;
-    }
-    st.flops_update = tmp.flops_update;
-    st.bytes_update = tmp.bytes_update;
-    st.launches_chase = tmp.launches_chase;
-    st.launches_left = tmp.launches_left;
-    st.launches_right = tmp.launches_right;
-    st.steps = tmp.steps;
-    st.windows = tmp.windows;
-    st.kernels_launched = tmp.kernels_launched;
+    CK(cudaGraphLaunch(it->second.exec, g.stream));
+    const hqr_stats& c = it->second.stats;  // launches / flops of the captured sequence
+    st.flops_update = c.flops_update;
+    st.bytes_update = c.bytes_update;
+    st.launches_chase = c.launches_chase;
+    st.launches_left = c.launches_left;
+    st.launches_right = c.launches_right;
+    st.steps = c.steps;
+    st.windows = c.windows;
+    st.kernels_launched = c.kernels_launched;
   } else {
     rc = enqueue_sweep(*cp, dH, dZ, n, prof, &classes, &st);
     if (rc) return rc;

@@ -17,8 +17,11 @@ struct StepArgs {
   const WindowDesc* wins;    // device copy of plan.windows
   int win_begin, win_count;  // this step's windows
   const double* coef;        // per bulge j: coef[2j] = sigma_j, coef[2j+1] = pi_j
-  double* qslots;            // Q slot s at qslots + s*KP*KP, column-major, ld = KP, zero padded
+  double* qslots;            // Q slot s at qslots + s*KP*QLD: column-major, ld = QLD, zero padded
   int KP;                    // padded factor side (32, 64, 96 or 128)
+  int QLD;                   // Q slot leading dimension = pad_ld(KP) (the update kernels' SMEM ld)
+  int slot_offset;           // this step's Q slot set: window slot s lives at slot s + slot_offset
+  int right_mode;            // right kernel: 0 = H rows above W and Z, 1 = H only, 2 = Z only
 };
 
 // One CTA per window: chase the step's bulges inside SMEM-resident windows, accumulate Q_W.
@@ -33,10 +36,15 @@ cudaError_t launch_left(const StepArgs& a, const WindowDesc* host_wins, int num_
                         cudaStream_t st, int64_t* items, double* flops, double* bytes);
 cudaError_t launch_right(const StepArgs& a, const WindowDesc* host_wins, int num_sms,
                          cudaStream_t st, int64_t* items, double* flops, double* bytes);
+// Q slot sets in flight: the Z update of step g may trail the chase of step g + kQSets - 1
+constexpr int kQSets = 4;
 
 // Largest window side whose chase fits in SMEM (H window + Q_W both resident).
 constexpr int kMaxWindow = 112;
 
 inline int padded_kp(int kw) { return kw <= 32 ? 32 : kw <= 64 ? 64 : kw <= 96 ? 96 : 128; }
+
+// SMEM leading dimension = 4 (mod 16) doubles: conflict-free mma.m8n8k4 fragment loads
+__host__ __device__ constexpr int pad_ld(int x) { return x + (((4 - x) % 16) + 16) % 16; }
 
 }  // namespace hqr

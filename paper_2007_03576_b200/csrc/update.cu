@@ -12,12 +12,17 @@
 // H(W_c, W_c') and are ordered (left kernel, then right kernel).
 //
 // Tensor-core path: FP64 mma.sync.m8n8k4 (SASS DMMA.8x8x4; tcgen05 has no f64 kind, SURVEY
-// §7.3 H3).  Each CTA (8 warps) keeps Q_W resident in SMEM for a contiguous run of tiles of the
-// same window and double-buffers the panel tiles with cp.async, so the next panel streams from
-// HBM while the current one is multiplied.  SMEM tiles use a leading dimension = 4 (mod 16)
-// doubles, which makes the m8n8k4 fragment loads (lane -> row lane/4, k lane%4) conflict-free.
-// Results go straight from the accumulator registers to HBM (in place: every output tile depends
-// only on its own input panel tile).
+// §7.3 H3).  Structure of Q_W: every bulge passing a row extends its support at most 2 columns to
+// the left, so Q_W[k][c] = 0 for k > c + 2*nbc (tests/test_abi_plan.py checks it on emulated
+// windows); each warp stops its K loop there (~1/4 fewer flops at k = 96).
+//
+// Main path (n even, "bulk" kernels): 8 consumer warps + 1 producer warp per CTA.  The producer
+// streams panel tiles into a 2-stage SMEM ring with the bulk-copy (TMA) engine
+// (cp.async.bulk ... mbarrier::complete_tx, SASS UBLKCP): one 1-D copy per panel column, 16-byte
+// aligned by starting at an even row.  Q_W (stored by the chase kernel in this SMEM layout) arrives
+// in one shot per window.  Consumers wait on the stage's mbarrier, run the DMMA K loop, release the
+// stage, then store the accumulators in place.  Generic path (n odd): same tiling, 8-byte cp.async.
+// SMEM tiles use a leading dimension = 4 (mod 16) doubles: conflict-free m8n8k4 fragment loads.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -28,10 +33,11 @@ namespace hqr {
 
 namespace {
 
-constexpr int kThreads = 256;
-constexpr int kMaxStepWindows = 128;  // windows per step handled by the in-kernel item decoder
+constexpr int kConsumerWarps = 8;
+constexpr int kThreadsGeneric = 256;
+constexpr int kThreadsBulk = 288;  // 8 consumer warps + 1 producer warp
+constexpr int kMaxStepWindows = 128;
 
-__host__ __device__ constexpr int pad_ld(int x) { return x + (((4 - x) % 16) + 16) % 16; }
 // tile widths: 64 columns / rows, 32 when the 128-wide factor leaves too little SMEM for two panels
 __host__ __device__ constexpr int left_cols(int KP) { return KP <= 96 ? 64 : 32; }
 __host__ __device__ constexpr int right_rows(int KP) { return KP <= 96 ? 64 : 32; }
@@ -42,89 +48,329 @@ __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
                : "d"(a), "d"(b));
 }
 
+// ---- async copy / mbarrier helpers ---------------------------------------------------------
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool pred) {
-  unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
   int sz = pred ? 8 : 0;
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(sz));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(smem_u32(smem)), "l"(gmem), "r"(sz));
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.shared::cta.b64 st, [%0];\n}\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n}\n"
+               ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+// 1-D bulk copy global -> shared through the TMA engine; completes tx bytes on `bar`
+__device__ __forceinline__ void bulk_g2s(void* smem, const void* gmem, unsigned bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+      ::"r"(smem_u32(smem)), "l"(gmem), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+
 // per-CTA item decoder: the step's windows with their tile counts (prefix sums in SMEM)
 struct StepItems {
-  int nw;
   int64_t pre[kMaxStepWindows + 1];
+  WindowDesc w[kMaxStepWindows];
+  int64_t rt[kMaxStepWindows];  // right kernel: H row tiles per window
 };
 
-// ----------------------------------------------------------------------------------------------
-// Left update: out[KP x 64] = Q_W^T[KP x KP] * P[KP x 64], P = H(W, c0 : c0+64)
-// A operand (Q^T) in SMEM as As[m][k] = Q[k + m*KP] (contiguous in k), B operand (panel) as
-// Bs[n][k] = H[(w0+k) + (c0+n)*ld] (contiguous in k).  Warps: 4 (m) x 2 (n), warp tile KP/4 x 32.
-// ----------------------------------------------------------------------------------------------
-template <int KP>
-__global__ void __launch_bounds__(kThreads, 1) left_kernel(StepArgs a, int64_t total_items) {
-  constexpr int NT = left_cols(KP);
-  constexpr int LD = pad_ld(KP);
-  constexpr int WM = KP / 4, WN = NT / 2;
+__device__ __forceinline__ int decode_item(const StepItems& si, int nw, int64_t it, int64_t& tile) {
+  int i = 0;
+  while (i + 1 < nw && si.pre[i + 1] <= it) ++i;
+  tile = it - si.pre[i];
+  return i;
+}
+
+// ================================================================================================
+// Bulk-path update kernel (n even).  LEFT:  out[KP x NT] = Q_W^T[KP x KP] * P[KP x NT],
+//   P = H(W, c0 : c0+NT); A = Q_W^T with Qs[m*QLD + k] = Q[k + m*QLD] (the chase kernel's slot
+//   layout), B = panel with Ps[nn*LDP + ro + k] = H[(w0+k) + (c0+nn)*n], ro = w0 & 1 so every
+//   column copy starts 16-byte aligned.
+// RIGHT: out[MT x KP] = P[MT x KP] * Q_W[KP x KP], P = H(r0 : r0+MT, W) (rows above W) or
+//   Z(r0 : r0+MT, W); A = panel with Ps[k*LDP + m] = M[(r0+m) + (w0+k)*n], B = Qs[nn*QLD + k].
+//   Items of window i: ceil(w0/MT) tiles of H rows [0, w0) (right_mode != 2), then ceil(n/MT) tiles
+//   of Z rows [0, n) (Z != nullptr and right_mode != 1).
+// Warp roles: warp 8 = producer (bulk copies), warps 0-3 = consumer group 0, warps 4-7 = group 1.
+// The groups ping-pong: group q computes the CTA's items j = q (mod 2) out of SMEM stage q, so one
+// group's epilogue (register -> HBM stores) overlaps the other group's DMMA main loop.  Inside a
+// group, 2 x 2 warps tile the output; a warp's K loop stops at the Q_W structure bound, and the
+// two warps sharing an SM sub-partition (w, w+4) get complementary row (LEFT) / column (RIGHT)
+// groups so both DMMA pipes of a sub-partition pair see the same K extent on average.
+// ================================================================================================
+template <int KP, bool LEFT>
+__global__ void __launch_bounds__(kThreadsBulk, 1) bulk_update_kernel(StepArgs a, int64_t total_items) {
+  constexpr int NT = left_cols(KP), MT = right_rows(KP);
+  constexpr int QLD = pad_ld(KP);
+  constexpr int LDP = LEFT ? pad_ld(KP + 2) : pad_ld(MT);
+  constexpr int STAGE = LEFT ? NT * LDP : KP * LDP;        // doubles per SMEM stage
+  constexpr int OM = LEFT ? KP : MT, ON = LEFT ? NT : KP;  // output tile
+  constexpr int WM = OM / 2, WN = ON / 2;                  // warp tile (2 x 2 warps per group)
   constexpr int FM = WM / 8, FN = WN / 8;
-  extern __shared__ double sm[];
-  double* As = sm;                    // KP x LD
-  double* Bs = As + KP * LD;          // 2 x NT x LD
+  extern __shared__ __align__(128) double sm[];
+  double* Qs = sm;                       // KP x QLD
+  double* Ps = Qs + KP * QLD;            // 2 stages
   __shared__ StepItems si;
-  __shared__ WindowDesc sw[kMaxStepWindows];
+  __shared__ __align__(8) uint64_t full[2], empty[2], qfull, qempty;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wm0 = (warp & 3) * WM, wn0 = (warp >> 2) * WN;
   const int64_t n = a.n;
-
+  const int nw = a.win_count;
+  const int64_t ztiles = (!LEFT && a.Z && a.right_mode != 1) ? (n + MT - 1) / MT : 0;
   if (tid == 0) {
-    si.nw = a.win_count;
     si.pre[0] = 0;
-    for (int i = 0; i < a.win_count; ++i) {
+    for (int i = 0; i < nw; ++i) {
       WindowDesc w = a.wins[a.win_begin + i];
-      sw[i] = w;
-      int64_t cols = n - 1 - w.w1;
-      si.pre[i + 1] = si.pre[i] + (cols + NT - 1) / NT;
+      si.w[i] = w;
+      if (LEFT) {
+        si.rt[i] = 0;
+        si.pre[i + 1] = si.pre[i] + (n - 1 - w.w1 + NT - 1) / NT;
+      } else {
+        si.rt[i] = (a.right_mode == 2) ? 0 : ((int64_t)w.w0 + MT - 1) / MT;
+        si.pre[i + 1] = si.pre[i] + si.rt[i] + ztiles;
+      }
     }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 4);
+    }
+    mbar_init(&qfull, 1);
+    mbar_init(&qempty, kConsumerWarps);
   }
+  for (int i = tid; i < 2 * STAGE; i += kThreadsBulk) Ps[i] = 0.0;  // never-copied rows stay finite
+  fence_proxy_async();
   __syncthreads();
 
   const int64_t G = gridDim.x;
   const int64_t it0 = total_items * blockIdx.x / G, it1 = total_items * (blockIdx.x + 1) / G;
-  auto decode = [&](int64_t it, int& wi, int64_t& tile) {
-    int i = 0;
-    while (si.pre[i + 1] <= it) ++i;
-    wi = i;
-    tile = it - si.pre[i];
-  };
-  auto load_panel = [&](int wi, int64_t tile, int buf) {
-    const WindowDesc& w = sw[wi];
-    const int kw = w.w1 - w.w0 + 1;
-    const int64_t c0 = w.w1 + 1 + tile * NT;
-    double* B = Bs + buf * NT * LD;
-    for (int f = tid; f < NT * KP; f += kThreads) {
-      int nn = f / KP, k = f - nn * KP;
-      int64_t col = c0 + nn;
-      bool ok = (k < kw) && (col < n);
-      const double* g = ok ? a.H + (w.w0 + k) + col * n : a.H;
-      cp_async8(B + nn * LD + k, g, ok);
-    }
-  };
-  auto load_q = [&](int wi) {
-    const double* Q = a.qslots + (size_t)sw[wi].slot * KP * KP;
-    for (int f = tid; f < KP * KP; f += kThreads) {
-      int m = f / KP, k = f - m * KP;
-      cp_async8(As + m * LD + k, Q + f, true);
+  // RIGHT: matrix and row range of a tile
+  auto panel = [&](int wi, int64_t tile, double*& M, int64_t& r0, int64_t& r1) {
+    if (tile < si.rt[wi]) {
+      M = a.H; r0 = tile * MT; r1 = si.w[wi].w0;
+    } else {
+      M = a.Z; r0 = (tile - si.rt[wi]) * MT; r1 = n;
     }
   };
 
+  if (warp == kConsumerWarps) {
+    // ---------------- producer warp: bulk copies (TMA engine) ----------------
+    int cur = -1;
+    unsigned nq = 0;
+    for (int64_t it = it0; it < it1; ++it) {
+      int64_t tile;
+      const int wi = decode_item(si, nw, it, tile);
+      const WindowDesc& w = si.w[wi];
+      if (wi != cur) {
+        if (cur >= 0) mbar_wait(&qempty, (nq - 1) & 1);  // both groups done with the previous Q_W
+        const double* Q = a.qslots + (size_t)(w.slot + a.slot_offset) * KP * QLD;
+        constexpr unsigned qbytes = KP * QLD * 8, chunk = qbytes / 32;
+        if (lane == 0) mbar_arrive_tx(&qfull, qbytes);
+        __syncwarp();
+        bulk_g2s(reinterpret_cast<char*>(Qs) + lane * chunk, reinterpret_cast<const char*>(Q) + lane * chunk,
+                 chunk, &qfull);
+        cur = wi;
+        ++nq;
+      }
+      const int64_t j = it - it0;
+      const int s = (int)(j & 1);
+      if (j >= 2) mbar_wait(&empty[s], (unsigned)((j >> 1) - 1) & 1);
+      const int kw = w.w1 - w.w0 + 1;
+      double* dst = Ps + s * STAGE;
+      if (LEFT) {
+        const int ro = w.w0 & 1;
+        const int L = (kw + ro + 1) & ~1;
+        const int64_t c0 = w.w1 + 1 + tile * NT;
+        const int ncols = (int)(n - c0 < NT ? n - c0 : NT);
+        if (lane == 0) mbar_arrive_tx(&full[s], (unsigned)(ncols * L * 8));
+        __syncwarp();
+        const double* src = a.H + (w.w0 - ro) + c0 * n;
+        for (int c = lane; c < ncols; c += 32) bulk_g2s(dst + c * LDP, src + c * n, (unsigned)(L * 8), &full[s]);
+      } else {
+        double* M;
+        int64_t r0, r1;
+        panel(wi, tile, M, r0, r1);
+        const int rows = (int)(r1 - r0 < MT ? r1 - r0 : MT);
+        const int L = (rows + 1) & ~1;
+        if (lane == 0) mbar_arrive_tx(&full[s], (unsigned)(kw * L * 8));
+        __syncwarp();
+        const double* src = M + r0 + (int64_t)w.w0 * n;
+        for (int k = lane; k < kw; k += 32) bulk_g2s(dst + k * LDP, src + k * n, (unsigned)(L * 8), &full[s]);
+      }
+    }
+  } else {
+    // ---------------- consumer groups ----------------
+    const int q = warp >> 2, i4 = warp & 3;
+    const int kg = (i4 & 1) ^ q;   // the index (row group LEFT / column group RIGHT) that sets K
+    const int og = i4 >> 1;        // the other output index
+    const int wm0 = (LEFT ? kg : og) * WM, wn0 = (LEFT ? og : kg) * WN;
+    const int lr = lane >> 2, lk = lane & 3;
+    int cur = -1;
+    unsigned nq = 0;
+    for (int64_t it = it0; it < it1; ++it) {
+      int64_t tile;
+      const int wi = decode_item(si, nw, it, tile);
+      if (wi != cur) {
+        if (cur >= 0) {  // this group has finished all its tiles of the previous window
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&qempty);
+        }
+        mbar_wait(&qfull, nq & 1);
+        cur = wi;
+        ++nq;
+      }
+      const int64_t j = it - it0;
+      if ((int)(j & 1) != q) continue;
+      const WindowDesc& w = si.w[wi];
+      const int s = q;
+      mbar_wait(&full[s], (unsigned)(j >> 1) & 1);
+      // Q_W[k][c] = 0 for k > c + 2 nbc: K stops after this warp's last row (LEFT) / column (RIGHT)
+      const int kend = min(KP, ((LEFT ? wm0 + WM : wn0 + WN) + 2 * w.nbc + 3) & ~3);
+      double acc[FM][FN][2];
+#pragma unroll
+      for (int i = 0; i < FM; ++i)
+#pragma unroll
+        for (int jn = 0; jn < FN; ++jn) acc[i][jn][0] = acc[i][jn][1] = 0.0;
+      const double* P = Ps + s * STAGE;
+      if (LEFT) {
+        const int ro = w.w0 & 1;
+        const double* A = Qs + (wm0 + lr) * QLD + lk;
+        const double* B = P + (wn0 + lr) * LDP + ro + lk;
+#pragma unroll 2
+        for (int kk = 0; kk < kend; kk += 4) {
+          double fa[FM], fb[FN];
+#pragma unroll
+          for (int i = 0; i < FM; ++i) fa[i] = A[8 * i * QLD + kk];
+#pragma unroll
+          for (int jn = 0; jn < FN; ++jn) fb[jn] = B[8 * jn * LDP + kk];
+#pragma unroll
+          for (int i = 0; i < FM; ++i)
+#pragma unroll
+            for (int jn = 0; jn < FN; ++jn) dmma(acc[i][jn], fa[i], fb[jn]);
+        }
+      } else {
+        const double* A = P + lk * LDP + wm0 + lr;
+        const double* B = Qs + (wn0 + lr) * QLD + lk;
+#pragma unroll 2
+        for (int kk = 0; kk < kend; kk += 4) {
+          double fa[FM], fb[FN];
+#pragma unroll
+          for (int i = 0; i < FM; ++i) fa[i] = A[kk * LDP + 8 * i];
+#pragma unroll
+          for (int jn = 0; jn < FN; ++jn) fb[jn] = B[8 * jn * QLD + kk];
+#pragma unroll
+          for (int i = 0; i < FM; ++i)
+#pragma unroll
+            for (int jn = 0; jn < FN; ++jn) dmma(acc[i][jn], fa[i], fb[jn]);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+      // epilogue: in-place stores straight from the accumulators
+      const int kw = w.w1 - w.w0 + 1;
+      if (LEFT) {
+        const int64_t c0 = w.w1 + 1 + tile * NT;
+#pragma unroll
+        for (int i = 0; i < FM; ++i) {
+          const int m = wm0 + 8 * i + lr;
+          if (m >= kw) continue;
+          double* row = a.H + (w.w0 + m);
+#pragma unroll
+          for (int jn = 0; jn < FN; ++jn)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const int64_t col = c0 + wn0 + 8 * jn + 2 * lk + e;
+              if (col < n) row[col * n] = acc[i][jn][e];
+            }
+        }
+      } else {
+        double* M;
+        int64_t r0, r1;
+        panel(wi, tile, M, r0, r1);
+#pragma unroll
+        for (int i = 0; i < FM; ++i) {
+          const int64_t row = r0 + wm0 + 8 * i + lr;
+          if (row >= r1) continue;
+          double* mr = M + row + (int64_t)w.w0 * n;
+#pragma unroll
+          for (int jn = 0; jn < FN; ++jn)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const int col = wn0 + 8 * jn + 2 * lk + e;
+              if (col < kw) mr[col * n] = acc[i][jn][e];
+            }
+        }
+      }
+    }
+  }
+}
+
+// ================================================================================================
+// Generic path (odd n: columns are not 16-byte aligned): 8 warps, 8-byte cp.async double buffer.
+// ================================================================================================
+template <int KP>
+__global__ void __launch_bounds__(kThreadsGeneric, 1) left_generic_kernel(StepArgs a, int64_t total_items) {
+  constexpr int NT = left_cols(KP);
+  constexpr int QLD = pad_ld(KP);
+  constexpr int LD = pad_ld(KP);
+  constexpr int WM = KP / 4, WN = NT / 2;
+  constexpr int FM = WM / 8, FN = WN / 8;
+  extern __shared__ __align__(128) double sm[];
+  double* As = sm;                    // KP x QLD
+  double* Bs = As + KP * QLD;         // 2 x NT x LD
+  __shared__ StepItems si;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm0 = (warp & 3) * WM, wn0 = (warp >> 2) * WN;
+  const int64_t n = a.n;
+  const int nw = a.win_count;
+  if (tid == 0) {
+    si.pre[0] = 0;
+    for (int i = 0; i < nw; ++i) {
+      WindowDesc w = a.wins[a.win_begin + i];
+      si.w[i] = w;
+      si.pre[i + 1] = si.pre[i] + (n - 1 - w.w1 + NT - 1) / NT;
+    }
+  }
+  __syncthreads();
+  const int64_t G = gridDim.x;
+  const int64_t it0 = total_items * blockIdx.x / G, it1 = total_items * (blockIdx.x + 1) / G;
+  auto load_panel = [&](int wi, int64_t tile, int buf) {
+    const WindowDesc& w = si.w[wi];
+    const int kw = w.w1 - w.w0 + 1;
+    const int64_t c0 = w.w1 + 1 + tile * NT;
+    double* B = Bs + buf * NT * LD;
+    for (int f = tid; f < NT * KP; f += kThreadsGeneric) {
+      int nn = f / KP, k = f - nn * KP;
+      int64_t col = c0 + nn;
+      bool ok = (k < kw) && (col < n);
+      cp_async8(B + nn * LD + k, ok ? a.H + (w.w0 + k) + col * n : a.H, ok);
+    }
+  };
+  auto load_q = [&](int wi) {
+    const double* Q = a.qslots + (size_t)(si.w[wi].slot + a.slot_offset) * KP * QLD;
+    for (int f = tid; f < KP * QLD; f += kThreadsGeneric) cp_async8(As + f, Q + f, true);
+  };
   int cur = -1, buf = 0;
   bool pref = false;
   for (int64_t it = it0; it < it1; ++it) {
-    int wi;
     int64_t tile;
-    decode(it, wi, tile);
+    const int wi = decode_item(si, nw, it, tile);
     if (wi != cur) {
       cp_async_wait<0>();
       __syncthreads();
@@ -138,9 +384,8 @@ __global__ void __launch_bounds__(kThreads, 1) left_kernel(StepArgs a, int64_t t
     }
     pref = false;
     if (it + 1 < it1) {
-      int wi2;
       int64_t tile2;
-      decode(it + 1, wi2, tile2);
+      const int wi2 = decode_item(si, nw, it + 1, tile2);
       if (wi2 == wi) {
         load_panel(wi2, tile2, buf ^ 1);
         cp_async_commit();
@@ -149,7 +394,6 @@ __global__ void __launch_bounds__(kThreads, 1) left_kernel(StepArgs a, int64_t t
     }
     if (pref) cp_async_wait<1>(); else cp_async_wait<0>();
     __syncthreads();
-
     double acc[FM][FN][2];
 #pragma unroll
     for (int i = 0; i < FM; ++i)
@@ -161,7 +405,7 @@ __global__ void __launch_bounds__(kThreads, 1) left_kernel(StepArgs a, int64_t t
     for (int kk = 0; kk < KP; kk += 4) {
       double fa[FM], fb[FN];
 #pragma unroll
-      for (int i = 0; i < FM; ++i) fa[i] = As[(wm0 + 8 * i + lr) * LD + kk + lk];
+      for (int i = 0; i < FM; ++i) fa[i] = As[(wm0 + 8 * i + lr) * QLD + kk + lk];
 #pragma unroll
       for (int j = 0; j < FN; ++j) fb[j] = B[(wn0 + 8 * j + lr) * LD + kk + lk];
 #pragma unroll
@@ -169,8 +413,7 @@ __global__ void __launch_bounds__(kThreads, 1) left_kernel(StepArgs a, int64_t t
 #pragma unroll
         for (int j = 0; j < FN; ++j) dmma(acc[i][j], fa[i], fb[j]);
     }
-    // store (in place)
-    const WindowDesc& w = sw[wi];
+    const WindowDesc& w = si.w[wi];
     const int kw = w.w1 - w.w0 + 1;
     const int64_t c0 = w.w1 + 1 + tile * NT;
 #pragma unroll
@@ -178,101 +421,76 @@ __global__ void __launch_bounds__(kThreads, 1) left_kernel(StepArgs a, int64_t t
       const int m = wm0 + 8 * i + lr;
       if (m >= kw) continue;
 #pragma unroll
-      for (int j = 0; j < FN; ++j) {
+      for (int j = 0; j < FN; ++j)
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
           const int64_t col = c0 + wn0 + 8 * j + 2 * lk + e;
           if (col < n) a.H[(w.w0 + m) + col * n] = acc[i][j][e];
         }
-      }
     }
     __syncthreads();
     buf ^= 1;
   }
 }
 
-// ----------------------------------------------------------------------------------------------
-// Right / Z update: out[64 x KP] = P[64 x KP] * Q_W[KP x KP], P = H(r0:r0+64, W) or Z(r0:r0+64, W)
-// A operand (panel) in SMEM as As[k][m] = P[(r0+m) + (w0+k)*ld] (contiguous in m), B operand as
-// Bs[n][k] = Q[k + n*KP] (contiguous in k).  Warps: 2 (m) x 4 (n), warp tile 32 x KP/4.
-// Items of window i: ceil(w0/64) tiles of H rows [0, w0), then (Z != nullptr) ceil(n/64) tiles of
-// Z rows [0, n).
-// ----------------------------------------------------------------------------------------------
 template <int KP>
-__global__ void __launch_bounds__(kThreads, 1) right_kernel(StepArgs a, int64_t total_items) {
+__global__ void __launch_bounds__(kThreadsGeneric, 1) right_generic_kernel(StepArgs a, int64_t total_items) {
   constexpr int MT = right_rows(KP);
-  constexpr int LDQ = pad_ld(KP);
+  constexpr int QLD = pad_ld(KP);
   constexpr int LDP = pad_ld(MT);
   constexpr int WM = MT / 2, WN = KP / 4;
   constexpr int FM = WM / 8, FN = WN / 8;
-  extern __shared__ double sm[];
-  double* Bs = sm;                    // Q: KP(n) x LDQ
-  double* As = Bs + KP * LDQ;         // 2 x KP(k) x LDP
+  extern __shared__ __align__(128) double sm[];
+  double* Bs = sm;                    // Q: KP(n) x QLD
+  double* As = Bs + KP * QLD;         // 2 x KP(k) x LDP
   __shared__ StepItems si;
-  __shared__ WindowDesc sw[kMaxStepWindows];
-  __shared__ int64_t rtiles[kMaxStepWindows];
-
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm0 = (warp & 1) * WM, wn0 = (warp >> 1) * WN;
   const int64_t n = a.n;
-  const int64_t ztiles = a.Z ? (n + MT - 1) / MT : 0;
-
+  const int nw = a.win_count;
+  const int64_t ztiles = (a.Z && a.right_mode != 1) ? (n + MT - 1) / MT : 0;
   if (tid == 0) {
-    si.nw = a.win_count;
     si.pre[0] = 0;
-    for (int i = 0; i < a.win_count; ++i) {
+    for (int i = 0; i < nw; ++i) {
       WindowDesc w = a.wins[a.win_begin + i];
-      sw[i] = w;
-      rtiles[i] = ((int64_t)w.w0 + MT - 1) / MT;
-      si.pre[i + 1] = si.pre[i] + rtiles[i] + ztiles;
+      si.w[i] = w;
+      si.rt[i] = (a.right_mode == 2) ? 0 : ((int64_t)w.w0 + MT - 1) / MT;
+      si.pre[i + 1] = si.pre[i] + si.rt[i] + ztiles;
     }
   }
   __syncthreads();
-
   const int64_t G = gridDim.x;
   const int64_t it0 = total_items * blockIdx.x / G, it1 = total_items * (blockIdx.x + 1) / G;
-  auto decode = [&](int64_t it, int& wi, int64_t& tile) {
-    int i = 0;
-    while (si.pre[i + 1] <= it) ++i;
-    wi = i;
-    tile = it - si.pre[i];
-  };
-  // panel rows [r0, r1) of matrix M (H or Z)
   auto panel = [&](int wi, int64_t tile, double*& M, int64_t& r0, int64_t& r1) {
-    if (tile < rtiles[wi]) {
-      M = a.H; r0 = tile * MT; r1 = sw[wi].w0;
+    if (tile < si.rt[wi]) {
+      M = a.H; r0 = tile * MT; r1 = si.w[wi].w0;
     } else {
-      M = a.Z; r0 = (tile - rtiles[wi]) * MT; r1 = n;
+      M = a.Z; r0 = (tile - si.rt[wi]) * MT; r1 = n;
     }
   };
   auto load_panel = [&](int wi, int64_t tile, int buf) {
-    const WindowDesc& w = sw[wi];
+    const WindowDesc& w = si.w[wi];
     const int kw = w.w1 - w.w0 + 1;
-    double* M; int64_t r0, r1;
+    double* M;
+    int64_t r0, r1;
     panel(wi, tile, M, r0, r1);
     double* A = As + buf * KP * LDP;
-    for (int f = tid; f < KP * MT; f += kThreads) {
+    for (int f = tid; f < KP * MT; f += kThreadsGeneric) {
       int k = f / MT, mm = f - k * MT;
       int64_t row = r0 + mm;
       bool ok = (k < kw) && (row < r1);
-      const double* g = ok ? M + row + (w.w0 + k) * n : M;
-      cp_async8(A + k * LDP + mm, g, ok);
+      cp_async8(A + k * LDP + mm, ok ? M + row + (w.w0 + k) * n : M, ok);
     }
   };
   auto load_q = [&](int wi) {
-    const double* Q = a.qslots + (size_t)sw[wi].slot * KP * KP;
-    for (int f = tid; f < KP * KP; f += kThreads) {
-      int nn = f / KP, k = f - nn * KP;
-      cp_async8(Bs + nn * LDQ + k, Q + f, true);
-    }
+    const double* Q = a.qslots + (size_t)(si.w[wi].slot + a.slot_offset) * KP * QLD;
+    for (int f = tid; f < KP * QLD; f += kThreadsGeneric) cp_async8(Bs + f, Q + f, true);
   };
-
   int cur = -1, buf = 0;
   bool pref = false;
   for (int64_t it = it0; it < it1; ++it) {
-    int wi;
     int64_t tile;
-    decode(it, wi, tile);
+    const int wi = decode_item(si, nw, it, tile);
     if (wi != cur) {
       cp_async_wait<0>();
       __syncthreads();
@@ -286,9 +504,8 @@ __global__ void __launch_bounds__(kThreads, 1) right_kernel(StepArgs a, int64_t 
     }
     pref = false;
     if (it + 1 < it1) {
-      int wi2;
       int64_t tile2;
-      decode(it + 1, wi2, tile2);
+      const int wi2 = decode_item(si, nw, it + 1, tile2);
       if (wi2 == wi) {
         load_panel(wi2, tile2, buf ^ 1);
         cp_async_commit();
@@ -297,7 +514,6 @@ __global__ void __launch_bounds__(kThreads, 1) right_kernel(StepArgs a, int64_t 
     }
     if (pref) cp_async_wait<1>(); else cp_async_wait<0>();
     __syncthreads();
-
     double acc[FM][FN][2];
 #pragma unroll
     for (int i = 0; i < FM; ++i)
@@ -311,63 +527,78 @@ __global__ void __launch_bounds__(kThreads, 1) right_kernel(StepArgs a, int64_t 
 #pragma unroll
       for (int i = 0; i < FM; ++i) fa[i] = A[(kk + lk) * LDP + wm0 + 8 * i + lr];
 #pragma unroll
-      for (int j = 0; j < FN; ++j) fb[j] = Bs[(wn0 + 8 * j + lr) * LDQ + kk + lk];
+      for (int j = 0; j < FN; ++j) fb[j] = Bs[(wn0 + 8 * j + lr) * QLD + kk + lk];
 #pragma unroll
       for (int i = 0; i < FM; ++i)
 #pragma unroll
         for (int j = 0; j < FN; ++j) dmma(acc[i][j], fa[i], fb[j]);
     }
-    const WindowDesc& w = sw[wi];
+    const WindowDesc& w = si.w[wi];
     const int kw = w.w1 - w.w0 + 1;
-    double* M; int64_t r0, r1;
+    double* M;
+    int64_t r0, r1;
     panel(wi, tile, M, r0, r1);
 #pragma unroll
     for (int i = 0; i < FM; ++i) {
       const int64_t row = r0 + wm0 + 8 * i + lr;
       if (row >= r1) continue;
 #pragma unroll
-      for (int j = 0; j < FN; ++j) {
+      for (int j = 0; j < FN; ++j)
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
           const int col = wn0 + 8 * j + 2 * lk + e;
           if (col < kw) M[row + (w.w0 + col) * n] = acc[i][j][e];
         }
-      }
     }
     __syncthreads();
     buf ^= 1;
   }
 }
 
-template <int KP>
-size_t left_smem() { return (size_t)(KP * pad_ld(KP) + 2 * left_cols(KP) * pad_ld(KP)) * sizeof(double); }
-template <int KP>
-size_t right_smem() { return (size_t)(KP * pad_ld(KP) + 2 * KP * pad_ld(right_rows(KP))) * sizeof(double); }
+// ---- launchers -------------------------------------------------------------------------------
+template <int KP> constexpr size_t left_bulk_smem() {
+  return (size_t)(KP * pad_ld(KP) + 2 * left_cols(KP) * pad_ld(KP + 2)) * sizeof(double);
+}
+template <int KP> constexpr size_t right_bulk_smem() {
+  return (size_t)(KP * pad_ld(KP) + 2 * KP * pad_ld(right_rows(KP))) * sizeof(double);
+}
+template <int KP> constexpr size_t left_generic_smem() {
+  return (size_t)(KP * pad_ld(KP) + 2 * left_cols(KP) * pad_ld(KP)) * sizeof(double);
+}
+template <int KP> constexpr size_t right_generic_smem() {
+  return (size_t)(KP * pad_ld(KP) + 2 * KP * pad_ld(right_rows(KP))) * sizeof(double);
+}
 
-template <int KP>
-cudaError_t launch_left_t(const StepArgs& a, int64_t items, int grid, cudaStream_t st) {
-  static bool configured = false;
-  size_t smem = left_smem<KP>();
+template <typename K>
+cudaError_t launch_k(K kern, size_t smem, int threads, const StepArgs& a, int64_t items, int grid,
+                     cudaStream_t st, bool& configured) {
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(left_kernel<KP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  left_kernel<KP><<<grid, kThreads, smem, st>>>(a, items);
+  kern<<<grid, threads, smem, st>>>(a, items);
   return cudaGetLastError();
 }
 
 template <int KP>
-cudaError_t launch_right_t(const StepArgs& a, int64_t items, int grid, cudaStream_t st) {
-  static bool configured = false;
-  size_t smem = right_smem<KP>();
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(right_kernel<KP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    configured = true;
+cudaError_t launch_left_t(const StepArgs& a, int64_t items, int grid, cudaStream_t st) {
+  if ((a.n & 1) == 0) {
+    static bool c = false;
+    return launch_k(bulk_update_kernel<KP, true>, left_bulk_smem<KP>(), kThreadsBulk, a, items, grid, st, c);
   }
-  right_kernel<KP><<<grid, kThreads, smem, st>>>(a, items);
-  return cudaGetLastError();
+  static bool c = false;
+  return launch_k(left_generic_kernel<KP>, left_generic_smem<KP>(), kThreadsGeneric, a, items, grid, st, c);
+}
+
+template <int KP>
+cudaError_t launch_right_t(const StepArgs& a, int64_t items, int grid, cudaStream_t st) {
+  if ((a.n & 1) == 0) {
+    static bool c = false;
+    return launch_k(bulk_update_kernel<KP, false>, right_bulk_smem<KP>(), kThreadsBulk, a, items, grid, st, c);
+  }
+  static bool c = false;
+  return launch_k(right_generic_kernel<KP>, right_generic_smem<KP>(), kThreadsGeneric, a, items, grid, st, c);
 }
 
 }  // namespace
@@ -376,10 +607,11 @@ cudaError_t launch_left(const StepArgs& a, const WindowDesc* hw, int num_sms, cu
                         int64_t* items_out, double* flops, double* bytes) {
   int64_t items = 0;
   double f = 0, b = 0;
+  const int NT = left_cols(a.KP);
   for (int i = 0; i < a.win_count; ++i) {
     int64_t cols = a.n - 1 - hw[i].w1;
     int64_t kw = hw[i].w1 - hw[i].w0 + 1;
-    items += (cols + left_cols(a.KP) - 1) / left_cols(a.KP);
+    items += (cols + NT - 1) / NT;
     f += 2.0 * kw * kw * (double)cols;
     b += 16.0 * kw * (double)cols;
   }
@@ -403,11 +635,12 @@ cudaError_t launch_right(const StepArgs& a, const WindowDesc* hw, int num_sms, c
   int64_t items = 0;
   double f = 0, b = 0;
   const int MT = right_rows(a.KP);
-  const int64_t zt = a.Z ? (a.n + MT - 1) / MT : 0;
+  const bool do_h = a.right_mode != 2, do_z = a.Z && a.right_mode != 1;
+  const int64_t zt = do_z ? (a.n + MT - 1) / MT : 0;
   for (int i = 0; i < a.win_count; ++i) {
     int64_t kw = hw[i].w1 - hw[i].w0 + 1;
-    items += (hw[i].w0 + MT - 1) / MT + zt;
-    double rows = (double)hw[i].w0 + (a.Z ? (double)a.n : 0.0);
+    items += (do_h ? (hw[i].w0 + MT - 1) / MT : 0) + zt;
+    double rows = (do_h ? (double)hw[i].w0 : 0.0) + (do_z ? (double)a.n : 0.0);
     f += 2.0 * kw * kw * rows;
     b += 16.0 * kw * rows;
   }

@@ -20,7 +20,7 @@ def _house(m, x):
     return x[1:m] / (x0 - b), (b - x0) / b, b
 
 
-def emulate(H, Z, ilo, ihi, sr, si, window):
+def emulate(H, Z, ilo, ihi, sr, si, window, on_window=None):
     n = H.shape[0]
     info, wins = hq.plan_query(n, ilo, ihi, len(sr), window)
     nb = len(sr) // 2
@@ -70,6 +70,8 @@ def emulate(H, Z, ilo, ihi, sr, si, window):
                     blk -= tau * np.outer(blk @ v, v)
             H[w0:w1 + 1, w0:w1 + 1] = Hw
             Qs.append((w0, w1, Q))
+            if on_window is not None:
+                on_window(nbc, Q)
         for w0, w1, Q in Qs:  # left updates
             H[w0:w1 + 1, w1 + 1:] = Q.T @ H[w0:w1 + 1, w1 + 1:]
         for w0, w1, Q in Qs:  # right + Z updates

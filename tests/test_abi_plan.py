@@ -122,3 +122,18 @@ def test_schedule_emulation_matches_oracle(n, ns, ilo, ihi, win, z0):
     assert np.all(np.tril(He, -2) == 0.0)
     assert np.array_equal(He[:ilo, :ilo], H0[:ilo, :ilo])
     assert np.array_equal(He[ihi + 1:, ihi + 1:], H0[ihi + 1:, ihi + 1:])
+
+
+@pytest.mark.parametrize("n,ns,win", [(600, 60, 96), (300, 40, 112), (200, 30, 40), (90, 40, 96)])
+def test_window_factor_lower_bandwidth(n, ns, win):
+    """update.cu skips Q_W[k][c] for k > c + 2*nbc: every bulge passing a row extends the row's
+    support at most 2 columns to the left.  Check it on every window of emulated sweeps."""
+    H0, Z0, re_, im_ = random_case(n + ns, n, ns)
+    worst = []
+
+    def chk(nbc, Q):
+        r, c = np.nonzero(Q)
+        worst.append(int((r - c).max()) - 2 * nbc)
+
+    emulate(H0.copy(order="F"), None, 0, n - 1, re_, im_, win, on_window=chk)
+    assert worst and max(worst) <= 0
