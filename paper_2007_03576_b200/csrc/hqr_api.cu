@@ -13,6 +13,7 @@
 
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -175,11 +176,23 @@ int enqueue_sweep(const CachedPlan& cp, double* H, double* Z, int64_t n, bool pr
   a.wins = cp.d_wins; a.coef = g.d_coef; a.qslots = g.d_q; a.KP = cp.KP;
   a.QLD = hqr::pad_ld(cp.KP);
   size_t ev = 0;
+  static const bool dbg_sync = getenv("HQR_DEBUG_SYNC") != nullptr;  // debugging: sync after launches
   auto mark = [&](int cls) {
+    if (dbg_sync) {
+      cudaError_t e = cudaStreamSynchronize(A);
+      if (e != cudaSuccess) fprintf(stderr, "hqr: CUDA error %d before mark class %d\n", (int)e, cls);
+    }
     if (!prof) return;
     cudaEventRecord(prof_event(ev++), A);
     if (classes) classes->push_back(cls);
   };
+  hqr::TensorMaps tm;
+  CK(hqr::make_tensor_maps(&tm, H, Z, n, cp.KP));
+  if (dbg_sync) {
+    const unsigned long long* q = reinterpret_cast<const unsigned long long*>(&tm.left_H);
+    fprintf(stderr, "hqr: tensor maps valid=%d KP=%d H=%p map@%p %llx %llx %llx\n", (int)tm.valid, cp.KP,
+            (const void*)H, (const void*)&tm.left_H, q[0], q[1], q[2]);
+  }
   if (split) {
     CK(cudaEventRecord(g.ev_fork, A));
     CK(cudaStreamWaitEvent(B, g.ev_fork, 0));
@@ -192,7 +205,8 @@ int enqueue_sweep(const CachedPlan& cp, double* H, double* Z, int64_t n, bool pr
     const WindowDesc* hw = P.windows.data() + a.win_begin;
     if (split && s >= hqr::kQSets) CK(cudaStreamWaitEvent(A, g.ev_z[set], 0));
     mark(0);
-    CK(hqr::launch_chase(a, P.max_kw, P.max_nbc, A));
+    static const bool dbg_skip_chase = getenv("HQR_DEBUG_SKIP_CHASE") != nullptr;
+    if (!dbg_skip_chase) CK(hqr::launch_chase(a, P.max_kw, P.max_nbc, A));
     mark(-1);
     st->launches_chase++;
     int64_t items;
@@ -202,14 +216,14 @@ int enqueue_sweep(const CachedPlan& cp, double* H, double* Z, int64_t n, bool pr
       CK(cudaStreamWaitEvent(B, g.ev_q[set], 0));
       StepArgs az = a;
       az.right_mode = 2;
-      CK(hqr::launch_right(az, hw, g.num_sms, B, &items, &fl, &by));
+      CK(hqr::launch_right(az, hw, g.num_sms, tm, B, &items, &fl, &by));
       if (items) st->launches_right++;
       st->flops_update += fl;
       st->bytes_update += by;
       CK(cudaEventRecord(g.ev_z[set], B));
     }
     mark(1);
-    CK(hqr::launch_left(a, hw, g.num_sms, A, &items, &fl, &by));
+    CK(hqr::launch_left(a, hw, g.num_sms, tm, A, &items, &fl, &by));
     mark(-1);
     if (items) st->launches_left++;
     st->flops_update += fl;
@@ -217,7 +231,7 @@ int enqueue_sweep(const CachedPlan& cp, double* H, double* Z, int64_t n, bool pr
     mark(2);
     StepArgs ar = a;
     ar.right_mode = split ? 1 : 0;
-    CK(hqr::launch_right(ar, hw, g.num_sms, A, &items, &fl, &by));
+    CK(hqr::launch_right(ar, hw, g.num_sms, tm, A, &items, &fl, &by));
     mark(-1);
     if (items) st->launches_right++;
     st->flops_update += fl;

@@ -2,6 +2,7 @@
 // (chase.cu, update.cu).  Product path only; shares nothing with oracle/.
 #pragma once
 #include <cstdint>
+#include <cuda.h>  // CUtensorMap (header only; the encoder is fetched through cudaGetDriverEntryPoint)
 #include <cuda_runtime.h>
 
 #include "plan.hpp"
@@ -28,14 +29,26 @@ struct StepArgs {
 cudaError_t launch_chase(const StepArgs& a, int max_kw, int max_nbc, cudaStream_t st);
 size_t chase_smem_bytes(int kw, int nbc);
 
+// 2-D TMA descriptors of H and Z (column-major, n x n) with the update kernels' SMEM boxes.
+// Valid only for even n (TMA global strides must be multiples of 16 bytes).
+struct TensorMaps {
+  CUtensorMap left_H;   // box {pad_ld(KP) rows, left_cols(KP) columns}
+  CUtensorMap right_H;  // box {pad_ld(right_rows(KP)) rows, KP columns}
+  CUtensorMap right_Z;
+  bool valid = false;
+};
+cudaError_t make_tensor_maps(TensorMaps* tm, const double* H, const double* Z, int64_t n, int KP);
+
 // Off-diagonal updates of one step.  Left: H(W, w1+1:n) <- Q_W^T H(W, w1+1:n) for every window.
 // Right (+Z): H(0:w0, W) <- H(0:w0, W) Q_W and Z(:, W) <- Z(:, W) Q_W.
 // host_wins: the step's windows on the host (to size the grid).  Returns the number of items
 // (tiles) through *items and the launch's GEMM flops through *flops.
 cudaError_t launch_left(const StepArgs& a, const WindowDesc* host_wins, int num_sms,
-                        cudaStream_t st, int64_t* items, double* flops, double* bytes);
+                        const TensorMaps& tm, cudaStream_t st, int64_t* items, double* flops,
+                        double* bytes);
 cudaError_t launch_right(const StepArgs& a, const WindowDesc* host_wins, int num_sms,
-                         cudaStream_t st, int64_t* items, double* flops, double* bytes);
+                         const TensorMaps& tm, cudaStream_t st, int64_t* items, double* flops,
+                         double* bytes);
 // Q slot sets in flight: the Z update of step g may trail the chase of step g + kQSets - 1
 constexpr int kQSets = 4;
 

@@ -26,6 +26,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 
 #include "kernels.hpp"
 
@@ -83,6 +85,12 @@ __device__ __forceinline__ void bulk_g2s(void* smem, const void* gmem, unsigned 
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
       ::"r"(smem_u32(smem)), "l"(gmem), "r"(bytes), "r"(smem_u32(bar)) : "memory");
 }
+// 2-D tensor (TMA) load of one box at (row c0, column c1); completes box bytes on `bar`
+__device__ __forceinline__ void tma_load_2d(void* smem, const CUtensorMap* tm, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n"
+      ::"r"(smem_u32(smem)), "l"(tm), "r"(c0), "r"(c1), "r"(smem_u32(bar)) : "memory");
+}
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
 
 // per-CTA item decoder: the step's windows with their tile counts (prefix sums in SMEM)
@@ -100,12 +108,17 @@ __device__ __forceinline__ int decode_item(const StepItems& si, int nw, int64_t 
 }
 
 // ================================================================================================
-// Bulk-path update kernel (n even).  LEFT:  out[KP x NT] = Q_W^T[KP x KP] * P[KP x NT],
+// TMA-path update kernel (n even).  LEFT:  out[KP x NT] = Q_W^T[KP x KP] * P[KP x NT],
 //   P = H(W, c0 : c0+NT); A = Q_W^T with Qs[m*QLD + k] = Q[k + m*QLD] (the chase kernel's slot
-//   layout), B = panel with Ps[nn*LDP + ro + k] = H[(w0+k) + (c0+nn)*n], ro = w0 & 1 so every
-//   column copy starts 16-byte aligned.
+//   layout, one 1-D bulk copy per window), B = panel, one 2-D TMA box {LDP rows, NT columns} at
+//   (w0 - ro, c0), ro = w0 & 1 (TMA's innermost coordinate must be 16-byte aligned):
+//   Ps[nn*LDP + ro + k] = H[(w0+k) + (c0+nn)*n]  (LDP >= KP + 1).
 // RIGHT: out[MT x KP] = P[MT x KP] * Q_W[KP x KP], P = H(r0 : r0+MT, W) (rows above W) or
-//   Z(r0 : r0+MT, W); A = panel with Ps[k*LDP + m] = M[(r0+m) + (w0+k)*n], B = Qs[nn*QLD + k].
+//   Z(r0 : r0+MT, W); A = panel, one TMA box {LDP rows, KP columns} at (r0, w0):
+//   Ps[k*LDP + m] = M[(r0+m) + (w0+k)*n]; B = Qs[nn*QLD + k].
+// LDP = 4 (mod 16) doubles makes the m8n8k4 fragment loads conflict-free; the box rows beyond the
+// window / tile (other matrix rows, or TMA's zero fill outside the matrix) are multiplied by the
+// zero padding of Q_W or land in output rows that are never stored.
 //   Items of window i: ceil(w0/MT) tiles of H rows [0, w0) (right_mode != 2), then ceil(n/MT) tiles
 //   of Z rows [0, n) (Z != nullptr and right_mode != 1).
 // Warp roles: warp 8 = producer (bulk copies), warps 0-3 = consumer group 0, warps 4-7 = group 1.
@@ -116,17 +129,20 @@ __device__ __forceinline__ int decode_item(const StepItems& si, int nw, int64_t 
 // groups so both DMMA pipes of a sub-partition pair see the same K extent on average.
 // ================================================================================================
 template <int KP, bool LEFT>
-__global__ void __launch_bounds__(kThreadsBulk, 1) bulk_update_kernel(StepArgs a, int64_t total_items) {
+__global__ void __launch_bounds__(kThreadsBulk, 1)
+    bulk_update_kernel(StepArgs a, int64_t total_items, const __grid_constant__ CUtensorMap tmH,
+                       const __grid_constant__ CUtensorMap tmZ) {
   constexpr int NT = left_cols(KP), MT = right_rows(KP);
   constexpr int QLD = pad_ld(KP);
-  constexpr int LDP = LEFT ? pad_ld(KP + 2) : pad_ld(MT);
+  constexpr int LDP = LEFT ? pad_ld(KP) : pad_ld(MT);
   constexpr int STAGE = LEFT ? NT * LDP : KP * LDP;        // doubles per SMEM stage
   constexpr int OM = LEFT ? KP : MT, ON = LEFT ? NT : KP;  // output tile
   constexpr int WM = OM / 2, WN = ON / 2;                  // warp tile (2 x 2 warps per group)
   constexpr int FM = WM / 8, FN = WN / 8;
-  extern __shared__ __align__(128) double sm[];
+  static_assert(!LEFT || LDP >= KP + 1, "left panel box must hold the odd-row shift");
+  extern __shared__ __align__(1024) double sm[];
   double* Qs = sm;                       // KP x QLD
-  double* Ps = Qs + KP * QLD;            // 2 stages
+  double* Ps = Qs + KP * QLD;            // 2 stages (128-byte aligned: TMA destinations)
   __shared__ StepItems si;
   __shared__ __align__(8) uint64_t full[2], empty[2], qfull, qempty;
 
@@ -191,28 +207,21 @@ __global__ void __launch_bounds__(kThreadsBulk, 1) bulk_update_kernel(StepArgs a
       const int64_t j = it - it0;
       const int s = (int)(j & 1);
       if (j >= 2) mbar_wait(&empty[s], (unsigned)((j >> 1) - 1) & 1);
-      const int kw = w.w1 - w.w0 + 1;
       double* dst = Ps + s * STAGE;
-      if (LEFT) {
-        const int ro = w.w0 & 1;
-        const int L = (kw + ro + 1) & ~1;
-        const int64_t c0 = w.w1 + 1 + tile * NT;
-        const int ncols = (int)(n - c0 < NT ? n - c0 : NT);
-        if (lane == 0) mbar_arrive_tx(&full[s], (unsigned)(ncols * L * 8));
-        __syncwarp();
-        const double* src = a.H + (w.w0 - ro) + c0 * n;
-        for (int c = lane; c < ncols; c += 32) bulk_g2s(dst + c * LDP, src + c * n, (unsigned)(L * 8), &full[s]);
-      } else {
-        double* M;
-        int64_t r0, r1;
-        panel(wi, tile, M, r0, r1);
-        const int rows = (int)(r1 - r0 < MT ? r1 - r0 : MT);
-        const int L = (rows + 1) & ~1;
-        if (lane == 0) mbar_arrive_tx(&full[s], (unsigned)(kw * L * 8));
-        __syncwarp();
-        const double* src = M + r0 + (int64_t)w.w0 * n;
-        for (int k = lane; k < kw; k += 32) bulk_g2s(dst + k * LDP, src + k * n, (unsigned)(L * 8), &full[s]);
+      if (lane == 0) {
+        mbar_arrive_tx(&full[s], (unsigned)(STAGE * 8));  // TMA always lands the full box
+        if (LEFT) {
+          // the innermost TMA coordinate must address a 16-byte boundary: start at the even row
+          // w0 - ro (ro = w0 & 1); the consumers offset their reads by ro
+          tma_load_2d(dst, &tmH, w.w0 & ~1, (int)(w.w1 + 1 + tile * NT), &full[s]);
+        } else {
+          double* M;
+          int64_t r0, r1;
+          panel(wi, tile, M, r0, r1);
+          tma_load_2d(dst, M == a.H ? &tmH : &tmZ, (int)r0, w.w0, &full[s]);
+        }
       }
+      __syncwarp();
     }
   } else {
     // ---------------- consumer groups ----------------
@@ -241,7 +250,11 @@ __global__ void __launch_bounds__(kThreadsBulk, 1) bulk_update_kernel(StepArgs a
       const int s = q;
       mbar_wait(&full[s], (unsigned)(j >> 1) & 1);
       // Q_W[k][c] = 0 for k > c + 2 nbc: K stops after this warp's last row (LEFT) / column (RIGHT)
+#ifdef HQR_BENCH_NO_TRIM  // benchmark-only knob (tools/gemm_bench.cu), never set in the product build
+      const int kend = KP;
+#else
       const int kend = min(KP, ((LEFT ? wm0 + WM : wn0 + WN) + 2 * w.nbc + 3) & ~3);
+#endif
       double acc[FM][FN][2];
 #pragma unroll
       for (int i = 0; i < FM; ++i)
@@ -249,9 +262,8 @@ __global__ void __launch_bounds__(kThreadsBulk, 1) bulk_update_kernel(StepArgs a
         for (int jn = 0; jn < FN; ++jn) acc[i][jn][0] = acc[i][jn][1] = 0.0;
       const double* P = Ps + s * STAGE;
       if (LEFT) {
-        const int ro = w.w0 & 1;
         const double* A = Qs + (wm0 + lr) * QLD + lk;
-        const double* B = P + (wn0 + lr) * LDP + ro + lk;
+        const double* B = P + (wn0 + lr) * LDP + (w.w0 & 1) + lk;
 #pragma unroll 2
         for (int kk = 0; kk < kend; kk += 4) {
           double fa[FM], fb[FN];
@@ -284,6 +296,9 @@ __global__ void __launch_bounds__(kThreadsBulk, 1) bulk_update_kernel(StepArgs a
       if (lane == 0) mbar_arrive(&empty[s]);
       // epilogue: in-place stores straight from the accumulators
       const int kw = w.w1 - w.w0 + 1;
+#ifdef HQR_BENCH_NO_STORE  // benchmark-only knob (tools/gemm_bench.cu), never set in the product build
+      if (acc[0][0][0] != 12345.678) continue;
+#endif
       if (LEFT) {
         const int64_t c0 = w.w1 + 1 + tile * NT;
 #pragma unroll
@@ -557,7 +572,7 @@ __global__ void __launch_bounds__(kThreadsGeneric, 1) right_generic_kernel(StepA
 
 // ---- launchers -------------------------------------------------------------------------------
 template <int KP> constexpr size_t left_bulk_smem() {
-  return (size_t)(KP * pad_ld(KP) + 2 * left_cols(KP) * pad_ld(KP + 2)) * sizeof(double);
+  return (size_t)(KP * pad_ld(KP) + 2 * left_cols(KP) * pad_ld(KP)) * sizeof(double);
 }
 template <int KP> constexpr size_t right_bulk_smem() {
   return (size_t)(KP * pad_ld(KP) + 2 * KP * pad_ld(right_rows(KP))) * sizeof(double);
@@ -570,41 +585,79 @@ template <int KP> constexpr size_t right_generic_smem() {
 }
 
 template <typename K>
-cudaError_t launch_k(K kern, size_t smem, int threads, const StepArgs& a, int64_t items, int grid,
-                     cudaStream_t st, bool& configured) {
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+cudaError_t set_smem(K kern, size_t smem, bool& configured) {
+  if (configured) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e == cudaSuccess) configured = true;
+  return e;
+}
+
+template <int KP, bool LEFT>
+cudaError_t launch_t(const StepArgs& a, const TensorMaps& tm, int64_t items, int grid, cudaStream_t st) {
+  if (tm.valid) {
+    static bool c = false;
+    const size_t smem = LEFT ? left_bulk_smem<KP>() : right_bulk_smem<KP>();
+    cudaError_t e = set_smem(bulk_update_kernel<KP, LEFT>, smem, c);
     if (e != cudaSuccess) return e;
-    configured = true;
+    bulk_update_kernel<KP, LEFT><<<grid, kThreadsBulk, smem, st>>>(a, items, LEFT ? tm.left_H : tm.right_H,
+                                                                     tm.right_Z);
+    return cudaGetLastError();
   }
-  kern<<<grid, threads, smem, st>>>(a, items);
+  static bool c = false;
+  if (LEFT) {
+    cudaError_t e = set_smem(left_generic_kernel<KP>, left_generic_smem<KP>(), c);
+    if (e != cudaSuccess) return e;
+    left_generic_kernel<KP><<<grid, kThreadsGeneric, left_generic_smem<KP>(), st>>>(a, items);
+  } else {
+    cudaError_t e = set_smem(right_generic_kernel<KP>, right_generic_smem<KP>(), c);
+    if (e != cudaSuccess) return e;
+    right_generic_kernel<KP><<<grid, kThreadsGeneric, right_generic_smem<KP>(), st>>>(a, items);
+  }
   return cudaGetLastError();
 }
 
-template <int KP>
-cudaError_t launch_left_t(const StepArgs& a, int64_t items, int grid, cudaStream_t st) {
-  if ((a.n & 1) == 0) {
-    static bool c = false;
-    return launch_k(bulk_update_kernel<KP, true>, left_bulk_smem<KP>(), kThreadsBulk, a, items, grid, st, c);
-  }
-  static bool c = false;
-  return launch_k(left_generic_kernel<KP>, left_generic_smem<KP>(), kThreadsGeneric, a, items, grid, st, c);
-}
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
+                                  CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                  CUtensorMapFloatOOBfill);
 
-template <int KP>
-cudaError_t launch_right_t(const StepArgs& a, int64_t items, int grid, cudaStream_t st) {
-  if ((a.n & 1) == 0) {
-    static bool c = false;
-    return launch_k(bulk_update_kernel<KP, false>, right_bulk_smem<KP>(), kThreadsBulk, a, items, grid, st, c);
+cudaError_t encode_2d(CUtensorMap* m, const double* base, int64_t n, unsigned box_rows, unsigned box_cols) {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q);
+    if (e != cudaSuccess || q != cudaDriverEntryPointSuccess || !p) return cudaErrorNotSupported;
+    fn = reinterpret_cast<EncodeTiledFn>(p);
   }
-  static bool c = false;
-  return launch_k(right_generic_kernel<KP>, right_generic_smem<KP>(), kThreadsGeneric, a, items, grid, st, c);
+  cuuint64_t dims[2] = {(cuuint64_t)n, (cuuint64_t)n};
+  cuuint64_t strides[1] = {(cuuint64_t)n * sizeof(double)};
+  cuuint32_t box[2] = {box_rows, box_cols};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims, strides, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
 }  // namespace
 
-cudaError_t launch_left(const StepArgs& a, const WindowDesc* hw, int num_sms, cudaStream_t st,
-                        int64_t* items_out, double* flops, double* bytes) {
+cudaError_t make_tensor_maps(TensorMaps* tm, const double* H, const double* Z, int64_t n, int KP) {
+  tm->valid = false;
+  if ((n & 1) || n < 2 || n > (int64_t)1 << 31 || (reinterpret_cast<uintptr_t>(H) & 15) ||
+      (Z && (reinterpret_cast<uintptr_t>(Z) & 15)))
+    return cudaSuccess;  // generic (cp.async) path
+  cudaError_t e = encode_2d(&tm->left_H, H, n, pad_ld(KP), left_cols(KP));
+  if (e == cudaSuccess) e = encode_2d(&tm->right_H, H, n, pad_ld(right_rows(KP)), KP);
+  if (e == cudaSuccess) e = Z ? encode_2d(&tm->right_Z, Z, n, pad_ld(right_rows(KP)), KP)
+                              : encode_2d(&tm->right_Z, H, n, pad_ld(right_rows(KP)), KP);
+  if (e != cudaSuccess) return e;
+  tm->valid = true;
+  return cudaSuccess;
+}
+
+cudaError_t launch_left(const StepArgs& a, const WindowDesc* hw, int num_sms, const TensorMaps& tm,
+                        cudaStream_t st, int64_t* items_out, double* flops, double* bytes) {
   int64_t items = 0;
   double f = 0, b = 0;
   const int NT = left_cols(a.KP);
@@ -622,16 +675,16 @@ cudaError_t launch_left(const StepArgs& a, const WindowDesc* hw, int num_sms, cu
   if (a.win_count > kMaxStepWindows) return cudaErrorInvalidValue;
   int grid = (int)std::min<int64_t>(items, num_sms);
   switch (a.KP) {
-    case 32: return launch_left_t<32>(a, items, grid, st);
-    case 64: return launch_left_t<64>(a, items, grid, st);
-    case 96: return launch_left_t<96>(a, items, grid, st);
-    case 128: return launch_left_t<128>(a, items, grid, st);
+    case 32: return launch_t<32, true>(a, tm, items, grid, st);
+    case 64: return launch_t<64, true>(a, tm, items, grid, st);
+    case 96: return launch_t<96, true>(a, tm, items, grid, st);
+    case 128: return launch_t<128, true>(a, tm, items, grid, st);
   }
   return cudaErrorInvalidValue;
 }
 
-cudaError_t launch_right(const StepArgs& a, const WindowDesc* hw, int num_sms, cudaStream_t st,
-                         int64_t* items_out, double* flops, double* bytes) {
+cudaError_t launch_right(const StepArgs& a, const WindowDesc* hw, int num_sms, const TensorMaps& tm,
+                         cudaStream_t st, int64_t* items_out, double* flops, double* bytes) {
   int64_t items = 0;
   double f = 0, b = 0;
   const int MT = right_rows(a.KP);
@@ -651,10 +704,10 @@ cudaError_t launch_right(const StepArgs& a, const WindowDesc* hw, int num_sms, c
   if (a.win_count > kMaxStepWindows) return cudaErrorInvalidValue;
   int grid = (int)std::min<int64_t>(items, num_sms);
   switch (a.KP) {
-    case 32: return launch_right_t<32>(a, items, grid, st);
-    case 64: return launch_right_t<64>(a, items, grid, st);
-    case 96: return launch_right_t<96>(a, items, grid, st);
-    case 128: return launch_right_t<128>(a, items, grid, st);
+    case 32: return launch_t<32, false>(a, tm, items, grid, st);
+    case 64: return launch_t<64, false>(a, tm, items, grid, st);
+    case 96: return launch_t<96, false>(a, tm, items, grid, st);
+    case 128: return launch_t<128, false>(a, tm, items, grid, st);
   }
   return cudaErrorInvalidValue;
 }
