@@ -40,9 +40,11 @@ constexpr int kThreadsGeneric = 256;
 constexpr int kThreadsBulk = 288;  // 8 consumer warps + 1 producer warp
 constexpr int kMaxStepWindows = 128;
 
-// tile widths: 64 columns / rows, 32 when the 128-wide factor leaves too little SMEM for two panels
-__host__ __device__ constexpr int left_cols(int KP) { return KP <= 96 ? 64 : 32; }
-__host__ __device__ constexpr int right_rows(int KP) { return KP <= 96 ? 64 : 32; }
+// Panel tile widths and SMEM ring depth: the factor Q_W (KP x pad_ld(KP)) stays resident, the ring
+// holds kStagesOf(KP) panel tiles; KP = 96 uses 48-wide tiles so three stages fit next to Q_W.
+__host__ __device__ constexpr int left_cols(int KP) { return KP <= 64 ? 64 : KP == 96 ? 48 : 32; }
+__host__ __device__ constexpr int right_rows(int KP) { return KP <= 64 ? 64 : KP == 96 ? 48 : 32; }
+__host__ __device__ constexpr int stages_of(int KP) { return KP <= 96 ? 3 : 2; }
 
 __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -121,9 +123,11 @@ __device__ __forceinline__ int decode_item(const StepItems& si, int nw, int64_t 
 // zero padding of Q_W or land in output rows that are never stored.
 //   Items of window i: ceil(w0/MT) tiles of H rows [0, w0) (right_mode != 2), then ceil(n/MT) tiles
 //   of Z rows [0, n) (Z != nullptr and right_mode != 1).
-// Warp roles: warp 8 = producer (bulk copies), warps 0-3 = consumer group 0, warps 4-7 = group 1.
-// The groups ping-pong: group q computes the CTA's items j = q (mod 2) out of SMEM stage q, so one
-// group's epilogue (register -> HBM stores) overlaps the other group's DMMA main loop.  Inside a
+// Warp roles: warp 8 = producer (TMA), warps 0-3 = consumer group 0, warps 4-7 = group 1.
+// The groups ping-pong: group q computes the CTA's items j = q (mod 2) out of the SMEM ring
+// (item j in stage j mod NS, NS = 3 for KP <= 96), so one group's epilogue (register -> HBM
+// stores) overlaps the other group's DMMA main loop, and the next item of a group is already
+// loading while its previous one is multiplied.  Inside a
 // group, 2 x 2 warps tile the output; a warp's K loop stops at the Q_W structure bound, and the
 // two warps sharing an SM sub-partition (w, w+4) get complementary row (LEFT) / column (RIGHT)
 // groups so both DMMA pipes of a sub-partition pair see the same K extent on average.
@@ -139,12 +143,14 @@ __global__ void __launch_bounds__(kThreadsBulk, 1)
   constexpr int OM = LEFT ? KP : MT, ON = LEFT ? NT : KP;  // output tile
   constexpr int WM = OM / 2, WN = ON / 2;                  // warp tile (2 x 2 warps per group)
   constexpr int FM = WM / 8, FN = WN / 8;
+  constexpr int NS = stages_of(KP);
   static_assert(!LEFT || LDP >= KP + 1, "left panel box must hold the odd-row shift");
+  static_assert((STAGE * 8) % 128 == 0 && (KP * QLD * 8) % 128 == 0, "TMA destinations 128-byte aligned");
   extern __shared__ __align__(1024) double sm[];
   double* Qs = sm;                       // KP x QLD
-  double* Ps = Qs + KP * QLD;            // 2 stages (128-byte aligned: TMA destinations)
+  double* Ps = Qs + KP * QLD;            // NS stages (128-byte aligned: TMA destinations)
   __shared__ StepItems si;
-  __shared__ __align__(8) uint64_t full[2], empty[2], qfull, qempty;
+  __shared__ __align__(8) uint64_t full[NS], empty[NS], qfull, qempty;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t n = a.n;
@@ -163,14 +169,14 @@ __global__ void __launch_bounds__(kThreadsBulk, 1)
         si.pre[i + 1] = si.pre[i] + si.rt[i] + ztiles;
       }
     }
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < NS; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 4);
     }
     mbar_init(&qfull, 1);
     mbar_init(&qempty, kConsumerWarps);
   }
-  for (int i = tid; i < 2 * STAGE; i += kThreadsBulk) Ps[i] = 0.0;  // never-copied rows stay finite
+  for (int i = tid; i < NS * STAGE; i += kThreadsBulk) Ps[i] = 0.0;
   fence_proxy_async();
   __syncthreads();
 
@@ -205,8 +211,8 @@ __global__ void __launch_bounds__(kThreadsBulk, 1)
         ++nq;
       }
       const int64_t j = it - it0;
-      const int s = (int)(j & 1);
-      if (j >= 2) mbar_wait(&empty[s], (unsigned)((j >> 1) - 1) & 1);
+      const int s = (int)(j % NS);
+      if (j >= NS) mbar_wait(&empty[s], (unsigned)((j / NS) - 1) & 1);
       double* dst = Ps + s * STAGE;
       if (lane == 0) {
         mbar_arrive_tx(&full[s], (unsigned)(STAGE * 8));  // TMA always lands the full box
@@ -247,89 +253,101 @@ __global__ void __launch_bounds__(kThreadsBulk, 1)
       const int64_t j = it - it0;
       if ((int)(j & 1) != q) continue;
       const WindowDesc& w = si.w[wi];
-      const int s = q;
-      mbar_wait(&full[s], (unsigned)(j >> 1) & 1);
+      const int s = (int)(j % NS);
+      mbar_wait(&full[s], (unsigned)(j / NS) & 1);
       // Q_W[k][c] = 0 for k > c + 2 nbc: K stops after this warp's last row (LEFT) / column (RIGHT)
 #ifdef HQR_BENCH_NO_TRIM  // benchmark-only knob (tools/gemm_bench.cu), never set in the product build
       const int kend = KP;
 #else
       const int kend = min(KP, ((LEFT ? wm0 + WM : wn0 + WN) + 2 * w.nbc + 3) & ~3);
 #endif
-      double acc[FM][FN][2];
+      // accumulators hold the TRANSPOSED output blocks (mma with the operands swapped), so each
+      // thread owns two consecutive output ROWS of one column: 16-byte stores into column-major
+      double acc[FN][FM][2];
 #pragma unroll
-      for (int i = 0; i < FM; ++i)
+      for (int jn = 0; jn < FN; ++jn)
 #pragma unroll
-        for (int jn = 0; jn < FN; ++jn) acc[i][jn][0] = acc[i][jn][1] = 0.0;
+        for (int i = 0; i < FM; ++i) acc[jn][i][0] = acc[jn][i][1] = 0.0;
       const double* P = Ps + s * STAGE;
+      // fragment sources: fa = M-side (rows of out), fb = N-side (columns of out)
+      const double* A;
+      const double* B;
+      int a_i, a_k, b_j, b_k;  // strides of fragment i / k-step for A, fragment j / k-step for B
       if (LEFT) {
-        const double* A = Qs + (wm0 + lr) * QLD + lk;
-        const double* B = P + (wn0 + lr) * LDP + (w.w0 & 1) + lk;
-#pragma unroll 2
-        for (int kk = 0; kk < kend; kk += 4) {
-          double fa[FM], fb[FN];
-#pragma unroll
-          for (int i = 0; i < FM; ++i) fa[i] = A[8 * i * QLD + kk];
-#pragma unroll
-          for (int jn = 0; jn < FN; ++jn) fb[jn] = B[8 * jn * LDP + kk];
-#pragma unroll
-          for (int i = 0; i < FM; ++i)
-#pragma unroll
-            for (int jn = 0; jn < FN; ++jn) dmma(acc[i][jn], fa[i], fb[jn]);
-        }
+        A = Qs + (wm0 + lr) * QLD + lk;                    a_i = 8 * QLD; a_k = 1;
+        B = P + (wn0 + lr) * LDP + (w.w0 & 1) + lk;        b_j = 8 * LDP; b_k = 1;
       } else {
-        const double* A = P + lk * LDP + wm0 + lr;
-        const double* B = Qs + (wn0 + lr) * QLD + lk;
-#pragma unroll 2
-        for (int kk = 0; kk < kend; kk += 4) {
-          double fa[FM], fb[FN];
+        A = P + lk * LDP + wm0 + lr;                       a_i = 8;       a_k = LDP;
+        B = Qs + (wn0 + lr) * QLD + lk;                    b_j = 8 * QLD; b_k = 1;
+      }
+      // software-pipelined K loop: fragments of k-step t+1 are loaded before the mma of step t
+      double fa[2][FM], fb[2][FN];
 #pragma unroll
-          for (int i = 0; i < FM; ++i) fa[i] = A[kk * LDP + 8 * i];
+      for (int i = 0; i < FM; ++i) fa[0][i] = A[i * a_i];
 #pragma unroll
-          for (int jn = 0; jn < FN; ++jn) fb[jn] = B[8 * jn * QLD + kk];
+      for (int jn = 0; jn < FN; ++jn) fb[0][jn] = B[jn * b_j];
+      for (int kk = 0; kk < kend; kk += 8) {
 #pragma unroll
-          for (int i = 0; i < FM; ++i)
+        for (int h = 0; h < 2; ++h) {
+          const int kn = kk + 4 * (h + 1);
+          if (kn - 4 >= kend) break;
+          if (kn < kend) {
 #pragma unroll
-            for (int jn = 0; jn < FN; ++jn) dmma(acc[i][jn], fa[i], fb[jn]);
+            for (int i = 0; i < FM; ++i) fa[h ^ 1][i] = A[i * a_i + kn * a_k];
+#pragma unroll
+            for (int jn = 0; jn < FN; ++jn) fb[h ^ 1][jn] = B[jn * b_j + kn * b_k];
+          }
+#pragma unroll
+          for (int jn = 0; jn < FN; ++jn)
+#pragma unroll
+            for (int i = 0; i < FM; ++i) dmma(acc[jn][i], fb[h][jn], fa[h][i]);
         }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
-      // epilogue: in-place stores straight from the accumulators
+      // epilogue: in-place stores straight from the accumulators; thread (lr, lk) owns
+      // out[m = m0 + 8i + 2lk + {0,1}][n = n0 + 8jn + lr]
       const int kw = w.w1 - w.w0 + 1;
 #ifdef HQR_BENCH_NO_STORE  // benchmark-only knob (tools/gemm_bench.cu), never set in the product build
       if (acc[0][0][0] != 12345.678) continue;
 #endif
       if (LEFT) {
         const int64_t c0 = w.w1 + 1 + tile * NT;
+        const bool even = (w.w0 & 1) == 0;
 #pragma unroll
-        for (int i = 0; i < FM; ++i) {
-          const int m = wm0 + 8 * i + lr;
-          if (m >= kw) continue;
-          double* row = a.H + (w.w0 + m);
+        for (int jn = 0; jn < FN; ++jn) {
+          const int64_t col = c0 + wn0 + 8 * jn + lr;
+          if (col >= n) continue;
+          double* cp = a.H + col * n + w.w0;
 #pragma unroll
-          for (int jn = 0; jn < FN; ++jn)
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-              const int64_t col = c0 + wn0 + 8 * jn + 2 * lk + e;
-              if (col < n) row[col * n] = acc[i][jn][e];
+          for (int i = 0; i < FM; ++i) {
+            const int m = wm0 + 8 * i + 2 * lk;
+            if (even && m + 1 < kw) {
+              *reinterpret_cast<double2*>(cp + m) = make_double2(acc[jn][i][0], acc[jn][i][1]);
+            } else {
+              if (m < kw) cp[m] = acc[jn][i][0];
+              if (m + 1 < kw) cp[m + 1] = acc[jn][i][1];
             }
+          }
         }
       } else {
         double* M;
         int64_t r0, r1;
         panel(wi, tile, M, r0, r1);
 #pragma unroll
-        for (int i = 0; i < FM; ++i) {
-          const int64_t row = r0 + wm0 + 8 * i + lr;
-          if (row >= r1) continue;
-          double* mr = M + row + (int64_t)w.w0 * n;
+        for (int jn = 0; jn < FN; ++jn) {
+          const int col = wn0 + 8 * jn + lr;
+          if (col >= kw) continue;
+          double* cp = M + (int64_t)(w.w0 + col) * n;
 #pragma unroll
-          for (int jn = 0; jn < FN; ++jn)
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-              const int col = wn0 + 8 * jn + 2 * lk + e;
-              if (col < kw) mr[col * n] = acc[i][jn][e];
+          for (int i = 0; i < FM; ++i) {
+            const int64_t row = r0 + wm0 + 8 * i + 2 * lk;  // even: 16-byte aligned pair
+            if (row + 1 < r1) {
+              *reinterpret_cast<double2*>(cp + row) = make_double2(acc[jn][i][0], acc[jn][i][1]);
+            } else if (row < r1) {
+              cp[row] = acc[jn][i][0];
             }
+          }
         }
       }
     }
@@ -572,10 +590,10 @@ __global__ void __launch_bounds__(kThreadsGeneric, 1) right_generic_kernel(StepA
 
 // ---- launchers -------------------------------------------------------------------------------
 template <int KP> constexpr size_t left_bulk_smem() {
-  return (size_t)(KP * pad_ld(KP) + 2 * left_cols(KP) * pad_ld(KP)) * sizeof(double);
+  return (size_t)(KP * pad_ld(KP) + stages_of(KP) * left_cols(KP) * pad_ld(KP)) * sizeof(double);
 }
 template <int KP> constexpr size_t right_bulk_smem() {
-  return (size_t)(KP * pad_ld(KP) + 2 * KP * pad_ld(right_rows(KP))) * sizeof(double);
+  return (size_t)(KP * pad_ld(KP) + stages_of(KP) * KP * pad_ld(right_rows(KP))) * sizeof(double);
 }
 template <int KP> constexpr size_t left_generic_smem() {
   return (size_t)(KP * pad_ld(KP) + 2 * left_cols(KP) * pad_ld(KP)) * sizeof(double);

@@ -27,6 +27,37 @@ __global__ void dmma_loop(double* out, int iters, double seed) {
   if (s == 12345.678) out[threadIdx.x] = s;  // keep live
 }
 
+// FM x FN outer-product tile with distinct A/B fragment registers (like the GEMM main loop),
+// operands perturbed every iteration so they stay live
+template <int FM, int FN>
+__global__ void dmma_tile_loop(double* out, int iters, double seed) {
+  double a[FM], b[FN];
+  double c[FM][FN][2];
+#pragma unroll
+  for (int i = 0; i < FM; ++i) a[i] = seed + i + threadIdx.x * 1e-3;
+#pragma unroll
+  for (int j = 0; j < FN; ++j) b[j] = seed - j;
+#pragma unroll
+  for (int i = 0; i < FM; ++i)
+#pragma unroll
+    for (int j = 0; j < FN; ++j) c[i][j][0] = c[i][j][1] = 0.0;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < FM; ++i)
+#pragma unroll
+      for (int j = 0; j < FN; ++j)
+        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                     : "+d"(c[i][j][0]), "+d"(c[i][j][1]) : "d"(a[i]), "d"(b[j]));
+    a[it % FM] = a[(it + 1) % FM];  // keep operands live without extra FP64 work
+  }
+  double s = 0;
+#pragma unroll
+  for (int i = 0; i < FM; ++i)
+#pragma unroll
+    for (int j = 0; j < FN; ++j) s += c[i][j][0] + c[i][j][1];
+  if (s == 12345.678) out[threadIdx.x] = s;
+}
+
 template <int NACC>
 __global__ void dfma_loop(double* out, int iters, double seed) {
   double a = seed + threadIdx.x * 1e-3, b = 1.0 - 1e-9 * threadIdx.x;
@@ -95,6 +126,24 @@ int main(int argc, char** argv) {
     double tf = flop / (ms * 1e-3) / 1e12;
     printf(", \"dmma_w%d_tflops\": %.3f", w, tf);
     if (tf > best_dmma) best_dmma = tf;
+  }
+  {
+    int ws[] = {4, 8, 12, 16};
+    for (int w : ws) {
+      int block = 32 * w, grid = sms;
+      double ms = time_kernel(dmma_tile_loop<3, 6>, grid, block, 1024, out, 5);
+      double flop = (double)grid * w * 1024 * 18 * 512.0;
+      printf(", \"dmma_tile3x6_w%d_tflops\": %.3f", w, flop / (ms * 1e-3) / 1e12);
+      ms = time_kernel(dmma_tile_loop<6, 4>, grid, block, 1024, out, 5);
+      flop = (double)grid * w * 1024 * 24 * 512.0;
+      printf(", \"dmma_tile6x4_w%d_tflops\": %.3f", w, flop / (ms * 1e-3) / 1e12);
+      ms = time_kernel(dmma_tile_loop<3, 3>, grid, block, 1024, out, 5);
+      flop = (double)grid * w * 1024 * 9 * 512.0;
+      printf(", \"dmma_tile3x3_w%d_tflops\": %.3f", w, flop / (ms * 1e-3) / 1e12);
+      ms = time_kernel(dmma_tile_loop<4, 4>, grid, block, 1024, out, 5);
+      flop = (double)grid * w * 1024 * 16 * 512.0;
+      printf(", \"dmma_tile4x4_w%d_tflops\": %.3f", w, flop / (ms * 1e-3) / 1e12);
+    }
   }
   double best_dfma = 0;
   for (int w : warps_list) {
