@@ -80,6 +80,19 @@ int hqr_setup(const hqr_config* cfg);
 int hqr_sweep(double* H, double* Z, int64_t n, int64_t ilo, int64_t ihi, const double* shifts_re,
               const double* shifts_im, int nshifts, int window);
 
+/*
+ * One sweep over several decoupled active blocks at once (concurrent processing
+ * of independent unreduced blocks; BASELINE configs[4]).  Block i is [ilo[i], ihi[i]] with
+ * nshifts[i] shifts, taken consecutively from shifts_re / shifts_im (block 0 first).  Blocks must be
+ * ascending and disjoint (ihi[i] < ilo[i+1]) and each decoupled from its neighbours.  The result
+ * equals sweeping the blocks one after another (their similarities commute); all blocks' windows
+ * share each wavefront step.  Codes as hqr_sweep, with -4 also for nblocks < 1, NULL block arrays,
+ * or overlapping / unsorted blocks.
+ */
+int hqr_sweep_multi(double* H, double* Z, int64_t n, int nblocks, const int64_t* ilo,
+                    const int64_t* ihi, const double* shifts_re, const double* shifts_im,
+                    const int* nshifts, int window);
+
 /* Release everything hqr_setup acquired.  Returns 0 (also when not set up) or 1000+cudaError_t. */
 int hqr_teardown(void);
 
@@ -91,12 +104,16 @@ int hqr_teardown(void);
 /*
  * Host-only introspection of the wavefront plan (no GPU needed; used by the tests).
  *   info[0..9] <- {k_eff, nbc_max, s, lag, nchains, nsteps, nwindows, max_kw, max_nbc, nb}
- *   windows    <- nwindows rows of 10 int32 {step, chain, w0, w1, t0, t1, b0, nbc, slot, last}
+ *   windows    <- nwindows rows of 12 int32
+ *                 {step, chain, w0, w1, t0, t1, b0, nbc, slot, last, ilo, ihi}
  *                 (may be NULL or cap too small: only info is written then)
  * Returns 0 or the same negative argument codes as hqr_sweep (matrix values are not inspected).
  */
 int hqr_plan_query(int64_t n, int64_t ilo, int64_t ihi, int nshifts, int window, int32_t* info,
                    int32_t* windows, int64_t cap);
+int hqr_plan_query_multi(int64_t n, int nblocks, const int64_t* ilo, const int64_t* ihi,
+                         const int* nshifts, int window, int32_t* info, int32_t* windows,
+                         int64_t cap);
 
 /* Statistics of the last successful hqr_sweep on this process. */
 typedef struct hqr_stats {

@@ -62,8 +62,8 @@ class Stats(ctypes.Structure):
         return {k: getattr(self, k) for k, _ in self._fields_}
 
 
-SYMBOLS = ["hqr_setup", "hqr_sweep", "hqr_teardown", "hqr_plan_query", "hqr_get_stats",
-           "hqr_error_string"]
+SYMBOLS = ["hqr_setup", "hqr_sweep", "hqr_sweep_multi", "hqr_teardown", "hqr_plan_query",
+           "hqr_plan_query_multi", "hqr_get_stats", "hqr_error_string"]
 
 
 def lib():
@@ -80,6 +80,14 @@ def lib():
                                 ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int,
                                 ctypes.c_int]
         L.hqr_sweep.restype = ctypes.c_int
+        L.hqr_sweep_multi.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int,
+                                      ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                      ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int]
+        L.hqr_sweep_multi.restype = ctypes.c_int
+        L.hqr_plan_query_multi.argtypes = [ctypes.c_int64, ctypes.c_int, ctypes.c_void_p,
+                                           ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int,
+                                           ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64]
+        L.hqr_plan_query_multi.restype = ctypes.c_int
         L.hqr_teardown.argtypes = []
         L.hqr_teardown.restype = ctypes.c_int
         L.hqr_plan_query.argtypes = [ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int,
@@ -146,22 +154,54 @@ def sweep(H, Z, ilo: int, ihi: int, shifts_re, shifts_im, window: int = DEFAULT_
         raise HQRError(rc, "hqr_sweep")
 
 
+def sweep_multi(H, Z, blocks, shifts_re, shifts_im, window: int = DEFAULT_WINDOW) -> None:
+    """One sweep over several decoupled active blocks: blocks = [(ilo, ihi, nshifts), ...]
+    (ascending, disjoint); shifts of block i follow those of blocks 0..i-1 (hqr_sweep_multi)."""
+    hp, n = _ptr_n(H)
+    zp, nz = _ptr_n(Z)
+    if hp is None:
+        raise HQRError(-1, "hqr_sweep_multi")
+    if zp is not None and nz != n:
+        raise ValueError("H and Z must have the same order")
+    ilo = np.array([b[0] for b in blocks], dtype=np.int64)
+    ihi = np.array([b[1] for b in blocks], dtype=np.int64)
+    ns = np.array([b[2] for b in blocks], dtype=np.int32)
+    sr = np.ascontiguousarray(shifts_re, dtype=np.float64)
+    si = np.ascontiguousarray(shifts_im, dtype=np.float64)
+    if sr.shape != si.shape or sr.shape[0] != int(ns.sum()):
+        raise ValueError("shift arrays must hold sum(nshifts) entries")
+    rc = lib().hqr_sweep_multi(hp, zp, n, len(blocks), ilo.ctypes.data, ihi.ctypes.data,
+                               sr.ctypes.data, si.ctypes.data, ns.ctypes.data, int(window))
+    if rc:
+        raise HQRError(rc, "hqr_sweep_multi")
+
+
 def sweep_raw(H_ptr, Z_ptr, n, ilo, ihi, sr_ptr, si_ptr, nshifts, window) -> int:
     """Direct ABI call (tests of the error codes); returns the C return code."""
     return lib().hqr_sweep(H_ptr, Z_ptr, n, ilo, ihi, sr_ptr, si_ptr, nshifts, window)
 
 
 def plan_query(n: int, ilo: int, ihi: int, nshifts: int, window: int):
-    """Host-only plan introspection: (info dict, windows int32 array [nw, 10]) or raises."""
+    """Host-only plan introspection: (info dict, windows int32 array [nw, 12]) or raises.
+    Window columns: step, chain, w0, w1, t0, t1, b0, nbc, slot, last, ilo, ihi."""
+    return plan_query_multi(n, [(ilo, ihi, nshifts)], window)
+
+
+def plan_query_multi(n: int, blocks, window: int):
+    """plan_query for several decoupled active blocks [(ilo, ihi, nshifts), ...]."""
+    ilo = np.array([b[0] for b in blocks], dtype=np.int64)
+    ihi = np.array([b[1] for b in blocks], dtype=np.int64)
+    ns = np.array([b[2] for b in blocks], dtype=np.int32)
     info = np.zeros(10, dtype=np.int32)
-    rc = lib().hqr_plan_query(n, ilo, ihi, nshifts, window, info.ctypes.data, None, 0)
+    args = (n, len(blocks), ilo.ctypes.data, ihi.ctypes.data, ns.ctypes.data, window)
+    rc = lib().hqr_plan_query_multi(*args, info.ctypes.data, None, 0)
     if rc:
-        raise HQRError(rc, "hqr_plan_query")
+        raise HQRError(rc, "hqr_plan_query_multi")
     nw = int(info[6])
-    wins = np.zeros((nw, 10), dtype=np.int32)
-    rc = lib().hqr_plan_query(n, ilo, ihi, nshifts, window, info.ctypes.data, wins.ctypes.data, nw)
+    wins = np.zeros((nw, 12), dtype=np.int32)
+    rc = lib().hqr_plan_query_multi(*args, info.ctypes.data, wins.ctypes.data, nw)
     if rc:
-        raise HQRError(rc, "hqr_plan_query")
+        raise HQRError(rc, "hqr_plan_query_multi")
     keys = ["k", "nbc_max", "s", "lag", "nchains", "nsteps", "nwindows", "max_kw", "max_nbc", "nb"]
     return dict(zip(keys, (int(v) for v in info))), wins
 

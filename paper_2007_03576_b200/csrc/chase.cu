@@ -71,11 +71,11 @@ __global__ void __launch_bounds__(kChaseThreads, 1) chase_kernel(StepArgs a) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t n = a.n;
   const int w0 = W.w0;
-  const int ilo = (int)a.ilo, ihi = (int)a.ihi;
+  const int ilo = W.ilo, ihi = W.ihi;  // the active block of this window's chain
 
   // load the window (coalesced along columns), Q_W = I
   {
-    const double* g = a.H + (int64_t)w0 * n + w0;
+    const double* g = a.H + (int64_t)(w0 - a.hcol0) * n + w0;
     for (int c = warp; c < kw; c += kChaseWarps) {
       const double* gc = g + (int64_t)c * n;
       for (int r = lane; r < kw; r += 32) {
@@ -186,7 +186,7 @@ __global__ void __launch_bounds__(kChaseThreads, 1) chase_kernel(StepArgs a) {
   // write back the window; store Q_W column-major with ld = QLD (= the update kernels' SMEM
   // layout), zero padded to KP x QLD
   {
-    double* g = a.H + (int64_t)w0 * n + w0;
+    double* g = a.H + (int64_t)(w0 - a.hcol0) * n + w0;
     for (int c = warp; c < kw; c += kChaseWarps) {
       double* gc = g + (int64_t)c * n;
       for (int r = lane; r < kw; r += 32) gc[r] = Hs[r + c * ldh];

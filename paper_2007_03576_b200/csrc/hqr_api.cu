@@ -30,16 +30,27 @@ using hqr::WindowDesc;
 
 namespace {
 
-struct PlanKey {
-  int64_t n, ilo, ihi;
-  int nshifts, window;
-  bool operator<(const PlanKey& o) const {
-    return std::tie(n, ilo, ihi, nshifts, window) < std::tie(o.n, o.ilo, o.ihi, o.nshifts, o.window);
-  }
+// (n, window, then ilo, ihi, nshifts of every block)
+typedef std::vector<int64_t> PlanKey;
+
+struct Blocks {
+  std::vector<int64_t> ilo, ihi;
+  std::vector<int> nshifts;
+  int count() const { return (int)ilo.size(); }
 };
 
+PlanKey plan_key(int64_t n, const Blocks& b, int window) {
+  PlanKey k{n, window};
+  for (int i = 0; i < b.count(); ++i) {
+    k.push_back(b.ilo[i]);
+    k.push_back(b.ihi[i]);
+    k.push_back(b.nshifts[i]);
+  }
+  return k;
+}
+
 struct GraphKey {
-  PlanKey pk;
+  PlanKey pk;   // plan key
   const double* H;
   const double* Z;
   bool operator<(const GraphKey& o) const {
@@ -88,10 +99,9 @@ int cuerr(cudaError_t e) { return e == cudaSuccess ? 0 : 1000 + (int)e; }
     if (e_ != cudaSuccess) return cuerr(e_);    \
   } while (0)
 
-// a1: argument validation that does not touch matrix values (shared by hqr_sweep / plan query)
-int validate_scalars(int64_t n, int64_t ilo, int64_t ihi, const double* sr, const double* si,
-                     int nshifts, int window, bool check_shifts) {
-  if (n < 1) return -3;
+// a1: argument validation that does not touch matrix values (shared by the sweeps / plan queries)
+int validate_block(int64_t n, int64_t ilo, int64_t ihi, const double* sr, const double* si,
+                   int nshifts, bool check_shifts) {
   if (ilo < 0 || ilo > ihi) return -4;
   if (ihi >= n || ihi - ilo + 1 < 3) return -5;
   const int64_t N = ihi - ilo + 1;
@@ -108,17 +118,32 @@ int validate_scalars(int64_t n, int64_t ilo, int64_t ihi, const double* sr, cons
       if (!real_pair && !conj_pair) return -7;
     }
   }
+  return 0;
+}
+
+int validate_blocks(int64_t n, const Blocks& b, const double* sr, const double* si, int window,
+                    bool check_shifts) {
+  if (n < 1) return -3;
+  if (b.count() < 1) return -4;
+  int64_t off = 0;
+  for (int i = 0; i < b.count(); ++i) {
+    if (i > 0 && b.ilo[i] <= b.ihi[i - 1]) return -4;  // ascending, disjoint
+    int rc = validate_block(n, b.ilo[i], b.ihi[i], sr ? sr + off : nullptr, si ? si + off : nullptr,
+                            b.nshifts[i], check_shifts);
+    if (rc) return rc;
+    off += b.nshifts[i];
+  }
   if (window <= 0) return -9;
   return 0;
 }
 
-int get_plan(int64_t n, int64_t ilo, int64_t ihi, int nshifts, int window, CachedPlan** out,
-             bool upload) {
-  PlanKey key{n, ilo, ihi, nshifts, window};
+int get_plan(int64_t n, const Blocks& b, int window, CachedPlan** out, bool upload) {
+  PlanKey key = plan_key(n, b, window);
   auto it = g.plans.find(key);
   if (it == g.plans.end()) {
     auto cp = std::make_unique<CachedPlan>();
-    int rc = hqr::make_plan(n, ilo, ihi, nshifts, window, hqr::kMaxWindow, &cp->plan);
+    int rc = hqr::make_plan_multi(n, b.count(), b.ilo.data(), b.ihi.data(), b.nshifts.data(), window,
+                                  hqr::kMaxWindow, &cp->plan);
     if (rc) return rc;
     cp->KP = hqr::padded_kp(cp->plan.max_kw);
     it = g.plans.emplace(key, std::move(cp)).first;
@@ -173,6 +198,7 @@ int enqueue_sweep(const CachedPlan& cp, double* H, double* Z, int64_t n, bool pr
   cudaStream_t A = g.stream, B = split ? g.zstream : g.stream;
   StepArgs a{};
   a.H = H; a.Z = Z; a.n = n; a.ilo = P.ilo; a.ihi = P.ihi;
+  a.hcol0 = 0; a.lc0 = 0; a.lc1 = n; a.zrows = n; a.ldz = n;
   a.wins = cp.d_wins; a.coef = g.d_coef; a.qslots = g.d_q; a.KP = cp.KP;
   a.QLD = hqr::pad_ld(cp.KP);
   size_t ev = 0;
@@ -187,7 +213,7 @@ int enqueue_sweep(const CachedPlan& cp, double* H, double* Z, int64_t n, bool pr
     if (classes) classes->push_back(cls);
   };
   hqr::TensorMaps tm;
-  CK(hqr::make_tensor_maps(&tm, H, Z, n, cp.KP));
+  CK(hqr::make_tensor_maps(&tm, H, n, Z, n, n, n, cp.KP));
   if (dbg_sync) {
     const unsigned long long* q = reinterpret_cast<const unsigned long long*>(&tm.left_H);
     fprintf(stderr, "hqr: tensor maps valid=%d KP=%d H=%p map@%p %llx %llx %llx\n", (int)tm.valid, cp.KP,
@@ -318,20 +344,25 @@ int hqr_teardown(void) {
   return cuerr(e);
 }
 
-int hqr_sweep(double* H, double* Z, int64_t n, int64_t ilo, int64_t ihi, const double* shifts_re,
-              const double* shifts_im, int nshifts, int window) {
+}  // extern "C"
+
+namespace {
+
+int sweep_impl(double* H, double* Z, int64_t n, const Blocks& blocks, const double* shifts_re,
+               const double* shifts_im, int window) {
   if (!H) return -1;
-  int rc = validate_scalars(n, ilo, ihi, shifts_re, shifts_im, nshifts, window, true);
+  int rc = validate_blocks(n, blocks, shifts_re, shifts_im, window, true);
   if (rc) return rc;
   {  // a7 plan (host only; validates the window)
     Plan tmp;
-    rc = hqr::make_plan(n, ilo, ihi, nshifts, window, hqr::kMaxWindow, &tmp);
+    rc = hqr::make_plan_multi(n, blocks.count(), blocks.ilo.data(), blocks.ihi.data(),
+                              blocks.nshifts.data(), window, hqr::kMaxWindow, &tmp);
     if (rc) return rc;
   }
   if (!g.ready) return -100;
   CK(cudaSetDevice(g.device));
   CachedPlan* cp = nullptr;
-  rc = get_plan(n, ilo, ihi, nshifts, window, &cp, true);
+  rc = get_plan(n, blocks, window, &cp, true);
   if (rc) return rc;
 
   hqr_stats st{};
@@ -339,23 +370,26 @@ int hqr_sweep(double* H, double* Z, int64_t n, int64_t ilo, int64_t ihi, const d
   const bool h_dev = is_device_ptr(H);
   const bool z_dev = Z ? is_device_ptr(Z) : true;
 
-  // decoupling check (-10): two scalars
-  double sub[2] = {0.0, 0.0};
-  if (ilo > 0 || ihi < n - 1) {
-    const double* p0 = H + ilo + (ilo - 1) * n;
-    const double* p1 = H + (ihi + 1) + ihi * n;
-    if (h_dev) {
-      if (ilo > 0) CK(cudaMemcpy(&sub[0], p0, sizeof(double), cudaMemcpyDeviceToHost));
-      if (ihi < n - 1) CK(cudaMemcpy(&sub[1], p1, sizeof(double), cudaMemcpyDeviceToHost));
-    } else {
-      if (ilo > 0) sub[0] = *p0;
-      if (ihi < n - 1) sub[1] = *p1;
+  // decoupling check (-10): two scalars per block
+  for (int i = 0; i < blocks.count(); ++i) {
+    const int64_t ilo = blocks.ilo[i], ihi = blocks.ihi[i];
+    double sub[2] = {0.0, 0.0};
+    if (ilo > 0 || ihi < n - 1) {
+      const double* p0 = H + ilo + (ilo - 1) * n;
+      const double* p1 = H + (ihi + 1) + ihi * n;
+      if (h_dev) {
+        if (ilo > 0) CK(cudaMemcpy(&sub[0], p0, sizeof(double), cudaMemcpyDeviceToHost));
+        if (ihi < n - 1) CK(cudaMemcpy(&sub[1], p1, sizeof(double), cudaMemcpyDeviceToHost));
+      } else {
+        if (ilo > 0) sub[0] = *p0;
+        if (ihi < n - 1) sub[1] = *p1;
+      }
+      if (sub[0] != 0.0 || sub[1] != 0.0) return -10;
     }
-    if (sub[0] != 0.0 || sub[1] != 0.0) return -10;
   }
 
-  // a1 pair the shifts: sigma = s + s', pi = s s' (real form, reading R1/R3)
-  const int nb = nshifts / 2;
+  // a1 pair the shifts: sigma = s + s', pi = s s' (real form, reading R1/R3); bulges of all blocks
+  const int nb = cp->plan.nb;
   std::vector<double> coef(2 * nb);
   for (int j = 0; j < nb; ++j) {
     coef[2 * j] = shifts_re[2 * j] + shifts_re[2 * j + 1];
@@ -400,7 +434,7 @@ int hqr_sweep(double* H, double* Z, int64_t n, int64_t ilo, int64_t ihi, const d
   const bool use_graph = !prof && !(g.flags & HQR_FLAG_NO_GRAPH);
   std::vector<int> classes;
   if (use_graph) {
-    GraphKey gk{{n, ilo, ihi, nshifts, window}, dH, dZ};
+    GraphKey gk{plan_key(n, blocks, window), dH, dZ};
     auto it = g.graphs.find(gk);
     if (it == g.graphs.end()) {
       cudaGraph_t graph;
@@ -476,12 +510,13 @@ int hqr_sweep(double* H, double* Z, int64_t n, int64_t ilo, int64_t ihi, const d
   return 0;
 }
 
-int hqr_plan_query(int64_t n, int64_t ilo, int64_t ihi, int nshifts, int window, int32_t* info,
-                   int32_t* windows, int64_t cap) {
-  int rc = validate_scalars(n, ilo, ihi, nullptr, nullptr, nshifts, window, false);
+int plan_query_impl(int64_t n, const Blocks& b, int window, int32_t* info, int32_t* windows,
+                    int64_t cap) {
+  int rc = validate_blocks(n, b, nullptr, nullptr, window, false);
   if (rc) return rc;
   Plan P;
-  rc = hqr::make_plan(n, ilo, ihi, nshifts, window, hqr::kMaxWindow, &P);
+  rc = hqr::make_plan_multi(n, b.count(), b.ilo.data(), b.ihi.data(), b.nshifts.data(), window,
+                            hqr::kMaxWindow, &P);
   if (rc) return rc;
   if (info) {
     int32_t v[10] = {P.k, P.nbc_max, P.s, P.lag, P.nchains, P.nsteps, (int32_t)P.windows.size(),
@@ -492,12 +527,51 @@ int hqr_plan_query(int64_t n, int64_t ilo, int64_t ihi, int nshifts, int window,
     for (int s = 0; s < P.nsteps; ++s)
       for (int i = P.step_begin[s]; i < P.step_begin[s + 1]; ++i) {
         const WindowDesc& w = P.windows[i];
-        int32_t* r = windows + 10 * (int64_t)i;
+        int32_t* r = windows + 12 * (int64_t)i;
         r[0] = s; r[1] = w.chain; r[2] = w.w0; r[3] = w.w1; r[4] = w.t0; r[5] = w.t1;
-        r[6] = w.b0; r[7] = w.nbc; r[8] = w.slot; r[9] = w.last;
+        r[6] = w.b0; r[7] = w.nbc; r[8] = w.slot; r[9] = w.last; r[10] = w.ilo; r[11] = w.ihi;
       }
   }
   return 0;
+}
+
+Blocks make_blocks(int nblocks, const int64_t* ilo, const int64_t* ihi, const int* nshifts) {
+  Blocks b;
+  for (int i = 0; i < nblocks; ++i) {
+    b.ilo.push_back(ilo[i]);
+    b.ihi.push_back(ihi[i]);
+    b.nshifts.push_back(nshifts[i]);
+  }
+  return b;
+}
+
+}  // namespace
+
+extern "C" {
+
+int hqr_sweep(double* H, double* Z, int64_t n, int64_t ilo, int64_t ihi, const double* shifts_re,
+              const double* shifts_im, int nshifts, int window) {
+  return sweep_impl(H, Z, n, make_blocks(1, &ilo, &ihi, &nshifts), shifts_re, shifts_im, window);
+}
+
+int hqr_sweep_multi(double* H, double* Z, int64_t n, int nblocks, const int64_t* ilo,
+                    const int64_t* ihi, const double* shifts_re, const double* shifts_im,
+                    const int* nshifts, int window) {
+  if (!H) return -1;
+  if (nblocks < 1 || !ilo || !ihi || !nshifts) return -4;
+  return sweep_impl(H, Z, n, make_blocks(nblocks, ilo, ihi, nshifts), shifts_re, shifts_im, window);
+}
+
+int hqr_plan_query(int64_t n, int64_t ilo, int64_t ihi, int nshifts, int window, int32_t* info,
+                   int32_t* windows, int64_t cap) {
+  return plan_query_impl(n, make_blocks(1, &ilo, &ihi, &nshifts), window, info, windows, cap);
+}
+
+int hqr_plan_query_multi(int64_t n, int nblocks, const int64_t* ilo, const int64_t* ihi,
+                         const int* nshifts, int window, int32_t* info, int32_t* windows,
+                         int64_t cap) {
+  if (nblocks < 1 || !ilo || !ihi || !nshifts) return -4;
+  return plan_query_impl(n, make_blocks(nblocks, ilo, ihi, nshifts), window, info, windows, cap);
 }
 
 int hqr_get_stats(hqr_stats* out) {

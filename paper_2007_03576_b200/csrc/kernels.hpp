@@ -11,9 +11,12 @@ namespace hqr {
 
 // Arguments of one wavefront step (device pointers).
 struct StepArgs {
-  double* H;                 // n x n column-major, ld = n
-  double* Z;                 // n x n column-major or nullptr
+  double* H;                 // this rank's H columns: global column j at H + (j - hcol0) * n (ld = n)
+  double* Z;                 // this rank's Z rows [0, zrows) x n columns, ld = ldz; or nullptr
   int64_t n;
+  int64_t hcol0;             // global index of local H column 0
+  int64_t lc0, lc1;          // left update: global columns [lc0, lc1) held (and updated) here
+  int64_t zrows, ldz;        // local Z rows and leading dimension
   int64_t ilo, ihi;
   const WindowDesc* wins;    // device copy of plan.windows
   int win_begin, win_count;  // this step's windows
@@ -37,7 +40,9 @@ struct TensorMaps {
   CUtensorMap right_Z;
   bool valid = false;
 };
-cudaError_t make_tensor_maps(TensorMaps* tm, const double* H, const double* Z, int64_t n, int KP);
+// H: n x hcols (local columns incl. halo), ld n; Z: zrows x n, ld ldz (nullptr: no Z map).
+cudaError_t make_tensor_maps(TensorMaps* tm, const double* H, int64_t hcols, const double* Z,
+                             int64_t zrows, int64_t ldz, int64_t n, int KP);
 
 // Off-diagonal updates of one step.  Left: H(W, w1+1:n) <- Q_W^T H(W, w1+1:n) for every window.
 // Right (+Z): H(0:w0, W) <- H(0:w0, W) Q_W and Z(:, W) <- Z(:, W) Q_W.
@@ -49,6 +54,14 @@ cudaError_t launch_left(const StepArgs& a, const WindowDesc* host_wins, int num_
 cudaError_t launch_right(const StepArgs& a, const WindowDesc* host_wins, int num_sms,
                          const TensorMaps& tm, cudaStream_t st, int64_t* items, double* flops,
                          double* bytes);
+// Left-update column range of window w on this rank: [c, c + cnt)
+__host__ __device__ inline void left_range(const StepArgs& a, const WindowDesc& w, int64_t& c,
+                                           int64_t& cnt) {
+  c = (int64_t)w.w1 + 1 > a.lc0 ? (int64_t)w.w1 + 1 : a.lc0;
+  cnt = a.lc1 - c;
+  if (cnt < 0) cnt = 0;
+}
+
 // Q slot sets in flight: the Z update of step g may trail the chase of step g + kQSets - 1
 constexpr int kQSets = 4;
 

@@ -17,7 +17,10 @@
 // w0 <= p and p + 4 <= w1 (the bulge and the row it creates stay inside); the window whose bottom is
 // ihi runs until the chain's top bulge has left through the final 2x2 reflector at p = ihi - 2.
 // If the whole active block fits one window (N <= k) a single window holds all bulges.
-// See DESIGN.md "Planner" for the derivation and tests/test_plan.py for the checks.
+// Several decoupled active blocks ("concurrent processing of several unreduced
+// blocks"; BASELINE configs[4]) are planned independently and merged step by step: their windows
+// lie in disjoint diagonal blocks, so one wavefront step simply carries windows of every block.
+// See DESIGN.md §6 for the derivation and tests/test_abi_plan.py for the checks.
 #pragma once
 #include <algorithm>
 #include <cstdint>
@@ -26,12 +29,13 @@
 namespace hqr {
 
 struct WindowDesc {     // one diagonal window = one CTA of the chase kernel in one wavefront step
-  int32_t chain;        // chain index (0 = lowest / first shifts)
+  int32_t chain;        // chain index (global over blocks; 0 = lowest chain of the first block)
   int32_t w0, w1;       // global row/col range [w0, w1] (inclusive)
   int32_t t0, t1;       // chain-local steps [t0, t1] (inclusive) run inside this window
   int32_t b0, nbc;      // bulges of the chain: global bulge indices b0 .. b0+nbc-1
   int32_t slot;         // Q workspace slot
   int32_t last;         // 1 if this is the chain's final window
+  int32_t ilo, ihi;     // the active block this window's chain sweeps
 };
 
 struct Plan {
@@ -49,88 +53,119 @@ struct Plan {
   std::vector<int32_t> step_begin;     // windows of step g: [step_begin[g], step_begin[g+1])
 };
 
-// Builds the plan.  k_eff = min(window, N, kmax).  Returns 0 or a negative code (-9: window
-// too small for a multi-window chain).  Inputs are assumed already validated otherwise.
-inline int make_plan(int64_t n, int64_t ilo, int64_t ihi, int nshifts, int window, int kmax,
-                     Plan* out) {
-  Plan P;
-  P.n = n; P.ilo = ilo; P.ihi = ihi;
-  P.nb = nshifts / 2;
+// Plans one active block [ilo, ihi] with nb bulges starting at global bulge b_base and global chain
+// c_base; appends each chain's window sequence and start step.  Returns 0 or -9.
+struct ChainPlan {
+  int g0;                              // global step of the chain's first window
+  std::vector<WindowDesc> windows;
+};
+
+inline int plan_block(int64_t ilo, int64_t ihi, int nb, int b_base, int c_base, int window, int kmax,
+                      std::vector<ChainPlan>* chains, int* k_out, int* nbc_out, int* s_out, int* lag_out) {
   const int64_t N = ihi - ilo + 1;
   int64_t k = std::min<int64_t>({(int64_t)window, N, (int64_t)kmax});
   if (k < N && k < 8) return -9;
-  P.k = (int)k;
-
-  struct ChainInfo { int b0, nbc, g0, nwin; };
-  std::vector<ChainInfo> chains;
-  std::vector<std::vector<WindowDesc>> chain_windows;
-
+  *k_out = (int)k;
   if (N <= k) {
     // one window holds the whole active block: a single chain with every bulge
-    P.nbc_max = P.nb; P.s = (int)N; P.lag = 1; P.nchains = 1;
+    ChainPlan cp;
+    cp.g0 = 0;
     WindowDesc w{};
-    w.chain = 0; w.w0 = (int32_t)ilo; w.w1 = (int32_t)ihi;
-    w.t0 = 0; w.t1 = (int32_t)(N + 3 * (int64_t)P.nb - 5);  // top bulge's last p = ihi-2
-    w.b0 = 0; w.nbc = P.nb; w.slot = 0; w.last = 1;
-    chain_windows.push_back({w});
-    chains.push_back({0, P.nb, 0, 1});
-  } else {
-    int nbc_cap = (int)((k - 2) / 6);
-    int C = (P.nb + nbc_cap - 1) / nbc_cap;
-    int base = P.nb / C, rem = P.nb % C;                 // remainders on the earliest chains
-    int nbc_max = base + (rem > 0 ? 1 : 0);
-    P.nbc_max = nbc_max;
-    P.s = (int)(k - 3 * nbc_max - 1);
-    P.lag = (int)((k + P.s - 1) / P.s);
-    P.nchains = C;
-    int b = 0;
-    for (int c = 0; c < C; ++c) {
-      int nbc = base + (c < rem ? 1 : 0);
-      std::vector<WindowDesc> ws;
-      for (int i = 0;; ++i) {
-        WindowDesc w{};
-        w.chain = c; w.b0 = b; w.nbc = nbc;
-        int64_t w0 = ilo + (int64_t)i * P.s;
-        int64_t w1 = std::min<int64_t>(w0 + k - 1, ihi);
-        w.w0 = (int32_t)w0; w.w1 = (int32_t)w1;
-        w.t0 = (i == 0) ? 0 : (int32_t)((int64_t)(i - 1) * P.s + k - 3);
-        if (w1 == ihi) {
-          w.t1 = (int32_t)(N + 3 * (int64_t)nbc - 5);
-          w.last = 1;
-        } else {
-          w.t1 = (int32_t)((int64_t)i * P.s + k - 4);
-          w.last = 0;
-        }
-        w.slot = c;
-        ws.push_back(w);
-        if (w.last) break;
-      }
-      chains.push_back({b, nbc, c * P.lag, (int)ws.size()});
-      chain_windows.push_back(ws);
-      b += nbc;
-    }
+    w.chain = c_base; w.w0 = (int32_t)ilo; w.w1 = (int32_t)ihi;
+    w.t0 = 0; w.t1 = (int32_t)(N + 3 * (int64_t)nb - 5);  // top bulge's last p = ihi-2
+    w.b0 = b_base; w.nbc = nb; w.slot = c_base; w.last = 1;
+    w.ilo = (int32_t)ilo; w.ihi = (int32_t)ihi;
+    cp.windows.push_back(w);
+    chains->push_back(cp);
+    *nbc_out = nb; *s_out = (int)N; *lag_out = 1;
+    return 0;
   }
-  // wavefront: step g runs window (g - g0_c) of every chain with 0 <= g - g0_c < nwin_c.
-  // Within a step, windows are listed top chain first (highest c) -- the paper's reverse
-  // interleaved insertion order -- which is also ascending row order.
+  const int nbc_cap = (int)((k - 2) / 6);
+  const int C = (nb + nbc_cap - 1) / nbc_cap;
+  const int base = nb / C, rem = nb % C;                 // remainders on the earliest chains
+  const int nbc_max = base + (rem > 0 ? 1 : 0);
+  const int s = (int)(k - 3 * nbc_max - 1);
+  const int lag = (int)((k + s - 1) / s);
+  *nbc_out = nbc_max; *s_out = s; *lag_out = lag;
+  int b = b_base;
+  for (int c = 0; c < C; ++c) {
+    const int nbc = base + (c < rem ? 1 : 0);
+    ChainPlan cp;
+    cp.g0 = c * lag;
+    for (int i = 0;; ++i) {
+      WindowDesc w{};
+      w.chain = c_base + c; w.b0 = b; w.nbc = nbc; w.slot = c_base + c;
+      w.ilo = (int32_t)ilo; w.ihi = (int32_t)ihi;
+      const int64_t w0 = ilo + (int64_t)i * s;
+      const int64_t w1 = std::min<int64_t>(w0 + k - 1, ihi);
+      w.w0 = (int32_t)w0; w.w1 = (int32_t)w1;
+      w.t0 = (i == 0) ? 0 : (int32_t)((int64_t)(i - 1) * s + k - 3);
+      if (w1 == ihi) {
+        w.t1 = (int32_t)(N + 3 * (int64_t)nbc - 5);
+        w.last = 1;
+      } else {
+        w.t1 = (int32_t)((int64_t)i * s + k - 4);
+        w.last = 0;
+      }
+      cp.windows.push_back(w);
+      if (w.last) break;
+    }
+    chains->push_back(cp);
+    b += nbc;
+  }
+  return 0;
+}
+
+// Builds the plan of one sweep over `nblocks` decoupled active blocks (ascending, disjoint).
+// Block i has nshifts[i] shifts; its bulges are numbered after those of blocks 0..i-1.
+// k_eff = min(window, N_i, kmax) per block.  Returns 0 or -9.  Other inputs must be valid.
+inline int make_plan_multi(int64_t n, int nblocks, const int64_t* ilo, const int64_t* ihi,
+                           const int* nshifts, int window, int kmax, Plan* out) {
+  Plan P;
+  P.n = n; P.ilo = ilo[0]; P.ihi = ihi[nblocks - 1];
+  std::vector<ChainPlan> chains;
+  int b_base = 0;
+  for (int i = 0; i < nblocks; ++i) {
+    int k, nbc, s, lag;
+    const int nb = nshifts[i] / 2;
+    int rc = plan_block(ilo[i], ihi[i], nb, b_base, (int)chains.size(), window, kmax, &chains, &k,
+                        &nbc, &s, &lag);
+    if (rc) return rc;
+    if (i == 0) { P.k = k; P.nbc_max = nbc; P.s = s; P.lag = lag; }
+    P.k = std::max(P.k, k);
+    P.nbc_max = std::max(P.nbc_max, nbc);
+    b_base += nb;
+  }
+  P.nb = b_base;
+  P.nchains = (int)chains.size();
+  // wavefront: step g runs window (g - g0) of every chain; windows of a step are disjoint
+  // diagonal blocks, listed top first (the paper's reverse interleaved insertion order)
   int nsteps = 0;
-  for (auto& ch : chains) nsteps = std::max(nsteps, ch.g0 + ch.nwin);
+  for (auto& ch : chains) nsteps = std::max(nsteps, ch.g0 + (int)ch.windows.size());
   P.nsteps = nsteps;
   P.step_begin.push_back(0);
   for (int g = 0; g < nsteps; ++g) {
-    for (int c = (int)chains.size() - 1; c >= 0; --c) {
-      int i = g - chains[c].g0;
-      if (i >= 0 && i < chains[c].nwin) {
-        WindowDesc w = chain_windows[c][i];
-        P.windows.push_back(w);
-        P.max_kw = std::max(P.max_kw, w.w1 - w.w0 + 1);
-        P.max_nbc = std::max(P.max_nbc, w.nbc);
-      }
+    const size_t first = P.windows.size();
+    for (auto& ch : chains) {
+      const int i = g - ch.g0;
+      if (i >= 0 && i < (int)ch.windows.size()) P.windows.push_back(ch.windows[i]);
+    }
+    std::sort(P.windows.begin() + first, P.windows.end(),
+              [](const WindowDesc& x, const WindowDesc& y) { return x.w0 < y.w0; });
+    for (size_t i = first; i < P.windows.size(); ++i) {
+      P.max_kw = std::max(P.max_kw, P.windows[i].w1 - P.windows[i].w0 + 1);
+      P.max_nbc = std::max(P.max_nbc, P.windows[i].nbc);
     }
     P.step_begin.push_back((int32_t)P.windows.size());
   }
   *out = std::move(P);
   return 0;
+}
+
+// Single active block.
+inline int make_plan(int64_t n, int64_t ilo, int64_t ihi, int nshifts, int window, int kmax,
+                     Plan* out) {
+  return make_plan_multi(n, 1, &ilo, &ihi, &nshifts, window, kmax, out);
 }
 
 }  // namespace hqr

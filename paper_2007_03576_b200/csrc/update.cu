@@ -155,15 +155,17 @@ __global__ void __launch_bounds__(kThreadsBulk, 1)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t n = a.n;
   const int nw = a.win_count;
-  const int64_t ztiles = (!LEFT && a.Z && a.right_mode != 1) ? (n + MT - 1) / MT : 0;
+  const int64_t ztiles = (!LEFT && a.Z && a.right_mode != 1) ? (a.zrows + MT - 1) / MT : 0;
   if (tid == 0) {
     si.pre[0] = 0;
     for (int i = 0; i < nw; ++i) {
       WindowDesc w = a.wins[a.win_begin + i];
       si.w[i] = w;
       if (LEFT) {
-        si.rt[i] = 0;
-        si.pre[i + 1] = si.pre[i] + (n - 1 - w.w1 + NT - 1) / NT;
+        int64_t c, cnt;
+        left_range(a, w, c, cnt);
+        si.rt[i] = c;  // LEFT: first column of the window's range
+        si.pre[i + 1] = si.pre[i] + (cnt + NT - 1) / NT;
       } else {
         si.rt[i] = (a.right_mode == 2) ? 0 : ((int64_t)w.w0 + MT - 1) / MT;
         si.pre[i + 1] = si.pre[i] + si.rt[i] + ztiles;
@@ -182,12 +184,14 @@ __global__ void __launch_bounds__(kThreadsBulk, 1)
 
   const int64_t G = gridDim.x;
   const int64_t it0 = total_items * blockIdx.x / G, it1 = total_items * (blockIdx.x + 1) / G;
-  // RIGHT: matrix and row range of a tile
-  auto panel = [&](int wi, int64_t tile, double*& M, int64_t& r0, int64_t& r1) {
+  // RIGHT: matrix, row range, leading dimension and column base of a tile (element (r, global
+  // column j) at M + r + (j - cb) * ld)
+  auto panel = [&](int wi, int64_t tile, double*& M, int64_t& r0, int64_t& r1, int64_t& ld,
+                   int64_t& cb) {
     if (tile < si.rt[wi]) {
-      M = a.H; r0 = tile * MT; r1 = si.w[wi].w0;
+      M = a.H; r0 = tile * MT; r1 = si.w[wi].w0; ld = n; cb = a.hcol0;
     } else {
-      M = a.Z; r0 = (tile - si.rt[wi]) * MT; r1 = n;
+      M = a.Z; r0 = (tile - si.rt[wi]) * MT; r1 = a.zrows; ld = a.ldz; cb = 0;
     }
   };
 
@@ -219,12 +223,12 @@ __global__ void __launch_bounds__(kThreadsBulk, 1)
         if (LEFT) {
           // the innermost TMA coordinate must address a 16-byte boundary: start at the even row
           // w0 - ro (ro = w0 & 1); the consumers offset their reads by ro
-          tma_load_2d(dst, &tmH, w.w0 & ~1, (int)(w.w1 + 1 + tile * NT), &full[s]);
+          tma_load_2d(dst, &tmH, w.w0 & ~1, (int)(si.rt[wi] + tile * NT - a.hcol0), &full[s]);
         } else {
           double* M;
-          int64_t r0, r1;
-          panel(wi, tile, M, r0, r1);
-          tma_load_2d(dst, M == a.H ? &tmH : &tmZ, (int)r0, w.w0, &full[s]);
+          int64_t r0, r1, ld, cb;
+          panel(wi, tile, M, r0, r1, ld, cb);
+          tma_load_2d(dst, M == a.H ? &tmH : &tmZ, (int)r0, (int)(w.w0 - cb), &full[s]);
         }
       }
       __syncwarp();
@@ -312,13 +316,13 @@ __global__ void __launch_bounds__(kThreadsBulk, 1)
       if (acc[0][0][0] != 12345.678) continue;
 #endif
       if (LEFT) {
-        const int64_t c0 = w.w1 + 1 + tile * NT;
+        const int64_t c0 = si.rt[wi] + tile * NT;
         const bool even = (w.w0 & 1) == 0;
 #pragma unroll
         for (int jn = 0; jn < FN; ++jn) {
           const int64_t col = c0 + wn0 + 8 * jn + lr;
-          if (col >= n) continue;
-          double* cp = a.H + col * n + w.w0;
+          if (col >= a.lc1) continue;
+          double* cp = a.H + (col - a.hcol0) * n + w.w0;
 #pragma unroll
           for (int i = 0; i < FM; ++i) {
             const int m = wm0 + 8 * i + 2 * lk;
@@ -332,13 +336,13 @@ __global__ void __launch_bounds__(kThreadsBulk, 1)
         }
       } else {
         double* M;
-        int64_t r0, r1;
-        panel(wi, tile, M, r0, r1);
+        int64_t r0, r1, ld, cb;
+        panel(wi, tile, M, r0, r1, ld, cb);
 #pragma unroll
         for (int jn = 0; jn < FN; ++jn) {
           const int col = wn0 + 8 * jn + lr;
           if (col >= kw) continue;
-          double* cp = M + (int64_t)(w.w0 + col) * n;
+          double* cp = M + (w.w0 + col - cb) * ld;
 #pragma unroll
           for (int i = 0; i < FM; ++i) {
             const int64_t row = r0 + wm0 + 8 * i + 2 * lk;  // even: 16-byte aligned pair
@@ -377,7 +381,10 @@ __global__ void __launch_bounds__(kThreadsGeneric, 1) left_generic_kernel(StepAr
     for (int i = 0; i < nw; ++i) {
       WindowDesc w = a.wins[a.win_begin + i];
       si.w[i] = w;
-      si.pre[i + 1] = si.pre[i] + (n - 1 - w.w1 + NT - 1) / NT;
+      int64_t c, cnt;
+      left_range(a, w, c, cnt);
+      si.rt[i] = c;
+      si.pre[i + 1] = si.pre[i] + (cnt + NT - 1) / NT;
     }
   }
   __syncthreads();
@@ -386,13 +393,13 @@ __global__ void __launch_bounds__(kThreadsGeneric, 1) left_generic_kernel(StepAr
   auto load_panel = [&](int wi, int64_t tile, int buf) {
     const WindowDesc& w = si.w[wi];
     const int kw = w.w1 - w.w0 + 1;
-    const int64_t c0 = w.w1 + 1 + tile * NT;
+    const int64_t c0 = si.rt[wi] + tile * NT;
     double* B = Bs + buf * NT * LD;
     for (int f = tid; f < NT * KP; f += kThreadsGeneric) {
       int nn = f / KP, k = f - nn * KP;
       int64_t col = c0 + nn;
-      bool ok = (k < kw) && (col < n);
-      cp_async8(B + nn * LD + k, ok ? a.H + (w.w0 + k) + col * n : a.H, ok);
+      bool ok = (k < kw) && (col < a.lc1);
+      cp_async8(B + nn * LD + k, ok ? a.H + (w.w0 + k) + (col - a.hcol0) * n : a.H, ok);
     }
   };
   auto load_q = [&](int wi) {
@@ -448,7 +455,7 @@ __global__ void __launch_bounds__(kThreadsGeneric, 1) left_generic_kernel(StepAr
     }
     const WindowDesc& w = si.w[wi];
     const int kw = w.w1 - w.w0 + 1;
-    const int64_t c0 = w.w1 + 1 + tile * NT;
+    const int64_t c0 = si.rt[wi] + tile * NT;
 #pragma unroll
     for (int i = 0; i < FM; ++i) {
       const int m = wm0 + 8 * i + lr;
@@ -458,7 +465,7 @@ __global__ void __launch_bounds__(kThreadsGeneric, 1) left_generic_kernel(StepAr
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
           const int64_t col = c0 + wn0 + 8 * j + 2 * lk + e;
-          if (col < n) a.H[(w.w0 + m) + col * n] = acc[i][j][e];
+          if (col < a.lc1) a.H[(w.w0 + m) + (col - a.hcol0) * n] = acc[i][j][e];
         }
     }
     __syncthreads();
@@ -481,7 +488,7 @@ __global__ void __launch_bounds__(kThreadsGeneric, 1) right_generic_kernel(StepA
   const int wm0 = (warp & 1) * WM, wn0 = (warp >> 1) * WN;
   const int64_t n = a.n;
   const int nw = a.win_count;
-  const int64_t ztiles = (a.Z && a.right_mode != 1) ? (n + MT - 1) / MT : 0;
+  const int64_t ztiles = (a.Z && a.right_mode != 1) ? (a.zrows + MT - 1) / MT : 0;
   if (tid == 0) {
     si.pre[0] = 0;
     for (int i = 0; i < nw; ++i) {
@@ -494,25 +501,26 @@ __global__ void __launch_bounds__(kThreadsGeneric, 1) right_generic_kernel(StepA
   __syncthreads();
   const int64_t G = gridDim.x;
   const int64_t it0 = total_items * blockIdx.x / G, it1 = total_items * (blockIdx.x + 1) / G;
-  auto panel = [&](int wi, int64_t tile, double*& M, int64_t& r0, int64_t& r1) {
+  auto panel = [&](int wi, int64_t tile, double*& M, int64_t& r0, int64_t& r1, int64_t& ld,
+                   int64_t& cb) {
     if (tile < si.rt[wi]) {
-      M = a.H; r0 = tile * MT; r1 = si.w[wi].w0;
+      M = a.H; r0 = tile * MT; r1 = si.w[wi].w0; ld = n; cb = a.hcol0;
     } else {
-      M = a.Z; r0 = (tile - si.rt[wi]) * MT; r1 = n;
+      M = a.Z; r0 = (tile - si.rt[wi]) * MT; r1 = a.zrows; ld = a.ldz; cb = 0;
     }
   };
   auto load_panel = [&](int wi, int64_t tile, int buf) {
     const WindowDesc& w = si.w[wi];
     const int kw = w.w1 - w.w0 + 1;
     double* M;
-    int64_t r0, r1;
-    panel(wi, tile, M, r0, r1);
+    int64_t r0, r1, ld, cb;
+    panel(wi, tile, M, r0, r1, ld, cb);
     double* A = As + buf * KP * LDP;
     for (int f = tid; f < KP * MT; f += kThreadsGeneric) {
       int k = f / MT, mm = f - k * MT;
       int64_t row = r0 + mm;
       bool ok = (k < kw) && (row < r1);
-      cp_async8(A + k * LDP + mm, ok ? M + row + (w.w0 + k) * n : M, ok);
+      cp_async8(A + k * LDP + mm, ok ? M + row + (w.w0 + k - cb) * ld : M, ok);
     }
   };
   auto load_q = [&](int wi) {
@@ -569,8 +577,8 @@ __global__ void __launch_bounds__(kThreadsGeneric, 1) right_generic_kernel(StepA
     const WindowDesc& w = si.w[wi];
     const int kw = w.w1 - w.w0 + 1;
     double* M;
-    int64_t r0, r1;
-    panel(wi, tile, M, r0, r1);
+    int64_t r0, r1, ld, cb;
+    panel(wi, tile, M, r0, r1, ld, cb);
 #pragma unroll
     for (int i = 0; i < FM; ++i) {
       const int64_t row = r0 + wm0 + 8 * i + lr;
@@ -580,7 +588,7 @@ __global__ void __launch_bounds__(kThreadsGeneric, 1) right_generic_kernel(StepA
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
           const int col = wn0 + 8 * j + 2 * lk + e;
-          if (col < kw) M[row + (w.w0 + col) * n] = acc[i][j][e];
+          if (col < kw) M[row + (w.w0 + col - cb) * ld] = acc[i][j][e];
         }
     }
     __syncthreads();
@@ -639,7 +647,8 @@ typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t,
                                   CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
                                   CUtensorMapFloatOOBfill);
 
-cudaError_t encode_2d(CUtensorMap* m, const double* base, int64_t n, unsigned box_rows, unsigned box_cols) {
+cudaError_t encode_2d(CUtensorMap* m, const double* base, int64_t rows, int64_t cols, int64_t ld,
+                      unsigned box_rows, unsigned box_cols) {
   static EncodeTiledFn fn = nullptr;
   if (!fn) {
     cudaDriverEntryPointQueryResult q;
@@ -648,8 +657,8 @@ cudaError_t encode_2d(CUtensorMap* m, const double* base, int64_t n, unsigned bo
     if (e != cudaSuccess || q != cudaDriverEntryPointSuccess || !p) return cudaErrorNotSupported;
     fn = reinterpret_cast<EncodeTiledFn>(p);
   }
-  cuuint64_t dims[2] = {(cuuint64_t)n, (cuuint64_t)n};
-  cuuint64_t strides[1] = {(cuuint64_t)n * sizeof(double)};
+  cuuint64_t dims[2] = {(cuuint64_t)rows, (cuuint64_t)cols};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * sizeof(double)};
   cuuint32_t box[2] = {box_rows, box_cols};
   cuuint32_t es[2] = {1, 1};
   CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims, strides, box, es,
@@ -660,15 +669,17 @@ cudaError_t encode_2d(CUtensorMap* m, const double* base, int64_t n, unsigned bo
 
 }  // namespace
 
-cudaError_t make_tensor_maps(TensorMaps* tm, const double* H, const double* Z, int64_t n, int KP) {
+cudaError_t make_tensor_maps(TensorMaps* tm, const double* H, int64_t hcols, const double* Z,
+                             int64_t zrows, int64_t ldz, int64_t n, int KP) {
   tm->valid = false;
+  // TMA needs 16-byte aligned bases and leading dimensions (even n, even ldz)
   if ((n & 1) || n < 2 || n > (int64_t)1 << 31 || (reinterpret_cast<uintptr_t>(H) & 15) ||
-      (Z && (reinterpret_cast<uintptr_t>(Z) & 15)))
+      (Z && ((reinterpret_cast<uintptr_t>(Z) & 15) || (ldz & 1) || zrows < 1)))
     return cudaSuccess;  // generic (cp.async) path
-  cudaError_t e = encode_2d(&tm->left_H, H, n, pad_ld(KP), left_cols(KP));
-  if (e == cudaSuccess) e = encode_2d(&tm->right_H, H, n, pad_ld(right_rows(KP)), KP);
-  if (e == cudaSuccess) e = Z ? encode_2d(&tm->right_Z, Z, n, pad_ld(right_rows(KP)), KP)
-                              : encode_2d(&tm->right_Z, H, n, pad_ld(right_rows(KP)), KP);
+  cudaError_t e = encode_2d(&tm->left_H, H, n, hcols, n, pad_ld(KP), left_cols(KP));
+  if (e == cudaSuccess) e = encode_2d(&tm->right_H, H, n, hcols, n, pad_ld(right_rows(KP)), KP);
+  if (e == cudaSuccess) e = Z ? encode_2d(&tm->right_Z, Z, zrows, n, ldz, pad_ld(right_rows(KP)), KP)
+                              : encode_2d(&tm->right_Z, H, n, hcols, n, pad_ld(right_rows(KP)), KP);
   if (e != cudaSuccess) return e;
   tm->valid = true;
   return cudaSuccess;
@@ -680,7 +691,8 @@ cudaError_t launch_left(const StepArgs& a, const WindowDesc* hw, int num_sms, co
   double f = 0, b = 0;
   const int NT = left_cols(a.KP);
   for (int i = 0; i < a.win_count; ++i) {
-    int64_t cols = a.n - 1 - hw[i].w1;
+    int64_t c0, cols;
+    left_range(a, hw[i], c0, cols);
     int64_t kw = hw[i].w1 - hw[i].w0 + 1;
     items += (cols + NT - 1) / NT;
     f += 2.0 * kw * kw * (double)cols;
@@ -707,11 +719,11 @@ cudaError_t launch_right(const StepArgs& a, const WindowDesc* hw, int num_sms, c
   double f = 0, b = 0;
   const int MT = right_rows(a.KP);
   const bool do_h = a.right_mode != 2, do_z = a.Z && a.right_mode != 1;
-  const int64_t zt = do_z ? (a.n + MT - 1) / MT : 0;
+  const int64_t zt = do_z ? (a.zrows + MT - 1) / MT : 0;
   for (int i = 0; i < a.win_count; ++i) {
     int64_t kw = hw[i].w1 - hw[i].w0 + 1;
     items += (do_h ? (hw[i].w0 + MT - 1) / MT : 0) + zt;
-    double rows = (do_h ? (double)hw[i].w0 : 0.0) + (do_z ? (double)a.n : 0.0);
+    double rows = (do_h ? (double)hw[i].w0 : 0.0) + (do_z ? (double)a.zrows : 0.0);
     f += 2.0 * kw * kw * rows;
     b += 16.0 * kw * rows;
   }

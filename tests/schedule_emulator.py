@@ -20,9 +20,12 @@ def _house(m, x):
     return x[1:m] / (x0 - b), (b - x0) / b, b
 
 
-def emulate(H, Z, ilo, ihi, sr, si, window, on_window=None):
+def emulate(H, Z, ilo, ihi, sr, si, window, on_window=None, blocks=None):
+    """blocks = [(ilo, ihi, nshifts), ...] for a multi-block sweep (ilo/ihi ignored then)."""
     n = H.shape[0]
-    info, wins = hq.plan_query(n, ilo, ihi, len(sr), window)
+    if blocks is None:
+        blocks = [(ilo, ihi, len(sr))]
+    info, wins = hq.plan_query_multi(n, blocks, window)
     nb = len(sr) // 2
     sig = [sr[2 * j] + sr[2 * j + 1] for j in range(nb)]
     pis = [sr[2 * j] * sr[2 * j + 1] - si[2 * j] * si[2 * j + 1] for j in range(nb)]
@@ -30,7 +33,7 @@ def emulate(H, Z, ilo, ihi, sr, si, window, on_window=None):
         sw = wins[wins[:, 0] == step]
         Qs = []
         for w in sw:
-            _, chain, w0, w1, t0, t1, b0, nbc, slot, last = (int(v) for v in w)
+            _, chain, w0, w1, t0, t1, b0, nbc, slot, last, ilo, ihi = (int(v) for v in w)
             kw = w1 - w0 + 1
             Hw = H[w0:w1 + 1, w0:w1 + 1].copy()
             Q = np.eye(kw)

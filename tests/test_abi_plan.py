@@ -137,3 +137,60 @@ def test_window_factor_lower_bandwidth(n, ns, win):
 
     emulate(H0.copy(order="F"), None, 0, n - 1, re_, im_, win, on_window=chk)
     assert worst and max(worst) <= 0
+
+
+def _blocks_case(n, sizes, ns_each, seed):
+    """decoupled blocks of the given sizes covering [0, n)"""
+    H0, Z0, _, _ = random_case(seed, n, 2, z0="orth")
+    from hqr_inputs import shifts
+    blocks, res, ims = [], [], []
+    lo = 0
+    for b, (sz, ns) in enumerate(zip(sizes, ns_each)):
+        hi = lo + sz - 1
+        if lo > 0:
+            H0[lo, lo - 1] = 0.0
+        re_, im_ = shifts("disk2", ns, seed, stream_offset=b + 1)
+        blocks.append((lo, hi, ns)); res.append(re_); ims.append(im_)
+        lo = hi + 1
+    return H0, Z0, blocks, np.concatenate(res), np.concatenate(ims)
+
+
+@pytest.mark.parametrize("n,sizes,ns_each,win", [
+    (400, [100, 100, 100, 100], [16, 16, 16, 16], 24), (300, [150, 150], [40, 20], 48),
+    (250, [40, 10, 200], [8, 4, 60], 96), (200, [200], [30], 32),
+])
+def test_multi_block_emulation_matches_oracle(n, sizes, ns_each, win):
+    H0, Z0, blocks, re_, im_ = _blocks_case(n, sizes, ns_each, 7)
+    Ho, Zo = H0.copy(order="F"), Z0.copy(order="F")
+    off = 0
+    for lo, hi, ns in blocks:                      # the oracle sweeps the blocks one after another
+        oracle.sweep(Ho, Zo, lo, hi, re_[off:off + ns], im_[off:off + ns])
+        off += ns
+    He, Ze = H0.copy(order="F"), Z0.copy(order="F")
+    info = emulate(He, Ze, 0, n - 1, re_, im_, win, blocks=blocks)
+    assert np.linalg.norm(He - Ho) / np.linalg.norm(H0) <= 1e-11
+    assert np.linalg.norm(Ze - Zo) <= 1e-11 * np.sqrt(n)
+    for lo, hi, _ in blocks[1:]:
+        assert He[lo, lo - 1] == 0.0
+    # blocks share wavefront steps
+    _, W = hq.plan_query_multi(n, blocks, win)
+    if len(blocks) > 1:
+        steps0 = set(W[W[:, 10] == blocks[0][0], 0])
+        steps1 = set(W[W[:, 10] == blocks[1][0], 0])
+        assert steps0 & steps1
+
+
+def test_multi_block_validation():
+    n = 100
+    sr = np.array([0.1, 0.2] * 4); si = np.zeros(8)
+    ilo = np.array([0, 40], dtype=np.int64); ihi = np.array([50, 99], dtype=np.int64)
+    ns = np.array([4, 4], dtype=np.int32)
+    H = np.asfortranarray(np.eye(n))
+    L = hq.lib()
+    args = lambda lo, hi: (H.ctypes.data, None, n, 2, lo.ctypes.data, hi.ctypes.data, sr.ctypes.data,
+                          si.ctypes.data, ns.ctypes.data, 16)
+    assert L.hqr_sweep_multi(*args(ilo, ihi)) == -4            # overlapping blocks
+    ilo2 = np.array([60, 0], dtype=np.int64); ihi2 = np.array([99, 50], dtype=np.int64)
+    assert L.hqr_sweep_multi(*args(ilo2, ihi2)) == -4          # unsorted
+    ilo3 = np.array([0, 51], dtype=np.int64); ihi3 = np.array([50, 99], dtype=np.int64)
+    assert L.hqr_sweep_multi(*args(ilo3, ihi3)) == -100        # valid, library not set up

@@ -131,3 +131,71 @@ def test_config1_full_parity():
     Hg, Zg = gpu_sweep(p.H, p.Z, p.ilo, p.ihi, p.shifts_re, p.shifts_im, p.window)
     Ho, Zo = oracle_sweep(p.H, p.Z, p.ilo, p.ihi, p.shifts_re, p.shifts_im)
     check(Hg, Zg, Ho, Zo, p.H, p.ilo, p.ihi)
+
+
+def _multi_case(n, sizes, ns_each, seed):
+    from hqr_inputs import shifts
+    H0, Z0, _, _ = random_case(seed, n, 2, z0="orth")
+    blocks, res, ims = [], [], []
+    lo = 0
+    for b, (sz, ns) in enumerate(zip(sizes, ns_each)):
+        hi = lo + sz - 1
+        if lo > 0:
+            H0[lo, lo - 1] = 0.0
+        re_, im_ = shifts("disk2", ns, seed, stream_offset=b + 1)
+        blocks.append((lo, hi, ns)); res.append(re_); ims.append(im_)
+        lo = hi + 1
+    return H0, Z0, blocks, np.concatenate(res), np.concatenate(ims)
+
+
+@pytest.mark.parametrize("n,sizes,ns_each,win", [
+    (400, [100, 100, 100, 100], [16, 16, 16, 16], 24), (1000, [250] * 4, [40] * 4, 96),
+    (601, [300, 301], [40, 30], 64), (250, [40, 10, 200], [8, 4, 60], 96),
+])
+def test_multi_block_parity(n, sizes, ns_each, win):
+    """BASELINE configs[4] in miniature: several decoupled blocks swept concurrently."""
+    H0, Z0, blocks, re_, im_ = _multi_case(n, sizes, ns_each, 11)
+    Hd, Zd = hq.to_device(H0), hq.to_device(Z0)
+    hq.sweep_multi(Hd, Zd, blocks, re_, im_, win)
+    Hg, Zg = hq.from_device(Hd), hq.from_device(Zd)
+    Ho, Zo = H0.copy(order="F"), Z0.copy(order="F")
+    off = 0
+    for lo, hi, ns in blocks:
+        oracle.sweep(Ho, Zo, lo, hi, re_[off:off + ns], im_[off:off + ns])
+        off += ns
+    check(Hg, Zg, Ho, Zo, H0, 0, n - 1)
+    for lo, _, _ in blocks[1:]:
+        assert Hg[lo, lo - 1] == 0.0
+
+
+def _gpu_invariants(Hd, Zd, H0d, Z0d, n):
+    """Properties that hold at any size, computed on the GPU (torch matmul is test infrastructure)."""
+    import torch
+    H, Z, H0, Z0 = Hd.t(), Zd.t(), H0d.t(), Z0d.t()   # row-major views of the transposes
+    low = torch.tril(Hd, -2)
+    assert int(torch.count_nonzero(low)) == 0
+    I = torch.eye(n, dtype=torch.float64, device=Hd.device)
+    orth = torch.linalg.norm(Zd.T @ Zd - I).item()
+    assert orth <= 1e-13 * n, orth
+    sim = (torch.linalg.norm(Zd @ Hd @ Zd.T - Z0d @ H0d @ Z0d.T) / torch.linalg.norm(H0d)).item()
+    assert sim <= 1e-13 * n, sim
+    return orth, sim
+
+
+@pytest.mark.parametrize("cfg", [2, 3])
+def test_full_size_parity_against_oracle(cfg):
+    """BASELINE configs[2] (n = 10000) and configs[3] (n = 20000) in the bench's launch
+    configuration (default window), element by element against the oracle run on the host cores,
+    plus the invariants computed on the GPU."""
+    import torch
+    p = make(cfg, z_device="cuda")
+    n = p.H.shape[0]
+    H0d, Z0d = hq.to_device(p.H), hq.to_device(p.Z)
+    Hd = hq.to_device(p.H)
+    Zd = hq.to_device(p.Z)
+    hq.sweep(Hd, Zd, p.ilo, p.ihi, p.shifts_re, p.shifts_im, hq.DEFAULT_WINDOW)
+    _gpu_invariants(Hd, Zd, H0d, Z0d, n)
+    Hg, Zg = hq.from_device(Hd), hq.from_device(Zd)
+    del Hd, Zd, H0d, Z0d
+    Ho, Zo = oracle_sweep(p.H, p.Z, p.ilo, p.ihi, p.shifts_re, p.shifts_im)
+    check(Hg, Zg, Ho, Zo, p.H, p.ilo, p.ihi)

@@ -56,10 +56,11 @@ int main(int argc, char** argv) {
   hqr::StepArgs a{};
   a.H = H; a.Z = Z; a.n = n; a.ilo = 0; a.ihi = n - 1; a.wins = dw; a.win_begin = 0; a.win_count = C;
   a.qslots = Q; a.KP = KP; a.QLD = QLD; a.slot_offset = 0;
+  a.hcol0 = 0; a.lc0 = 0; a.lc1 = n; a.zrows = n; a.ldz = n;
   cudaEvent_t e0, e1;
   CK(cudaEventCreate(&e0)); CK(cudaEventCreate(&e1));
   hqr::TensorMaps tm;
-  CK(hqr::make_tensor_maps(&tm, H, Z, n, KP));
+  CK(hqr::make_tensor_maps(&tm, H, n, Z, n, n, n, KP));
   {
     const unsigned long long* q = reinterpret_cast<const unsigned long long*>(&tm.left_H);
     fprintf(stderr, "bench: tensor maps valid=%d KP=%d H=%p map@%p %llx %llx %llx\n", (int)tm.valid, KP,

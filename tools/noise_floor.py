@@ -1,0 +1,39 @@
+"""Oracle self noise floor: two valid reflector orders of the same sweep (sequential Francis steps vs
+pipelined bulges), on BASELINE configs -- the rounding-level difference any correct reordering
+(including the GPU's wavefront) can show.  Writes a JSON line.  Calls only oracle/ and hqr_inputs."""
+import json
+import sys
+import time
+
+import numpy as np
+
+sys.path.insert(0, __file__.rsplit("/tools/", 1)[0])
+import oracle  # noqa: E402
+from hqr_inputs import make  # noqa: E402
+
+
+def main(cfg):
+    p = make(cfg)
+    n = p.H.shape[0]
+    t0 = time.time()
+    Hs, Zs = p.H.copy(order="F"), p.Z.copy(order="F")
+    oracle.sweep(Hs, Zs, p.ilo, p.ihi, p.shifts_re, p.shifts_im, order="sequential")
+    t1 = time.time()
+    Hp, Zp = p.H.copy(order="F"), p.Z.copy(order="F")
+    oracle.sweep(Hp, Zp, p.ilo, p.ihi, p.shifts_re, p.shifts_im, order="pipelined")
+    t2 = time.time()
+    dH = Hs - Hp
+    i, j = np.unravel_index(np.argmax(np.abs(dH)), dH.shape)
+    sub = np.abs(np.diag(Hs, -1))
+    out = {"cfg": cfg, "n": n, "nshifts": len(p.shifts_re),
+           "dH_rel_fro": float(np.linalg.norm(dH) / np.linalg.norm(p.H)),
+           "dZ_fro_over_sqrt_n": float(np.linalg.norm(Zs - Zp) / np.sqrt(n)),
+           "dH_max": float(np.abs(dH).max()), "dH_argmax": [int(i), int(j)],
+           "min_abs_subdiag_after": float(sub.min()), "argmin_subdiag": int(np.argmin(sub)),
+           "oracle_seconds": [t1 - t0, t2 - t1]}
+    print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    for c in sys.argv[1:]:
+        main(int(c))
