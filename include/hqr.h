@@ -93,6 +93,47 @@ int hqr_sweep_multi(double* H, double* Z, int64_t n, int nblocks, const int64_t*
                     const int64_t* ihi, const double* shifts_re, const double* shifts_im,
                     const int* nshifts, int window);
 
+/*
+ * ---- Sharded sweep over several GPUs -------------------------------------------
+ * Layout for `world` ranks (one process per GPU): rank r owns H columns [cb[r], cb[r+1]) -- all n
+ * rows, column-major, ld = n -- and must allocate `halo` further columns after them (work space for
+ * a neighbour's lent columns), and owns Z rows [rb[r], rb[r+1]) -- all n columns, column-major,
+ * ld = rb[r+1] - rb[r].  cb[r] = n sqrt(r / world) and rb[r] = n r / world, rounded down to even.
+ * hqr_dist_layout writes cb[0..world], rb[0..world], halo (any pointer may be NULL).  Returns 0,
+ * -1 (n < 1), -2 (world < 1) or -11 (a shard would be narrower than HQR_MAX_WINDOW + 8 columns).
+ */
+int hqr_dist_layout(int64_t n, int world, int64_t* col_bounds, int64_t* row_bounds, int* halo);
+
+/* Host-only: per wavefront step, what rank `rank` does (for tests).  out[6*s .. 6*s+5] =
+ * {step, lend_out, lend_in, lc0, lc1, n_owned_windows}.  Returns 0, the number of steps when out is
+ * NULL or cap < steps, or the negative codes of hqr_sweep / hqr_dist_layout (-7: bad rank). */
+int hqr_dist_query(int64_t n, int64_t ilo, int64_t ihi, int nshifts, int window, int world,
+                   int rank, int64_t* out, int64_t cap);
+
+/* 128-byte ncclUniqueId for hqr_config.nccl_id (call on rank 0, share the bytes). */
+int hqr_nccl_unique_id(void* out);
+
+/*
+ * Collective: one sweep of the distributed matrix (every rank calls it with identical scalars and
+ * shifts after hqr_setup with world > 1).  H_local / Z_local: this rank's device shards in the
+ * hqr_dist_layout layout (Z_local may be NULL).  Each window's factor is broadcast from the rank
+ * owning its first column (ncclBroadcast over NVLink); a window straddling a shard boundary borrows
+ * the neighbour's leading columns for the step (ncclSend/Recv).  Codes as hqr_sweep plus -11.
+ */
+int hqr_sweep_dist(double* H_local, double* Z_local, int64_t n, int64_t ilo, int64_t ihi,
+                   const double* shifts_re, const double* shifts_im, int nshifts, int window);
+
+/*
+ * The sharded algorithm with `vworld` virtual ranks on this one GPU (test / single-GPU check of the
+ * multi-GPU path): H, Z are full device matrices (as in hqr_sweep); the library scatters them into
+ * per-rank shards, runs exactly the per-rank kernel sequence of hqr_sweep_dist with device copies
+ * in place of NCCL transfers, and gathers the result.  Codes as hqr_sweep plus -10 (vworld < 1)
+ * and -11.
+ */
+int hqr_sweep_virtual(double* H, double* Z, int64_t n, int64_t ilo, int64_t ihi,
+                      const double* shifts_re, const double* shifts_im, int nshifts, int window,
+                      int vworld);
+
 /* Release everything hqr_setup acquired.  Returns 0 (also when not set up) or 1000+cudaError_t. */
 int hqr_teardown(void);
 

@@ -26,7 +26,7 @@ ERRORS = {
     -5: "ihi >= n or active block shorter than 3", -6: "non-finite shift",
     -7: "shift pair not two reals / exact conjugates", -8: "nshifts odd, < 2 or > N",
     -9: "window out of range", -10: "active block not decoupled", -100: "not set up",
-    -101: "no usable sm_100 CUDA device",
+    -101: "no usable sm_100 CUDA device", -11: "matrix too small for the shard count",
 }
 
 FLAG_NO_GRAPH = 1
@@ -63,7 +63,8 @@ class Stats(ctypes.Structure):
 
 
 SYMBOLS = ["hqr_setup", "hqr_sweep", "hqr_sweep_multi", "hqr_teardown", "hqr_plan_query",
-           "hqr_plan_query_multi", "hqr_get_stats", "hqr_error_string"]
+           "hqr_plan_query_multi", "hqr_get_stats", "hqr_error_string", "hqr_dist_layout",
+           "hqr_dist_query", "hqr_nccl_unique_id", "hqr_sweep_dist", "hqr_sweep_virtual"]
 
 
 def lib():
@@ -88,6 +89,23 @@ def lib():
                                            ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int,
                                            ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64]
         L.hqr_plan_query_multi.restype = ctypes.c_int
+        L.hqr_dist_layout.argtypes = [ctypes.c_int64, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p,
+                                      ctypes.c_void_p]
+        L.hqr_dist_layout.restype = ctypes.c_int
+        L.hqr_dist_query.argtypes = [ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int,
+                                     ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_void_p,
+                                     ctypes.c_int64]
+        L.hqr_dist_query.restype = ctypes.c_int
+        L.hqr_nccl_unique_id.argtypes = [ctypes.c_void_p]
+        L.hqr_nccl_unique_id.restype = ctypes.c_int
+        L.hqr_sweep_dist.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64,
+                                     ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int,
+                                     ctypes.c_int]
+        L.hqr_sweep_dist.restype = ctypes.c_int
+        L.hqr_sweep_virtual.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
+                                        ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p,
+                                        ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int]
+        L.hqr_sweep_virtual.restype = ctypes.c_int
         L.hqr_teardown.argtypes = []
         L.hqr_teardown.restype = ctypes.c_int
         L.hqr_plan_query.argtypes = [ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int,
@@ -174,6 +192,59 @@ def sweep_multi(H, Z, blocks, shifts_re, shifts_im, window: int = DEFAULT_WINDOW
                                sr.ctypes.data, si.ctypes.data, ns.ctypes.data, int(window))
     if rc:
         raise HQRError(rc, "hqr_sweep_multi")
+
+
+def dist_layout(n: int, world: int):
+    """(col_bounds, row_bounds, halo) of the sharded layout (include/hqr.h hqr_dist_layout)."""
+    cb = np.zeros(world + 1, dtype=np.int64)
+    rb = np.zeros(world + 1, dtype=np.int64)
+    halo = ctypes.c_int()
+    rc = lib().hqr_dist_layout(n, world, cb.ctypes.data, rb.ctypes.data, ctypes.byref(halo))
+    if rc:
+        raise HQRError(rc, "hqr_dist_layout")
+    return cb, rb, halo.value
+
+
+def dist_query(n, ilo, ihi, nshifts, window, world, rank) -> np.ndarray:
+    """Per-step rank roles: rows {step, lend_out, lend_in, lc0, lc1, n_owned}."""
+    steps = lib().hqr_dist_query(n, ilo, ihi, nshifts, window, world, rank, None, 0)
+    if steps < 0:
+        raise HQRError(steps, "hqr_dist_query")
+    out = np.zeros((steps, 6), dtype=np.int64)
+    rc = lib().hqr_dist_query(n, ilo, ihi, nshifts, window, world, rank, out.ctypes.data, steps)
+    if rc:
+        raise HQRError(rc, "hqr_dist_query")
+    return out
+
+
+def nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    rc = lib().hqr_nccl_unique_id(buf)
+    if rc:
+        raise HQRError(rc, "hqr_nccl_unique_id")
+    return buf.raw
+
+
+def sweep_dist(H_local_ptr: int, Z_local_ptr, n, ilo, ihi, shifts_re, shifts_im, window) -> None:
+    """Collective sharded sweep on this rank's shards (raw device pointers, hqr_dist_layout)."""
+    sr = np.ascontiguousarray(shifts_re, dtype=np.float64)
+    si = np.ascontiguousarray(shifts_im, dtype=np.float64)
+    rc = lib().hqr_sweep_dist(H_local_ptr, Z_local_ptr, n, ilo, ihi, sr.ctypes.data, si.ctypes.data,
+                              int(sr.shape[0]), int(window))
+    if rc:
+        raise HQRError(rc, "hqr_sweep_dist")
+
+
+def sweep_virtual(H, Z, ilo, ihi, shifts_re, shifts_im, window, vworld: int) -> None:
+    """The sharded algorithm with `vworld` virtual ranks on one GPU (device H, Z as in sweep)."""
+    hp, n = _ptr_n(H)
+    zp, _ = _ptr_n(Z)
+    sr = np.ascontiguousarray(shifts_re, dtype=np.float64)
+    si = np.ascontiguousarray(shifts_im, dtype=np.float64)
+    rc = lib().hqr_sweep_virtual(hp, zp, n, ilo, ihi, sr.ctypes.data, si.ctypes.data, int(sr.shape[0]),
+                                 int(window), int(vworld))
+    if rc:
+        raise HQRError(rc, "hqr_sweep_virtual")
 
 
 def sweep_raw(H_ptr, Z_ptr, n, ilo, ihi, sr_ptr, si_ptr, nshifts, window) -> int:

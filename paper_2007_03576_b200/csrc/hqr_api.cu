@@ -20,7 +20,10 @@
 #include <tuple>
 #include <vector>
 
+#include <nccl.h>
+
 #include "../../include/hqr.h"
+#include "dist.hpp"
 #include "kernels.hpp"
 #include "plan.hpp"
 
@@ -88,11 +91,21 @@ struct State {
   std::map<GraphKey, CachedGraph> graphs;
   std::vector<cudaEvent_t> prof_events;
   hqr_stats stats{};
+  ncclComm_t comm = nullptr;       // world > 1
+  // virtual shards (hqr_sweep_virtual): library-owned per-rank buffers on this one GPU
+  std::vector<double*> vH, vZ;
+  std::vector<size_t> vH_cap, vZ_cap;
 };
 
 State g;
 
 int cuerr(cudaError_t e) { return e == cudaSuccess ? 0 : 1000 + (int)e; }
+int ncclerr(ncclResult_t e) { return e == ncclSuccess ? 0 : 2000 + (int)e; }
+#define NK(x)                                   \
+  do {                                          \
+    ncclResult_t e_ = (x);                      \
+    if (e_ != ncclSuccess) return ncclerr(e_);  \
+  } while (0)
 #define CK(x)                                   \
   do {                                          \
     cudaError_t e_ = (x);                       \
@@ -281,7 +294,7 @@ int hqr_setup(const hqr_config* cfg) {
   if (!cfg) return -1;
   if (g.ready) hqr_teardown();
   if (cfg->world < 1 || cfg->rank < 0 || cfg->rank >= cfg->world) return -1;
-  if (cfg->world > 1) return -1;  // multi-GPU sharding: see DESIGN.md §Multi-GPU (not in this build)
+  if (cfg->world > 1 && !cfg->nccl_id) return -1;
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= cfg->device || cfg->device < 0) {
     cudaGetLastError();
@@ -307,6 +320,11 @@ int hqr_setup(const hqr_config* cfg) {
   for (int i = 0; i < hqr::kQSets; ++i) {
     CK(cudaEventCreateWithFlags(&g.ev_q[i], cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&g.ev_z[i], cudaEventDisableTiming));
+  }
+  if (g.world > 1) {
+    ncclUniqueId id;
+    std::memcpy(&id, cfg->nccl_id, sizeof(id));
+    NK(ncclCommInitRank(&g.comm, g.world, id, g.rank));
   }
   g.ready = true;
   return 0;
@@ -339,6 +357,13 @@ int hqr_teardown(void) {
   }
   cudaStreamDestroy(g.zstream);
   cudaStreamDestroy(g.stream);
+  if (g.comm) {
+    ncclCommDestroy(g.comm);
+    g.comm = nullptr;
+  }
+  for (auto p : g.vH) if (p) cudaFree(p);
+  for (auto p : g.vZ) if (p) cudaFree(p);
+  g.vH.clear(); g.vZ.clear(); g.vH_cap.clear(); g.vZ_cap.clear();
   g.ready = false;
   cudaError_t e = cudaGetLastError();
   return cuerr(e);
@@ -535,6 +560,187 @@ int plan_query_impl(int64_t n, const Blocks& b, int window, int32_t* info, int32
   return 0;
 }
 
+// ================================================================================================
+// Sharded sweep (dist.hpp).  One executor for both transports:
+//   NCCL     one rank per process / GPU: ncclSend/Recv for the lent column slabs, ncclBroadcast of
+//            every window's factor from its owner (grouped per step);
+//   VIRTUAL  every rank's shard lives on this one GPU (hqr_sweep_virtual, for tests): the slabs move
+//            with device-to-device copies and all ranks share one Q slot array, so the broadcast is a
+//            no-op.  The per-rank kernel sequence is identical.
+// Per step: (1) lend straddling slabs, (2) chase owned windows, (3) broadcast factors, (4) left
+// update of every window on the held columns, (5) right update of owned windows, Z update of every
+// window on the local rows, (6) return the slabs.
+// ================================================================================================
+struct RankCtx {
+  int rank;
+  double* H;                      // local columns [cb[r], cb[r+1] + halo), ld n
+  double* Z;                      // local rows [rb[r], rb[r+1]), ld = rows, or nullptr
+  int64_t hcols, zrows;
+  std::vector<hqr::RankStep> steps;
+  std::vector<WindowDesc> owned;  // owned windows of all steps, grouped by step
+  std::vector<int32_t> owned_begin;
+  WindowDesc* d_owned = nullptr;
+  hqr::TensorMaps tm;
+};
+
+int prepare_rank(const CachedPlan& cp, const hqr::DistLayout& L, RankCtx* rc) {
+  const Plan& P = cp.plan;
+  rc->steps.resize(P.nsteps);
+  rc->owned.clear();
+  rc->owned_begin.assign(1, 0);
+  for (int s = 0; s < P.nsteps; ++s) {
+    hqr::rank_step(P, L, rc->rank, s, &rc->steps[s]);
+    for (int32_t i : rc->steps[s].owned) rc->owned.push_back(P.windows[i]);
+    rc->owned_begin.push_back((int32_t)rc->owned.size());
+  }
+  if (!rc->owned.empty()) {
+    CK(cudaMalloc(&rc->d_owned, rc->owned.size() * sizeof(WindowDesc)));
+    CK(cudaMemcpy(rc->d_owned, rc->owned.data(), rc->owned.size() * sizeof(WindowDesc),
+                  cudaMemcpyHostToDevice));
+  }
+  return 0;
+}
+
+int run_dist(const CachedPlan& cp, const hqr::DistLayout& L, std::vector<RankCtx>& ranks, bool nccl,
+             hqr_stats* st) {
+  const Plan& P = cp.plan;
+  const int64_t n = P.n;
+  cudaStream_t A = g.stream;
+  for (auto& rc : ranks) {
+    CK(hqr::make_tensor_maps(&rc.tm, rc.H, rc.hcols, rc.Z, rc.zrows, rc.zrows, n, cp.KP));
+  }
+  const size_t qsz = (size_t)cp.KP * hqr::pad_ld(cp.KP);
+  for (int s = 0; s < P.nsteps; ++s) {
+    const int so = (s % hqr::kQSets) * P.nchains;
+    // (1) lend: rank r+1's leading columns -> rank r's halo
+    if (nccl) {
+      RankCtx& rc = ranks[0];
+      const hqr::RankStep& rs = rc.steps[s];
+      if (rs.lend_out || rs.lend_in) {
+        NK(ncclGroupStart());
+        if (rs.lend_out) NK(ncclSend(rc.H, (size_t)rs.lend_out * n, ncclDouble, rc.rank - 1, g.comm, A));
+        if (rs.lend_in)
+          NK(ncclRecv(rc.H + (L.cb[rc.rank + 1] - L.cb[rc.rank]) * n, (size_t)rs.lend_in * n, ncclDouble,
+                      rc.rank + 1, g.comm, A));
+        NK(ncclGroupEnd());
+      }
+    } else {
+      for (size_t r = 0; r + 1 < ranks.size(); ++r) {
+        const int64_t cnt = ranks[r].steps[s].lend_in;
+        if (cnt)
+          CK(cudaMemcpyAsync(ranks[r].H + (L.cb[r + 1] - L.cb[r]) * n, ranks[r + 1].H,
+                             (size_t)cnt * n * sizeof(double), cudaMemcpyDeviceToDevice, A));
+      }
+    }
+    // (2) chase owned windows
+    for (auto& rc : ranks) {
+      const int nown = rc.owned_begin[s + 1] - rc.owned_begin[s];
+      if (!nown) continue;
+      StepArgs a{};
+      a.H = rc.H; a.Z = rc.Z; a.n = n; a.hcol0 = L.cb[rc.rank];
+      a.lc0 = rc.steps[s].lc0; a.lc1 = rc.steps[s].lc1; a.zrows = rc.zrows; a.ldz = rc.zrows;
+      a.wins = rc.d_owned; a.win_begin = rc.owned_begin[s]; a.win_count = nown;
+      a.coef = g.d_coef; a.qslots = g.d_q; a.KP = cp.KP; a.QLD = hqr::pad_ld(cp.KP); a.slot_offset = so;
+      CK(hqr::launch_chase(a, P.max_kw, P.max_nbc, A));
+      st->launches_chase++;
+    }
+    // (3) broadcast every window's factor from its owner
+    if (nccl) {
+      NK(ncclGroupStart());
+      for (int i = P.step_begin[s]; i < P.step_begin[s + 1]; ++i) {
+        const WindowDesc& w = P.windows[i];
+        double* q = g.d_q + (size_t)(w.slot + so) * qsz;
+        NK(ncclBroadcast(q, q, qsz, ncclDouble, hqr::owner_of_col(L, w.w0), g.comm, A));
+      }
+      NK(ncclGroupEnd());
+    }
+    // (4) left update of every window on the held columns; (5) right (owned) and Z (all)
+    for (auto& rc : ranks) {
+      StepArgs a{};
+      a.H = rc.H; a.Z = rc.Z; a.n = n; a.hcol0 = L.cb[rc.rank];
+      a.lc0 = rc.steps[s].lc0; a.lc1 = rc.steps[s].lc1; a.zrows = rc.zrows; a.ldz = rc.zrows;
+      a.wins = cp.d_wins; a.win_begin = P.step_begin[s]; a.win_count = P.step_begin[s + 1] - P.step_begin[s];
+      a.coef = g.d_coef; a.qslots = g.d_q; a.KP = cp.KP; a.QLD = hqr::pad_ld(cp.KP); a.slot_offset = so;
+      const WindowDesc* hw = P.windows.data() + a.win_begin;
+      int64_t items;
+      double fl, by;
+      CK(hqr::launch_left(a, hw, g.num_sms, rc.tm, A, &items, &fl, &by));
+      if (items) st->launches_left++;
+      st->flops_update += fl;
+      st->bytes_update += by;
+      const int nown = rc.owned_begin[s + 1] - rc.owned_begin[s];
+      if (nown) {
+        StepArgs ar = a;
+        ar.wins = rc.d_owned; ar.win_begin = rc.owned_begin[s]; ar.win_count = nown;
+        ar.right_mode = 1;
+        CK(hqr::launch_right(ar, rc.owned.data() + rc.owned_begin[s], g.num_sms, rc.tm, A, &items, &fl, &by));
+        if (items) st->launches_right++;
+        st->flops_update += fl;
+        st->bytes_update += by;
+      }
+      if (rc.Z) {
+        StepArgs az = a;
+        az.right_mode = 2;
+        CK(hqr::launch_right(az, hw, g.num_sms, rc.tm, A, &items, &fl, &by));
+        if (items) st->launches_right++;
+        st->flops_update += fl;
+        st->bytes_update += by;
+      }
+    }
+    // (6) return the lent slabs
+    if (nccl) {
+      RankCtx& rc = ranks[0];
+      const hqr::RankStep& rs = rc.steps[s];
+      if (rs.lend_out || rs.lend_in) {
+        NK(ncclGroupStart());
+        if (rs.lend_in)
+          NK(ncclSend(rc.H + (L.cb[rc.rank + 1] - L.cb[rc.rank]) * n, (size_t)rs.lend_in * n, ncclDouble,
+                      rc.rank + 1, g.comm, A));
+        if (rs.lend_out) NK(ncclRecv(rc.H, (size_t)rs.lend_out * n, ncclDouble, rc.rank - 1, g.comm, A));
+        NK(ncclGroupEnd());
+      }
+    } else {
+      for (size_t r = 0; r + 1 < ranks.size(); ++r) {
+        const int64_t cnt = ranks[r].steps[s].lend_in;
+        if (cnt)
+          CK(cudaMemcpyAsync(ranks[r + 1].H, ranks[r].H + (L.cb[r + 1] - L.cb[r]) * n,
+                             (size_t)cnt * n * sizeof(double), cudaMemcpyDeviceToDevice, A));
+      }
+    }
+  }
+  st->steps = P.nsteps;
+  st->windows = (int64_t)P.windows.size();
+  st->kernels_launched = st->launches_chase + st->launches_left + st->launches_right;
+  return 0;
+}
+
+// common validation + shift upload for the sharded entry points
+int dist_prepare(int64_t n, int64_t ilo, int64_t ihi, const double* sr, const double* si, int nshifts,
+                 int window, int world, CachedPlan** cpo, hqr::DistLayout* L) {
+  Blocks b;
+  b.ilo = {ilo}; b.ihi = {ihi}; b.nshifts = {nshifts};
+  int rc = validate_blocks(n, b, sr, si, window, true);
+  if (rc) return rc;
+  rc = hqr::make_layout(n, world, hqr::kMaxWindow, L);
+  if (rc) return rc;
+  if (!g.ready) return -100;
+  CK(cudaSetDevice(g.device));
+  rc = get_plan(n, b, window, cpo, true);
+  if (rc) return rc;
+  CachedPlan* cp = *cpo;
+  const int nb = cp->plan.nb;
+  std::vector<double> coef(2 * nb);
+  for (int j = 0; j < nb; ++j) {
+    coef[2 * j] = sr[2 * j] + sr[2 * j + 1];
+    coef[2 * j + 1] = sr[2 * j] * sr[2 * j + 1] - si[2 * j] * si[2 * j + 1];
+  }
+  rc = ensure(&g.d_coef, &g.coef_cap, coef.size());
+  if (rc) return rc;
+  CK(cudaMemcpyAsync(g.d_coef, coef.data(), coef.size() * sizeof(double), cudaMemcpyHostToDevice, g.stream));
+  rc = ensure(&g.d_q, &g.q_cap, (size_t)hqr::kQSets * cp->plan.nchains * cp->KP * hqr::pad_ld(cp->KP));
+  return rc;
+}
+
 Blocks make_blocks(int nblocks, const int64_t* ilo, const int64_t* ihi, const int* nshifts) {
   Blocks b;
   for (int i = 0; i < nblocks; ++i) {
@@ -574,6 +780,142 @@ int hqr_plan_query_multi(int64_t n, int nblocks, const int64_t* ilo, const int64
   return plan_query_impl(n, make_blocks(nblocks, ilo, ihi, nshifts), window, info, windows, cap);
 }
 
+int hqr_dist_layout(int64_t n, int world, int64_t* col_bounds, int64_t* row_bounds, int* halo) {
+  if (n < 1) return -1;
+  if (world < 1) return -2;
+  hqr::DistLayout L;
+  int rc = hqr::make_layout(n, world, hqr::kMaxWindow, &L);
+  if (rc) return rc;
+  for (int r = 0; r <= world; ++r) {
+    if (col_bounds) col_bounds[r] = L.cb[r];
+    if (row_bounds) row_bounds[r] = L.rb[r];
+  }
+  if (halo) *halo = L.halo;
+  return 0;
+}
+
+int hqr_dist_query(int64_t n, int64_t ilo, int64_t ihi, int nshifts, int window, int world, int rank,
+                   int64_t* out, int64_t cap) {
+  Blocks b;
+  b.ilo = {ilo}; b.ihi = {ihi}; b.nshifts = {nshifts};
+  int rc = validate_blocks(n, b, nullptr, nullptr, window, false);
+  if (rc) return rc;
+  if (world < 1 || rank < 0 || rank >= world) return -7;
+  hqr::DistLayout L;
+  rc = hqr::make_layout(n, world, hqr::kMaxWindow, &L);
+  if (rc) return rc;
+  Plan P;
+  rc = hqr::make_plan(n, ilo, ihi, nshifts, window, hqr::kMaxWindow, &P);
+  if (rc) return rc;
+  if (!out || cap < P.nsteps) return P.nsteps;
+  for (int s = 0; s < P.nsteps; ++s) {
+    hqr::RankStep rs;
+    hqr::rank_step(P, L, rank, s, &rs);
+    int64_t* row = out + 6 * (int64_t)s;
+    row[0] = s; row[1] = rs.lend_out; row[2] = rs.lend_in; row[3] = rs.lc0; row[4] = rs.lc1;
+    row[5] = (int64_t)rs.owned.size();
+  }
+  return 0;
+}
+
+int hqr_nccl_unique_id(void* out) {
+  if (!out) return -1;
+  ncclUniqueId id;
+  NK(ncclGetUniqueId(&id));
+  std::memcpy(out, &id, sizeof(id));
+  return 0;
+}
+
+int hqr_sweep_dist(double* H_local, double* Z_local, int64_t n, int64_t ilo, int64_t ihi,
+                   const double* shifts_re, const double* shifts_im, int nshifts, int window) {
+  if (!H_local) return -1;
+  CachedPlan* cp = nullptr;
+  hqr::DistLayout L;
+  int rc = dist_prepare(n, ilo, ihi, shifts_re, shifts_im, nshifts, window, g.world, &cp, &L);
+  if (rc) return rc;
+  if (g.world > 1 && !g.comm) return -100;
+  hqr_stats st{};
+  st.window_eff = cp->plan.k;
+  std::vector<RankCtx> ranks(1);
+  RankCtx& r = ranks[0];
+  r.rank = g.rank;
+  r.H = H_local;
+  r.Z = Z_local;
+  r.hcols = L.cb[g.rank + 1] - L.cb[g.rank] + L.halo;
+  r.zrows = L.rb[g.rank + 1] - L.rb[g.rank];
+  rc = prepare_rank(*cp, L, &r);
+  if (rc) return rc;
+  CK(cudaEventRecord(g.ev0, g.stream));
+  rc = run_dist(*cp, L, ranks, g.world > 1, &st);
+  if (rc) return rc;
+  CK(cudaEventRecord(g.ev1, g.stream));
+  CK(cudaStreamSynchronize(g.stream));
+  if (r.d_owned) cudaFree(r.d_owned);
+  float ms = 0;
+  CK(cudaEventElapsedTime(&ms, g.ev0, g.ev1));
+  st.ms_total = ms;
+  g.stats = st;
+  return 0;
+}
+
+int hqr_sweep_virtual(double* H, double* Z, int64_t n, int64_t ilo, int64_t ihi, const double* shifts_re,
+                      const double* shifts_im, int nshifts, int window, int vworld) {
+  if (!H) return -1;
+  if (vworld < 1) return -10;
+  CachedPlan* cp = nullptr;
+  hqr::DistLayout L;
+  int rc = dist_prepare(n, ilo, ihi, shifts_re, shifts_im, nshifts, window, vworld, &cp, &L);
+  if (rc) return rc;
+  if (!is_device_ptr(H) || (Z && !is_device_ptr(Z))) return -1;
+  hqr_stats st{};
+  st.window_eff = cp->plan.k;
+  g.vH.resize(vworld, nullptr); g.vZ.resize(vworld, nullptr);
+  g.vH_cap.resize(vworld, 0); g.vZ_cap.resize(vworld, 0);
+  std::vector<RankCtx> ranks(vworld);
+  for (int r = 0; r < vworld; ++r) {
+    RankCtx& rc_ = ranks[r];
+    rc_.rank = r;
+    rc_.hcols = L.cb[r + 1] - L.cb[r] + L.halo;
+    rc_.zrows = L.rb[r + 1] - L.rb[r];
+    rc = ensure(&g.vH[r], &g.vH_cap[r], (size_t)n * rc_.hcols);
+    if (rc) return rc;
+    rc_.H = g.vH[r];
+    // scatter: owned columns (contiguous), Z rows (strided)
+    CK(cudaMemcpyAsync(rc_.H, H + L.cb[r] * n, (size_t)(L.cb[r + 1] - L.cb[r]) * n * sizeof(double),
+                       cudaMemcpyDeviceToDevice, g.stream));
+    rc_.Z = nullptr;
+    if (Z) {
+      rc = ensure(&g.vZ[r], &g.vZ_cap[r], (size_t)rc_.zrows * n);
+      if (rc) return rc;
+      rc_.Z = g.vZ[r];
+      CK(cudaMemcpy2DAsync(rc_.Z, rc_.zrows * sizeof(double), Z + L.rb[r], n * sizeof(double),
+                           rc_.zrows * sizeof(double), n, cudaMemcpyDeviceToDevice, g.stream));
+    }
+    rc = prepare_rank(*cp, L, &rc_);
+    if (rc) return rc;
+  }
+  CK(cudaEventRecord(g.ev0, g.stream));
+  rc = run_dist(*cp, L, ranks, false, &st);
+  if (rc) return rc;
+  CK(cudaEventRecord(g.ev1, g.stream));
+  for (int r = 0; r < vworld; ++r) {  // gather
+    RankCtx& rc_ = ranks[r];
+    CK(cudaMemcpyAsync(H + L.cb[r] * n, rc_.H, (size_t)(L.cb[r + 1] - L.cb[r]) * n * sizeof(double),
+                       cudaMemcpyDeviceToDevice, g.stream));
+    if (Z)
+      CK(cudaMemcpy2DAsync(Z + L.rb[r], n * sizeof(double), rc_.Z, rc_.zrows * sizeof(double),
+                           rc_.zrows * sizeof(double), n, cudaMemcpyDeviceToDevice, g.stream));
+  }
+  CK(cudaStreamSynchronize(g.stream));
+  for (auto& rc_ : ranks)
+    if (rc_.d_owned) cudaFree(rc_.d_owned);
+  float ms = 0;
+  CK(cudaEventElapsedTime(&ms, g.ev0, g.ev1));
+  st.ms_total = ms;
+  g.stats = st;
+  return 0;
+}
+
 int hqr_get_stats(hqr_stats* out) {
   if (!out) return -1;
   *out = g.stats;
@@ -594,6 +936,7 @@ const char* hqr_error_string(int code) {
     case -10: return "active block not decoupled (H[ilo,ilo-1] or H[ihi+1,ihi] nonzero)";
     case -100: return "library not set up (call hqr_setup)";
     case -101: return "no usable sm_100 CUDA device";
+    case -11: return "matrix too small for the number of shards (each needs >= HQR_MAX_WINDOW + 8 columns)";
   }
   if (code >= 2000) return "NCCL error (code - 2000 = ncclResult_t)";
   if (code >= 1000) return "CUDA error (code - 1000 = cudaError_t)";

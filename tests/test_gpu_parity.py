@@ -199,3 +199,18 @@ def test_full_size_parity_against_oracle(cfg):
     del Hd, Zd, H0d, Z0d
     Ho, Zo = oracle_sweep(p.H, p.Z, p.ilo, p.ihi, p.shifts_re, p.shifts_im)
     check(Hg, Zg, Ho, Zo, p.H, p.ilo, p.ihi)
+
+
+@pytest.mark.parametrize("vworld,case", [(1, (60, 1000, 40, 96)), (2, (61, 1200, 60, 64)),
+                                         (4, (62, 2000, 80, 96)), (8, (63, 2400, 64, 96)),
+                                         (3, (64, 1501, 30, 40))])
+def test_sharded_virtual_ranks(vworld, case):
+    """The multi-GPU algorithm (H column shards with lent slabs, Z row shards, per-rank kernels) with
+    vworld virtual ranks on this GPU (hqr_sweep_virtual) against the oracle."""
+    seed, n, ns, win = case
+    H0, Z0, re_, im_ = random_case(seed, n, ns, z0="orth", shift_kind="disk2")
+    Hd, Zd = hq.to_device(H0), hq.to_device(Z0)
+    hq.sweep_virtual(Hd, Zd, 0, n - 1, re_, im_, win, vworld)
+    Hg, Zg = hq.from_device(Hd), hq.from_device(Zd)
+    Ho, Zo = oracle_sweep(H0, Z0, 0, n - 1, re_, im_)
+    check(Hg, Zg, Ho, Zo, H0, 0, n - 1)
