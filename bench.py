@@ -143,8 +143,8 @@ def main():
     ap.add_argument("--config", type=int, default=3)
     ap.add_argument("--window", type=int, default=96)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--cpu-bulges", type=int, default=2, help="oracle sample size (shift pairs)")
-    ap.add_argument("--ref-bulges", type=int, default=1)
+    ap.add_argument("--cpu-bulges", type=int, default=32, help="oracle sample size (shift pairs)")
+    ap.add_argument("--ref-bulges", type=int, default=16)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--n", type=int, default=None, help="override n (debug)")
@@ -161,32 +161,53 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
-        # The sharded multi-GPU sweep (H block-column / Z block-row, Q broadcast) is not in this
-        # build: every rank runs its own full sweep (replicas) -- reported as such.
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
 
     t0 = time.time()
     prob = make(args.config, z_device="cuda" if torch.cuda.is_available() else "cpu", n_override=args.n)
     n = prob.H.shape[0]
     gen_s = time.time() - t0
     nshifts = len(prob.shifts_re)
-    hq.setup(local)
 
-    H0 = hq.to_device(prob.H, dev)
-    Z0 = hq.to_device(prob.Z, dev)
-    H = torch.empty_like(H0.t()).t()
-    Z = torch.empty_like(Z0.t()).t()
+    if world == 1:
+        hq.setup(local)
+        H0 = hq.to_device(prob.H, dev)
+        Z0 = hq.to_device(prob.Z, dev)
+        H = torch.empty_like(H0.t()).t()
+        Z = torch.empty_like(Z0.t()).t()
 
-    def restore():
-        H.t().copy_(H0.t())
-        Z.t().copy_(Z0.t())
+        def restore():
+            H.t().copy_(H0.t())
+            Z.t().copy_(Z0.t())
 
-    def one():
-        hq.sweep(H, Z, prob.ilo, prob.ihi, prob.shifts_re, prob.shifts_im, args.window)
+        def one():
+            hq.sweep(H, Z, prob.ilo, prob.ihi, prob.shifts_re, prob.shifts_im, args.window)
+    else:
+        # sharded sweep: this rank's H column shard (+ halo) and Z row shard
+        import torch.distributed as dist
+        uid = [hq.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        hq.setup(local, rank=rank, world=world, nccl_id=uid[0])
+        cb, rb, halo = hq.dist_layout(n, world)
+        c0, c1, r0, r1 = int(cb[rank]), int(cb[rank + 1]), int(rb[rank]), int(rb[rank + 1])
+        # column-major shards as row-major tensors of their transposes: row j = local column j
+        H0 = torch.zeros((c1 - c0 + halo, n), dtype=torch.float64, device=dev)
+        H0[:c1 - c0].copy_(torch.from_numpy(np.ascontiguousarray(prob.H[:, c0:c1].T)))
+        Z0 = torch.from_numpy(np.ascontiguousarray(prob.Z[r0:r1, :].T)).to(dev)
+        H = torch.empty_like(H0)
+        Z = torch.empty_like(Z0)
+
+        def restore():
+            H.copy_(H0)
+            Z.copy_(Z0)
+
+        def one():
+            hq.sweep_dist(H.data_ptr(), Z.data_ptr(), n, prob.ilo, prob.ihi, prob.shifts_re,
+                          prob.shifts_im, args.window)
 
     for _ in range(args.warmup):
         restore()
@@ -219,36 +240,46 @@ def main():
         ms = float(t.item())
     st = hq.stats()
     fa = f_alg(n, prob.ilo, prob.ihi, nshifts // 2, True)
-    value = fa * world / (ms * 1e-3) / 1e9   # replicas: each rank one full sweep
+    value = fa / (ms * 1e-3) / 1e9   # one sweep (strong scaling: the same sweep on every N)
     peak_sus, peak_burst = fp64_peak()
     gflops_exec = (st["flops_update"] + st["flops_chase"]) / (ms * 1e-3) / 1e9
 
-    # per-kernel CUDA-event times: the same sweep in profiling mode (events around every launch)
-    hq.teardown()
-    hq.setup(local, flags=hq.FLAG_PROFILE)
-    prof = []
-    for _ in range(max(1, min(args.steps, 2))):
-        restore()
-        torch.cuda.synchronize()
-        one()
-        prof.append(hq.stats())
-    hq.teardown()
-    ps = prof[-1]
-    upd_ms = ps["ms_left"] + ps["ms_right"]
-    upd_launches = ps["launches_left"] + ps["launches_right"]
-    achieved = ps["flops_update"] / (upd_ms * 1e-3) / 1e12  # TF/s over all update launches
-    roofline = {"bound": "tensor", "kernel": "update (left + right/Z DMMA GEMM)",
-                "achieved": achieved, "peak": peak_sus, "unit": "TFLOP/s", "frac": achieved / peak_sus,
-                "traffic": None,
-                "peak_source": "measured FP64 DMMA sustained, profiles/fp64_peaks_r01.json "
-                               "(MEASURED_PEAKS.json has no fp64 entry)",
-                "flops_per_launch": ps["flops_update"] / max(1, upd_launches),
-                "avg_launch_ms": upd_ms / max(1, upd_launches),
-                "share_of_step": upd_ms / max(1e-9, ps["ms_chase"] + upd_ms),
-                "ms_chase": ps["ms_chase"], "ms_left": ps["ms_left"], "ms_right": ps["ms_right"]}
+    if world == 1:
+        # per-kernel CUDA-event times: the same sweep in profiling mode (events around every launch)
+        hq.teardown()
+        hq.setup(local, flags=hq.FLAG_PROFILE)
+        prof = []
+        for _ in range(max(1, min(args.steps, 2))):
+            restore()
+            torch.cuda.synchronize()
+            one()
+            prof.append(hq.stats())
+        hq.teardown()
+        ps = prof[-1]
+        upd_ms = ps["ms_left"] + ps["ms_right"]
+        upd_launches = ps["launches_left"] + ps["launches_right"]
+        achieved = ps["flops_update"] / (upd_ms * 1e-3) / 1e12  # TF/s over all update launches
+        roofline = {"bound": "tensor", "kernel": "update (left + right/Z DMMA GEMM)",
+                    "achieved": achieved, "peak": peak_sus, "unit": "TFLOP/s", "frac": achieved / peak_sus,
+                    "traffic": None,
+                    "peak_source": "measured FP64 DMMA sustained, profiles/fp64_peaks_r01.json "
+                                   "(MEASURED_PEAKS.json has no fp64 entry)",
+                    "flops_per_launch": ps["flops_update"] / max(1, upd_launches),
+                    "avg_launch_ms": upd_ms / max(1, upd_launches),
+                    "share_of_step": upd_ms / max(1e-9, ps["ms_chase"] + upd_ms),
+                    "ms_chase": ps["ms_chase"], "ms_left": ps["ms_left"], "ms_right": ps["ms_right"]}
+    else:
+        # per-rank GEMM flops over the whole sweep time (lower bound of the kernels' own rate)
+        fl = torch.tensor([st["flops_update"]], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(fl, op=torch.distributed.ReduceOp.MAX)
+        achieved = float(fl.item()) / (ms * 1e-3) / 1e12
+        roofline = {"bound": "tensor", "kernel": "update GEMMs of the busiest rank over the sweep",
+                    "achieved": achieved, "peak": peak_sus, "unit": "TFLOP/s", "frac": achieved / peak_sus,
+                    "traffic": None, "peak_source": "measured FP64 DMMA sustained, profiles/fp64_peaks_r01.json"}
+        hq.teardown()
 
     e2e = None
-    if not args.no_e2e and rank == 0:
+    if not args.no_e2e and rank == 0 and world == 1:
         hq.setup(local)
         Hh = torch.empty((n, n), dtype=torch.float64, pin_memory=True)
         Zh = torch.empty((n, n), dtype=torch.float64, pin_memory=True)
@@ -279,15 +310,16 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-            "higher_is_better": True, "scaling": "weak" if world > 1 else "strong",
+            "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, BASELINE.json configs)",
             "config": {"workload": f"configs[{args.config}]", "n": n, "nshifts": nshifts,
                        "window": st["window_eff"], "z": "random orthogonal" if args.config in (1, 3) else "identity",
-                       "parallelism": "replicas" if world > 1 else "1 GPU",
+                       "parallelism": (f"{world} GPUs: H block-column (sqrt-balanced), Z block-row, "
+                                       "per-window Q ncclBroadcast, lent slabs") if world > 1 else "1 GPU",
                        "l2": "inputs (2 x %.1f GB) larger than L2" % (n * n * 8 / 1e9),
                        "restore": "H, Z restored from pristine device copies before each step (untimed)"},
             "seconds_per_sweep": ms * 1e-3,
-            "gflops_alg": value / world, "gflops_exec": gflops_exec,
+            "gflops_alg": value, "gflops_exec": gflops_exec,
             "frac_fp64_peak_exec": gflops_exec / 1e3 / peak_sus,
             "flops_exec_over_alg": (st["flops_update"] + st["flops_chase"]) / fa,
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,

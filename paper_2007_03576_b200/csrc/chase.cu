@@ -8,20 +8,24 @@
 // (P:198-203): bulge introduction from the first column of (H - s I)(H - s' I), 3x3
 // Householder reflectors chasing the bulge, a final 2x2 reflector at p = ihi - 2.
 //
-// Per step, two phases separated by __syncthreads:
+// Warp roles.  16 chase warps run the steps; per step two phases separated by a named barrier:
 //   phase 1  (one warp per bulge) compute the reflector from column p (or the intro vector),
 //            store beta / exact zeros in column p, apply it from the left to rows p+1..p+m,
-//            columns p+1..w1 (lanes across columns);
-//   phase 2  (same warp; reflector from a SMEM table) apply it from the right to columns p+1..p+m of the window rows
-//            w0..p+m+1 and of Q_W rows 0..p0+3 (p0 = the chain's deepest bulge; deeper rows of
-//            Q_W are still identity rows), lanes across rows.
+//            columns p+1..w1 (lanes across columns), publish it in an SMEM ring;
+//   phase 2  (same warp) apply it from the right to columns p+1..p+m of the window rows
+//            w0..p+m+1 (lanes across rows).
+// 8 accumulation warps take the reflectors from the ring (mbarrier full/empty handshake, up to
+// kRing steps behind) and apply them to Q_W rows 0..p0+3 (p0 = the chain's deepest bulge; deeper
+// rows of Q_W are still identity rows).  Q_W is not read by the chase, so its update leaves the
+// chase's critical path; the accumulation warps keep the steps in order (a named barrier) because
+// neighbouring bulges of consecutive steps share a column.
 // Bulges are 3 apart, so within a phase different bulges touch disjoint rows (phase 1) or
 // disjoint columns (phase 2).  Phase 1 of bulge j writes beta into H[p+1,p] before phase 2 of the
 // bulge above (at p-3) updates that entry -- the sequential order.
 //
-// The kernel is latency-bound (a chain of small dependent reflectors), so it runs 16 warps (one
-// per bulge), keeps every index 32-bit, specialises the common 3-reflector, and computes each
-// reflector with one square root and one division.
+// The kernel is latency-bound (a chain of small dependent reflectors): one chase warp per bulge,
+// 32-bit indices, the common 3-reflector specialised, one square root and one division per
+// reflector.
 //
 // SMEM layout: column-major H window and Q_W with an odd leading dimension (kw | 1): a warp
 // walking a row (phase 1) or a column (phase 2) hits 32 distinct banks.
@@ -34,8 +38,11 @@ namespace hqr {
 
 namespace {
 
-constexpr int kChaseThreads = 512;
-constexpr int kChaseWarps = kChaseThreads / 32;
+constexpr int kHWarps = 16;                      // chase warps: reflectors, left, right (window)
+constexpr int kQWarps = 8;                       // accumulation warps: Q_W <- Q_W P
+constexpr int kChaseThreads = 32 * (kHWarps + kQWarps);
+constexpr int kRing = 8;                         // steps of reflectors in flight to the Q warps
+constexpr int kMaxRingBulges = 64;               // bulges per step the ring holds
 
 // Householder reflector (reading R2): P = I - tau v v^T, v = [1, v1, v2],
 // P x = beta e1 with beta = -sign(x0) ||x||, sign(0) = +1; zero tail -> identity.
@@ -58,25 +65,79 @@ __device__ __forceinline__ void house(double x0, double x1, double x2, double& v
   beta = b;
 }
 
+struct Refl {      // one reflector in the ring: P = I - tau v v^T acting on local columns pl+1..pl+m
+  double v1, v2, tau;
+  int pl, m;       // pl = INT_MIN: no reflector (inactive bulge or tau = 0)
+};
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.shared::cta.b64 st, [%0];\n}\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void named_sync(int id, int threads) {
+  asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(threads) : "memory");
+}
+
+// Apply reflector r from the right to `rows` rows of three (two) consecutive SMEM columns starting
+// at c1 (ld = ldh); lanes across rows.
+__device__ __forceinline__ void right_apply(double* c1, int ldh, int rows, const Refl& r, int lane) {
+  if (r.m == 3) {
+    for (int i = lane; i < rows; i += 32) {
+      double* x = c1 + i;
+      const double h0 = x[0], h1 = x[ldh], h2 = x[2 * ldh];
+      const double tw = r.tau * fma(r.v2, h2, fma(r.v1, h1, h0));
+      x[0] = h0 - tw;
+      x[ldh] = fma(-tw, r.v1, h1);
+      x[2 * ldh] = fma(-tw, r.v2, h2);
+    }
+  } else {
+    for (int i = lane; i < rows; i += 32) {
+      double* x = c1 + i;
+      const double h0 = x[0], h1 = x[ldh];
+      const double tw = r.tau * fma(r.v1, h1, h0);
+      x[0] = h0 - tw;
+      x[ldh] = fma(-tw, r.v1, h1);
+    }
+  }
+}
+
 __global__ void __launch_bounds__(kChaseThreads, 1) chase_kernel(StepArgs a) {
   extern __shared__ double sm[];
+  __shared__ Refl ring[kRing][kMaxRingBulges];
+  __shared__ __align__(8) uint64_t full[kRing], empty[kRing];
   const WindowDesc W = a.wins[a.win_begin + blockIdx.x];
   const int kw = W.w1 - W.w0 + 1;
   const int ldh = kw | 1;
   double* Hs = sm;
   double* Qs = Hs + kw * ldh;
-  double* R = Qs + kw * ldh;                          // per bulge: v1, v2, tau
-  int* Rp = reinterpret_cast<int*>(R + 3 * W.nbc);    // per bulge: local p (INT_MIN = skip)
-  int* Rm = Rp + W.nbc;                               // per bulge: m (2 or 3)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t n = a.n;
   const int w0 = W.w0;
   const int ilo = W.ilo, ihi = W.ihi;  // the active block of this window's chain
+  const int nbc = W.nbc;
 
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kRing; ++i) {
+      mbar_init(&full[i], kHWarps);
+      mbar_init(&empty[i], kQWarps);
+    }
+  }
   // load the window (coalesced along columns), Q_W = I
   {
     const double* g = a.H + (int64_t)(w0 - a.hcol0) * n + w0;
-    for (int c = warp; c < kw; c += kChaseWarps) {
+    for (int c = warp; c < kw; c += kHWarps + kQWarps) {
       const double* gc = g + (int64_t)c * n;
       for (int r = lane; r < kw; r += 32) {
         Hs[r + c * ldh] = gc[r];
@@ -87,114 +148,112 @@ __global__ void __launch_bounds__(kChaseThreads, 1) chase_kernel(StepArgs a) {
   __syncthreads();
 
   const int rmaxH = ihi - w0;  // last window row inside the active block
-  for (int t = W.t0; t <= W.t1; ++t) {
-    // rows of Q_W below the chain's deepest reflector so far are still identity rows
-    const int rQ = min(ilo - 1 + t - w0 + 3, kw - 1);
-    // ---- phase 1: reflectors + left application ------------------------------------------
-    // warp -> bulges jj = warp, warp + 16, ...; the reflector goes to the SMEM table for phase 2
-    for (int jj = warp; jj < W.nbc; jj += kChaseWarps) {
-      const int p = ilo - 1 + t - 3 * jj;
-      if (p < ilo - 1 || p > ihi - 2) {
-        if (lane == 0) Rp[jj] = INT_MIN;
-        continue;
+  if (warp < kHWarps) {
+    // ======================= chase warps =======================
+    for (int t = W.t0; t <= W.t1; ++t) {
+      const int j = t - W.t0, slot = j % kRing;
+      if (j >= kRing) mbar_wait(&empty[slot], (unsigned)((j / kRing) - 1) & 1);
+      // ---- phase 1: reflectors + left application (warp -> bulges warp, warp + 16, ...) ------
+      for (int jj = warp; jj < nbc; jj += kHWarps) {
+        Refl R;
+        R.pl = INT_MIN;
+        R.m = 3;
+        const int p = ilo - 1 + t - 3 * jj;
+        if (p >= ilo - 1 && p <= ihi - 2) {
+          const int pl = p - w0;
+          const int m = (p <= ihi - 3) ? 3 : 2;
+          double x0, x1, x2;
+          if (p == ilo - 1) {  // bulge introduction; the window starts at ilo
+            const int jb = W.b0 + jj;
+            const double sigma = a.coef[2 * jb], pi = a.coef[2 * jb + 1];
+            const double h00 = Hs[0], h10 = Hs[1], h01 = Hs[ldh], h11 = Hs[1 + ldh], h21 = Hs[2 + ldh];
+            x0 = h00 * (h00 - sigma) + h01 * h10 + pi;
+            x1 = h10 * (h00 + h11 - sigma);
+            x2 = h10 * h21;
+          } else {
+            const double* col = Hs + pl * ldh + pl;
+            x0 = col[1];
+            x1 = col[2];
+            x2 = (m == 3) ? col[3] : 0.0;
+          }
+          double v1, v2, tau, beta;
+          house(x0, x1, x2, v1, v2, tau, beta);
+          __syncwarp();
+          if (lane == 0 && p >= ilo) {
+            double* col = Hs + pl * ldh + pl;
+            col[1] = beta;
+            col[2] = 0.0;
+            if (m == 3) col[3] = 0.0;
+          }
+          if (tau != 0.0) {
+            R.v1 = v1; R.v2 = v2; R.tau = tau; R.pl = pl; R.m = m;
+            const int c0 = (p == ilo - 1) ? 0 : pl + 1;
+            double* hrow = Hs + (pl + 1);
+            if (m == 3) {
+              for (int c = c0 + lane; c < kw; c += 32) {
+                double* hc = hrow + c * ldh;
+                const double h0 = hc[0], h1 = hc[1], h2 = hc[2];
+                const double tw = tau * fma(v2, h2, fma(v1, h1, h0));
+                hc[0] = h0 - tw;
+                hc[1] = fma(-tw, v1, h1);
+                hc[2] = fma(-tw, v2, h2);
+              }
+            } else {
+              for (int c = c0 + lane; c < kw; c += 32) {
+                double* hc = hrow + c * ldh;
+                const double h0 = hc[0], h1 = hc[1];
+                const double tw = tau * fma(v1, h1, h0);
+                hc[0] = h0 - tw;
+                hc[1] = fma(-tw, v1, h1);
+              }
+            }
+          }
+        }
+        if (lane == 0) ring[slot][jj] = R;
       }
-      const int pl = p - w0;
-      const int m = (p <= ihi - 3) ? 3 : 2;
-      double x0, x1, x2;
-      if (p == ilo - 1) {  // bulge introduction; the window starts at ilo: local (0,0)
-        const int j = W.b0 + jj;
-        const double sigma = a.coef[2 * j], pi = a.coef[2 * j + 1];
-        const double h00 = Hs[0], h10 = Hs[1], h01 = Hs[ldh], h11 = Hs[1 + ldh], h21 = Hs[2 + ldh];
-        x0 = h00 * (h00 - sigma) + h01 * h10 + pi;
-        x1 = h10 * (h00 + h11 - sigma);
-        x2 = h10 * h21;
-      } else {
-        const double* col = Hs + pl * ldh + pl;
-        x0 = col[1];
-        x1 = col[2];
-        x2 = (m == 3) ? col[3] : 0.0;
-      }
-      double v1, v2, tau, beta;
-      house(x0, x1, x2, v1, v2, tau, beta);
       __syncwarp();
-      if (lane == 0) {
-        if (p >= ilo) {
-          double* col = Hs + pl * ldh + pl;
-          col[1] = beta;
-          col[2] = 0.0;
-          if (m == 3) col[3] = 0.0;
-        }
-        R[3 * jj] = v1; R[3 * jj + 1] = v2; R[3 * jj + 2] = tau;
-        Rp[jj] = (tau == 0.0) ? INT_MIN : pl;
-        Rm[jj] = m;
+      if (lane == 0) mbar_arrive(&full[slot]);   // this warp's reflectors of step t are published
+      named_sync(1, 32 * kHWarps);                // phase 1 of every bulge before any phase 2
+      // ---- phase 2: right application to the window rows w0..p+m+1 -------------------------
+      for (int jj = warp; jj < nbc; jj += kHWarps) {
+        const Refl R = ring[slot][jj];
+        if (R.pl == INT_MIN) continue;
+        right_apply(Hs + (R.pl + 1) * ldh, ldh, min(R.pl + R.m + 1, rmaxH) + 1, R, lane);
       }
-      if (tau == 0.0) continue;
-      const int c0 = (p == ilo - 1) ? 0 : pl + 1;
-      double* hrow = Hs + (pl + 1);
-      if (m == 3) {
-        for (int c = c0 + lane; c < kw; c += 32) {
-          double* hc = hrow + c * ldh;
-          const double h0 = hc[0], h1 = hc[1], h2 = hc[2];
-          const double tw = tau * fma(v2, h2, fma(v1, h1, h0));
-          hc[0] = h0 - tw;
-          hc[1] = fma(-tw, v1, h1);
-          hc[2] = fma(-tw, v2, h2);
-        }
-      } else {
-        for (int c = c0 + lane; c < kw; c += 32) {
-          double* hc = hrow + c * ldh;
-          const double h0 = hc[0], h1 = hc[1];
-          const double tw = tau * fma(v1, h1, h0);
-          hc[0] = h0 - tw;
-          hc[1] = fma(-tw, v1, h1);
-        }
-      }
+      named_sync(1, 32 * kHWarps);
     }
-    __syncthreads();
-    // ---- phase 2: right application to the window and to Q_W (same warp, same bulges) ------
-    for (int jj = warp; jj < W.nbc; jj += kChaseWarps) {
-      const int pl = Rp[jj];
-      if (pl == INT_MIN) continue;
-      const double v1 = R[3 * jj], v2 = R[3 * jj + 1], tau = R[3 * jj + 2];
-      const int m = Rm[jj];
-      const int rH = min(pl + m + 1, rmaxH);
-      const int nrows = rH + 1 + rQ + 1;  // window rows 0..rH, then Q_W rows 0..rQ
-      double* c1H = Hs + (pl + 1) * ldh;
-      double* c1Q = Qs + (pl + 1) * ldh;
-      if (m == 3) {
-        for (int i = lane; i < nrows; i += 32) {
-          double* x = (i <= rH) ? c1H + i : c1Q + (i - rH - 1);
-          const double h0 = x[0], h1 = x[ldh], h2 = x[2 * ldh];
-          const double tw = tau * fma(v2, h2, fma(v1, h1, h0));
-          x[0] = h0 - tw;
-          x[ldh] = fma(-tw, v1, h1);
-          x[2 * ldh] = fma(-tw, v2, h2);
-        }
-      } else {
-        for (int i = lane; i < nrows; i += 32) {
-          double* x = (i <= rH) ? c1H + i : c1Q + (i - rH - 1);
-          const double h0 = x[0], h1 = x[ldh];
-          const double tw = tau * fma(v1, h1, h0);
-          x[0] = h0 - tw;
-          x[ldh] = fma(-tw, v1, h1);
-        }
+  } else {
+    // ============ accumulation warps: Q_W(:, p+1..p+m) <- Q_W(:, p+1..p+m) P, one step behind ====
+    const int qw = warp - kHWarps;
+    for (int t = W.t0; t <= W.t1; ++t) {
+      const int j = t - W.t0, slot = j % kRing;
+      mbar_wait(&full[slot], (unsigned)(j / kRing) & 1);
+      // rows of Q_W below the chain's deepest reflector so far are still identity rows
+      const int rQ = min(ilo - 1 + t - w0 + 3, kw - 1);
+      for (int jj = qw; jj < nbc; jj += kQWarps) {
+        const Refl R = ring[slot][jj];
+        if (R.pl == INT_MIN) continue;
+        right_apply(Qs + (R.pl + 1) * ldh, ldh, rQ + 1, R, lane);
       }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[slot]);
+      named_sync(2, 32 * kQWarps);  // steps in order: neighbouring bulges share a column
     }
-    __syncthreads();
   }
+  __syncthreads();
 
   // write back the window; store Q_W column-major with ld = QLD (= the update kernels' SMEM
   // layout), zero padded to KP x QLD
   {
     double* g = a.H + (int64_t)(w0 - a.hcol0) * n + w0;
-    for (int c = warp; c < kw; c += kChaseWarps) {
+    for (int c = warp; c < kw; c += kHWarps + kQWarps) {
       double* gc = g + (int64_t)c * n;
       for (int r = lane; r < kw; r += 32) gc[r] = Hs[r + c * ldh];
     }
   }
   const int KP = a.KP, QLD = a.QLD;
   double* Q = a.qslots + (size_t)(W.slot + a.slot_offset) * KP * QLD;
-  for (int c = warp; c < KP; c += kChaseWarps)
+  for (int c = warp; c < KP; c += kHWarps + kQWarps)
     for (int r = lane; r < QLD; r += 32)
       Q[r + c * QLD] = (r < kw && c < kw) ? Qs[r + c * ldh] : 0.0;
 }
@@ -202,11 +261,13 @@ __global__ void __launch_bounds__(kChaseThreads, 1) chase_kernel(StepArgs a) {
 }  // namespace
 
 size_t chase_smem_bytes(int kw, int nbc) {
+  (void)nbc;
   const int ldh = kw | 1;
-  return (size_t)2 * kw * ldh * sizeof(double) + (size_t)nbc * (3 * sizeof(double) + 2 * sizeof(int));
+  return (size_t)2 * kw * ldh * sizeof(double);
 }
 
 cudaError_t launch_chase(const StepArgs& a, int max_kw, int max_nbc, cudaStream_t st) {
+  if (max_nbc > kMaxRingBulges) return cudaErrorInvalidConfiguration;
   size_t smem = chase_smem_bytes(max_kw, max_nbc);
   static size_t configured = 0;
   if (smem > configured) {
