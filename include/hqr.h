@@ -44,10 +44,14 @@ typedef struct hqr_config {
   int flags;            /* bit 0: HQR_FLAG_NO_GRAPH -- launch kernels directly instead of         */
                         /*        replaying a captured CUDA graph                                 */
                         /* bit 1: HQR_FLAG_PROFILE  -- time every kernel class with CUDA events   */
+                        /*        (per-kernel launches, no fused step kernel)                     */
+                        /* bit 2: HQR_FLAG_NO_FUSE  -- separate chase / left / right launches     */
+                        /*        instead of the fused step kernel                                */
 } hqr_config;
 
 #define HQR_FLAG_NO_GRAPH 1
 #define HQR_FLAG_PROFILE 2
+#define HQR_FLAG_NO_FUSE 4
 
 /* Initialise the library on cfg->device: streams, events, workspace, NCCL communicator (world > 1).
  * Returns 0, -1 (cfg NULL or inconsistent rank/world/nccl_id), -101 (no usable sm_100 device),

@@ -32,6 +32,7 @@
 #include <climits>
 #include <cuda_runtime.h>
 
+#include "device_common.cuh"
 #include "kernels.hpp"
 
 namespace hqr {
@@ -43,75 +44,6 @@ constexpr int kQWarps = 8;                       // accumulation warps: Q_W <- Q
 constexpr int kChaseThreads = 32 * (kHWarps + kQWarps);
 constexpr int kRing = 8;                         // steps of reflectors in flight to the Q warps
 constexpr int kMaxRingBulges = 64;               // bulges per step the ring holds
-
-// Householder reflector (reading R2): P = I - tau v v^T, v = [1, v1, v2],
-// P x = beta e1 with beta = -sign(x0) ||x||, sign(0) = +1; zero tail -> identity.
-// With d = x0 - beta and r = 1 / (d * beta): v_i = x_i / d = x_i * beta * r, tau = -d / beta = -d*d*r.
-__device__ __forceinline__ void house(double x0, double x1, double x2, double& v1, double& v2,
-                                      double& tau, double& beta) {
-  const double tail2 = fma(x1, x1, x2 * x2);
-  if (tail2 == 0.0) {
-    v1 = 0.0; v2 = 0.0; tau = 0.0; beta = x0;
-    return;
-  }
-  const double nrm = sqrt(fma(x0, x0, tail2));
-  const double b = (x0 >= 0.0) ? -nrm : nrm;
-  const double d = x0 - b;
-  const double r = 1.0 / (d * b);
-  const double br = b * r;
-  v1 = x1 * br;
-  v2 = x2 * br;
-  tau = -d * d * r;
-  beta = b;
-}
-
-struct Refl {      // one reflector in the ring: P = I - tau v v^T acting on local columns pl+1..pl+m
-  double v1, v2, tau;
-  int pl, m;       // pl = INT_MIN: no reflector (inactive bulge or tau = 0)
-};
-
-__device__ __forceinline__ unsigned smem_u32(const void* p) {
-  return static_cast<unsigned>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.shared::cta.b64 st, [%0];\n}\n" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
-  asm volatile(
-      "{\n .reg .pred p;\n"
-      "WAIT_%=:\n"
-      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
-}
-__device__ __forceinline__ void named_sync(int id, int threads) {
-  asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(threads) : "memory");
-}
-
-// Apply reflector r from the right to `rows` rows of three (two) consecutive SMEM columns starting
-// at c1 (ld = ldh); lanes across rows.
-__device__ __forceinline__ void right_apply(double* c1, int ldh, int rows, const Refl& r, int lane) {
-  if (r.m == 3) {
-    for (int i = lane; i < rows; i += 32) {
-      double* x = c1 + i;
-      const double h0 = x[0], h1 = x[ldh], h2 = x[2 * ldh];
-      const double tw = r.tau * fma(r.v2, h2, fma(r.v1, h1, h0));
-      x[0] = h0 - tw;
-      x[ldh] = fma(-tw, r.v1, h1);
-      x[2 * ldh] = fma(-tw, r.v2, h2);
-    }
-  } else {
-    for (int i = lane; i < rows; i += 32) {
-      double* x = c1 + i;
-      const double h0 = x[0], h1 = x[ldh];
-      const double tw = r.tau * fma(r.v1, h1, h0);
-      x[0] = h0 - tw;
-      x[ldh] = fma(-tw, r.v1, h1);
-    }
-  }
-}
 
 __global__ void __launch_bounds__(kChaseThreads, 1) chase_kernel(StepArgs a) {
   extern __shared__ double sm[];

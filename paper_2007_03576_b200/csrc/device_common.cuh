@@ -1,0 +1,125 @@
+// device_common.cuh -- sm_100a device helpers shared by the product kernels (update.cu, chase.cu,
+// step.cu): FP64 mma.sync, mbarrier / bulk-copy / 2-D TMA wrappers, tile geometry.  Product path.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <climits>
+#include <cstdint>
+
+#include "kernels.hpp"
+
+namespace hqr {
+
+// Panel tile widths and SMEM ring depth: the factor Q_W (KP x pad_ld(KP)) stays resident, the ring
+// holds kStagesOf(KP) panel tiles; KP = 96 uses 48-wide tiles so three stages fit next to Q_W.
+__host__ __device__ constexpr int left_cols(int KP) { return KP <= 64 ? 64 : KP == 96 ? 48 : 32; }
+__host__ __device__ constexpr int right_rows(int KP) { return KP <= 64 ? 64 : KP == 96 ? 48 : 32; }
+__host__ __device__ constexpr int stages_of(int KP) { return KP <= 96 ? 3 : 2; }
+
+__device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+
+// ---- async copy / mbarrier helpers ---------------------------------------------------------
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool pred) {
+  int sz = pred ? 8 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(smem_u32(smem)), "l"(gmem), "r"(sz));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.shared::cta.b64 st, [%0];\n}\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n}\n"
+               ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+// 1-D bulk copy global -> shared through the TMA engine; completes tx bytes on `bar`
+__device__ __forceinline__ void bulk_g2s(void* smem, const void* gmem, unsigned bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+      ::"r"(smem_u32(smem)), "l"(gmem), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+// 2-D tensor (TMA) load of one box at (row c0, column c1); completes box bytes on `bar`
+__device__ __forceinline__ void tma_load_2d(void* smem, const CUtensorMap* tm, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n"
+      ::"r"(smem_u32(smem)), "l"(tm), "r"(c0), "r"(c1), "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+
+
+__device__ __forceinline__ void named_sync(int id, int threads) {
+  asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(threads) : "memory");
+}
+
+// Householder reflector (reading R2): P = I - tau v v^T, v = [1, v1, v2],
+// P x = beta e1 with beta = -sign(x0) ||x||, sign(0) = +1; zero tail -> identity.
+// With d = x0 - beta and r = 1 / (d * beta): v_i = x_i / d = x_i * beta * r, tau = -d / beta = -d*d*r.
+__device__ __forceinline__ void house(double x0, double x1, double x2, double& v1, double& v2,
+                                      double& tau, double& beta) {
+  const double tail2 = fma(x1, x1, x2 * x2);
+  if (tail2 == 0.0) {
+    v1 = 0.0; v2 = 0.0; tau = 0.0; beta = x0;
+    return;
+  }
+  const double nrm = sqrt(fma(x0, x0, tail2));
+  const double b = (x0 >= 0.0) ? -nrm : nrm;
+  const double d = x0 - b;
+  const double r = 1.0 / (d * b);
+  const double br = b * r;
+  v1 = x1 * br;
+  v2 = x2 * br;
+  tau = -d * d * r;
+  beta = b;
+}
+
+struct Refl {      // one reflector in the ring: P = I - tau v v^T acting on local columns pl+1..pl+m
+  double v1, v2, tau;
+  int pl, m;       // pl = INT_MIN: no reflector (inactive bulge or tau = 0)
+};
+
+
+// Apply reflector r from the right to `rows` rows of three (two) consecutive SMEM columns starting
+// at c1 (ld = ldh); lanes across rows.
+__device__ __forceinline__ void right_apply(double* c1, int ldh, int rows, const Refl& r, int lane) {
+  if (r.m == 3) {
+    for (int i = lane; i < rows; i += 32) {
+      double* x = c1 + i;
+      const double h0 = x[0], h1 = x[ldh], h2 = x[2 * ldh];
+      const double tw = r.tau * fma(r.v2, h2, fma(r.v1, h1, h0));
+      x[0] = h0 - tw;
+      x[ldh] = fma(-tw, r.v1, h1);
+      x[2 * ldh] = fma(-tw, r.v2, h2);
+    }
+  } else {
+    for (int i = lane; i < rows; i += 32) {
+      double* x = c1 + i;
+      const double h0 = x[0], h1 = x[ldh];
+      const double tw = r.tau * fma(r.v1, h1, h0);
+      x[0] = h0 - tw;
+      x[ldh] = fma(-tw, r.v1, h1);
+    }
+  }
+}
+
+
+}  // namespace hqr

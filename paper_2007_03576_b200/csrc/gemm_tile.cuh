@@ -1,0 +1,155 @@
+// gemm_tile.cuh -- one off-diagonal update tile on the FP64 tensor cores (mma.sync m8n8k4, SASS
+// DMMA.8x8x4), shared by the per-step update kernels (update.cu) and the fused step kernel
+// (step.cu).  Product path.
+//
+// LEFT  out[KP x NT] = Q_W^T[KP x KP] * P[KP x NT], P = H(W, c0 : c0+NT)
+// RIGHT out[MT x KP] = P[MT x KP] * Q_W[KP x KP],  P = H(r0 : r0+MT, W) or Z(r0 : r0+MT, W)
+// SMEM: Q_W resident as Qs[c*QLD + k] = Q_W[k][c] (the chase kernel's slot layout); the panel is one
+// 2-D TMA box: LEFT Ps[nn*LDP + ro + k] = H[(w0+k) + (c0+nn)*n] (ro = w0 & 1: TMA's innermost
+// coordinate must be 16-byte aligned), RIGHT Ps[k*LDP + m] = M[(r0+m) + (w0+k)*ld].  LDP = 4 (mod 16)
+// doubles makes the fragment loads conflict-free.  Box rows beyond the window / tile (other matrix
+// rows, or TMA's zero fill outside the matrix) meet the zero padding of Q_W or land in output rows
+// that are never stored.
+// A consumer group = 4 warps tiling the output 2 x 2.  The K loop stops at the Q_W structure bound
+// (Q_W[k][c] = 0 for k > c + 2 nbc, see update.cu); the two warps of a group pair that share an SM
+// sub-partition get complementary K extents.  Accumulators hold transposed output blocks so a thread
+// owns two consecutive output rows of one column: 16-byte stores into column-major storage.
+#pragma once
+#include "device_common.cuh"
+
+namespace hqr {
+
+template <int KP, bool LEFT>
+struct Geom {
+  static constexpr int NT = left_cols(KP), MT = right_rows(KP);
+  static constexpr int QLD = pad_ld(KP);
+  static constexpr int LDP = LEFT ? pad_ld(KP) : pad_ld(MT);
+  static constexpr int STAGE = LEFT ? NT * LDP : KP * LDP;        // doubles per SMEM stage
+  static constexpr int OM = LEFT ? KP : MT, ON = LEFT ? NT : KP;  // output tile
+  static constexpr int WM = OM / 2, WN = ON / 2;                  // warp tile
+  static constexpr int FM = WM / 8, FN = WN / 8;
+  static_assert(!LEFT || LDP >= KP + 1, "left panel box must hold the odd-row shift");
+  static_assert((STAGE * 8) % 128 == 0 && (KP * QLD * 8) % 128 == 0, "TMA destinations 128-byte aligned");
+};
+
+// Where one tile lives.  LEFT: columns [c0, c0 + NT) of H, clipped at lc1.  RIGHT: rows [r0, r1)
+// of M (H or Z), element (r, global column j) at M + r + (j - cb) * ld.
+struct TileRef {
+  int w0, kw, nbc;
+  double* M;
+  int64_t c0, lc1;   // LEFT
+  int64_t r0, r1;    // RIGHT
+  int64_t ld, cb;    // M's leading dimension and column base (LEFT: n, hcol0)
+  bool isZ;
+};
+
+// Producer (one lane): arm the stage barrier with the box size and issue the TMA box load.
+template <int KP, bool LEFT>
+__device__ __forceinline__ void produce_tile(double* dst, uint64_t* full, const CUtensorMap* tmH,
+                                             const CUtensorMap* tmZ, const TileRef& t) {
+  using G = Geom<KP, LEFT>;
+  mbar_arrive_tx(full, (unsigned)(G::STAGE * 8));  // TMA always lands the full box
+  if (LEFT)
+    tma_load_2d(dst, tmH, t.w0 & ~1, (int)(t.c0 - t.cb), full);
+  else
+    tma_load_2d(dst, t.isZ ? tmZ : tmH, (int)t.r0, (int)(t.w0 - t.cb), full);
+}
+
+// Consumer warp `i4` (0..3) of group `q` (0..1): K loop over the stage `P` with Q_W in `Qs`,
+// release the stage (`empty`), store the tile in place.
+template <int KP, bool LEFT>
+__device__ __forceinline__ void consume_tile(const double* Qs, const double* P, uint64_t* empty,
+                                             const TileRef& t, int q, int i4, int lane) {
+  using G = Geom<KP, LEFT>;
+  constexpr int FM = G::FM, FN = G::FN, WM = G::WM, WN = G::WN, QLD = G::QLD, LDP = G::LDP;
+  const int kg = (i4 & 1) ^ q;   // the index (row group LEFT / column group RIGHT) that sets K
+  const int og = i4 >> 1;
+  const int wm0 = (LEFT ? kg : og) * WM, wn0 = (LEFT ? og : kg) * WN;
+  const int lr = lane >> 2, lk = lane & 3;
+#ifdef HQR_BENCH_NO_TRIM  // benchmark-only knob (tools/gemm_bench.cu), never set in the product build
+  const int kend = KP;
+#else
+  const int kend = min(KP, ((LEFT ? wm0 + WM : wn0 + WN) + 2 * t.nbc + 3) & ~3);
+#endif
+  double acc[FN][FM][2];
+#pragma unroll
+  for (int jn = 0; jn < FN; ++jn)
+#pragma unroll
+    for (int i = 0; i < FM; ++i) acc[jn][i][0] = acc[jn][i][1] = 0.0;
+  const double* A;
+  const double* B;
+  int a_i, a_k, b_j, b_k;
+  if (LEFT) {
+    A = Qs + (wm0 + lr) * QLD + lk;                  a_i = 8 * QLD; a_k = 1;
+    B = P + (wn0 + lr) * LDP + (t.w0 & 1) + lk;      b_j = 8 * LDP; b_k = 1;
+  } else {
+    A = P + lk * LDP + wm0 + lr;                     a_i = 8;       a_k = LDP;
+    B = Qs + (wn0 + lr) * QLD + lk;                  b_j = 8 * QLD; b_k = 1;
+  }
+  // software-pipelined K loop: fragments of k-step t+1 are loaded before the mma of step t
+  double fa[2][FM], fb[2][FN];
+#pragma unroll
+  for (int i = 0; i < FM; ++i) fa[0][i] = A[i * a_i];
+#pragma unroll
+  for (int jn = 0; jn < FN; ++jn) fb[0][jn] = B[jn * b_j];
+  for (int kk = 0; kk < kend; kk += 8) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int kn = kk + 4 * (h + 1);
+      if (kn - 4 >= kend) break;
+      if (kn < kend) {
+#pragma unroll
+        for (int i = 0; i < FM; ++i) fa[h ^ 1][i] = A[i * a_i + kn * a_k];
+#pragma unroll
+        for (int jn = 0; jn < FN; ++jn) fb[h ^ 1][jn] = B[jn * b_j + kn * b_k];
+      }
+#pragma unroll
+      for (int jn = 0; jn < FN; ++jn)
+#pragma unroll
+        for (int i = 0; i < FM; ++i) dmma(acc[jn][i], fb[h][jn], fa[h][i]);
+    }
+  }
+  __syncwarp();
+  if (lane == 0) mbar_arrive(empty);
+#ifdef HQR_BENCH_NO_STORE  // benchmark-only knob (tools/gemm_bench.cu), never set in the product build
+  if (acc[0][0][0] != 12345.678) return;
+#endif
+  // epilogue: thread (lr, lk) owns out[m = m0 + 8i + 2lk + {0,1}][n = n0 + 8jn + lr]
+  if (LEFT) {
+    const bool even = (t.w0 & 1) == 0;
+#pragma unroll
+    for (int jn = 0; jn < FN; ++jn) {
+      const int64_t col = t.c0 + wn0 + 8 * jn + lr;
+      if (col >= t.lc1) continue;
+      double* cp = t.M + (col - t.cb) * t.ld + t.w0;
+#pragma unroll
+      for (int i = 0; i < FM; ++i) {
+        const int m = wm0 + 8 * i + 2 * lk;
+        if (even && m + 1 < t.kw) {
+          *reinterpret_cast<double2*>(cp + m) = make_double2(acc[jn][i][0], acc[jn][i][1]);
+        } else {
+          if (m < t.kw) cp[m] = acc[jn][i][0];
+          if (m + 1 < t.kw) cp[m + 1] = acc[jn][i][1];
+        }
+      }
+    }
+  } else {
+#pragma unroll
+    for (int jn = 0; jn < FN; ++jn) {
+      const int col = wn0 + 8 * jn + lr;
+      if (col >= t.kw) continue;
+      double* cp = t.M + (t.w0 + col - t.cb) * t.ld;
+#pragma unroll
+      for (int i = 0; i < FM; ++i) {
+        const int64_t row = t.r0 + wm0 + 8 * i + 2 * lk;  // even: 16-byte aligned pair
+        if (row + 1 < t.r1) {
+          *reinterpret_cast<double2*>(cp + row) = make_double2(acc[jn][i][0], acc[jn][i][1]);
+        } else if (row < t.r1) {
+          cp[row] = acc[jn][i][0];
+        }
+      }
+    }
+  }
+}
+
+}  // namespace hqr

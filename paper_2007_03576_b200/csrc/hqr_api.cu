@@ -26,6 +26,7 @@
 #include "dist.hpp"
 #include "kernels.hpp"
 #include "plan.hpp"
+#include "step.hpp"
 
 using hqr::Plan;
 using hqr::StepArgs;
@@ -66,10 +67,19 @@ struct CachedGraph {
   hqr_stats stats;
 };
 
+struct FusedTasks {            // task queues of every step for the fused step kernel
+  std::vector<hqr::Task> tasks;
+  std::vector<int32_t> begin, nL, nRn;
+  hqr::Task* d_tasks = nullptr;
+  hqr::StepCounters* d_ctr = nullptr;
+  double flops = 0, bytes = 0;
+};
+
 struct CachedPlan {
   Plan plan;
   WindowDesc* d_wins = nullptr;
   int KP = 0;
+  std::unique_ptr<FusedTasks> fused[2];  // [Z absent, Z present]
 };
 
 struct State {
@@ -286,6 +296,88 @@ int enqueue_sweep(const CachedPlan& cp, double* H, double* Z, int64_t n, bool pr
   return 0;
 }
 
+// Fused path (single GPU, TMA-capable layout): chase(0), then one step-kernel launch per step that
+// runs the step's updates and the next step's chase from a prioritised task queue (step.cu).
+constexpr int kFusedChunk = 12;  // tiles per GEMM task
+
+int get_fused(CachedPlan& cp, bool has_z, int64_t n, FusedTasks** out) {
+  auto& slot = cp.fused[has_z ? 1 : 0];
+  if (!slot) {
+    auto f = std::make_unique<FusedTasks>();
+    const Plan& P = cp.plan;
+    // sp(g): smallest first row of any window of a later step (suffix minimum), rounded to even
+    std::vector<int64_t> sp(P.nsteps, INT64_MAX);
+    int64_t run = INT64_MAX;
+    for (int g = P.nsteps - 1; g >= 0; --g) {
+      sp[g] = (run == INT64_MAX) ? run : (run & ~(int64_t)1);
+      for (int i = P.step_begin[g]; i < P.step_begin[g + 1]; ++i) run = std::min<int64_t>(run, P.windows[i].w0);
+    }
+    StepArgs a{};
+    a.n = n; a.hcol0 = 0; a.lc0 = 0; a.lc1 = n; a.zrows = n; a.ldz = n; a.KP = cp.KP;
+    a.Z = has_z ? reinterpret_cast<double*>(1) : nullptr;  // only tested for presence
+    for (int g = 0; g < P.nsteps; ++g) {
+      f->begin.push_back((int32_t)f->tasks.size());
+      const WindowDesc* w = P.windows.data() + P.step_begin[g];
+      const int nw = P.step_begin[g + 1] - P.step_begin[g];
+      const WindowDesc* wn = (g + 1 < P.nsteps) ? P.windows.data() + P.step_begin[g + 1] : nullptr;
+      const int nn = (g + 1 < P.nsteps) ? P.step_begin[g + 2] - P.step_begin[g + 1] : 0;
+      int nl, nrn;
+      hqr::build_step_tasks(a, w, nw, wn, nn, sp[g], kFusedChunk, &f->tasks, &nl, &nrn);
+      f->nL.push_back(nl);
+      f->nRn.push_back(nrn);
+      for (int i = 0; i < nw; ++i) {
+        const double kw = w[i].w1 - w[i].w0 + 1;
+        const double rows = (double)(n - 1 - w[i].w1) + (double)w[i].w0 + (has_z ? (double)n : 0.0);
+        f->flops += 2.0 * kw * kw * rows;
+        f->bytes += 16.0 * kw * rows;
+      }
+    }
+    f->begin.push_back((int32_t)f->tasks.size());
+    CK(cudaMalloc(&f->d_tasks, f->tasks.size() * sizeof(hqr::Task)));
+    CK(cudaMemcpy(f->d_tasks, f->tasks.data(), f->tasks.size() * sizeof(hqr::Task), cudaMemcpyHostToDevice));
+    CK(cudaMalloc(&f->d_ctr, (size_t)P.nsteps * sizeof(hqr::StepCounters)));
+    slot = std::move(f);
+  }
+  *out = slot.get();
+  return 0;
+}
+
+int enqueue_fused(CachedPlan& cp, double* H, double* Z, int64_t n, const hqr::TensorMaps& tm,
+                  hqr_stats* st) {
+  const Plan& P = cp.plan;
+  FusedTasks* f = nullptr;
+  int rc = get_fused(cp, Z != nullptr, n, &f);
+  if (rc) return rc;
+  cudaStream_t A = g.stream;
+  CK(cudaMemsetAsync(f->d_ctr, 0, (size_t)P.nsteps * sizeof(hqr::StepCounters), A));
+  auto args = [&](int s) {
+    StepArgs a{};
+    a.H = H; a.Z = Z; a.n = n; a.ilo = P.ilo; a.ihi = P.ihi;
+    a.hcol0 = 0; a.lc0 = 0; a.lc1 = n; a.zrows = n; a.ldz = n;
+    a.wins = cp.d_wins; a.coef = g.d_coef; a.qslots = g.d_q; a.KP = cp.KP; a.QLD = hqr::pad_ld(cp.KP);
+    if (s < P.nsteps) {
+      a.win_begin = P.step_begin[s];
+      a.win_count = P.step_begin[s + 1] - P.step_begin[s];
+      a.slot_offset = (s % hqr::kQSets) * P.nchains;
+    }
+    return a;
+  };
+  CK(hqr::launch_chase(args(0), P.max_kw, P.max_nbc, A));
+  st->launches_chase++;
+  for (int s = 0; s < P.nsteps; ++s) {
+    const int nt = f->begin[s + 1] - f->begin[s];
+    CK(hqr::launch_step(args(s), args(s + 1), f->d_tasks + f->begin[s], nt, f->nL[s], f->nRn[s],
+                        f->d_ctr + s, tm, P.max_kw, g.num_sms, A));
+    st->launches_left++;  // one fused launch per step (counted once)
+  }
+  st->flops_update = f->flops;
+  st->bytes_update = f->bytes;
+  st->steps = P.nsteps;
+  st->windows = (int64_t)P.windows.size();
+  st->kernels_launched = st->launches_chase + st->launches_left;
+  return 0;
+}
+
 }  // namespace
 
 extern "C" {
@@ -336,8 +428,14 @@ int hqr_teardown(void) {
   cudaStreamSynchronize(g.stream);
   for (auto& kv : g.graphs) cudaGraphExecDestroy(kv.second.exec);
   g.graphs.clear();
-  for (auto& kv : g.plans)
+  for (auto& kv : g.plans) {
     if (kv.second->d_wins) cudaFree(kv.second->d_wins);
+    for (auto& f : kv.second->fused)
+      if (f) {
+        if (f->d_tasks) cudaFree(f->d_tasks);
+        if (f->d_ctr) cudaFree(f->d_ctr);
+      }
+  }
   g.plans.clear();
   for (auto e : g.prof_events) cudaEventDestroy(e);
   g.prof_events.clear();
@@ -458,6 +556,15 @@ int sweep_impl(double* H, double* Z, int64_t n, const Blocks& blocks, const doub
   const bool prof = (g.flags & HQR_FLAG_PROFILE) != 0;
   const bool use_graph = !prof && !(g.flags & HQR_FLAG_NO_GRAPH);
   std::vector<int> classes;
+  hqr::TensorMaps tmf;
+  CK(hqr::make_tensor_maps(&tmf, dH, n, dZ, n, n, n, cp->KP));
+  const bool fused = tmf.valid && !(g.flags & HQR_FLAG_NO_FUSE) && !prof &&
+                     cp->plan.max_nbc <= hqr::kMaxChaseBulges;
+  if (fused) {  // build / upload the task queues outside any stream capture
+    FusedTasks* f = nullptr;
+    rc = get_fused(*cp, dZ != nullptr, n, &f);
+    if (rc) return rc;
+  }
   if (use_graph) {
     GraphKey gk{plan_key(n, blocks, window), dH, dZ};
     auto it = g.graphs.find(gk);
@@ -465,7 +572,8 @@ int sweep_impl(double* H, double* Z, int64_t n, const Blocks& blocks, const doub
       cudaGraph_t graph;
       CK(cudaStreamBeginCapture(g.stream, cudaStreamCaptureModeThreadLocal));
       hqr_stats cap{};
-      int rc2 = enqueue_sweep(*cp, dH, dZ, n, false, nullptr, &cap);
+      int rc2 = fused ? enqueue_fused(*cp, dH, dZ, n, tmf, &cap)
+                      : enqueue_sweep(*cp, dH, dZ, n, false, nullptr, &cap);
       cudaError_t ec = cudaStreamEndCapture(g.stream, &graph);
       if (rc2) return rc2;
       CK(ec);
@@ -484,6 +592,9 @@ int sweep_impl(double* H, double* Z, int64_t n, const Blocks& blocks, const doub
     st.steps = c.steps;
     st.windows = c.windows;
     st.kernels_launched = c.kernels_launched;
+  } else if (fused) {
+    rc = enqueue_fused(*cp, dH, dZ, n, tmf, &st);
+    if (rc) return rc;
   } else {
     rc = enqueue_sweep(*cp, dH, dZ, n, prof, &classes, &st);
     if (rc) return rc;

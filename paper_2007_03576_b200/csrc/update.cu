@@ -29,6 +29,8 @@
 #include <cstdio>
 #include <cstdlib>
 
+#include "device_common.cuh"
+#include "gemm_tile.cuh"
 #include "kernels.hpp"
 
 namespace hqr {
@@ -39,61 +41,6 @@ constexpr int kConsumerWarps = 8;
 constexpr int kThreadsGeneric = 256;
 constexpr int kThreadsBulk = 288;  // 8 consumer warps + 1 producer warp
 constexpr int kMaxStepWindows = 128;
-
-// Panel tile widths and SMEM ring depth: the factor Q_W (KP x pad_ld(KP)) stays resident, the ring
-// holds kStagesOf(KP) panel tiles; KP = 96 uses 48-wide tiles so three stages fit next to Q_W.
-__host__ __device__ constexpr int left_cols(int KP) { return KP <= 64 ? 64 : KP == 96 ? 48 : 32; }
-__host__ __device__ constexpr int right_rows(int KP) { return KP <= 64 ? 64 : KP == 96 ? 48 : 32; }
-__host__ __device__ constexpr int stages_of(int KP) { return KP <= 96 ? 3 : 2; }
-
-__device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
-               : "+d"(c[0]), "+d"(c[1])
-               : "d"(a), "d"(b));
-}
-
-// ---- async copy / mbarrier helpers ---------------------------------------------------------
-__device__ __forceinline__ unsigned smem_u32(const void* p) {
-  return static_cast<unsigned>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool pred) {
-  int sz = pred ? 8 : 0;
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(smem_u32(smem)), "l"(gmem), "r"(sz));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
-
-__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.shared::cta.b64 st, [%0];\n}\n" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, unsigned bytes) {
-  asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n}\n"
-               ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
-  asm volatile(
-      "{\n .reg .pred p;\n"
-      "WAIT_%=:\n"
-      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
-}
-// 1-D bulk copy global -> shared through the TMA engine; completes tx bytes on `bar`
-__device__ __forceinline__ void bulk_g2s(void* smem, const void* gmem, unsigned bytes, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
-      ::"r"(smem_u32(smem)), "l"(gmem), "r"(bytes), "r"(smem_u32(bar)) : "memory");
-}
-// 2-D tensor (TMA) load of one box at (row c0, column c1); completes box bytes on `bar`
-__device__ __forceinline__ void tma_load_2d(void* smem, const CUtensorMap* tm, int c0, int c1, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n"
-      ::"r"(smem_u32(smem)), "l"(tm), "r"(c0), "r"(c1), "r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
 
 // per-CTA item decoder: the step's windows with their tile counts (prefix sums in SMEM)
 struct StepItems {
@@ -136,16 +83,9 @@ template <int KP, bool LEFT>
 __global__ void __launch_bounds__(kThreadsBulk, 1)
     bulk_update_kernel(StepArgs a, int64_t total_items, const __grid_constant__ CUtensorMap tmH,
                        const __grid_constant__ CUtensorMap tmZ) {
-  constexpr int NT = left_cols(KP), MT = right_rows(KP);
-  constexpr int QLD = pad_ld(KP);
-  constexpr int LDP = LEFT ? pad_ld(KP) : pad_ld(MT);
-  constexpr int STAGE = LEFT ? NT * LDP : KP * LDP;        // doubles per SMEM stage
-  constexpr int OM = LEFT ? KP : MT, ON = LEFT ? NT : KP;  // output tile
-  constexpr int WM = OM / 2, WN = ON / 2;                  // warp tile (2 x 2 warps per group)
-  constexpr int FM = WM / 8, FN = WN / 8;
+  using G = Geom<KP, LEFT>;
+  constexpr int NT = G::NT, MT = G::MT, QLD = G::QLD, STAGE = G::STAGE;
   constexpr int NS = stages_of(KP);
-  static_assert(!LEFT || LDP >= KP + 1, "left panel box must hold the odd-row shift");
-  static_assert((STAGE * 8) % 128 == 0 && (KP * QLD * 8) % 128 == 0, "TMA destinations 128-byte aligned");
   extern __shared__ __align__(1024) double sm[];
   double* Qs = sm;                       // KP x QLD
   double* Ps = Qs + KP * QLD;            // NS stages (128-byte aligned: TMA destinations)
@@ -182,21 +122,27 @@ __global__ void __launch_bounds__(kThreadsBulk, 1)
   fence_proxy_async();
   __syncthreads();
 
-  const int64_t G = gridDim.x;
-  const int64_t it0 = total_items * blockIdx.x / G, it1 = total_items * (blockIdx.x + 1) / G;
-  // RIGHT: matrix, row range, leading dimension and column base of a tile (element (r, global
-  // column j) at M + r + (j - cb) * ld)
-  auto panel = [&](int wi, int64_t tile, double*& M, int64_t& r0, int64_t& r1, int64_t& ld,
-                   int64_t& cb) {
-    if (tile < si.rt[wi]) {
-      M = a.H; r0 = tile * MT; r1 = si.w[wi].w0; ld = n; cb = a.hcol0;
+  const int64_t G0 = gridDim.x;
+  const int64_t it0 = total_items * blockIdx.x / G0, it1 = total_items * (blockIdx.x + 1) / G0;
+  auto tile_ref = [&](int wi, int64_t tile) {
+    const WindowDesc& w = si.w[wi];
+    TileRef t;
+    t.w0 = w.w0; t.kw = w.w1 - w.w0 + 1; t.nbc = w.nbc;
+    if (LEFT) {
+      t.M = a.H; t.c0 = si.rt[wi] + tile * NT; t.lc1 = a.lc1; t.ld = n; t.cb = a.hcol0; t.isZ = false;
+      t.r0 = t.r1 = 0;
+    } else if (tile < si.rt[wi]) {
+      t.M = a.H; t.r0 = tile * MT; t.r1 = w.w0; t.ld = n; t.cb = a.hcol0; t.isZ = false;
+      t.c0 = t.lc1 = 0;
     } else {
-      M = a.Z; r0 = (tile - si.rt[wi]) * MT; r1 = a.zrows; ld = a.ldz; cb = 0;
+      t.M = a.Z; t.r0 = (tile - si.rt[wi]) * MT; t.r1 = a.zrows; t.ld = a.ldz; t.cb = 0; t.isZ = true;
+      t.c0 = t.lc1 = 0;
     }
+    return t;
   };
 
   if (warp == kConsumerWarps) {
-    // ---------------- producer warp: bulk copies (TMA engine) ----------------
+    // ---------------- producer warp: TMA ----------------
     int cur = -1;
     unsigned nq = 0;
     for (int64_t it = it0; it < it1; ++it) {
@@ -217,29 +163,12 @@ __global__ void __launch_bounds__(kThreadsBulk, 1)
       const int64_t j = it - it0;
       const int s = (int)(j % NS);
       if (j >= NS) mbar_wait(&empty[s], (unsigned)((j / NS) - 1) & 1);
-      double* dst = Ps + s * STAGE;
-      if (lane == 0) {
-        mbar_arrive_tx(&full[s], (unsigned)(STAGE * 8));  // TMA always lands the full box
-        if (LEFT) {
-          // the innermost TMA coordinate must address a 16-byte boundary: start at the even row
-          // w0 - ro (ro = w0 & 1); the consumers offset their reads by ro
-          tma_load_2d(dst, &tmH, w.w0 & ~1, (int)(si.rt[wi] + tile * NT - a.hcol0), &full[s]);
-        } else {
-          double* M;
-          int64_t r0, r1, ld, cb;
-          panel(wi, tile, M, r0, r1, ld, cb);
-          tma_load_2d(dst, M == a.H ? &tmH : &tmZ, (int)r0, (int)(w.w0 - cb), &full[s]);
-        }
-      }
+      if (lane == 0) produce_tile<KP, LEFT>(Ps + s * STAGE, &full[s], &tmH, &tmZ, tile_ref(wi, tile));
       __syncwarp();
     }
   } else {
-    // ---------------- consumer groups ----------------
+    // ---------------- consumer groups: group q takes items j = q (mod 2) ----------------
     const int q = warp >> 2, i4 = warp & 3;
-    const int kg = (i4 & 1) ^ q;   // the index (row group LEFT / column group RIGHT) that sets K
-    const int og = i4 >> 1;        // the other output index
-    const int wm0 = (LEFT ? kg : og) * WM, wn0 = (LEFT ? og : kg) * WN;
-    const int lr = lane >> 2, lk = lane & 3;
     int cur = -1;
     unsigned nq = 0;
     for (int64_t it = it0; it < it1; ++it) {
@@ -256,104 +185,9 @@ __global__ void __launch_bounds__(kThreadsBulk, 1)
       }
       const int64_t j = it - it0;
       if ((int)(j & 1) != q) continue;
-      const WindowDesc& w = si.w[wi];
       const int s = (int)(j % NS);
       mbar_wait(&full[s], (unsigned)(j / NS) & 1);
-      // Q_W[k][c] = 0 for k > c + 2 nbc: K stops after this warp's last row (LEFT) / column (RIGHT)
-#ifdef HQR_BENCH_NO_TRIM  // benchmark-only knob (tools/gemm_bench.cu), never set in the product build
-      const int kend = KP;
-#else
-      const int kend = min(KP, ((LEFT ? wm0 + WM : wn0 + WN) + 2 * w.nbc + 3) & ~3);
-#endif
-      // accumulators hold the TRANSPOSED output blocks (mma with the operands swapped), so each
-      // thread owns two consecutive output ROWS of one column: 16-byte stores into column-major
-      double acc[FN][FM][2];
-#pragma unroll
-      for (int jn = 0; jn < FN; ++jn)
-#pragma unroll
-        for (int i = 0; i < FM; ++i) acc[jn][i][0] = acc[jn][i][1] = 0.0;
-      const double* P = Ps + s * STAGE;
-      // fragment sources: fa = M-side (rows of out), fb = N-side (columns of out)
-      const double* A;
-      const double* B;
-      int a_i, a_k, b_j, b_k;  // strides of fragment i / k-step for A, fragment j / k-step for B
-      if (LEFT) {
-        A = Qs + (wm0 + lr) * QLD + lk;                    a_i = 8 * QLD; a_k = 1;
-        B = P + (wn0 + lr) * LDP + (w.w0 & 1) + lk;        b_j = 8 * LDP; b_k = 1;
-      } else {
-        A = P + lk * LDP + wm0 + lr;                       a_i = 8;       a_k = LDP;
-        B = Qs + (wn0 + lr) * QLD + lk;                    b_j = 8 * QLD; b_k = 1;
-      }
-      // software-pipelined K loop: fragments of k-step t+1 are loaded before the mma of step t
-      double fa[2][FM], fb[2][FN];
-#pragma unroll
-      for (int i = 0; i < FM; ++i) fa[0][i] = A[i * a_i];
-#pragma unroll
-      for (int jn = 0; jn < FN; ++jn) fb[0][jn] = B[jn * b_j];
-      for (int kk = 0; kk < kend; kk += 8) {
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int kn = kk + 4 * (h + 1);
-          if (kn - 4 >= kend) break;
-          if (kn < kend) {
-#pragma unroll
-            for (int i = 0; i < FM; ++i) fa[h ^ 1][i] = A[i * a_i + kn * a_k];
-#pragma unroll
-            for (int jn = 0; jn < FN; ++jn) fb[h ^ 1][jn] = B[jn * b_j + kn * b_k];
-          }
-#pragma unroll
-          for (int jn = 0; jn < FN; ++jn)
-#pragma unroll
-            for (int i = 0; i < FM; ++i) dmma(acc[jn][i], fb[h][jn], fa[h][i]);
-        }
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);
-      // epilogue: in-place stores straight from the accumulators; thread (lr, lk) owns
-      // out[m = m0 + 8i + 2lk + {0,1}][n = n0 + 8jn + lr]
-      const int kw = w.w1 - w.w0 + 1;
-#ifdef HQR_BENCH_NO_STORE  // benchmark-only knob (tools/gemm_bench.cu), never set in the product build
-      if (acc[0][0][0] != 12345.678) continue;
-#endif
-      if (LEFT) {
-        const int64_t c0 = si.rt[wi] + tile * NT;
-        const bool even = (w.w0 & 1) == 0;
-#pragma unroll
-        for (int jn = 0; jn < FN; ++jn) {
-          const int64_t col = c0 + wn0 + 8 * jn + lr;
-          if (col >= a.lc1) continue;
-          double* cp = a.H + (col - a.hcol0) * n + w.w0;
-#pragma unroll
-          for (int i = 0; i < FM; ++i) {
-            const int m = wm0 + 8 * i + 2 * lk;
-            if (even && m + 1 < kw) {
-              *reinterpret_cast<double2*>(cp + m) = make_double2(acc[jn][i][0], acc[jn][i][1]);
-            } else {
-              if (m < kw) cp[m] = acc[jn][i][0];
-              if (m + 1 < kw) cp[m + 1] = acc[jn][i][1];
-            }
-          }
-        }
-      } else {
-        double* M;
-        int64_t r0, r1, ld, cb;
-        panel(wi, tile, M, r0, r1, ld, cb);
-#pragma unroll
-        for (int jn = 0; jn < FN; ++jn) {
-          const int col = wn0 + 8 * jn + lr;
-          if (col >= kw) continue;
-          double* cp = M + (w.w0 + col - cb) * ld;
-#pragma unroll
-          for (int i = 0; i < FM; ++i) {
-            const int64_t row = r0 + wm0 + 8 * i + 2 * lk;  // even: 16-byte aligned pair
-            if (row + 1 < r1) {
-              *reinterpret_cast<double2*>(cp + row) = make_double2(acc[jn][i][0], acc[jn][i][1]);
-            } else if (row < r1) {
-              cp[row] = acc[jn][i][0];
-            }
-          }
-        }
-      }
+      consume_tile<KP, LEFT>(Qs, Ps + s * STAGE, &empty[s], tile_ref(wi, tile), q, i4, lane);
     }
   }
 }
