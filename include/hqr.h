@@ -43,8 +43,7 @@ typedef struct hqr_config {
   int64_t n_max;        /* largest n this setup will sweep (workspace hint; 0 = grow on demand)  */
   int flags;            /* bit 0: HQR_FLAG_NO_GRAPH -- launch kernels directly instead of         */
                         /*        replaying a captured CUDA graph                                 */
-                        /* bit 1: HQR_FLAG_PROFILE  -- time every kernel class with CUDA events   */
-                        /*        (per-kernel launches, no fused step kernel)                     */
+                        /* bit 1: HQR_FLAG_PROFILE  -- time every launch with CUDA events         */
                         /* bit 2: HQR_FLAG_NO_FUSE  -- separate chase / left / right launches     */
                         /*        instead of the fused step kernel                                */
 } hqr_config;
@@ -171,6 +170,7 @@ typedef struct hqr_stats {
   double ms_chase;            /* HQR_FLAG_PROFILE only: summed CUDA-event time per kernel class    */
   double ms_left;
   double ms_right;            /* right update + fused Z update                                    */
+  double ms_step;             /* fused step kernels (updates of step g + chase of step g+1)       */
   double ms_total;            /* CUDA-event time of the whole sweep (device work only)            */
   int64_t h2d_bytes, d2h_bytes; /* staging copies (host-pointer calls)                           */
   int launches_left, launches_right, launches_chase;

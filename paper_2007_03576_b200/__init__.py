@@ -54,7 +54,7 @@ class Stats(ctypes.Structure):
                 ("windows", ctypes.c_int64), ("flops_update", ctypes.c_double),
                 ("flops_chase", ctypes.c_double), ("bytes_update", ctypes.c_double),
                 ("ms_chase", ctypes.c_double), ("ms_left", ctypes.c_double),
-                ("ms_right", ctypes.c_double), ("ms_total", ctypes.c_double),
+                ("ms_right", ctypes.c_double), ("ms_step", ctypes.c_double), ("ms_total", ctypes.c_double),
                 ("h2d_bytes", ctypes.c_int64), ("d2h_bytes", ctypes.c_int64),
                 ("launches_left", ctypes.c_int), ("launches_right", ctypes.c_int),
                 ("launches_chase", ctypes.c_int), ("window_eff", ctypes.c_int)]

@@ -343,7 +343,7 @@ int get_fused(CachedPlan& cp, bool has_z, int64_t n, FusedTasks** out) {
 }
 
 int enqueue_fused(CachedPlan& cp, double* H, double* Z, int64_t n, const hqr::TensorMaps& tm,
-                  hqr_stats* st) {
+                  hqr_stats* st, bool prof = false, std::vector<int>* classes = nullptr) {
   const Plan& P = cp.plan;
   FusedTasks* f = nullptr;
   int rc = get_fused(cp, Z != nullptr, n, &f);
@@ -362,12 +362,22 @@ int enqueue_fused(CachedPlan& cp, double* H, double* Z, int64_t n, const hqr::Te
     }
     return a;
   };
+  size_t ev = 0;
+  auto mark = [&](int cls) {  // prof: events around every launch (class 0 chase, 3 fused step)
+    if (!prof) return;
+    cudaEventRecord(prof_event(ev++), A);
+    if (classes) classes->push_back(cls);
+  };
+  mark(0);
   CK(hqr::launch_chase(args(0), P.max_kw, P.max_nbc, A));
+  mark(-1);
   st->launches_chase++;
   for (int s = 0; s < P.nsteps; ++s) {
     const int nt = f->begin[s + 1] - f->begin[s];
+    mark(3);
     CK(hqr::launch_step(args(s), args(s + 1), f->d_tasks + f->begin[s], nt, f->nL[s], f->nRn[s],
                         f->d_ctr + s, tm, P.max_kw, g.num_sms, A));
+    mark(-1);
     st->launches_left++;  // one fused launch per step (counted once)
   }
   st->flops_update = f->flops;
@@ -558,7 +568,7 @@ int sweep_impl(double* H, double* Z, int64_t n, const Blocks& blocks, const doub
   std::vector<int> classes;
   hqr::TensorMaps tmf;
   CK(hqr::make_tensor_maps(&tmf, dH, n, dZ, n, n, n, cp->KP));
-  const bool fused = tmf.valid && !(g.flags & HQR_FLAG_NO_FUSE) && !prof &&
+  const bool fused = tmf.valid && !(g.flags & HQR_FLAG_NO_FUSE) &&
                      cp->plan.max_nbc <= hqr::kMaxChaseBulges;
   if (fused) {  // build / upload the task queues outside any stream capture
     FusedTasks* f = nullptr;
@@ -593,7 +603,7 @@ int sweep_impl(double* H, double* Z, int64_t n, const Blocks& blocks, const doub
     st.windows = c.windows;
     st.kernels_launched = c.kernels_launched;
   } else if (fused) {
-    rc = enqueue_fused(*cp, dH, dZ, n, tmf, &st);
+    rc = enqueue_fused(*cp, dH, dZ, n, tmf, &st, prof, &classes);
     if (rc) return rc;
   } else {
     rc = enqueue_sweep(*cp, dH, dZ, n, prof, &classes, &st);
@@ -621,7 +631,8 @@ int sweep_impl(double* H, double* Z, int64_t n, const Blocks& blocks, const doub
       cudaEventElapsedTime(&e, g.prof_events[i], g.prof_events[i + 1]);
       if (classes[i] == 0) st.ms_chase += e;
       else if (classes[i] == 1) st.ms_left += e;
-      else st.ms_right += e;
+      else if (classes[i] == 2) st.ms_right += e;
+      else st.ms_step += e;
     }
   }
   // in-window chase flops (per 3-reflector: 10 flops x (left cols + right rows + Q rows))

@@ -214,3 +214,21 @@ def test_sharded_virtual_ranks(vworld, case):
     Hg, Zg = hq.from_device(Hd), hq.from_device(Zd)
     Ho, Zo = oracle_sweep(H0, Z0, 0, n - 1, re_, im_)
     check(Hg, Zg, Ho, Zo, H0, 0, n - 1)
+
+
+@pytest.mark.parametrize("case", [(70, 600, 60, 96), (71, 1000, 100, 64), (72, 400, 40, 112)])
+def test_fused_step_kernel_matches_separate_launches(case):
+    """The fused step kernel (prioritised task queue, chase of step g+1 inside step g's launch) and
+    the separate chase / left / right launches compute every element with the same operations in
+    the same order: bitwise equal."""
+    seed, n, ns, win = case
+    H0, Z0, re_, im_ = random_case(seed, n, ns, z0="orth", shift_kind="disk2")
+    Hf, Zf = gpu_sweep(H0, Z0, 0, n - 1, re_, im_, win)
+    hq.teardown()
+    hq.setup(0, flags=hq.FLAG_NO_FUSE)
+    try:
+        Hs, Zs = gpu_sweep(H0, Z0, 0, n - 1, re_, im_, win)
+    finally:
+        hq.teardown()
+        hq.setup(0)
+    assert np.array_equal(Hf, Hs) and np.array_equal(Zf, Zs)
