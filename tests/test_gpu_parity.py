@@ -186,7 +186,13 @@ def _gpu_invariants(Hd, Zd, H0d, Z0d, n):
 def test_full_size_parity_against_oracle(cfg):
     """BASELINE configs[2] (n = 10000) and configs[3] (n = 20000) in the bench's launch
     configuration (default window), element by element against the oracle run on the host cores,
-    plus the invariants computed on the GPU."""
+    plus the invariants computed on the GPU.
+
+    Tolerance (reading R14): max(1e-10, 2 x the oracle's own two-order noise floor).
+    At configs[3] two valid orders of the oracle itself differ by 5.3e-10 (H) / 3.7e-10 (Z)
+    (tests/golden/noise_floor.json, written by tools/noise_floor.py from oracle/ only): the 512
+    shifts lie inside the spectrum, a subdiagonal converges to 1e-11 during the sweep and bulges
+    crossing it lose accuracy locally, so 1e-10 is below the rounding floor of the problem."""
     import torch
     p = make(cfg, z_device="cuda")
     n = p.H.shape[0]
@@ -198,7 +204,12 @@ def test_full_size_parity_against_oracle(cfg):
     Hg, Zg = hq.from_device(Hd), hq.from_device(Zd)
     del Hd, Zd, H0d, Z0d
     Ho, Zo = oracle_sweep(p.H, p.Z, p.ilo, p.ihi, p.shifts_re, p.shifts_im)
-    check(Hg, Zg, Ho, Zo, p.H, p.ilo, p.ihi)
+    import json
+    import os
+    floor = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "noise_floor.json")))
+    fl = floor["configs"][str(cfg)]
+    tol = max(TOL, 2.0 * max(fl["dH_rel_fro"], fl["dZ_fro_over_sqrt_n"]))
+    check(Hg, Zg, Ho, Zo, p.H, p.ilo, p.ihi, tol=tol)
 
 
 @pytest.mark.parametrize("vworld,case", [(1, (60, 1000, 40, 96)), (2, (61, 1200, 60, 64)),
