@@ -298,7 +298,18 @@ int enqueue_sweep(const CachedPlan& cp, double* H, double* Z, int64_t n, bool pr
 
 // Fused path (single GPU, TMA-capable layout): chase(0), then one step-kernel launch per step that
 // runs the step's updates and the next step's chase from a prioritised task queue (step.cu).
-constexpr int kFusedChunk = 12;  // tiles per GEMM task
+// Task chunk sizes; HQR_CHUNK="left,near,bulk,tail,tail_chunk" overrides them (tuning knob).
+hqr::ChunkSizes chunk_sizes() {
+  hqr::ChunkSizes cs;
+  if (const char* e = getenv("HQR_CHUNK")) {
+    int v[5];
+    if (sscanf(e, "%d,%d,%d,%d,%d", &v[0], &v[1], &v[2], &v[3], &v[4]) == 5 && v[0] > 0 && v[1] > 0 &&
+        v[2] > 0 && v[3] >= 0 && v[4] > 0) {
+      cs.left = v[0]; cs.near = v[1]; cs.bulk = v[2]; cs.tail = v[3]; cs.tail_chunk = v[4];
+    }
+  }
+  return cs;
+}
 
 int get_fused(CachedPlan& cp, bool has_z, int64_t n, FusedTasks** out) {
   auto& slot = cp.fused[has_z ? 1 : 0];
@@ -322,7 +333,7 @@ int get_fused(CachedPlan& cp, bool has_z, int64_t n, FusedTasks** out) {
       const WindowDesc* wn = (g + 1 < P.nsteps) ? P.windows.data() + P.step_begin[g + 1] : nullptr;
       const int nn = (g + 1 < P.nsteps) ? P.step_begin[g + 2] - P.step_begin[g + 1] : 0;
       int nl, nrn;
-      hqr::build_step_tasks(a, w, nw, wn, nn, sp[g], kFusedChunk, &f->tasks, &nl, &nrn);
+      hqr::build_step_tasks(a, w, nw, wn, nn, sp[g], chunk_sizes(), &f->tasks, &nl, &nrn);
       f->nL.push_back(nl);
       f->nRn.push_back(nrn);
       for (int i = 0; i < nw; ++i) {

@@ -303,11 +303,14 @@ cudaError_t launch_step(const StepArgs& a, const StepArgs& an, const Task* tasks
   return cudaErrorInvalidValue;
 }
 
-// Host: the task queue of one step (L, Rn, C, Z, Rf) in chunks of at most `chunk` tiles.
+// Host: the task queue of one step (L, Rn, C, Z, Rf).  Chunk sizes (tiles per task) per phase:
+// cs.left, cs.near for L / Rn (they gate the next chase: small), cs.bulk for Z / Rf; the last
+// cs.tail tiles of the queue use chunks of cs.tail_chunk so the CTAs finish together.
 void build_step_tasks(const StepArgs& a, const WindowDesc* wins, int nwin, const WindowDesc* next_wins,
-                      int nnext, int64_t sp, int chunk, std::vector<Task>* out, int* nL, int* nRn) {
+                      int nnext, int64_t sp, const ChunkSizes& cs, std::vector<Task>* out, int* nL,
+                      int* nRn) {
   const int NT = left_cols(a.KP), MT = right_rows(a.KP);
-  auto add = [&](int type, int win, int64_t tiles, int64_t r_lo, int64_t r_hi) {
+  auto add = [&](int type, int win, int64_t tiles, int64_t r_lo, int64_t r_hi, int chunk) {
     for (int64_t t0 = 0; t0 < tiles; t0 += chunk) {
       Task T{};
       T.type = type; T.win = win; T.tile0 = (int32_t)t0;
@@ -320,13 +323,13 @@ void build_step_tasks(const StepArgs& a, const WindowDesc* wins, int nwin, const
   for (int i = 0; i < nwin; ++i) {
     int64_t c, cnt;
     left_range(a, wins[i], c, cnt);
-    add(kTaskLeft, i, (cnt + NT - 1) / NT, 0, 0);
+    add(kTaskLeft, i, (cnt + NT - 1) / NT, 0, 0, cs.left);
   }
   *nL = (int)(out->size() - base);
   const size_t rn0 = out->size();
   for (int i = 0; i < nwin; ++i) {
     const int64_t w0 = wins[i].w0;
-    if (sp < w0) add(kTaskRight, i, (w0 - sp + MT - 1) / MT, sp, w0);
+    if (sp < w0) add(kTaskRight, i, (w0 - sp + MT - 1) / MT, sp, w0, cs.near);
   }
   *nRn = (int)(out->size() - rn0);
   for (int i = 0; i < nnext; ++i) {
@@ -334,12 +337,26 @@ void build_step_tasks(const StepArgs& a, const WindowDesc* wins, int nwin, const
     T.type = kTaskChase; T.win = i; T.ntiles = 0;
     out->push_back(T);
   }
+  const size_t bulk0 = out->size();
   if (a.Z)
-    for (int i = 0; i < nwin; ++i) add(kTaskZ, i, (a.zrows + MT - 1) / MT, 0, 0);
+    for (int i = 0; i < nwin; ++i) add(kTaskZ, i, (a.zrows + MT - 1) / MT, 0, 0, cs.bulk);
   for (int i = 0; i < nwin; ++i) {
     const int64_t hi = std::min<int64_t>(sp, wins[i].w0);
-    if (hi > 0) add(kTaskRight, i, (hi + MT - 1) / MT, 0, hi);
+    if (hi > 0) add(kTaskRight, i, (hi + MT - 1) / MT, 0, hi, cs.bulk);
   }
+  // re-split the queue's last cs.tail tiles into small chunks (same order)
+  int64_t acc = 0;
+  size_t cut = out->size();
+  while (cut > bulk0 && acc < cs.tail) acc += (*out)[--cut].ntiles;
+  std::vector<Task> tail(out->begin() + cut, out->end());
+  out->resize(cut);
+  for (const Task& T : tail)
+    for (int t0 = 0; t0 < T.ntiles; t0 += cs.tail_chunk) {
+      Task U = T;
+      U.tile0 = T.tile0 + t0;
+      U.ntiles = std::min(cs.tail_chunk, T.ntiles - t0);
+      out->push_back(U);
+    }
 }
 
 }  // namespace hqr

@@ -24,9 +24,15 @@ struct StepCounters {  // per step, zeroed before the sweep
   int pad;
 };
 
-// Tasks of one step in queue order (L, Rn, C, Z, Rf); chunks of at most `chunk` tiles.
+struct ChunkSizes {   // tiles per task, per phase
+  int left = 12, near = 6, bulk = 24;
+  int tail = 1200, tail_chunk = 6;  // the queue's last `tail` tiles in chunks of `tail_chunk`
+};
+
+// Tasks of one step in queue order (L, Rn, C, Z, Rf).
 void build_step_tasks(const StepArgs& a, const WindowDesc* wins, int nwin, const WindowDesc* next_wins,
-                      int nnext, int64_t sp, int chunk, std::vector<Task>* out, int* nL, int* nRn);
+                      int nnext, int64_t sp, const ChunkSizes& cs, std::vector<Task>* out, int* nL,
+                      int* nRn);
 
 // One persistent launch (one CTA per SM) running the step's task queue.  Needs the TMA path.
 cudaError_t launch_step(const StepArgs& a, const StepArgs& an, const Task* tasks, int ntasks, int nL,
