@@ -58,6 +58,55 @@ __global__ void dmma_tile_loop(double* out, int iters, double seed) {
   if (s == 12345.678) out[threadIdx.x] = s;
 }
 
+// The update-tile K loop in isolation: fragments from SMEM (conflict-free layout, ld = 4 mod 16),
+// one k-step of prefetch, FM x FN accumulators; `iters` passes over a 96-deep K.
+template <int FM, int FN>
+__global__ void dmma_smem_loop(double* out, int iters, double seed) {
+  extern __shared__ double sm[];
+  constexpr int LD = 100;
+  for (int i = threadIdx.x; i < 2 * 64 * LD; i += blockDim.x) sm[i] = seed + (i % 97) * 1e-3;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const double* A = sm + ((warp & 1) * 8 * FM + (lane >> 2)) * LD + (lane & 3);
+  const double* B = sm + 64 * LD + ((warp >> 1) % 2 * 8 * FN + (lane >> 2)) * LD + (lane & 3);
+  double acc[FN][FM][2];
+#pragma unroll
+  for (int j = 0; j < FN; ++j)
+#pragma unroll
+    for (int i = 0; i < FM; ++i) acc[j][i][0] = acc[j][i][1] = 0.0;
+  for (int it = 0; it < iters; ++it) {
+    double fa[2][FM], fb[2][FN];
+#pragma unroll
+    for (int i = 0; i < FM; ++i) fa[0][i] = A[i * 8 * LD];
+#pragma unroll
+    for (int j = 0; j < FN; ++j) fb[0][j] = B[j * 8 * LD];
+    for (int kk = 0; kk < 96; kk += 8) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int kn = kk + 4 * (h + 1);
+        if (kn < 96) {
+#pragma unroll
+          for (int i = 0; i < FM; ++i) fa[h ^ 1][i] = A[i * 8 * LD + kn];
+#pragma unroll
+          for (int j = 0; j < FN; ++j) fb[h ^ 1][j] = B[j * 8 * LD + kn];
+        }
+#pragma unroll
+        for (int j = 0; j < FN; ++j)
+#pragma unroll
+          for (int i = 0; i < FM; ++i)
+            asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                         : "+d"(acc[j][i][0]), "+d"(acc[j][i][1]) : "d"(fb[h][j]), "d"(fa[h][i]));
+      }
+    }
+  }
+  double s = 0;
+#pragma unroll
+  for (int j = 0; j < FN; ++j)
+#pragma unroll
+    for (int i = 0; i < FM; ++i) s += acc[j][i][0] + acc[j][i][1];
+  if (s == 12345.678) out[threadIdx.x] = s;
+}
+
 template <int NACC>
 __global__ void dfma_loop(double* out, int iters, double seed) {
   double a = seed + threadIdx.x * 1e-3, b = 1.0 - 1e-9 * threadIdx.x;
@@ -143,6 +192,26 @@ int main(int argc, char** argv) {
       ms = time_kernel(dmma_tile_loop<4, 4>, grid, block, 1024, out, 5);
       flop = (double)grid * w * 1024 * 16 * 512.0;
       printf(", \"dmma_tile4x4_w%d_tflops\": %.3f", w, flop / (ms * 1e-3) / 1e12);
+    }
+  }
+  {
+    int ws[] = {4, 8, 12, 16};
+    for (int w : ws) {
+      int block = 32 * w, grid = sms;
+      size_t smem = 2 * 64 * 100 * 8;
+      cudaFuncSetAttribute(dmma_smem_loop<6, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cudaFuncSetAttribute(dmma_smem_loop<4, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+      dmma_smem_loop<6, 3><<<grid, block, smem>>>(out, 200, 0.5);
+      cudaEventRecord(e0); dmma_smem_loop<6, 3><<<grid, block, smem>>>(out, 200, 0.5); cudaEventRecord(e1);
+      cudaEventSynchronize(e1); float ms; cudaEventElapsedTime(&ms, e0, e1);
+      double flop = (double)grid * w * 200 * 24 * 18 * 512.0;
+      printf(", \"dmma_smem6x3_w%d_tflops\": %.3f", w, flop / (ms * 1e-3) / 1e12);
+      dmma_smem_loop<4, 4><<<grid, block, smem>>>(out, 200, 0.5);
+      cudaEventRecord(e0); dmma_smem_loop<4, 4><<<grid, block, smem>>>(out, 200, 0.5); cudaEventRecord(e1);
+      cudaEventSynchronize(e1); cudaEventElapsedTime(&ms, e0, e1);
+      flop = (double)grid * w * 200 * 24 * 16 * 512.0;
+      printf(", \"dmma_smem4x4_w%d_tflops\": %.3f", w, flop / (ms * 1e-3) / 1e12);
     }
   }
   double best_dfma = 0;
