@@ -202,7 +202,7 @@ __global__ void __launch_bounds__(kThreadsGeneric, 1) left_generic_kernel(StepAr
   constexpr int LD = pad_ld(KP);
   constexpr int WM = KP / 4, WN = NT / 2;
   constexpr int FM = WM / 8, FN = WN / 8;
-  extern __shared__ __align__(128) double sm[];
+  extern __shared__ __align__(1024) double sm[];
   double* As = sm;                    // KP x QLD
   double* Bs = As + KP * QLD;         // 2 x NT x LD
   __shared__ StepItems si;
@@ -314,7 +314,7 @@ __global__ void __launch_bounds__(kThreadsGeneric, 1) right_generic_kernel(StepA
   constexpr int LDP = pad_ld(MT);
   constexpr int WM = MT / 2, WN = KP / 4;
   constexpr int FM = WM / 8, FN = WN / 8;
-  extern __shared__ __align__(128) double sm[];
+  extern __shared__ __align__(1024) double sm[];
   double* Bs = sm;                    // Q: KP(n) x QLD
   double* As = Bs + KP * QLD;         // 2 x KP(k) x LDP
   __shared__ StepItems si;
