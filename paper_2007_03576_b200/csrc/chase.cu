@@ -185,9 +185,7 @@ __global__ void __launch_bounds__(kChaseThreads, 1) chase_kernel(StepArgs a) {
   }
   const int KP = a.KP, QLD = a.QLD;
   double* Q = a.qslots + (size_t)(W.slot + a.slot_offset) * KP * QLD;
-  for (int c = warp; c < KP; c += kHWarps + kQWarps)
-    for (int r = lane; r < QLD; r += 32)
-      Q[r + c * QLD] = (r < kw && c < kw) ? Qs[r + c * ldh] : 0.0;
+  store_q_slot(Q, Qs, ldh, kw, KP, QLD, warp, kHWarps + kQWarps, lane);
 }
 
 }  // namespace

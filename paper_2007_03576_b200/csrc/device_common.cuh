@@ -122,4 +122,39 @@ __device__ __forceinline__ void right_apply(double* c1, int ldh, int rows, const
 }
 
 
+// Store the accumulated factor Q_W (kw x kw in SMEM, Qs[r + c*ldq]) into its workspace slot
+// (KP x QLD doubles, column-major, ld = QLD, zero padded), and record the support of every block of
+// 8 columns in the slot's padding rows (never read as matrix entries, QLD >= KP + 4):
+//   slot[KP + 8b*QLD] = klo_b, slot[KP + 1 + 8b*QLD] = khi_b,
+// multiples of 4 with Q_W[r][c] == 0 for every r outside [klo_b, khi_b), c in [8b, 8b+8) (empty
+// block: 0, 0).  The update GEMMs skip the K steps outside a block's extent: the skipped products
+// are exact zeros, so the result is unchanged.  The support is a band (each bulge passing a row
+// extends its support at most 2 columns left and about s columns right) that covers
+// ~60% of a k = 96 window; it is read from the data, not assumed.
+__device__ __forceinline__ void store_q_slot(double* __restrict__ Q, const double* __restrict__ Qs, int ldq,
+                                             int kw, int KP, int QLD, int warp, int nwarps, int lane) {
+  for (int b = warp; b < KP / 8; b += nwarps) {
+    int lo = INT_MAX, hi = -1;
+    for (int c = 8 * b; c < 8 * b + 8; ++c) {
+      double* qc = Q + (size_t)c * QLD;
+      for (int r = lane; r < QLD; r += 32) {
+        const double v = (r < kw && c < kw) ? Qs[r + c * ldq] : 0.0;
+        qc[r] = v;
+        if (v != 0.0) {
+          lo = min(lo, r);
+          hi = max(hi, r);
+        }
+      }
+    }
+    lo = __reduce_min_sync(0xffffffffu, lo);
+    hi = __reduce_max_sync(0xffffffffu, hi);
+    __syncwarp();
+    if (lane == 0) {
+      const bool empty = hi < 0;
+      Q[KP + (size_t)8 * b * QLD] = empty ? 0.0 : (double)(lo & ~3);
+      Q[KP + 1 + (size_t)8 * b * QLD] = empty ? 0.0 : (double)((hi + 4) & ~3);
+    }
+  }
+}
+
 }  // namespace hqr

@@ -10,10 +10,11 @@
 // doubles makes the fragment loads conflict-free.  Box rows beyond the window / tile (other matrix
 // rows, or TMA's zero fill outside the matrix) meet the zero padding of Q_W or land in output rows
 // that are never stored.
-// A consumer group = 4 warps tiling the output 2 x 2.  The K loop stops at the Q_W structure bound
-// (Q_W[k][c] = 0 for k > c + 2 nbc, see update.cu); the two warps of a group pair that share an SM
-// sub-partition get complementary K extents.  Accumulators hold transposed output blocks so a thread
-// owns two consecutive output rows of one column: 16-byte stores into column-major storage.
+// A consumer group = 4 warps tiling the output 2 x 2 (interleaved 8-column blocks of Q_W x halves
+// of the other dimension).  Each block of Q_W columns multiplies only its K extent (the band
+// store_q_slot records next to Q_W, ~70% of the dense K work at k = 96).  Accumulators hold
+// transposed output blocks so a thread owns two consecutive output rows of one column: 16-byte
+// stores into column-major storage.
 #pragma once
 #include "device_common.cuh"
 
@@ -26,7 +27,13 @@ struct Geom {
   static constexpr int LDP = LEFT ? pad_ld(KP) : pad_ld(MT);
   static constexpr int STAGE = LEFT ? NT * LDP : KP * LDP;        // doubles per SMEM stage
   static constexpr int OM = LEFT ? KP : MT, ON = LEFT ? NT : KP;  // output tile
-  static constexpr int WM = OM / 2, WN = ON / 2;                  // warp tile
+#ifndef HQR_KLOOP
+#define HQR_KLOOP 2
+#endif
+  // warp tile: KLOOP 0/1 = 2 x 2 (interleaved Q_W column blocks x halves), 2/3 = Q_W quarters
+  static constexpr bool QUARTERS = HQR_KLOOP >= 2;
+  static constexpr int WM = QUARTERS ? (LEFT ? OM / 4 : OM) : OM / 2;
+  static constexpr int WN = QUARTERS ? (LEFT ? ON : ON / 4) : ON / 2;
   static constexpr int FM = WM / 8, FN = WN / 8;
   static_assert(!LEFT || LDP >= KP + 1, "left panel box must hold the odd-row shift");
   static_assert((STAGE * 8) % 128 == 0 && (KP * QLD * 8) % 128 == 0, "TMA destinations 128-byte aligned");
@@ -57,20 +64,39 @@ __device__ __forceinline__ void produce_tile(double* dst, uint64_t* full, const 
 
 // Consumer warp `i4` (0..3) of group `q` (0..1): K loop over the stage `P` with Q_W in `Qs`,
 // release the stage (`empty`), store the tile in place.
+// The warp covers NB blocks of 8 Q_W columns, qblk(b), and a range of the other output dimension.
+// Block b only multiplies the K range [klo_b, khi_b) that store_q_slot recorded.
 template <int KP, bool LEFT>
 __device__ __forceinline__ void consume_tile(const double* Qs, const double* P, uint64_t* empty,
                                              const TileRef& t, int q, int i4, int lane) {
   using G = Geom<KP, LEFT>;
   constexpr int FM = G::FM, FN = G::FN, WM = G::WM, WN = G::WN, QLD = G::QLD, LDP = G::LDP;
-  const int kg = (i4 & 1) ^ q;   // the index (row group LEFT / column group RIGHT) that sets K
-  const int og = i4 >> 1;
-  const int wm0 = (LEFT ? kg : og) * WM, wn0 = (LEFT ? og : kg) * WN;
+  constexpr int NB = LEFT ? FM : FN;  // Q_W column blocks of this warp
+  constexpr bool QU = G::QUARTERS;
+  // KLOOP 0/1: blocks 2b + kg (even/odd interleave), other dimension half og.
+  // KLOOP 2/3: blocks qq*NB + b (quarter qq; group 1 takes the opposite quarter so the two warps of
+  // an SM sub-partition together cover an average share of the band), whole other dimension.
+  const int kg = (i4 & 1) ^ q;
+  const int og = QU ? 0 : (i4 >> 1);
+  const int qq = (i4 + 2 * q) & 3;
+  const int qb0 = QU ? qq * NB : kg, qbs = QU ? 1 : 2;   // Q block of b: qb0 + b*qbs
   const int lr = lane >> 2, lk = lane & 3;
+  int klo[NB], khi[NB];
+  int kbeg = KP, kend = 0;
+#pragma unroll
+  for (int b = 0; b < NB; ++b) {
 #ifdef HQR_BENCH_NO_TRIM  // benchmark-only knob (tools/gemm_bench.cu), never set in the product build
-  const int kend = KP;
+    klo[b] = 0; khi[b] = KP;
 #else
-  const int kend = min(KP, ((LEFT ? wm0 + WM : wn0 + WN) + 2 * t.nbc + 3) & ~3);
+    const double* meta = Qs + (size_t)(8 * (qb0 + b * qbs)) * QLD + KP;
+    klo[b] = (int)meta[0];
+    khi[b] = (int)meta[1];
 #endif
+    if (khi[b] > klo[b]) {
+      kbeg = min(kbeg, klo[b]);
+      kend = max(kend, khi[b]);
+    }
+  }
   double acc[FN][FM][2];
 #pragma unroll
   for (int jn = 0; jn < FN; ++jn)
@@ -80,33 +106,67 @@ __device__ __forceinline__ void consume_tile(const double* Qs, const double* P, 
   const double* B;
   int a_i, a_k, b_j, b_k;
   if (LEFT) {
-    A = Qs + (wm0 + lr) * QLD + lk;                  a_i = 8 * QLD; a_k = 1;
-    B = P + (wn0 + lr) * LDP + (t.w0 & 1) + lk;      b_j = 8 * LDP; b_k = 1;
+    A = Qs + (8 * qb0 + lr) * QLD + lk;                   a_i = 8 * qbs * QLD; a_k = 1;
+    B = P + (og * WN + lr) * LDP + (t.w0 & 1) + lk;       b_j = 8 * LDP;       b_k = 1;
   } else {
-    A = P + lk * LDP + wm0 + lr;                     a_i = 8;       a_k = LDP;
-    B = Qs + (wn0 + lr) * QLD + lk;                  b_j = 8 * QLD; b_k = 1;
+    A = P + lk * LDP + og * WM + lr;                      a_i = 8;             a_k = LDP;
+    B = Qs + (8 * qb0 + lr) * QLD + lk;                   b_j = 8 * qbs * QLD; b_k = 1;
   }
-  // software-pipelined K loop: fragments of k-step t+1 are loaded before the mma of step t
+  // software-pipelined K loop: fragments of k-step k+4 are loaded before the mma of step k
   double fa[2][FM], fb[2][FN];
 #pragma unroll
-  for (int i = 0; i < FM; ++i) fa[0][i] = A[i * a_i];
+  for (int h = 0; h < 2; ++h) {
 #pragma unroll
-  for (int jn = 0; jn < FN; ++jn) fb[0][jn] = B[jn * b_j];
-  for (int kk = 0; kk < kend; kk += 8) {
+    for (int i = 0; i < FM; ++i) fa[h][i] = 0.0;
+#pragma unroll
+    for (int jn = 0; jn < FN; ++jn) fb[h][jn] = 0.0;
+  }
+  constexpr bool PRED_LD = HQR_KLOOP != 2;
+  auto load = [&](int h, int k) {
+#pragma unroll
+    for (int i = 0; i < FM; ++i)
+      if (!LEFT || !PRED_LD || (k >= klo[i] && k < khi[i])) fa[h][i] = A[i * a_i + k * a_k];
+#pragma unroll
+    for (int jn = 0; jn < FN; ++jn)
+      if (LEFT || !PRED_LD || (k >= klo[jn] && k < khi[jn])) fb[h][jn] = B[jn * b_j + k * b_k];
+  };
+  if (kbeg < kend) load(0, kbeg);
+  for (int kk = kbeg; kk < kend; kk += 8) {
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-      const int kn = kk + 4 * (h + 1);
-      if (kn - 4 >= kend) break;
-      if (kn < kend) {
+      const int k = kk + 4 * h;
+      if (k >= kend) break;
+      if (k + 4 < kend) load(h ^ 1, k + 4);
+#if HQR_KLOOP == 0
 #pragma unroll
-        for (int i = 0; i < FM; ++i) fa[h ^ 1][i] = A[i * a_i + kn * a_k];
+      for (int jn = 0; jn < FN; ++jn)
 #pragma unroll
-        for (int jn = 0; jn < FN; ++jn) fb[h ^ 1][jn] = B[jn * b_j + kn * b_k];
-      }
+        for (int i = 0; i < FM; ++i) {
+          const int b = LEFT ? i : jn;
+          if (k >= klo[b] && k < khi[b]) dmma(acc[jn][i], fb[h][jn], fa[h][i]);
+        }
+#elif HQR_KLOOP == 2
 #pragma unroll
       for (int jn = 0; jn < FN; ++jn)
 #pragma unroll
         for (int i = 0; i < FM; ++i) dmma(acc[jn][i], fb[h][jn], fa[h][i]);
+#else
+      if (LEFT) {
+#pragma unroll
+        for (int i = 0; i < FM; ++i)
+          if (k >= klo[i] && k < khi[i]) {
+#pragma unroll
+            for (int jn = 0; jn < FN; ++jn) dmma(acc[jn][i], fb[h][jn], fa[h][i]);
+          }
+      } else {
+#pragma unroll
+        for (int jn = 0; jn < FN; ++jn)
+          if (k >= klo[jn] && k < khi[jn]) {
+#pragma unroll
+            for (int i = 0; i < FM; ++i) dmma(acc[jn][i], fb[h][jn], fa[h][i]);
+          }
+      }
+#endif
     }
   }
   __syncwarp();
@@ -119,12 +179,12 @@ __device__ __forceinline__ void consume_tile(const double* Qs, const double* P, 
     const bool even = (t.w0 & 1) == 0;
 #pragma unroll
     for (int jn = 0; jn < FN; ++jn) {
-      const int64_t col = t.c0 + wn0 + 8 * jn + lr;
+      const int64_t col = t.c0 + og * WN + 8 * jn + lr;
       if (col >= t.lc1) continue;
       double* cp = t.M + (col - t.cb) * t.ld + t.w0;
 #pragma unroll
       for (int i = 0; i < FM; ++i) {
-        const int m = wm0 + 8 * i + 2 * lk;
+        const int m = 8 * (qb0 + i * qbs) + 2 * lk;
         if (even && m + 1 < t.kw) {
           *reinterpret_cast<double2*>(cp + m) = make_double2(acc[jn][i][0], acc[jn][i][1]);
         } else {
@@ -136,12 +196,12 @@ __device__ __forceinline__ void consume_tile(const double* Qs, const double* P, 
   } else {
 #pragma unroll
     for (int jn = 0; jn < FN; ++jn) {
-      const int col = wn0 + 8 * jn + lr;
+      const int col = 8 * (qb0 + jn * qbs) + lr;
       if (col >= t.kw) continue;
       double* cp = t.M + (t.w0 + col - t.cb) * t.ld;
 #pragma unroll
       for (int i = 0; i < FM; ++i) {
-        const int64_t row = t.r0 + wm0 + 8 * i + 2 * lk;  // even: 16-byte aligned pair
+        const int64_t row = t.r0 + og * WM + 8 * i + 2 * lk;  // even: 16-byte aligned pair
         if (row + 1 < t.r1) {
           *reinterpret_cast<double2*>(cp + row) = make_double2(acc[jn][i][0], acc[jn][i][1]);
         } else if (row < t.r1) {

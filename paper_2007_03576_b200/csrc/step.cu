@@ -138,8 +138,7 @@ __device__ void chase_window_9w(const StepArgs& a, const WindowDesc& W, double* 
   }
   const int KP = a.KP, QLD = a.QLD;
   double* Q = a.qslots + (size_t)(W.slot + a.slot_offset) * KP * QLD;
-  for (int c = warp; c < KP; c += kStepWarps)
-    for (int r = lane; r < QLD; r += 32) Q[r + c * QLD] = (r < kw && c < kw) ? Qs[r + c * ldh] : 0.0;
+  store_q_slot(Q, Qs, ldh, kw, KP, QLD, warp, kStepWarps, lane);
 }
 
 // ---- one GEMM chunk: `ntiles` tiles of one window, Q_W loaded once -----------------------------

@@ -12,9 +12,10 @@
 // H(W_c, W_c') and are ordered (left kernel, then right kernel).
 //
 // Tensor-core path: FP64 mma.sync.m8n8k4 (SASS DMMA.8x8x4; tcgen05 has no f64 kind, SURVEY
-// §7.3 H3).  Structure of Q_W: every bulge passing a row extends its support at most 2 columns to
-// the left, so Q_W[k][c] = 0 for k > c + 2*nbc (tests/test_abi_plan.py checks it on emulated
-// windows); each warp stops its K loop there (~1/4 fewer flops at k = 96).
+// §7.3 H3).  Structure of Q_W: a band -- every bulge passing a row extends its support at most 2
+// columns to the left and about s columns to the right -- so each 8-column block of Q_W has a short
+// nonzero row range; the chase records it next to Q_W (store_q_slot) and the tile K loops skip the
+// zero K steps (~30% fewer flops at k = 96).
 //
 // Main path (n even, "bulk" kernels): 8 consumer warps + 1 producer warp per CTA.  The producer
 // streams panel tiles into a 2-stage SMEM ring with the bulk-copy (TMA) engine
@@ -75,9 +76,8 @@ __device__ __forceinline__ int decode_item(const StepItems& si, int nw, int64_t 
 // (item j in stage j mod NS, NS = 3 for KP <= 96), so one group's epilogue (register -> HBM
 // stores) overlaps the other group's DMMA main loop, and the next item of a group is already
 // loading while its previous one is multiplied.  Inside a
-// group, 2 x 2 warps tile the output; a warp's K loop stops at the Q_W structure bound, and the
-// two warps sharing an SM sub-partition (w, w+4) get complementary row (LEFT) / column (RIGHT)
-// groups so both DMMA pipes of a sub-partition pair see the same K extent on average.
+// group, 2 x 2 warps tile the output (gemm_tile.cuh); each 8-column block of Q_W multiplies only
+// its recorded K extent.
 // ================================================================================================
 template <int KP, bool LEFT>
 __global__ void __launch_bounds__(kThreadsBulk, 1)
