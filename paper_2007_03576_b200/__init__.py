@@ -72,9 +72,11 @@ def lib():
     """Load (building first if stale) libhqr_b200.so.  Raises if it cannot be loaded."""
     global _lib
     if _lib is None:
-        path = _build.LIB
-        if not os.path.exists(path) or _build._stale():
-            _build.build()
+        path = os.environ.get("HQR_LIB")  # debugging: an alternative build of the same library
+        if not path:
+            path = _build.LIB
+            if not os.path.exists(path) or _build._stale():
+                _build.build()
         L = ctypes.CDLL(path)
         L.hqr_setup.argtypes = [ctypes.POINTER(_Config)]
         L.hqr_setup.restype = ctypes.c_int

@@ -38,7 +38,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     inc, lib = nccl_dirs()
     cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
            "-Xcompiler", "-fPIC", "-shared", "-cudart", "shared", "--expt-relaxed-constexpr",
-           "-I", inc, "-o", LIB] + [os.path.join(CSRC, f) for f in SOURCES] + [
+           "-I", inc, "-o", LIB] + os.environ.get("HQR_NVCC_EXTRA", "").split() + [os.path.join(CSRC, f) for f in SOURCES] + [
            "-L", lib, "-l:libnccl.so.2", "-Xlinker", "-rpath=" + lib]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")

@@ -6,6 +6,7 @@
 
 #include <climits>
 #include <cstdint>
+#include <cstdio>
 
 #include "kernels.hpp"
 
@@ -45,12 +46,53 @@ __device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, unsigned bytes) {
   asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n}\n"
                ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
 }
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+#if defined(HQR_WATCHDOG) || defined(HQR_CLOOP)  // debugging builds only
+__device__ __forceinline__ bool mbar_try(uint64_t* bar, unsigned parity) {
+  unsigned ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity) : "memory");
+  return ok != 0;
+}
+#endif
+#if defined(HQR_CLOOP)
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity, int tag = 0) {
+  while (!mbar_try(bar, parity)) {
+  }
+}
+#elif defined(HQR_WATCHDOG)  // bounded waits that report where they hung, then trap
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity, int tag = 0) {
+  long long it = 0;
+  while (!mbar_try(bar, parity)) {
+#ifndef HQR_WD_LIMIT
+#define HQR_WD_LIMIT 26
+#endif
+    if (++it == (1ll << HQR_WD_LIMIT)) {
+#ifndef HQR_WD_NOPRINT
+      printf("hqr watchdog: block %d thread %d tag %d bar smem+%u parity %u\n", blockIdx.x, threadIdx.x, tag,
+             smem_u32(bar), parity);
+#endif
+      __trap();
+    }
+  }
+}
+#else
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity, int tag = 0) {
+  (void)tag;
   asm volatile(
       "{\n .reg .pred p;\n"
       "WAIT_%=:\n"
       " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
       " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+#endif
+// non-blocking test of a phase (parity as mbar_wait)
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, unsigned parity) {
+  unsigned ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity) : "memory");
+  return ok != 0;
 }
 // 1-D bulk copy global -> shared through the TMA engine; completes tx bytes on `bar`
 __device__ __forceinline__ void bulk_g2s(void* smem, const void* gmem, unsigned bytes, uint64_t* bar) {

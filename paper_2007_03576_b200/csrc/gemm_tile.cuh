@@ -66,9 +66,14 @@ __device__ __forceinline__ void produce_tile(double* dst, uint64_t* full, const 
 // release the stage (`empty`), store the tile in place.
 // The warp covers NB blocks of 8 Q_W columns, qblk(b), and a range of the other output dimension.
 // Block b only multiplies the K range [klo_b, khi_b) that store_q_slot recorded.
-template <int KP, bool LEFT>
+struct NoMid {
+  __device__ void operator()() const {}
+};
+
+// `mid()` runs between the K loop (stage released) and the epilogue stores.
+template <int KP, bool LEFT, class Mid = NoMid>
 __device__ __forceinline__ void consume_tile(const double* Qs, const double* P, uint64_t* empty,
-                                             const TileRef& t, int q, int i4, int lane) {
+                                             const TileRef& t, int q, int i4, int lane, Mid mid = Mid()) {
   using G = Geom<KP, LEFT>;
   constexpr int FM = G::FM, FN = G::FN, WM = G::WM, WN = G::WN, QLD = G::QLD, LDP = G::LDP;
   constexpr int NB = LEFT ? FM : FN;  // Q_W column blocks of this warp
@@ -171,6 +176,7 @@ __device__ __forceinline__ void consume_tile(const double* Qs, const double* P, 
   }
   __syncwarp();
   if (lane == 0) mbar_arrive(empty);
+  mid();
 #ifdef HQR_BENCH_NO_STORE  // benchmark-only knob (tools/gemm_bench.cu), never set in the product build
   if (acc[0][0][0] != 12345.678) return;
 #endif

@@ -69,7 +69,7 @@ struct CachedGraph {
 
 struct FusedTasks {            // task queues of every step for the fused step kernel
   std::vector<hqr::Task> tasks;
-  std::vector<int32_t> begin, nL, nRn;
+  std::vector<int32_t> begin, nL, nRn, nLt, nRnt;
   hqr::Task* d_tasks = nullptr;
   hqr::StepCounters* d_ctr = nullptr;
   double flops = 0, bytes = 0;
@@ -336,6 +336,10 @@ int get_fused(CachedPlan& cp, bool has_z, int64_t n, FusedTasks** out) {
       hqr::build_step_tasks(a, w, nw, wn, nn, sp[g], chunk_sizes(), &f->tasks, &nl, &nrn);
       f->nL.push_back(nl);
       f->nRn.push_back(nrn);
+      int lt = 0, rnt = 0;
+      for (int i = 0; i < nl + nrn; ++i) (i < nl ? lt : rnt) += f->tasks[f->begin.back() + i].ntiles;
+      f->nLt.push_back(lt);
+      f->nRnt.push_back(rnt);
       for (int i = 0; i < nw; ++i) {
         const double kw = w[i].w1 - w[i].w0 + 1;
         const double rows = (double)(n - 1 - w[i].w1) + (double)w[i].w0 + (has_z ? (double)n : 0.0);
@@ -387,6 +391,7 @@ int enqueue_fused(CachedPlan& cp, double* H, double* Z, int64_t n, const hqr::Te
     const int nt = f->begin[s + 1] - f->begin[s];
     mark(3);
     CK(hqr::launch_step(args(s), args(s + 1), f->d_tasks + f->begin[s], nt, f->nL[s], f->nRn[s],
+                        f->nLt[s], f->nRnt[s],
                         f->d_ctr + s, tm, P.max_kw, g.num_sms, A));
     mark(-1);
     st->launches_left++;  // one fused launch per step (counted once)
@@ -439,6 +444,7 @@ int hqr_setup(const hqr_config* cfg) {
     std::memcpy(&id, cfg->nccl_id, sizeof(id));
     NK(ncclCommInitRank(&g.comm, g.world, id, g.rank));
   }
+  if (getenv("HQR_PROGRESS_SECS")) hqr::debug_progress_init();
   g.ready = true;
   return 0;
 }

@@ -20,6 +20,14 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#ifdef HQR_PROGRESS  // debugging build only: per-warp progress in host-mapped memory, dumped on a hang
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+#include <thread>
+#include <cstring>
+#include <unistd.h>
+#endif
 
 #include "device_common.cuh"
 #include "gemm_tile.cuh"
@@ -39,6 +47,34 @@ __device__ __forceinline__ int ld_acquire(const int* p) {
   int v;
   asm volatile("ld.acquire.gpu.global.b32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
   return v;
+}
+
+#ifdef HQR_PROGRESS
+__device__ int* g_prog;
+// per-warp ring of the last 64 events: g_prog[((block * 16 + warp) * 65)] = count, then 64 slots
+#define PROG(tag) do { if (lane == 0) { int* _b = g_prog + (blockIdx.x * 16 + warp) * 65; \
+    const int _n = __ldcg(_b); __stcg(_b + 1 + (_n & 63), (tag)); __stcg(_b, _n + 1); } } while (0)
+#else
+#define PROG(tag) do { } while (0)
+#endif
+
+// spin until *p >= target (acquire); the watchdog build reports a hang and traps
+__device__ __forceinline__ void spin_until(const int* p, int target, int tag) {
+#ifdef HQR_WATCHDOG
+  long long it = 0;
+#endif
+  int v;
+  while ((v = ld_acquire(p)) < target) {
+    __nanosleep(64);
+#ifdef HQR_WATCHDOG
+    if (++it == (1ll << (HQR_WD_LIMIT - 2))) {
+#ifndef HQR_WD_NOPRINT
+      printf("hqr watchdog: block %d spin tag %d value %d target %d\n", blockIdx.x, tag, v, target);
+#endif
+      __trap();
+    }
+#endif
+  }
 }
 
 // ---- chase of one window with the CTA's 9 warps (same arithmetic as chase.cu) ------------------
@@ -141,78 +177,66 @@ __device__ void chase_window_9w(const StepArgs& a, const WindowDesc& W, double* 
   store_q_slot(Q, Qs, ldh, kw, KP, QLD, warp, kStepWarps, lane);
 }
 
-// ---- one GEMM chunk: `ntiles` tiles of one window, Q_W loaded once -----------------------------
+// ---- streaming task pipeline ------------------------------------------------------------------
+// The producer warp (warp 8, lane 0 acting) claims tasks, waits for their dependencies, loads Q_W
+// when the window changes, and streams the tasks' panel tiles through the SMEM ring; every stage
+// carries a descriptor.  The consumer groups take the ring's tiles in order (group q: tiles
+// j = q mod 2) with no CTA-wide barrier between tasks.  Completion is counted per tile and warp
+// (release adds) for the tasks other tasks depend on.  A chase task drains the ring (markers to
+// both groups), then all 9 warps chase one window in the whole SMEM.
+constexpr int kDescTile = 0, kDescChase = 1, kDescExit = 2;
+
+struct StageDesc {
+  int pos;     // ring position this descriptor belongs to (see the consumer's wait)
+  int kind;    // kDescTile / kDescChase / kDescExit
+  int left;    // tile: LEFT (1) or RIGHT/Z (0)
+  int ctr;     // tile: 0, or 1 / 2 = add cnt_add into l_done / rn_done after the stores
+  int qe;      // tile: Q_W load epoch it multiplies with
+  int cnt_add; // tile with ctr != 0: tiles of the task this group has done (this warp adds them)
+  TileRef t;
+};
+
+__device__ __forceinline__ void red_release_add(int* p, int v) {
+  asm volatile("red.release.gpu.global.add.s32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
+}
+
 template <int KP, bool LEFT>
-__device__ void gemm_chunk(const StepArgs& a, const WindowDesc& w, const Task& T, double* sm,
-                           uint64_t* full, uint64_t* empty, uint64_t* qfull, int& j, unsigned& nq,
-                           const CUtensorMap* tmL, const CUtensorMap* tmR, const CUtensorMap* tmZ,
-                           int stage_stride) {
+__device__ __forceinline__ TileRef make_tile_ref(const StepArgs& a, const WindowDesc& w, const Task& T, int i) {
   using G = Geom<KP, LEFT>;
-  constexpr int NS = stages_of(KP), QLD = G::QLD;
-  double* Qs = sm;
-  double* Ps = sm + KP * QLD;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  auto tile_ref = [&](int i) {
-    TileRef t;
-    t.w0 = w.w0; t.kw = w.w1 - w.w0 + 1; t.nbc = w.nbc;
-    if (LEFT) {
-      int64_t c, cnt;
-      left_range(a, w, c, cnt);
-      t.M = a.H; t.c0 = c + (int64_t)(T.tile0 + i) * G::NT; t.lc1 = a.lc1; t.ld = a.n; t.cb = a.hcol0;
-      t.isZ = false; t.r0 = t.r1 = 0;
-    } else if (T.type == kTaskZ) {
-      t.M = a.Z; t.r0 = (int64_t)(T.tile0 + i) * G::MT; t.r1 = a.zrows; t.ld = a.ldz; t.cb = 0;
-      t.isZ = true; t.c0 = t.lc1 = 0;
-    } else {
-      t.M = a.H; t.r0 = T.r_lo + (int64_t)(T.tile0 + i) * G::MT; t.r1 = T.r_hi; t.ld = a.n;
-      t.cb = a.hcol0; t.isZ = false; t.c0 = t.lc1 = 0;
-    }
-    return t;
-  };
-  if (warp == 8) {
-    const double* Q = a.qslots + (size_t)(w.slot + a.slot_offset) * KP * QLD;
-    constexpr unsigned qbytes = KP * QLD * 8, chunk = qbytes / 32;
-    fence_proxy_async_all();  // generic writes of earlier tasks before this task's TMA reads
-    if (lane == 0) mbar_arrive_tx(qfull, qbytes);
-    __syncwarp();
-    bulk_g2s(reinterpret_cast<char*>(Qs) + lane * chunk, reinterpret_cast<const char*>(Q) + lane * chunk,
-             chunk, qfull);
-    for (int i = 0; i < T.ntiles; ++i) {
-      const int jj = j + i, s = jj % NS;
-      if (jj >= NS) mbar_wait(&empty[s], (unsigned)((jj / NS) - 1) & 1);
-      if (lane == 0)
-        produce_tile<KP, LEFT>(Ps + s * stage_stride, &full[s], LEFT ? tmL : tmR, tmZ, tile_ref(i));
-      __syncwarp();
-    }
+  TileRef t;
+  t.w0 = w.w0; t.kw = w.w1 - w.w0 + 1; t.nbc = w.nbc;
+  if (LEFT) {
+    int64_t c, cnt;
+    left_range(a, w, c, cnt);
+    t.M = a.H; t.c0 = c + (int64_t)(T.tile0 + i) * G::NT; t.lc1 = a.lc1; t.ld = a.n; t.cb = a.hcol0;
+    t.isZ = false; t.r0 = t.r1 = 0;
+  } else if (T.type == kTaskZ) {
+    t.M = a.Z; t.r0 = (int64_t)(T.tile0 + i) * G::MT; t.r1 = a.zrows; t.ld = a.ldz; t.cb = 0;
+    t.isZ = true; t.c0 = t.lc1 = 0;
   } else {
-    const int q = warp >> 2, i4 = warp & 3;
-    mbar_wait(qfull, nq & 1);
-    for (int i = 0; i < T.ntiles; ++i) {
-      const int jj = j + i, s = jj % NS;
-      if ((jj & 1) != q) continue;
-      mbar_wait(&full[s], (unsigned)(jj / NS) & 1);
-      consume_tile<KP, LEFT>(Qs, Ps + s * stage_stride, &empty[s], tile_ref(i), q, i4, lane);
-    }
+    t.M = a.H; t.r0 = T.r_lo + (int64_t)(T.tile0 + i) * G::MT; t.r1 = T.r_hi; t.ld = a.n;
+    t.cb = a.hcol0; t.isZ = false; t.c0 = t.lc1 = 0;
   }
-  j += T.ntiles;
-  ++nq;
+  return t;
 }
 
 template <int KP>
 __global__ void __launch_bounds__(kStepThreads, 1)
     step_kernel(StepArgs a, StepArgs an, const Task* __restrict__ tasks, int ntasks, int nL, int nRn,
-                StepCounters* ctr, const __grid_constant__ CUtensorMap tmL,
+                int nLt, int nRnt, StepCounters* ctr, const __grid_constant__ CUtensorMap tmL,
                 const __grid_constant__ CUtensorMap tmR, const __grid_constant__ CUtensorMap tmZ) {
   constexpr int NS = stages_of(KP);
+  constexpr int QLD = pad_ld(KP);
   constexpr int SS = Geom<KP, true>::STAGE > Geom<KP, false>::STAGE ? Geom<KP, true>::STAGE
                                                                     : Geom<KP, false>::STAGE;
   extern __shared__ __align__(1024) double sm[];
   __shared__ __align__(8) uint64_t full[NS], empty[NS], qfull;
-  __shared__ Task cur;
-  __shared__ int cur_idx;
+  __shared__ StageDesc desc[NS];
   __shared__ WindowDesc cw;
   __shared__ ChaseSmem R;
-  const int tid = threadIdx.x;
+  double* Qs = sm;
+  double* Ps = sm + KP * QLD;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (tid == 0) {
     for (int s = 0; s < NS; ++s) {
       mbar_init(&full[s], 1);
@@ -220,43 +244,172 @@ __global__ void __launch_bounds__(kStepThreads, 1)
     }
     mbar_init(&qfull, 1);
   }
+  if (tid < NS) desc[tid].pos = -1;
   fence_proxy_async();
   __syncthreads();
-  int j = 0;        // tiles through the ring so far (identical in every warp)
-  unsigned nq = 0;  // Q_W loads so far
-  for (;;) {
-    if (tid == 0) {
-      const int t = atomicAdd(&ctr->next, 1);
-      cur_idx = t;
-      if (t < ntasks) {
-        cur = tasks[t];
-        const Task& T = cur;
-        // dependencies: on tasks earlier in the queue only
-        if (T.type == kTaskRight || T.type == kTaskChase)
-          while (ld_acquire(&ctr->l_done) < nL) __nanosleep(64);
-        if (T.type == kTaskChase)
-          while (ld_acquire(&ctr->rn_done) < nRn) __nanosleep(64);
-        cw = (T.type == kTaskChase) ? an.wins[an.win_begin + T.win] : a.wins[a.win_begin + T.win];
+
+  if (warp == 8) {
+    // ================================ producer / scheduler ================================
+    int j = 0;          // ring positions used (tiles + markers)
+    int qe = -1;        // Q_W loads so far - 1
+    int q_win = -1;     // window whose Q_W is resident (-1: none)
+    // Producer-side waits are done by lane 0 alone, then __syncwarp: a lane that saw the phase
+    // complete may publish the next position before its sibling lanes poll again, and the
+    // consumers can complete one more phase in between -- a parity wait would then never return.
+    auto wait_slot = [&](int jj) {  // stage of ring position jj free
+      PROG(5000000 + jj);
+      if (jj >= NS && lane == 0) mbar_wait(&empty[jj % NS], (unsigned)((jj / NS) - 1) & 1, 1000000 + jj);
+      __syncwarp();
+    };
+    auto marker = [&](int kind) {   // one marker per consumer group
+      for (int g = 0; g < 2; ++g, ++j) {
+        wait_slot(j);
+        if (lane == 0) {
+          desc[j % NS].kind = kind;
+          desc[j % NS].pos = j;
+          mbar_arrive(&full[j % NS]);
+        }
+        __syncwarp();
       }
+    };
+    for (;;) {
+      int t = 0;
+      PROG(1000000 + j);
+      if (lane == 0) t = atomicAdd(&ctr->next, 1);
+      t = __shfl_sync(0xffffffffu, t, 0);
+      if (t >= ntasks) {
+        marker(kDescExit);
+        PROG(8000000 + j);
+        break;
+      }
+      const Task T = tasks[t];
+      if (lane == 0) {
+        // dependencies on earlier tasks only (per-tile, per-warp completion counts)
+        if (T.type == kTaskRight || T.type == kTaskChase) PROG(2000000 + t);
+        if (T.type == kTaskRight || T.type == kTaskChase)
+          spin_until(&ctr->l_done, 4 * nLt, 1);
+        if (T.type == kTaskChase) PROG(3000000 + t);
+        if (T.type == kTaskChase) spin_until(&ctr->rn_done, 4 * nRnt, 2);
+        fence_proxy_async_all();  // other SMs' generic stores before this SM's TMA reads
+      }
+      __syncwarp();
+      if (T.type == kTaskChase) {
+        marker(kDescChase);
+        PROG(7000000 + j);
+        if (lane == 0) cw = an.wins[an.win_begin + T.win];
+        __syncthreads();
+        chase_window_9w(an, cw, sm, R);
+        __syncthreads();
+        q_win = -1;
+        continue;
+      }
+      const WindowDesc w = a.wins[a.win_begin + T.win];
+      // A new window needs its Q_W.  Its first NS-1 panel tiles are issued first (their stages free
+      // up as the previous tiles are released); once every earlier position has been released --
+      // no tile reads the old Q_W any more -- Q_W is loaded, so the panel loads overlap the drain.
+      const bool new_q = T.win != q_win;
+      if (new_q) {
+        ++qe;
+        q_win = T.win;
+      }
+      const int p0 = j;
+      auto load_q = [&]() {
+        PROG(4000000 + j);
+        if (lane == 0)
+          for (int jj = max(0, p0 - NS); jj < p0; ++jj)
+            mbar_wait(&empty[jj % NS], (unsigned)(jj / NS) & 1, 2000000 + jj);
+        __syncwarp();
+        const double* Q = a.qslots + (size_t)(w.slot + a.slot_offset) * KP * QLD;
+        constexpr unsigned qbytes = KP * QLD * 8, chunk = qbytes / 32;
+        if (lane == 0) mbar_arrive_tx(&qfull, qbytes);
+        __syncwarp();
+        bulk_g2s(reinterpret_cast<char*>(Qs) + lane * chunk, reinterpret_cast<const char*>(Q) + lane * chunk,
+                 chunk, &qfull);
+      };
+      const bool left = T.type == kTaskLeft;
+      const int cnt = left ? 1 : (T.type == kTaskRight && t < nL + nRn) ? 2 : 0;
+      const int nq_pre = new_q ? min(T.ntiles, NS - 1) : 0;  // tiles issued before the Q_W load
+      for (int i = 0; i < T.ntiles; ++i, ++j) {
+        if (new_q && i == nq_pre) load_q();
+        wait_slot(j);
+        if (lane == 0) {
+          StageDesc& d = desc[j % NS];
+          d.pos = j; d.kind = kDescTile; d.left = left; d.qe = qe;
+          // completion count: on each group's last tile of the task, that group's tile count
+          // (the group of tile i takes the task's tiles i, i-2, ..., i.e. i/2 + 1 of them)
+          d.ctr = (cnt && i + 2 >= T.ntiles) ? cnt : 0;
+          d.cnt_add = i / 2 + 1;
+          if (left) {
+            d.t = make_tile_ref<KP, true>(a, w, T, i);
+            produce_tile<KP, true>(Ps + (j % NS) * SS, &full[j % NS], &tmL, &tmZ, d.t);
+          } else {
+            d.t = make_tile_ref<KP, false>(a, w, T, i);
+            produce_tile<KP, false>(Ps + (j % NS) * SS, &full[j % NS], &tmR, &tmZ, d.t);
+          }
+        }
+        __syncwarp();
+      }
+      if (new_q && nq_pre == T.ntiles) load_q();  // short task: the Q_W load after its tiles
     }
-    __syncthreads();
-    const int t = cur_idx;
-    if (t >= ntasks) break;
-    const Task T = cur;
-    const WindowDesc w = cw;
-    if (T.type == kTaskChase) {
-      chase_window_9w(an, w, sm, R);
-    } else if (T.type == kTaskLeft) {
-      gemm_chunk<KP, true>(a, w, T, sm, full, empty, &qfull, j, nq, &tmL, &tmR, &tmZ, SS);
-    } else {
-      gemm_chunk<KP, false>(a, w, T, sm, full, empty, &qfull, j, nq, &tmL, &tmR, &tmZ, SS);
-    }
-    __syncthreads();  // every store of the task issued; the SMEM may be reused
-    if (tid == 0) {
-      __threadfence();
-      fence_proxy_async_all();
-      if (T.type == kTaskLeft) atomicAdd(&ctr->l_done, 1);
-      else if (T.type == kTaskRight && t < nL + nRn) atomicAdd(&ctr->rn_done, 1);
+  } else {
+    // ================================ consumers ================================
+    const int q = warp >> 2, i4 = warp & 3;
+    int last_qe = -1;
+    // Completion counts (tiles x 4 warps) of the tasks other tasks wait on are published with a
+    // release add.  The release waits for the warp's outstanding stores, so it is deferred: it is
+    // issued after the next tile's K loop (the earlier stores have landed by then), or at once
+    // when the warp would otherwise wait with counts pending (never sit on them: others may wait).
+    int pend_l = 0, pend_rn = 0;
+    auto flush = [&]() {
+      __syncwarp();
+      if (lane == 0) {
+        if (pend_l) red_release_add(&ctr->l_done, pend_l);
+        if (pend_rn) red_release_add(&ctr->rn_done, pend_rn);
+      }
+      pend_l = pend_rn = 0;
+    };
+    for (int j = q;; j += 2) {
+      const int s = j % NS;
+      PROG(11000000 + j);
+      // The stage's previous phase belongs to the other group and may still be in flight; a parity
+      // wait cannot tell phase p from p - 2, so first wait until the producer has published this
+      // position (which it does only after the previous phase was consumed), then on the barrier.
+      if ((pend_l | pend_rn) && *reinterpret_cast<volatile int*>(&desc[s].pos) != j) flush();
+      while (*reinterpret_cast<volatile int*>(&desc[s].pos) != j) {
+      }
+      mbar_wait(&full[s], (unsigned)(j / NS) & 1, 3000000 + j);
+      const int kind = desc[s].kind;
+      if (kind != kDescTile) {
+        if (pend_l | pend_rn) flush();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+        if (kind == kDescExit) {
+          PROG(15000000 + j);
+          break;
+        }
+        PROG(14000000 + j);
+        __syncthreads();
+        chase_window_9w(an, cw, sm, R);
+        __syncthreads();
+        continue;
+      }
+      const int qe = desc[s].qe, cnt = desc[s].ctr, add = desc[s].cnt_add;
+      const bool left = desc[s].left;
+      const TileRef t = desc[s].t;
+      if (qe != last_qe) {
+        if ((pend_l | pend_rn) && !mbar_test(&qfull, (unsigned)qe & 1)) flush();
+        PROG(12000000 + qe);
+        mbar_wait(&qfull, (unsigned)qe & 1, 4000000 + qe);
+        last_qe = qe;
+      }
+      PROG(13000000 + j);
+      auto mid = [&]() {
+        if (pend_l | pend_rn) flush();
+      };
+      if (left) consume_tile<KP, true>(Qs, Ps + s * SS, &empty[s], t, q, i4, lane, mid);
+      else consume_tile<KP, false>(Qs, Ps + s * SS, &empty[s], t, q, i4, lane, mid);
+      if (cnt == 1) pend_l += add;
+      else if (cnt == 2) pend_rn += add;
     }
   }
 }
@@ -272,7 +425,7 @@ size_t step_smem(int max_kw) {
 
 template <int KP>
 cudaError_t launch_step_t(const StepArgs& a, const StepArgs& an, const Task* tasks, int ntasks, int nL,
-                          int nRn, StepCounters* ctr, const TensorMaps& tm, int max_kw, int num_sms,
+                          int nRn, int nLt, int nRnt, StepCounters* ctr, const TensorMaps& tm, int max_kw, int num_sms,
                           cudaStream_t st) {
   static size_t configured = 0;
   const size_t smem = step_smem<KP>(max_kw);
@@ -282,22 +435,63 @@ cudaError_t launch_step_t(const StepArgs& a, const StepArgs& an, const Task* tas
     configured = smem;
   }
   const int grid = std::max(1, std::min(ntasks, num_sms));
-  step_kernel<KP><<<grid, kStepThreads, smem, st>>>(a, an, tasks, ntasks, nL, nRn, ctr, tm.left_H,
+  step_kernel<KP><<<grid, kStepThreads, smem, st>>>(a, an, tasks, ntasks, nL, nRn, nLt, nRnt, ctr, tm.left_H,
                                                      tm.right_H, tm.right_Z);
   return cudaGetLastError();
 }
 
 }  // namespace
 
+#ifdef HQR_PROGRESS
+void debug_progress_init() {
+  static int* d = nullptr;
+  if (d) return;
+  const size_t count = 1024 * 16 * 65, bytes = count * sizeof(int);
+  cudaMalloc(&d, bytes);
+  cudaMemset(d, 0, bytes);
+  cudaMemcpyToSymbol(g_prog, &d, sizeof(d));
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const char* e = getenv("HQR_PROGRESS_SECS");
+  const int secs = e ? atoi(e) : 20;
+  std::thread([secs, dev, bytes, count] {
+    std::this_thread::sleep_for(std::chrono::seconds(secs));
+    cudaSetDevice(dev);
+    int* h = (int*)malloc(bytes);
+    cudaStream_t st;
+    cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+    cudaError_t err = cudaMemcpyAsync(h, d, bytes, cudaMemcpyDeviceToHost, st);
+    if (err == cudaSuccess) err = cudaStreamSynchronize(st);
+    fprintf(stderr, "hqr progress dump (%s): blocks whose producer did not exit, last events per warp\n",
+            cudaGetErrorString(err));
+    for (int b = 0; b < 148; ++b) {
+      const int* pw = h + (b * 16 + 8) * 65;
+      const int last = pw[1 + ((pw[0] - 1) & 63)];
+      if (last / 1000000 == 8) continue;
+      for (int w = 0; w < 9; ++w) {
+        const int* r = h + (b * 16 + w) * 65;
+        fprintf(stderr, "b%d w%d n=%d:", b, w, r[0]);
+        for (int k = r[0] > 40 ? r[0] - 40 : 0; k < r[0]; ++k) fprintf(stderr, " %d", r[1 + (k & 63)]);
+        fprintf(stderr, "\n");
+      }
+    }
+    fflush(stderr);
+    _exit(3);
+  }).detach();
+}
+#else
+void debug_progress_init() {}
+#endif
+
 cudaError_t launch_step(const StepArgs& a, const StepArgs& an, const Task* tasks, int ntasks, int nL,
-                        int nRn, StepCounters* ctr, const TensorMaps& tm, int max_kw, int num_sms,
+                        int nRn, int nLt, int nRnt, StepCounters* ctr, const TensorMaps& tm, int max_kw, int num_sms,
                         cudaStream_t st) {
   if (!tm.valid) return cudaErrorNotSupported;
   switch (a.KP) {
-    case 32: return launch_step_t<32>(a, an, tasks, ntasks, nL, nRn, ctr, tm, max_kw, num_sms, st);
-    case 64: return launch_step_t<64>(a, an, tasks, ntasks, nL, nRn, ctr, tm, max_kw, num_sms, st);
-    case 96: return launch_step_t<96>(a, an, tasks, ntasks, nL, nRn, ctr, tm, max_kw, num_sms, st);
-    case 128: return launch_step_t<128>(a, an, tasks, ntasks, nL, nRn, ctr, tm, max_kw, num_sms, st);
+    case 32: return launch_step_t<32>(a, an, tasks, ntasks, nL, nRn, nLt, nRnt, ctr, tm, max_kw, num_sms, st);
+    case 64: return launch_step_t<64>(a, an, tasks, ntasks, nL, nRn, nLt, nRnt, ctr, tm, max_kw, num_sms, st);
+    case 96: return launch_step_t<96>(a, an, tasks, ntasks, nL, nRn, nLt, nRnt, ctr, tm, max_kw, num_sms, st);
+    case 128: return launch_step_t<128>(a, an, tasks, ntasks, nL, nRn, nLt, nRnt, ctr, tm, max_kw, num_sms, st);
   }
   return cudaErrorInvalidValue;
 }

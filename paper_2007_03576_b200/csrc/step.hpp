@@ -19,8 +19,8 @@ struct Task {       // one claimable unit of work of a wavefront step
 
 struct StepCounters {  // per step, zeroed before the sweep
   int next;     // next task to claim
-  int l_done;   // completed left chunks
-  int rn_done;  // completed near-right chunks
+  int l_done;   // left tiles done x 4 (one release add per consumer warp)
+  int rn_done;  // near-right tiles done x 4
   int pad;
 };
 
@@ -35,8 +35,13 @@ void build_step_tasks(const StepArgs& a, const WindowDesc* wins, int nwin, const
                       int* nRn);
 
 // One persistent launch (one CTA per SM) running the step's task queue.  Needs the TMA path.
+// nL / nRn: tasks of the L / Rn phases; nLt / nRnt: their tiles (completion is counted per tile).
 cudaError_t launch_step(const StepArgs& a, const StepArgs& an, const Task* tasks, int ntasks, int nL,
-                        int nRn, StepCounters* ctr, const TensorMaps& tm, int max_kw, int num_sms,
+                        int nRn, int nLt, int nRnt, StepCounters* ctr, const TensorMaps& tm, int max_kw, int num_sms,
                         cudaStream_t st);
+
+// Debugging builds (-DHQR_PROGRESS): progress buffer in host-mapped memory, dumped after
+// HQR_PROGRESS_SECS seconds (then the process exits).  No-op otherwise.
+void debug_progress_init();
 
 }  // namespace hqr

@@ -91,6 +91,7 @@ __global__ void __launch_bounds__(kThreadsBulk, 1)
   double* Ps = Qs + KP * QLD;            // NS stages (128-byte aligned: TMA destinations)
   __shared__ StepItems si;
   __shared__ __align__(8) uint64_t full[NS], empty[NS], qfull, qempty;
+  __shared__ int seq[NS];  // item whose panel stage s holds (published by the producer)
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t n = a.n;
@@ -117,6 +118,7 @@ __global__ void __launch_bounds__(kThreadsBulk, 1)
     }
     mbar_init(&qfull, 1);
     mbar_init(&qempty, kConsumerWarps);
+    for (int s = 0; s < NS; ++s) seq[s] = -1;
   }
   for (int i = tid; i < NS * STAGE; i += kThreadsBulk) Ps[i] = 0.0;
   fence_proxy_async();
@@ -150,7 +152,10 @@ __global__ void __launch_bounds__(kThreadsBulk, 1)
       const int wi = decode_item(si, nw, it, tile);
       const WindowDesc& w = si.w[wi];
       if (wi != cur) {
-        if (cur >= 0) mbar_wait(&qempty, (nq - 1) & 1);  // both groups done with the previous Q_W
+        // producer waits: lane 0 alone (a lane that saw the phase may publish before its siblings
+        // poll again, and the barrier could then complete another phase)
+        if (cur >= 0 && lane == 0) mbar_wait(&qempty, (nq - 1) & 1);  // both groups done with Q_W
+        __syncwarp();
         const double* Q = a.qslots + (size_t)(w.slot + a.slot_offset) * KP * QLD;
         constexpr unsigned qbytes = KP * QLD * 8, chunk = qbytes / 32;
         if (lane == 0) mbar_arrive_tx(&qfull, qbytes);
@@ -162,8 +167,12 @@ __global__ void __launch_bounds__(kThreadsBulk, 1)
       }
       const int64_t j = it - it0;
       const int s = (int)(j % NS);
-      if (j >= NS) mbar_wait(&empty[s], (unsigned)((j / NS) - 1) & 1);
-      if (lane == 0) produce_tile<KP, LEFT>(Ps + s * STAGE, &full[s], &tmH, &tmZ, tile_ref(wi, tile));
+      if (j >= NS && lane == 0) mbar_wait(&empty[s], (unsigned)((j / NS) - 1) & 1);
+      __syncwarp();
+      if (lane == 0) {
+        *reinterpret_cast<volatile int*>(&seq[s]) = (int)j;
+        produce_tile<KP, LEFT>(Ps + s * STAGE, &full[s], &tmH, &tmZ, tile_ref(wi, tile));
+      }
       __syncwarp();
     }
   } else {
@@ -186,6 +195,10 @@ __global__ void __launch_bounds__(kThreadsBulk, 1)
       const int64_t j = it - it0;
       if ((int)(j & 1) != q) continue;
       const int s = (int)(j % NS);
+      // the stage's previous phase belongs to the other group and may still be in flight (a parity
+      // wait cannot tell phase p from p - 2): wait until the producer has published item j first
+      while (*reinterpret_cast<volatile int*>(&seq[s]) != (int)j) {
+      }
       mbar_wait(&full[s], (unsigned)(j / NS) & 1);
       consume_tile<KP, LEFT>(Qs, Ps + s * STAGE, &empty[s], tile_ref(wi, tile), q, i4, lane);
     }
