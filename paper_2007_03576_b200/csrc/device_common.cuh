@@ -12,11 +12,18 @@
 
 namespace hqr {
 
-// Panel tile widths and SMEM ring depth: the factor Q_W (KP x pad_ld(KP)) stays resident, the ring
-// holds kStagesOf(KP) panel tiles; KP = 96 uses 48-wide tiles so three stages fit next to Q_W.
-__host__ __device__ constexpr int left_cols(int KP) { return KP <= 64 ? 64 : KP == 96 ? 48 : 32; }
-__host__ __device__ constexpr int right_rows(int KP) { return KP <= 64 ? 64 : KP == 96 ? 48 : 32; }
-__host__ __device__ constexpr int stages_of(int KP) { return KP <= 96 ? 3 : 2; }
+// TMA-path panel tiles and SMEM ring depth (update.cu bulk kernels, step.cu): Q_W (KP x pad_ld(KP))
+// stays resident next to a ring of stages_of(KP) panel tiles.  An even ring gives each consumer
+// group its own stages; KP = 96 uses 40-wide tiles so four stages fit next to Q_W (204.8 KB).
+__host__ __device__ constexpr int left_cols(int KP) { return KP <= 64 ? 64 : KP == 96 ? 40 : 32; }
+__host__ __device__ constexpr int right_rows(int KP) { return KP <= 64 ? 64 : KP == 96 ? 40 : 32; }
+__host__ __device__ constexpr int stages_of(int KP) { return KP <= 96 ? 4 : 2; }
+// Panel leading dimension: m8n8k4 fragment loads (8 consecutive doubles x 4 strided rows) are
+// conflict-free (2 wavefronts) unless the stride is 0 (mod 16) doubles.
+__host__ __device__ constexpr int panel_ld(int x) { return (x % 16 == 0) ? x + 4 : x; }
+// cp.async (odd n) kernels keep their own tiles
+__host__ __device__ constexpr int gen_left_cols(int KP) { return KP <= 64 ? 64 : KP == 96 ? 48 : 32; }
+__host__ __device__ constexpr int gen_right_rows(int KP) { return KP <= 64 ? 64 : KP == 96 ? 48 : 32; }
 
 __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"

@@ -24,7 +24,7 @@ template <int KP, bool LEFT>
 struct Geom {
   static constexpr int NT = left_cols(KP), MT = right_rows(KP);
   static constexpr int QLD = pad_ld(KP);
-  static constexpr int LDP = LEFT ? pad_ld(KP) : pad_ld(MT);
+  static constexpr int LDP = LEFT ? pad_ld(KP) : panel_ld(MT);
   static constexpr int STAGE = LEFT ? NT * LDP : KP * LDP;        // doubles per SMEM stage
   static constexpr int OM = LEFT ? KP : MT, ON = LEFT ? NT : KP;  // output tile
 #ifndef HQR_KLOOP

@@ -36,7 +36,7 @@ size_t chase_smem_bytes(int kw, int nbc);
 // Valid only for even n (TMA global strides must be multiples of 16 bytes).
 struct TensorMaps {
   CUtensorMap left_H;   // box {pad_ld(KP) rows, left_cols(KP) columns}
-  CUtensorMap right_H;  // box {pad_ld(right_rows(KP)) rows, KP columns}
+  CUtensorMap right_H;  // box {panel_ld(right_rows(KP)) rows, KP columns}
   CUtensorMap right_Z;
   bool valid = false;
 };

@@ -210,7 +210,7 @@ __global__ void __launch_bounds__(kThreadsBulk, 1)
 // ================================================================================================
 template <int KP>
 __global__ void __launch_bounds__(kThreadsGeneric, 1) left_generic_kernel(StepArgs a, int64_t total_items) {
-  constexpr int NT = left_cols(KP);
+  constexpr int NT = gen_left_cols(KP);
   constexpr int QLD = pad_ld(KP);
   constexpr int LD = pad_ld(KP);
   constexpr int WM = KP / 4, WN = NT / 2;
@@ -322,7 +322,7 @@ __global__ void __launch_bounds__(kThreadsGeneric, 1) left_generic_kernel(StepAr
 
 template <int KP>
 __global__ void __launch_bounds__(kThreadsGeneric, 1) right_generic_kernel(StepArgs a, int64_t total_items) {
-  constexpr int MT = right_rows(KP);
+  constexpr int MT = gen_right_rows(KP);
   constexpr int QLD = pad_ld(KP);
   constexpr int LDP = pad_ld(MT);
   constexpr int WM = MT / 2, WN = KP / 4;
@@ -448,13 +448,13 @@ template <int KP> constexpr size_t left_bulk_smem() {
   return (size_t)(KP * pad_ld(KP) + stages_of(KP) * left_cols(KP) * pad_ld(KP)) * sizeof(double);
 }
 template <int KP> constexpr size_t right_bulk_smem() {
-  return (size_t)(KP * pad_ld(KP) + stages_of(KP) * KP * pad_ld(right_rows(KP))) * sizeof(double);
+  return (size_t)(KP * pad_ld(KP) + stages_of(KP) * KP * panel_ld(right_rows(KP))) * sizeof(double);
 }
 template <int KP> constexpr size_t left_generic_smem() {
-  return (size_t)(KP * pad_ld(KP) + 2 * left_cols(KP) * pad_ld(KP)) * sizeof(double);
+  return (size_t)(KP * pad_ld(KP) + 2 * gen_left_cols(KP) * pad_ld(KP)) * sizeof(double);
 }
 template <int KP> constexpr size_t right_generic_smem() {
-  return (size_t)(KP * pad_ld(KP) + 2 * KP * pad_ld(right_rows(KP))) * sizeof(double);
+  return (size_t)(KP * pad_ld(KP) + 2 * KP * pad_ld(gen_right_rows(KP))) * sizeof(double);
 }
 
 template <typename K>
@@ -524,9 +524,9 @@ cudaError_t make_tensor_maps(TensorMaps* tm, const double* H, int64_t hcols, con
       (Z && ((reinterpret_cast<uintptr_t>(Z) & 15) || (ldz & 1) || zrows < 1)))
     return cudaSuccess;  // generic (cp.async) path
   cudaError_t e = encode_2d(&tm->left_H, H, n, hcols, n, pad_ld(KP), left_cols(KP));
-  if (e == cudaSuccess) e = encode_2d(&tm->right_H, H, n, hcols, n, pad_ld(right_rows(KP)), KP);
-  if (e == cudaSuccess) e = Z ? encode_2d(&tm->right_Z, Z, zrows, n, ldz, pad_ld(right_rows(KP)), KP)
-                              : encode_2d(&tm->right_Z, H, n, hcols, n, pad_ld(right_rows(KP)), KP);
+  if (e == cudaSuccess) e = encode_2d(&tm->right_H, H, n, hcols, n, panel_ld(right_rows(KP)), KP);
+  if (e == cudaSuccess) e = Z ? encode_2d(&tm->right_Z, Z, zrows, n, ldz, panel_ld(right_rows(KP)), KP)
+                              : encode_2d(&tm->right_Z, H, n, hcols, n, panel_ld(right_rows(KP)), KP);
   if (e != cudaSuccess) return e;
   tm->valid = true;
   return cudaSuccess;
@@ -536,7 +536,7 @@ cudaError_t launch_left(const StepArgs& a, const WindowDesc* hw, int num_sms, co
                         cudaStream_t st, int64_t* items_out, double* flops, double* bytes) {
   int64_t items = 0;
   double f = 0, b = 0;
-  const int NT = left_cols(a.KP);
+  const int NT = tm.valid ? left_cols(a.KP) : gen_left_cols(a.KP);
   for (int i = 0; i < a.win_count; ++i) {
     int64_t c0, cols;
     left_range(a, hw[i], c0, cols);
@@ -564,7 +564,7 @@ cudaError_t launch_right(const StepArgs& a, const WindowDesc* hw, int num_sms, c
                          cudaStream_t st, int64_t* items_out, double* flops, double* bytes) {
   int64_t items = 0;
   double f = 0, b = 0;
-  const int MT = right_rows(a.KP);
+  const int MT = tm.valid ? right_rows(a.KP) : gen_right_rows(a.KP);
   const bool do_h = a.right_mode != 2, do_z = a.Z && a.right_mode != 1;
   const int64_t zt = do_z ? (a.zrows + MT - 1) / MT : 0;
   for (int i = 0; i < a.win_count; ++i) {
