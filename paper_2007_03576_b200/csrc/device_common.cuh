@@ -18,9 +18,9 @@ namespace hqr {
 __host__ __device__ constexpr int left_cols(int KP) { return KP <= 64 ? 64 : KP == 96 ? 40 : 32; }
 __host__ __device__ constexpr int right_rows(int KP) { return KP <= 64 ? 64 : KP == 96 ? 40 : 32; }
 __host__ __device__ constexpr int stages_of(int KP) { return KP <= 96 ? 4 : 2; }
-// Panel leading dimension: m8n8k4 fragment loads (8 consecutive doubles x 4 strided rows) are
-// conflict-free (2 wavefronts) unless the stride is 0 (mod 16) doubles.
-__host__ __device__ constexpr int panel_ld(int x) { return (x % 16 == 0) ? x + 4 : x; }
+// Panel leading dimension: an m8n8k4 fragment load (per half-warp: 4 consecutive doubles x 4 strided
+// rows) is conflict-free iff the stride is an odd multiple of 4 doubles: smallest such ld >= x.
+__host__ __device__ constexpr int panel_ld(int x) { return x + ((4 - x) % 8 + 8) % 8; }
 // cp.async (odd n) kernels keep their own tiles
 __host__ __device__ constexpr int gen_left_cols(int KP) { return KP <= 64 ? 64 : KP == 96 ? 48 : 32; }
 __host__ __device__ constexpr int gen_right_rows(int KP) { return KP <= 64 ? 64 : KP == 96 ? 48 : 32; }

@@ -6,15 +6,14 @@
 // RIGHT out[MT x KP] = P[MT x KP] * Q_W[KP x KP],  P = H(r0 : r0+MT, W) or Z(r0 : r0+MT, W)
 // SMEM: Q_W resident as Qs[c*QLD + k] = Q_W[k][c] (the chase kernel's slot layout); the panel is one
 // 2-D TMA box: LEFT Ps[nn*LDP + ro + k] = H[(w0+k) + (c0+nn)*n] (ro = w0 & 1: TMA's innermost
-// coordinate must be 16-byte aligned), RIGHT Ps[k*LDP + m] = M[(r0+m) + (w0+k)*ld].  LDP = 4 (mod 16)
-// doubles makes the fragment loads conflict-free.  Box rows beyond the window / tile (other matrix
-// rows, or TMA's zero fill outside the matrix) meet the zero padding of Q_W or land in output rows
-// that are never stored.
-// A consumer group = 4 warps tiling the output 2 x 2 (interleaved 8-column blocks of Q_W x halves
-// of the other dimension).  Each block of Q_W columns multiplies only its K extent (the band
-// store_q_slot records next to Q_W, ~70% of the dense K work at k = 96).  Accumulators hold
-// transposed output blocks so a thread owns two consecutive output rows of one column: 16-byte
-// stores into column-major storage.
+// coordinate must be 16-byte aligned), RIGHT Ps[k*LDP + m] = M[(r0+m) + (w0+k)*ld].  LDP = an odd
+// multiple of 4 doubles makes the fragment loads conflict-free.  Box rows beyond the window / tile
+// (other matrix rows, or TMA's zero fill outside the matrix) meet the zero padding of Q_W or land
+// in output rows that are never stored.
+// A consumer group = 4 warps, one quarter of the Q_W columns each (LEFT: output rows, RIGHT: output
+// columns) times the whole other dimension; a warp multiplies only the K extent of its quarter (the
+// band store_q_slot records next to Q_W).  Accumulators hold transposed output blocks so a thread
+// owns two consecutive output rows of one column: 16-byte stores into column-major storage.
 #pragma once
 #include "device_common.cuh"
 
@@ -27,13 +26,9 @@ struct Geom {
   static constexpr int LDP = LEFT ? pad_ld(KP) : panel_ld(MT);
   static constexpr int STAGE = LEFT ? NT * LDP : KP * LDP;        // doubles per SMEM stage
   static constexpr int OM = LEFT ? KP : MT, ON = LEFT ? NT : KP;  // output tile
-#ifndef HQR_KLOOP
-#define HQR_KLOOP 2
-#endif
-  // warp tile: KLOOP 0/1 = 2 x 2 (interleaved Q_W column blocks x halves), 2/3 = Q_W quarters
-  static constexpr bool QUARTERS = HQR_KLOOP >= 2;
-  static constexpr int WM = QUARTERS ? (LEFT ? OM / 4 : OM) : OM / 2;
-  static constexpr int WN = QUARTERS ? (LEFT ? ON : ON / 4) : ON / 2;
+  // warp tile: one quarter of the Q_W columns x the whole other output dimension
+  static constexpr int WM = LEFT ? OM / 4 : OM;
+  static constexpr int WN = LEFT ? ON : ON / 4;
   static constexpr int FM = WM / 8, FN = WN / 8;
   static_assert(!LEFT || LDP >= KP + 1, "left panel box must hold the odd-row shift");
   static_assert((STAGE * 8) % 128 == 0 && (KP * QLD * 8) % 128 == 0, "TMA destinations 128-byte aligned");
@@ -62,44 +57,36 @@ __device__ __forceinline__ void produce_tile(double* dst, uint64_t* full, const 
     tma_load_2d(dst, t.isZ ? tmZ : tmH, (int)t.r0, (int)(t.w0 - t.cb), full);
 }
 
-// Consumer warp `i4` (0..3) of group `q` (0..1): K loop over the stage `P` with Q_W in `Qs`,
-// release the stage (`empty`), store the tile in place.
-// The warp covers NB blocks of 8 Q_W columns, qblk(b), and a range of the other output dimension.
-// Block b only multiplies the K range [klo_b, khi_b) that store_q_slot recorded.
 struct NoMid {
   __device__ void operator()() const {}
 };
 
-// `mid()` runs between the K loop (stage released) and the epilogue stores.
+// One consumer warp: the output rows (LEFT) / columns (RIGHT) of Q_W column quarter `qq` (0..3)
+// times the whole other tile dimension.  K loop over the stage `P` with Q_W in `Qs`, release the
+// stage (`empty`), run `mid()`, store the tile in place.  The warp multiplies only the K range
+// [min klo_b, max khi_b) of its 8-column blocks b (store_q_slot's band extents): a quarter's blocks
+// have similar extents, so the union is tight and the DMMAs need no predication.
 template <int KP, bool LEFT, class Mid = NoMid>
 __device__ __forceinline__ void consume_tile(const double* Qs, const double* P, uint64_t* empty,
-                                             const TileRef& t, int q, int i4, int lane, Mid mid = Mid()) {
+                                             const TileRef& t, int qq, int lane, Mid mid = Mid()) {
   using G = Geom<KP, LEFT>;
   constexpr int FM = G::FM, FN = G::FN, WM = G::WM, WN = G::WN, QLD = G::QLD, LDP = G::LDP;
   constexpr int NB = LEFT ? FM : FN;  // Q_W column blocks of this warp
-  constexpr bool QU = G::QUARTERS;
-  // KLOOP 0/1: blocks 2b + kg (even/odd interleave), other dimension half og.
-  // KLOOP 2/3: blocks qq*NB + b (quarter qq; group 1 takes the opposite quarter so the two warps of
-  // an SM sub-partition together cover an average share of the band), whole other dimension.
-  const int kg = (i4 & 1) ^ q;
-  const int og = QU ? 0 : (i4 >> 1);
-  const int qq = (i4 + 2 * q) & 3;
-  const int qb0 = QU ? qq * NB : kg, qbs = QU ? 1 : 2;   // Q block of b: qb0 + b*qbs
+  (void)WM; (void)WN;
+  const int qb0 = qq * NB;            // first Q_W column block
   const int lr = lane >> 2, lk = lane & 3;
-  int klo[NB], khi[NB];
   int kbeg = KP, kend = 0;
 #pragma unroll
   for (int b = 0; b < NB; ++b) {
 #ifdef HQR_BENCH_NO_TRIM  // benchmark-only knob (tools/gemm_bench.cu), never set in the product build
-    klo[b] = 0; khi[b] = KP;
+    const int lo = 0, hi = KP;
 #else
-    const double* meta = Qs + (size_t)(8 * (qb0 + b * qbs)) * QLD + KP;
-    klo[b] = (int)meta[0];
-    khi[b] = (int)meta[1];
+    const double* meta = Qs + (size_t)(8 * (qb0 + b)) * QLD + KP;
+    const int lo = (int)meta[0], hi = (int)meta[1];
 #endif
-    if (khi[b] > klo[b]) {
-      kbeg = min(kbeg, klo[b]);
-      kend = max(kend, khi[b]);
+    if (hi > lo) {
+      kbeg = min(kbeg, lo);
+      kend = max(kend, hi);
     }
   }
   double acc[FN][FM][2];
@@ -111,29 +98,19 @@ __device__ __forceinline__ void consume_tile(const double* Qs, const double* P, 
   const double* B;
   int a_i, a_k, b_j, b_k;
   if (LEFT) {
-    A = Qs + (8 * qb0 + lr) * QLD + lk;                   a_i = 8 * qbs * QLD; a_k = 1;
-    B = P + (og * WN + lr) * LDP + (t.w0 & 1) + lk;       b_j = 8 * LDP;       b_k = 1;
+    A = Qs + (8 * qb0 + lr) * QLD + lk;             a_i = 8 * QLD; a_k = 1;
+    B = P + lr * LDP + (t.w0 & 1) + lk;             b_j = 8 * LDP; b_k = 1;
   } else {
-    A = P + lk * LDP + og * WM + lr;                      a_i = 8;             a_k = LDP;
-    B = Qs + (8 * qb0 + lr) * QLD + lk;                   b_j = 8 * qbs * QLD; b_k = 1;
+    A = P + lk * LDP + lr;                          a_i = 8;       a_k = LDP;
+    B = Qs + (8 * qb0 + lr) * QLD + lk;             b_j = 8 * QLD; b_k = 1;
   }
   // software-pipelined K loop: fragments of k-step k+4 are loaded before the mma of step k
   double fa[2][FM], fb[2][FN];
-#pragma unroll
-  for (int h = 0; h < 2; ++h) {
-#pragma unroll
-    for (int i = 0; i < FM; ++i) fa[h][i] = 0.0;
-#pragma unroll
-    for (int jn = 0; jn < FN; ++jn) fb[h][jn] = 0.0;
-  }
-  constexpr bool PRED_LD = HQR_KLOOP != 2;
   auto load = [&](int h, int k) {
 #pragma unroll
-    for (int i = 0; i < FM; ++i)
-      if (!LEFT || !PRED_LD || (k >= klo[i] && k < khi[i])) fa[h][i] = A[i * a_i + k * a_k];
+    for (int i = 0; i < FM; ++i) fa[h][i] = A[i * a_i + k * a_k];
 #pragma unroll
-    for (int jn = 0; jn < FN; ++jn)
-      if (LEFT || !PRED_LD || (k >= klo[jn] && k < khi[jn])) fb[h][jn] = B[jn * b_j + k * b_k];
+    for (int jn = 0; jn < FN; ++jn) fb[h][jn] = B[jn * b_j + k * b_k];
   };
   if (kbeg < kend) load(0, kbeg);
   for (int kk = kbeg; kk < kend; kk += 8) {
@@ -142,36 +119,10 @@ __device__ __forceinline__ void consume_tile(const double* Qs, const double* P, 
       const int k = kk + 4 * h;
       if (k >= kend) break;
       if (k + 4 < kend) load(h ^ 1, k + 4);
-#if HQR_KLOOP == 0
-#pragma unroll
-      for (int jn = 0; jn < FN; ++jn)
-#pragma unroll
-        for (int i = 0; i < FM; ++i) {
-          const int b = LEFT ? i : jn;
-          if (k >= klo[b] && k < khi[b]) dmma(acc[jn][i], fb[h][jn], fa[h][i]);
-        }
-#elif HQR_KLOOP == 2
 #pragma unroll
       for (int jn = 0; jn < FN; ++jn)
 #pragma unroll
         for (int i = 0; i < FM; ++i) dmma(acc[jn][i], fb[h][jn], fa[h][i]);
-#else
-      if (LEFT) {
-#pragma unroll
-        for (int i = 0; i < FM; ++i)
-          if (k >= klo[i] && k < khi[i]) {
-#pragma unroll
-            for (int jn = 0; jn < FN; ++jn) dmma(acc[jn][i], fb[h][jn], fa[h][i]);
-          }
-      } else {
-#pragma unroll
-        for (int jn = 0; jn < FN; ++jn)
-          if (k >= klo[jn] && k < khi[jn]) {
-#pragma unroll
-            for (int i = 0; i < FM; ++i) dmma(acc[jn][i], fb[h][jn], fa[h][i]);
-          }
-      }
-#endif
     }
   }
   __syncwarp();
@@ -185,12 +136,12 @@ __device__ __forceinline__ void consume_tile(const double* Qs, const double* P, 
     const bool even = (t.w0 & 1) == 0;
 #pragma unroll
     for (int jn = 0; jn < FN; ++jn) {
-      const int64_t col = t.c0 + og * WN + 8 * jn + lr;
+      const int64_t col = t.c0 + 8 * jn + lr;
       if (col >= t.lc1) continue;
       double* cp = t.M + (col - t.cb) * t.ld + t.w0;
 #pragma unroll
       for (int i = 0; i < FM; ++i) {
-        const int m = 8 * (qb0 + i * qbs) + 2 * lk;
+        const int m = 8 * (qb0 + i) + 2 * lk;
         if (even && m + 1 < t.kw) {
           *reinterpret_cast<double2*>(cp + m) = make_double2(acc[jn][i][0], acc[jn][i][1]);
         } else {
@@ -202,12 +153,12 @@ __device__ __forceinline__ void consume_tile(const double* Qs, const double* P, 
   } else {
 #pragma unroll
     for (int jn = 0; jn < FN; ++jn) {
-      const int col = 8 * (qb0 + jn * qbs) + lr;
+      const int col = 8 * (qb0 + jn) + lr;
       if (col >= t.kw) continue;
       double* cp = t.M + (t.w0 + col - t.cb) * t.ld;
 #pragma unroll
       for (int i = 0; i < FM; ++i) {
-        const int64_t row = t.r0 + og * WM + 8 * i + 2 * lk;  // even: 16-byte aligned pair
+        const int64_t row = t.r0 + 8 * i + 2 * lk;  // even: 16-byte aligned pair
         if (row + 1 < t.r1) {
           *reinterpret_cast<double2*>(cp + row) = make_double2(acc[jn][i][0], acc[jn][i][1]);
         } else if (row < t.r1) {

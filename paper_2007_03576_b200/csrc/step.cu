@@ -16,7 +16,7 @@
 // CTAs are resident, so the queue cannot deadlock.  L before R orders the blocks H(W_c, W_c') that
 // a left update of the upper window and a right update of the lower window both modify.
 // The GEMM chunks reuse the TMA/DMMA tile of gemm_tile.cuh (one Q_W per chunk); the chase runs the
-// two-phase step of chase.cu with the CTA's 9 warps.
+// two-phase step of chase.cu with all of the CTA's warps.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -38,7 +38,10 @@ namespace hqr {
 
 namespace {
 
-constexpr int kStepThreads = 288;  // 8 consumer warps + 1 producer warp (GEMM); 9 chase warps
+constexpr int kGroups = 2;  // consumer groups of 4 warps (one warp per SM sub-partition each); 3 groups
+                            // cap registers at 128 (4 warps on one sub-partition) and spill: slower
+constexpr int kProducerWarp = 4 * kGroups;
+constexpr int kStepThreads = 32 * (4 * kGroups + 1);  // consumers + 1 producer warp; all chase
 constexpr int kStepWarps = kStepThreads / 32;
 
 __device__ __forceinline__ void fence_proxy_async_all() { asm volatile("fence.proxy.async;\n" ::: "memory"); }
@@ -77,7 +80,7 @@ __device__ __forceinline__ void spin_until(const int* p, int target, int tag) {
   }
 }
 
-// ---- chase of one window with the CTA's 9 warps (same arithmetic as chase.cu) ------------------
+// ---- chase of one window with all of the CTA's warps (same arithmetic as chase.cu) ------------------
 struct ChaseSmem {
   double v1[kMaxChaseBulges], v2[kMaxChaseBulges], tau[kMaxChaseBulges];
   int pl[kMaxChaseBulges], m[kMaxChaseBulges];
@@ -183,7 +186,7 @@ __device__ void chase_window_9w(const StepArgs& a, const WindowDesc& W, double* 
 // carries a descriptor.  The consumer groups take the ring's tiles in order (group q: tiles
 // j = q mod 2) with no CTA-wide barrier between tasks.  Completion is counted per tile and warp
 // (release adds) for the tasks other tasks depend on.  A chase task drains the ring (markers to
-// both groups), then all 9 warps chase one window in the whole SMEM.
+// every group), then all warps chase one window in the whole SMEM.
 constexpr int kDescTile = 0, kDescChase = 1, kDescExit = 2;
 
 struct StageDesc {
@@ -248,7 +251,7 @@ __global__ void __launch_bounds__(kStepThreads, 1)
   fence_proxy_async();
   __syncthreads();
 
-  if (warp == 8) {
+  if (warp == kProducerWarp) {
     // ================================ producer / scheduler ================================
     int j = 0;          // ring positions used (tiles + markers)
     int qe = -1;        // Q_W loads so far - 1
@@ -262,7 +265,7 @@ __global__ void __launch_bounds__(kStepThreads, 1)
       __syncwarp();
     };
     auto marker = [&](int kind) {   // one marker per consumer group
-      for (int g = 0; g < 2; ++g, ++j) {
+      for (int g = 0; g < kGroups; ++g, ++j) {
         wait_slot(j);
         if (lane == 0) {
           desc[j % NS].kind = kind;
@@ -336,9 +339,9 @@ __global__ void __launch_bounds__(kStepThreads, 1)
           StageDesc& d = desc[j % NS];
           d.pos = j; d.kind = kDescTile; d.left = left; d.qe = qe;
           // completion count: on each group's last tile of the task, that group's tile count
-          // (the group of tile i takes the task's tiles i, i-2, ..., i.e. i/2 + 1 of them)
-          d.ctr = (cnt && i + 2 >= T.ntiles) ? cnt : 0;
-          d.cnt_add = i / 2 + 1;
+          // (the group of tile i takes the task's tiles i, i-G, ..., i.e. i/G + 1 of them)
+          d.ctr = (cnt && i + kGroups >= T.ntiles) ? cnt : 0;
+          d.cnt_add = i / kGroups + 1;
           if (left) {
             d.t = make_tile_ref<KP, true>(a, w, T, i);
             produce_tile<KP, true>(Ps + (j % NS) * SS, &full[j % NS], &tmL, &tmZ, d.t);
@@ -353,7 +356,7 @@ __global__ void __launch_bounds__(kStepThreads, 1)
     }
   } else {
     // ================================ consumers ================================
-    const int q = warp >> 2, i4 = warp & 3;
+    const int q = warp >> 2, i4 = warp & 3;  // group, sub-partition
     int last_qe = -1;
     // Completion counts (tiles x 4 warps) of the tasks other tasks wait on are published with a
     // release add.  The release waits for the warp's outstanding stores, so it is deferred: it is
@@ -368,7 +371,7 @@ __global__ void __launch_bounds__(kStepThreads, 1)
       }
       pend_l = pend_rn = 0;
     };
-    for (int j = q;; j += 2) {
+    for (int j = q;; j += kGroups) {
       const int s = j % NS;
       PROG(11000000 + j);
       // The stage's previous phase belongs to the other group and may still be in flight; a parity
@@ -406,8 +409,11 @@ __global__ void __launch_bounds__(kStepThreads, 1)
       auto mid = [&]() {
         if (pend_l | pend_rn) flush();
       };
-      if (left) consume_tile<KP, true>(Qs, Ps + s * SS, &empty[s], t, q, i4, lane, mid);
-      else consume_tile<KP, false>(Qs, Ps + s * SS, &empty[s], t, q, i4, lane, mid);
+      // Q_W quarters: with two groups the warps of an SM sub-partition take opposite quarters (their
+      // band shares add up to about half); otherwise the quarter rotates with the ring position
+      const int qq = kGroups == 2 ? (i4 + 2 * q) & 3 : (i4 + j) & 3;
+      if (left) consume_tile<KP, true>(Qs, Ps + s * SS, &empty[s], t, qq, lane, mid);
+      else consume_tile<KP, false>(Qs, Ps + s * SS, &empty[s], t, qq, lane, mid);
       if (cnt == 1) pend_l += add;
       else if (cnt == 2) pend_rn += add;
     }

@@ -200,7 +200,8 @@ __global__ void __launch_bounds__(kThreadsBulk, 1)
       while (*reinterpret_cast<volatile int*>(&seq[s]) != (int)j) {
       }
       mbar_wait(&full[s], (unsigned)(j / NS) & 1);
-      consume_tile<KP, LEFT>(Qs, Ps + s * STAGE, &empty[s], tile_ref(wi, tile), q, i4, lane);
+      // quarters: the two warps of an SM sub-partition (groups 0, 1) take opposite quarters
+      consume_tile<KP, LEFT>(Qs, Ps + s * STAGE, &empty[s], tile_ref(wi, tile), (i4 + 2 * q) & 3, lane);
     }
   }
 }
