@@ -106,6 +106,13 @@ __device__ __forceinline__ void consume_tile(const double* Qs, const double* P, 
   }
   // software-pipelined K loop: fragments of k-step k+4 are loaded before the mma of step k
   double fa[2][FM], fb[2][FN];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+#pragma unroll
+    for (int i = 0; i < FM; ++i) fa[h][i] = 0.0;
+#pragma unroll
+    for (int jn = 0; jn < FN; ++jn) fb[h][jn] = 0.0;
+  }
   auto load = [&](int h, int k) {
 #pragma unroll
     for (int i = 0; i < FM; ++i) fa[h][i] = A[i * a_i + k * a_k];
