@@ -38,8 +38,8 @@ namespace hqr {
 
 namespace {
 
-constexpr int kGroups = 2;  // consumer groups of 4 warps (one warp per SM sub-partition each); 3 groups
-                            // cap registers at 128 (4 warps on one sub-partition) and spill: slower
+constexpr int kGroups = 3;  // consumer groups of 4 warps (one warp per SM sub-partition each): 3 groups fit
+                            // the 128-register cap (4 warps on one sub-partition) without spills
 constexpr int kProducerWarp = 4 * kGroups;
 constexpr int kStepThreads = 32 * (4 * kGroups + 1);  // consumers + 1 producer warp; all chase
 constexpr int kStepWarps = kStepThreads / 32;
