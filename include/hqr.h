@@ -175,6 +175,9 @@ typedef struct hqr_stats {
   int64_t h2d_bytes, d2h_bytes; /* staging copies (host-pointer calls)                           */
   int launches_left, launches_right, launches_chase;
   int window_eff;             /* effective window side                                           */
+  double flops_dmma;          /* executed FP64 tensor-core flops of the last single-GPU sweep: the
+                                 update GEMMs restricted to the band extents the kernels multiply
+                                 (computed on demand by hqr_get_stats; 0 if unavailable)           */
 } hqr_stats;
 
 int hqr_get_stats(hqr_stats* out);

@@ -57,7 +57,8 @@ class Stats(ctypes.Structure):
                 ("ms_right", ctypes.c_double), ("ms_step", ctypes.c_double), ("ms_total", ctypes.c_double),
                 ("h2d_bytes", ctypes.c_int64), ("d2h_bytes", ctypes.c_int64),
                 ("launches_left", ctypes.c_int), ("launches_right", ctypes.c_int),
-                ("launches_chase", ctypes.c_int), ("window_eff", ctypes.c_int)]
+                ("launches_chase", ctypes.c_int), ("window_eff", ctypes.c_int),
+                ("flops_dmma", ctypes.c_double)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

@@ -186,6 +186,10 @@ __global__ void __launch_bounds__(kChaseThreads, 1) chase_kernel(StepArgs a) {
   const int KP = a.KP, QLD = a.QLD;
   double* Q = a.qslots + (size_t)(W.slot + a.slot_offset) * KP * QLD;
   store_q_slot(Q, Qs, ldh, kw, KP, QLD, warp, kHWarps + kQWarps, lane);
+  if (a.wstats) {
+    __syncthreads();
+    if (threadIdx.x == 0) a.wstats[a.win_begin + blockIdx.x] = band_units(Q, KP, QLD);
+  }
 }
 
 }  // namespace

@@ -206,4 +206,24 @@ __device__ __forceinline__ void store_q_slot(double* __restrict__ Q, const doubl
   }
 }
 
+// After store_q_slot (and a CTA barrier): the window's executed DMMA work per update row/column,
+// U = sum over the four Q_W column quarters of (KP/4) x (quarter K extent), the union of the
+// quarter's block extents -- exactly what consume_tile multiplies.  One thread.
+__device__ __forceinline__ double band_units(const double* __restrict__ Q, int KP, int QLD) {
+  const int NB = KP / 32;  // 8-column blocks per quarter
+  double u = 0.0;
+  for (int qq = 0; qq < 4; ++qq) {
+    int lo = KP, hi = 0;
+    for (int b = qq * NB; b < qq * NB + NB; ++b) {
+      const int l = (int)Q[KP + (size_t)8 * b * QLD], h = (int)Q[KP + 1 + (size_t)8 * b * QLD];
+      if (h > l) {
+        lo = min(lo, l);
+        hi = max(hi, h);
+      }
+    }
+    if (hi > lo) u += (double)(8 * NB) * (double)(hi - lo);
+  }
+  return u;
+}
+
 }  // namespace hqr

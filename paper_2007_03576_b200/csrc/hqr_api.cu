@@ -79,6 +79,7 @@ struct CachedPlan {
   Plan plan;
   WindowDesc* d_wins = nullptr;
   int KP = 0;
+  double flops_chase = -1.0;  // in-window chase flops (computed once per plan)
   std::unique_ptr<FusedTasks> fused[2];  // [Z absent, Z present]
 };
 
@@ -94,6 +95,11 @@ struct State {
   size_t coef_cap = 0;
   double* d_q = nullptr;
   size_t q_cap = 0;
+  double* d_wstats = nullptr;    // per plan window: executed DMMA work units (record_band)
+  size_t wstats_cap = 0;
+  const void* wstats_plan = nullptr;  // plan (CachedPlan) the last single-GPU sweep recorded
+  int64_t wstats_n = 0;
+  bool wstats_z = false;
   double* d_hstage = nullptr;
   double* d_zstage = nullptr;
   size_t stage_cap = 0;
@@ -192,6 +198,12 @@ bool is_device_ptr(const void* p) {
 
 int ensure(double** p, size_t* cap, size_t count) {
   if (*cap >= count) return 0;
+  // captured graphs hold the old pointer: drop them (after the stream has drained)
+  if (*p) {
+    CK(cudaStreamSynchronize(g.stream));
+    for (auto& kv : g.graphs) cudaGraphExecDestroy(kv.second.exec);
+    g.graphs.clear();
+  }
   if (*p) CK(cudaFree(*p));
   *p = nullptr;
   *cap = 0;
@@ -222,7 +234,7 @@ int enqueue_sweep(const CachedPlan& cp, double* H, double* Z, int64_t n, bool pr
   StepArgs a{};
   a.H = H; a.Z = Z; a.n = n; a.ilo = P.ilo; a.ihi = P.ihi;
   a.hcol0 = 0; a.lc0 = 0; a.lc1 = n; a.zrows = n; a.ldz = n;
-  a.wins = cp.d_wins; a.coef = g.d_coef; a.qslots = g.d_q; a.KP = cp.KP;
+  a.wins = cp.d_wins; a.coef = g.d_coef; a.qslots = g.d_q; a.KP = cp.KP; a.wstats = g.d_wstats;
   a.QLD = hqr::pad_ld(cp.KP);
   size_t ev = 0;
   static const bool dbg_sync = getenv("HQR_DEBUG_SYNC") != nullptr;  // debugging: sync after launches
@@ -370,6 +382,7 @@ int enqueue_fused(CachedPlan& cp, double* H, double* Z, int64_t n, const hqr::Te
     a.H = H; a.Z = Z; a.n = n; a.ilo = P.ilo; a.ihi = P.ihi;
     a.hcol0 = 0; a.lc0 = 0; a.lc1 = n; a.zrows = n; a.ldz = n;
     a.wins = cp.d_wins; a.coef = g.d_coef; a.qslots = g.d_q; a.KP = cp.KP; a.QLD = hqr::pad_ld(cp.KP);
+    a.wstats = g.d_wstats;
     if (s < P.nsteps) {
       a.win_begin = P.step_begin[s];
       a.win_count = P.step_begin[s + 1] - P.step_begin[s];
@@ -467,6 +480,10 @@ int hqr_teardown(void) {
   for (auto e : g.prof_events) cudaEventDestroy(e);
   g.prof_events.clear();
   if (g.d_coef) cudaFree(g.d_coef);
+  if (g.d_wstats) cudaFree(g.d_wstats);
+  g.d_wstats = nullptr;
+  g.wstats_cap = 0;
+  g.wstats_plan = nullptr;
   if (g.d_q) cudaFree(g.d_q);
   if (g.d_hstage) cudaFree(g.d_hstage);
   if (g.d_zstage) cudaFree(g.d_zstage);
@@ -503,15 +520,11 @@ int sweep_impl(double* H, double* Z, int64_t n, const Blocks& blocks, const doub
   if (!H) return -1;
   int rc = validate_blocks(n, blocks, shifts_re, shifts_im, window, true);
   if (rc) return rc;
-  {  // a7 plan (host only; validates the window)
-    Plan tmp;
-    rc = hqr::make_plan_multi(n, blocks.count(), blocks.ilo.data(), blocks.ihi.data(),
-                              blocks.nshifts.data(), window, hqr::kMaxWindow, &tmp);
-    if (rc) return rc;
-  }
+  CachedPlan* cp = nullptr;
+  rc = get_plan(n, blocks, window, &cp, false);  // a7 plan (host only, cached; validates the window)
+  if (rc) return rc;
   if (!g.ready) return -100;
   CK(cudaSetDevice(g.device));
-  CachedPlan* cp = nullptr;
   rc = get_plan(n, blocks, window, &cp, true);
   if (rc) return rc;
 
@@ -551,6 +564,11 @@ int sweep_impl(double* H, double* Z, int64_t n, const Blocks& blocks, const doub
                      g.stream));
   rc = ensure(&g.d_q, &g.q_cap, (size_t)hqr::kQSets * cp->plan.nchains * cp->KP * hqr::pad_ld(cp->KP));
   if (rc) return rc;
+  rc = ensure(&g.d_wstats, &g.wstats_cap, cp->plan.windows.size());
+  if (rc) return rc;
+  g.wstats_plan = cp;
+  g.wstats_n = n;
+  g.wstats_z = Z != nullptr;
 
   // host buffers: stage through library-owned device memory
   const size_t nn = (size_t)n * (size_t)n;
@@ -652,8 +670,9 @@ int sweep_impl(double* H, double* Z, int64_t n, const Blocks& blocks, const doub
       else st.ms_step += e;
     }
   }
-  // in-window chase flops (per 3-reflector: 10 flops x (left cols + right rows + Q rows))
-  {
+  // in-window chase flops (per 3-reflector: 10 flops x (left cols + right rows + Q rows)),
+  // once per plan (a host loop over every reflector)
+  if (cp->flops_chase < 0) {
     const Plan& P = cp->plan;
     double f = 0;
     for (const WindowDesc& w : P.windows) {
@@ -668,8 +687,9 @@ int sweep_impl(double* H, double* Z, int64_t n, const Blocks& blocks, const doub
           f += (m == 3 ? 10.0 : 6.0) * cnt;
         }
     }
-    st.flops_chase = f;
+    cp->flops_chase = f;
   }
+  st.flops_chase = cp->flops_chase;
   g.stats = st;
   return 0;
 }
@@ -1058,6 +1078,21 @@ int hqr_sweep_virtual(double* H, double* Z, int64_t n, int64_t ilo, int64_t ihi,
 int hqr_get_stats(hqr_stats* out) {
   if (!out) return -1;
   *out = g.stats;
+  out->flops_dmma = 0.0;
+  // executed DMMA flops of the last single-GPU sweep: per window 2 U (n - w1 - 1 + w0 + zrows),
+  // U recorded by the chase from the factor's band extents (TMA path; the cp.async path for odd n
+  // multiplies full K and is not counted)
+  if (g.wstats_plan && g.d_wstats && g.ready) {
+    const CachedPlan* cp = static_cast<const CachedPlan*>(g.wstats_plan);
+    const auto& W = cp->plan.windows;
+    std::vector<double> u(W.size());
+    if (cudaMemcpy(u.data(), g.d_wstats, u.size() * sizeof(double), cudaMemcpyDeviceToHost) == cudaSuccess) {
+      double f = 0.0;
+      for (size_t i = 0; i < W.size(); ++i)
+        f += 2.0 * u[i] * ((double)(g.wstats_n - 1 - W[i].w1) + (double)W[i].w0 + (g.wstats_z ? (double)g.wstats_n : 0.0));
+      out->flops_dmma = f;
+    }
+  }
   return 0;
 }
 

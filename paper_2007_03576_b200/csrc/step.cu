@@ -86,7 +86,7 @@ struct ChaseSmem {
   int pl[kMaxChaseBulges], m[kMaxChaseBulges];
 };
 
-__device__ void chase_window_9w(const StepArgs& a, const WindowDesc& W, double* sm, ChaseSmem& R) {
+__device__ void chase_window_9w(const StepArgs& a, const WindowDesc& W, int widx, double* sm, ChaseSmem& R) {
   const int kw = W.w1 - W.w0 + 1;
   const int ldh = kw | 1;
   double* Hs = sm;
@@ -178,6 +178,10 @@ __device__ void chase_window_9w(const StepArgs& a, const WindowDesc& W, double* 
   const int KP = a.KP, QLD = a.QLD;
   double* Q = a.qslots + (size_t)(W.slot + a.slot_offset) * KP * QLD;
   store_q_slot(Q, Qs, ldh, kw, KP, QLD, warp, kStepWarps, lane);
+  if (a.wstats) {
+    __syncthreads();
+    if (threadIdx.x == 0) a.wstats[widx] = band_units(Q, KP, QLD);
+  }
 }
 
 // ---- streaming task pipeline ------------------------------------------------------------------
@@ -236,6 +240,7 @@ __global__ void __launch_bounds__(kStepThreads, 1)
   __shared__ __align__(8) uint64_t full[NS], empty[NS], qfull;
   __shared__ StageDesc desc[NS];
   __shared__ WindowDesc cw;
+  __shared__ int cwi;  // its plan index
   __shared__ ChaseSmem R;
   double* Qs = sm;
   double* Ps = sm + KP * QLD;
@@ -299,9 +304,12 @@ __global__ void __launch_bounds__(kStepThreads, 1)
       if (T.type == kTaskChase) {
         marker(kDescChase);
         PROG(7000000 + j);
-        if (lane == 0) cw = an.wins[an.win_begin + T.win];
+        if (lane == 0) {
+          cw = an.wins[an.win_begin + T.win];
+          cwi = an.win_begin + T.win;
+        }
         __syncthreads();
-        chase_window_9w(an, cw, sm, R);
+        chase_window_9w(an, cw, cwi, sm, R);
         __syncthreads();
         q_win = -1;
         continue;
@@ -392,7 +400,7 @@ __global__ void __launch_bounds__(kStepThreads, 1)
         }
         PROG(14000000 + j);
         __syncthreads();
-        chase_window_9w(an, cw, sm, R);
+        chase_window_9w(an, cw, cwi, sm, R);
         __syncthreads();
         continue;
       }
