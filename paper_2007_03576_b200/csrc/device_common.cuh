@@ -207,21 +207,34 @@ __device__ __forceinline__ void store_q_slot(double* __restrict__ Q, const doubl
 }
 
 // After store_q_slot (and a CTA barrier): the window's executed DMMA work per update row/column,
-// U = sum over the four Q_W column quarters of (KP/4) x (quarter K extent), the union of the
-// quarter's block extents -- exactly what consume_tile multiplies.  One thread.
+// U = sum over the four Q_W column quarters and over the K segments consume_tile cuts from the
+// quarter's block extents of 8 x (active blocks) x (segment length) -- exactly what consume_tile
+// multiplies.  One thread.
 __device__ __forceinline__ double band_units(const double* __restrict__ Q, int KP, int QLD) {
   const int NB = KP / 32;  // 8-column blocks per quarter
   double u = 0.0;
   for (int qq = 0; qq < 4; ++qq) {
-    int lo = KP, hi = 0;
-    for (int b = qq * NB; b < qq * NB + NB; ++b) {
-      const int l = (int)Q[KP + (size_t)8 * b * QLD], h = (int)Q[KP + 1 + (size_t)8 * b * QLD];
-      if (h > l) {
-        lo = min(lo, l);
-        hi = max(hi, h);
+    int lo[4], hi[4], kbeg = KP, kend = 0;
+    for (int b = 0; b < NB; ++b) {
+      lo[b] = (int)Q[KP + (size_t)8 * (qq * NB + b) * QLD];
+      hi[b] = (int)Q[KP + 1 + (size_t)8 * (qq * NB + b) * QLD];
+      if (hi[b] > lo[b]) {
+        kbeg = min(kbeg, lo[b]);
+        kend = max(kend, hi[b]);
+      } else {
+        lo[b] = KP; hi[b] = 0;
       }
     }
-    if (hi > lo) u += (double)(8 * NB) * (double)(hi - lo);
+    for (int k = kbeg; k < kend;) {
+      int f = NB, l = -1, nxt = kend;
+      for (int b = 0; b < NB; ++b) {
+        if (lo[b] <= k && k < hi[b]) { f = min(f, b); l = max(l, b); }
+        if (lo[b] > k) nxt = min(nxt, lo[b]);
+        if (hi[b] > k) nxt = min(nxt, hi[b]);
+      }
+      if (l >= f) u += 8.0 * (double)(l - f + 1) * (double)(nxt - k);
+      k = nxt;
+    }
   }
   return u;
 }
