@@ -57,15 +57,70 @@ __device__ __forceinline__ void produce_tile(double* dst, uint64_t* full, const 
     tma_load_2d(dst, t.isZ ? tmZ : tmH, (int)t.r0, (int)(t.w0 - t.cb), full);
 }
 
+// K steps [ks, ke) of one warp, multiplying only the Q_W column blocks F..L of its quarter (LEFT:
+// fragment rows i, RIGHT: fragment columns jn); software-pipelined: the fragments of k-step k+4 are
+// loaded before the DMMAs of step k.
+template <int FM, int FN, bool LEFT, int F, int L>
+__device__ __forceinline__ void kseg(double (&acc)[FN][FM][2], const double* A, int a_i, int a_k,
+                                     const double* B, int b_j, int b_k, int ks, int ke) {
+  constexpr int I0 = LEFT ? F : 0, I1 = LEFT ? L : FM - 1;
+  constexpr int J0 = LEFT ? 0 : F, J1 = LEFT ? FN - 1 : L;
+  double fa[2][FM], fb[2][FN];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+#pragma unroll
+    for (int i = 0; i < FM; ++i) fa[h][i] = 0.0;
+#pragma unroll
+    for (int jn = 0; jn < FN; ++jn) fb[h][jn] = 0.0;
+  }
+  auto load = [&](int h, int k) {
+#pragma unroll
+    for (int i = I0; i <= I1; ++i) fa[h][i] = A[i * a_i + k * a_k];
+#pragma unroll
+    for (int jn = J0; jn <= J1; ++jn) fb[h][jn] = B[jn * b_j + k * b_k];
+  };
+  load(0, ks);
+  for (int kk = ks; kk < ke; kk += 8) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int k = kk + 4 * h;
+      if (k >= ke) break;
+      if (k + 4 < ke) load(h ^ 1, k + 4);
+#pragma unroll
+      for (int jn = J0; jn <= J1; ++jn)
+#pragma unroll
+        for (int i = I0; i <= I1; ++i) dmma(acc[jn][i], fb[h][jn], fa[h][i]);
+    }
+  }
+}
+
+// runtime (f, l) -> kseg<F, L> for every 0 <= F <= L < NB
+template <int FM, int FN, bool LEFT, int NB, int F = 0, int L = 0>
+__device__ __forceinline__ void kseg_dispatch(int f, int l, double (&acc)[FN][FM][2], const double* A, int a_i,
+                                              int a_k, const double* B, int b_j, int b_k, int ks, int ke) {
+  if constexpr (F < NB) {
+    if constexpr (L < NB) {
+      if (f == F && l == L) {
+        kseg<FM, FN, LEFT, F, L>(acc, A, a_i, a_k, B, b_j, b_k, ks, ke);
+        return;
+      }
+      kseg_dispatch<FM, FN, LEFT, NB, F, L + 1>(f, l, acc, A, a_i, a_k, B, b_j, b_k, ks, ke);
+    } else {
+      kseg_dispatch<FM, FN, LEFT, NB, F + 1, F + 1>(f, l, acc, A, a_i, a_k, B, b_j, b_k, ks, ke);
+    }
+  }
+}
+
 struct NoMid {
   __device__ void operator()() const {}
 };
 
 // One consumer warp: the output rows (LEFT) / columns (RIGHT) of Q_W column quarter `qq` (0..3)
 // times the whole other tile dimension.  K loop over the stage `P` with Q_W in `Qs`, release the
-// stage (`empty`), run `mid()`, store the tile in place.  The warp multiplies only the K range
-// [min klo_b, max khi_b) of its 8-column blocks b (store_q_slot's band extents): a quarter's blocks
-// have similar extents, so the union is tight and the DMMAs need no predication.
+// stage (`empty`), run `mid()`, store the tile in place.  Each 8-column block b of the quarter is
+// multiplied only over its K extent [klo_b, khi_b) (store_q_slot's band extents): the K axis is cut
+// at the extents' boundaries into segments with a fixed set of active blocks, each run by an
+// unrolled loop over exactly those blocks (no predicated DMMAs).
 template <int KP, bool LEFT, class Mid = NoMid>
 __device__ __forceinline__ void consume_tile(const double* Qs, const double* P, uint64_t* empty,
                                              const TileRef& t, int qq, int lane, Mid mid = Mid()) {
@@ -75,18 +130,22 @@ __device__ __forceinline__ void consume_tile(const double* Qs, const double* P, 
   (void)WM; (void)WN;
   const int qb0 = qq * NB;            // first Q_W column block
   const int lr = lane >> 2, lk = lane & 3;
+  int lo[NB], hi[NB];
   int kbeg = KP, kend = 0;
 #pragma unroll
   for (int b = 0; b < NB; ++b) {
 #ifdef HQR_BENCH_NO_TRIM  // benchmark-only knob (tools/gemm_bench.cu), never set in the product build
-    const int lo = 0, hi = KP;
+    lo[b] = 0; hi[b] = KP;
 #else
     const double* meta = Qs + (size_t)(8 * (qb0 + b)) * QLD + KP;
-    const int lo = (int)meta[0], hi = (int)meta[1];
+    lo[b] = (int)meta[0];
+    hi[b] = (int)meta[1];
 #endif
-    if (hi > lo) {
-      kbeg = min(kbeg, lo);
-      kend = max(kend, hi);
+    if (hi[b] > lo[b]) {
+      kbeg = min(kbeg, lo[b]);
+      kend = max(kend, hi[b]);
+    } else {
+      lo[b] = KP; hi[b] = 0;  // empty block: never active
     }
   }
   double acc[FN][FM][2];
@@ -104,33 +163,22 @@ __device__ __forceinline__ void consume_tile(const double* Qs, const double* P, 
     A = P + lk * LDP + lr;                          a_i = 8;       a_k = LDP;
     B = Qs + (8 * qb0 + lr) * QLD + lk;             b_j = 8 * QLD; b_k = 1;
   }
-  // software-pipelined K loop: fragments of k-step k+4 are loaded before the mma of step k
-  double fa[2][FM], fb[2][FN];
+  // K segments between consecutive block extent boundaries; in each, the active blocks form a
+  // contiguous range [f, l] (the band: lo and hi grow with the block; a non-contiguous set would
+  // be covered by its hull, whose extra blocks are zero there) and only they are multiplied
+  for (int k = kbeg; k < kend;) {
+    int f = NB, l = -1, nxt = kend;
 #pragma unroll
-  for (int h = 0; h < 2; ++h) {
-#pragma unroll
-    for (int i = 0; i < FM; ++i) fa[h][i] = 0.0;
-#pragma unroll
-    for (int jn = 0; jn < FN; ++jn) fb[h][jn] = 0.0;
-  }
-  auto load = [&](int h, int k) {
-#pragma unroll
-    for (int i = 0; i < FM; ++i) fa[h][i] = A[i * a_i + k * a_k];
-#pragma unroll
-    for (int jn = 0; jn < FN; ++jn) fb[h][jn] = B[jn * b_j + k * b_k];
-  };
-  if (kbeg < kend) load(0, kbeg);
-  for (int kk = kbeg; kk < kend; kk += 8) {
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int k = kk + 4 * h;
-      if (k >= kend) break;
-      if (k + 4 < kend) load(h ^ 1, k + 4);
-#pragma unroll
-      for (int jn = 0; jn < FN; ++jn)
-#pragma unroll
-        for (int i = 0; i < FM; ++i) dmma(acc[jn][i], fb[h][jn], fa[h][i]);
+    for (int b = 0; b < NB; ++b) {
+      if (lo[b] <= k && k < hi[b]) {
+        f = min(f, b);
+        l = max(l, b);
+      }
+      if (lo[b] > k) nxt = min(nxt, lo[b]);
+      if (hi[b] > k) nxt = min(nxt, hi[b]);
     }
+    if (l >= f) kseg_dispatch<FM, FN, LEFT, NB>(f, l, acc, A, a_i, a_k, B, b_j, b_k, k, nxt);
+    k = nxt;
   }
   __syncwarp();
   if (lane == 0) mbar_arrive(empty);
