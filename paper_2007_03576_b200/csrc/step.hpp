@@ -25,8 +25,8 @@ struct StepCounters {  // per step, zeroed before the sweep
 };
 
 struct ChunkSizes {   // tiles per task, per phase
-  int left = 12, near = 6, bulk = 24;
-  int tail = 1200, tail_chunk = 6;  // the queue's last `tail` tiles in chunks of `tail_chunk`
+  int left = 16, near = 8, bulk = 32;
+  int tail = 1500, tail_chunk = 8;  // the queue's last `tail` tiles in chunks of `tail_chunk`
 };
 
 // Tasks of one step in queue order (L, Rn, C, Z, Rf).
