@@ -106,6 +106,8 @@ struct State {
   std::map<PlanKey, std::unique_ptr<CachedPlan>> plans;
   std::map<GraphKey, CachedGraph> graphs;
   std::vector<cudaEvent_t> prof_events;
+  cudaStream_t cin = nullptr, cout = nullptr;  // host-buffer sweeps: copies in / out
+  std::vector<cudaEvent_t> io_events;          // their synchronisation (no timing)
   hqr_stats stats{};
   ncclComm_t comm = nullptr;       // world > 1
   // virtual shards (hqr_sweep_virtual): library-owned per-rank buffers on this one GPU
@@ -369,8 +371,99 @@ int get_fused(CachedPlan& cp, bool has_z, int64_t n, FusedTasks** out) {
   return 0;
 }
 
+cudaEvent_t io_event(size_t i) {
+  while (g.io_events.size() <= i) {
+    cudaEvent_t e;
+    cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+    g.io_events.push_back(e);
+  }
+  return g.io_events[i];
+}
+
+// Host-buffer sweep (the e2e path): the copies overlap the fused steps instead of bracketing them.
+// H goes up first (step 0's left update reads rows of every column); Z goes up in column chunks
+// behind it, and step s waits only for the Z columns its windows touch (the lowest chain reaches
+// column c after about c/s steps).  Column c of H and Z is final once every later window starts
+// below it (w0 > c: no later left, right, Z update or chase touches it), so finished column chunks
+// go down during the sweep on a second copy stream (the link is full duplex).
+struct IoPlan {
+  double* Hh = nullptr;  // caller's host H (nullptr: H is device-resident)
+  double* Zh = nullptr;  // caller's host Z (nullptr: device-resident or absent)
+  double* dH = nullptr;
+  double* dZ = nullptr;
+  int64_t n = 0;
+  std::vector<int64_t> need_z;  // step s needs Z columns [0, need_z[s])
+  std::vector<int64_t> fin;     // after launch s, columns [0, fin[s]) are final
+  int64_t chunk = 512;
+  int64_t z_waited = 0, out_done = 0;
+  size_t ev = 0;
+  int64_t h2d = 0, d2h = 0;
+
+  void plan(const Plan& P) {
+    need_z.assign(P.nsteps, 0);
+    fin.assign(P.nsteps, n);
+    int64_t run = n;
+    for (int s = P.nsteps - 1; s >= 0; --s) {
+      fin[s] = run;  // min w0 over the windows of later steps
+      for (int i = P.step_begin[s]; i < P.step_begin[s + 1]; ++i) {
+        run = std::min<int64_t>(run, P.windows[i].w0);
+        need_z[s] = std::max<int64_t>(need_z[s], P.windows[i].w1 + 1);
+      }
+    }
+  }
+  int start(cudaStream_t A) {  // before chase(0)
+    const size_t col = (size_t)n * sizeof(double);
+    CK(cudaStreamWaitEvent(g.cin, g.ev0, 0));
+    if (Hh) {
+      CK(cudaMemcpyAsync(dH, Hh, col * n, cudaMemcpyHostToDevice, g.cin));
+      h2d += (int64_t)(col * n);
+    }
+    cudaEvent_t e = io_event(ev++);
+    CK(cudaEventRecord(e, g.cin));
+    CK(cudaStreamWaitEvent(A, e, 0));
+    if (Zh) {
+      for (int64_t c = 0; c < n; c += chunk) {
+        const int64_t w = std::min(chunk, n - c);
+        CK(cudaMemcpyAsync(dZ + c * n, Zh + c * n, col * w, cudaMemcpyHostToDevice, g.cin));
+        CK(cudaEventRecord(io_event(ev + c / chunk), g.cin));
+      }
+      h2d += (int64_t)(col * n);
+    }
+    return 0;
+  }
+  int before(int s, cudaStream_t A) {  // before launch s
+    if (!Zh) return 0;
+    while (z_waited < need_z[s]) {
+      CK(cudaStreamWaitEvent(A, io_event(ev + z_waited / chunk), 0));
+      z_waited = std::min(n, (z_waited / chunk + 1) * chunk);
+    }
+    return 0;
+  }
+  int after(int s, cudaStream_t A, bool last) {  // after launch s
+    const int64_t f = last ? n : fin[s];
+    if (f <= out_done || (!last && f - out_done < chunk)) return 0;
+    const size_t col = (size_t)n * sizeof(double);
+    const size_t zev = ev + (size_t)((n + chunk - 1) / chunk);
+    cudaEvent_t e = io_event(zev + (size_t)s);
+    CK(cudaEventRecord(e, A));
+    CK(cudaStreamWaitEvent(g.cout, e, 0));
+    const int64_t w = f - out_done;
+    if (Hh) CK(cudaMemcpyAsync(Hh + out_done * n, dH + out_done * n, col * w, cudaMemcpyDeviceToHost, g.cout));
+    if (Zh) CK(cudaMemcpyAsync(Zh + out_done * n, dZ + out_done * n, col * w, cudaMemcpyDeviceToHost, g.cout));
+    d2h += (int64_t)(col * w) * ((Hh ? 1 : 0) + (Zh ? 1 : 0));
+    out_done = f;
+    if (last) {
+      cudaEvent_t done = io_event(zev + fin.size());
+      CK(cudaEventRecord(done, g.cout));
+      CK(cudaStreamWaitEvent(A, done, 0));
+    }
+    return 0;
+  }
+};
+
 int enqueue_fused(CachedPlan& cp, double* H, double* Z, int64_t n, const hqr::TensorMaps& tm,
-                  hqr_stats* st, bool prof = false, std::vector<int>* classes = nullptr) {
+                  hqr_stats* st, bool prof = false, std::vector<int>* classes = nullptr,
+                  IoPlan* io = nullptr) {
   const Plan& P = cp.plan;
   FusedTasks* f = nullptr;
   int rc = get_fused(cp, Z != nullptr, n, &f);
@@ -396,18 +489,29 @@ int enqueue_fused(CachedPlan& cp, double* H, double* Z, int64_t n, const hqr::Te
     cudaEventRecord(prof_event(ev++), A);
     if (classes) classes->push_back(cls);
   };
+  if (io) {
+    io->plan(P);
+    rc = io->start(A);
+    if (rc) return rc;
+  }
   mark(0);
   CK(hqr::launch_chase(args(0), P.max_kw, P.max_nbc, A));
   mark(-1);
   st->launches_chase++;
   for (int s = 0; s < P.nsteps; ++s) {
     const int nt = f->begin[s + 1] - f->begin[s];
+    if (io && (rc = io->before(s, A))) return rc;
     mark(3);
     CK(hqr::launch_step(args(s), args(s + 1), f->d_tasks + f->begin[s], nt, f->nL[s], f->nRn[s],
                         f->nLt[s], f->nRnt[s],
                         f->d_ctr + s, tm, P.max_kw, g.num_sms, A));
     mark(-1);
     st->launches_left++;  // one fused launch per step (counted once)
+    if (io && (rc = io->after(s, A, s + 1 == P.nsteps))) return rc;
+  }
+  if (io) {
+    st->h2d_bytes = io->h2d;
+    st->d2h_bytes = io->d2h;
   }
   st->flops_update = f->flops;
   st->bytes_update = f->bytes;
@@ -444,6 +548,8 @@ int hqr_setup(const hqr_config* cfg) {
   CK(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
   CK(cudaStreamCreateWithPriority(&g.stream, cudaStreamNonBlocking, prio_hi));
   CK(cudaStreamCreateWithPriority(&g.zstream, cudaStreamNonBlocking, prio_lo));
+  CK(cudaStreamCreateWithFlags(&g.cin, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&g.cout, cudaStreamNonBlocking));
   CK(cudaEventCreate(&g.ev0));
   CK(cudaEventCreate(&g.ev1));
   CK(cudaEventCreateWithFlags(&g.ev_fork, cudaEventDisableTiming));
@@ -498,6 +604,10 @@ int hqr_teardown(void) {
     cudaEventDestroy(g.ev_z[i]);
   }
   cudaStreamDestroy(g.zstream);
+  cudaStreamDestroy(g.cin);
+  cudaStreamDestroy(g.cout);
+  for (cudaEvent_t e : g.io_events) cudaEventDestroy(e);
+  g.io_events.clear();
   cudaStreamDestroy(g.stream);
   if (g.comm) {
     ncclCommDestroy(g.comm);
@@ -586,16 +696,8 @@ int sweep_impl(double* H, double* Z, int64_t n, const Blocks& blocks, const doub
       CK(cudaMalloc(&g.d_zstage, need * sizeof(double)));
       g.stage_cap = need;
     }
-    if (!h_dev) {
-      dH = g.d_hstage;
-      CK(cudaMemcpyAsync(dH, H, nn * sizeof(double), cudaMemcpyHostToDevice, g.stream));
-      st.h2d_bytes += nn * sizeof(double);
-    }
-    if (Z && !z_dev) {
-      dZ = g.d_zstage;
-      CK(cudaMemcpyAsync(dZ, Z, nn * sizeof(double), cudaMemcpyHostToDevice, g.stream));
-      st.h2d_bytes += nn * sizeof(double);
-    }
+    if (!h_dev) dH = g.d_hstage;
+    if (Z && !z_dev) dZ = g.d_zstage;
   }
 
   const bool prof = (g.flags & HQR_FLAG_PROFILE) != 0;
@@ -610,7 +712,30 @@ int sweep_impl(double* H, double* Z, int64_t n, const Blocks& blocks, const doub
     rc = get_fused(*cp, dZ != nullptr, n, &f);
     if (rc) return rc;
   }
-  if (use_graph) {
+  // host buffers with the fused path: copies overlapped with the steps (IoPlan); otherwise the
+  // whole matrices are staged before and after the sweep
+  const bool host_io = (!h_dev || (Z && !z_dev));
+  const bool overlap = host_io && fused && !prof;
+  if (host_io && !overlap) {
+    if (!h_dev) {
+      CK(cudaMemcpyAsync(dH, H, nn * sizeof(double), cudaMemcpyHostToDevice, g.stream));
+      st.h2d_bytes += nn * sizeof(double);
+    }
+    if (Z && !z_dev) {
+      CK(cudaMemcpyAsync(dZ, Z, nn * sizeof(double), cudaMemcpyHostToDevice, g.stream));
+      st.h2d_bytes += nn * sizeof(double);
+    }
+  }
+  if (overlap) {
+    IoPlan io;
+    io.Hh = h_dev ? nullptr : H;
+    io.Zh = (Z && !z_dev) ? Z : nullptr;
+    io.dH = dH;
+    io.dZ = dZ;
+    io.n = n;
+    rc = enqueue_fused(*cp, dH, dZ, n, tmf, &st, false, nullptr, &io);
+    if (rc) return rc;
+  } else if (use_graph) {
     GraphKey gk{plan_key(n, blocks, window), dH, dZ};
     auto it = g.graphs.find(gk);
     if (it == g.graphs.end()) {
@@ -645,11 +770,11 @@ int sweep_impl(double* H, double* Z, int64_t n, const Blocks& blocks, const doub
     if (rc) return rc;
   }
 
-  if (!h_dev) {
+  if (!h_dev && !overlap) {
     CK(cudaMemcpyAsync(H, dH, nn * sizeof(double), cudaMemcpyDeviceToHost, g.stream));
     st.d2h_bytes += nn * sizeof(double);
   }
-  if (Z && !z_dev) {
+  if (Z && !z_dev && !overlap) {
     CK(cudaMemcpyAsync(Z, dZ, nn * sizeof(double), cudaMemcpyDeviceToHost, g.stream));
     st.d2h_bytes += nn * sizeof(double);
   }

@@ -95,6 +95,31 @@ def test_no_z_and_host_pointer_path():
     assert st["h2d_bytes"] == 2 * 180 * 180 * 8 and st["d2h_bytes"] == 2 * 180 * 180 * 8
 
 
+@pytest.mark.parametrize("mode", ["both_host", "h_host", "z_host"])
+def test_host_buffers_overlapped_copies(mode):
+    """Host H / Z: the copies run in column chunks overlapped with the steps (IoPlan in
+    hqr_api.cu); several chunks and an interior active block.  Bitwise equal to device buffers."""
+    n, ilo, ihi = 2400, 37, 2290
+    H0, Z0, re_, im_ = random_case(53, n, 64, ilo, ihi, z0="orth")
+    Hg, Zg = gpu_sweep(H0, Z0, ilo, ihi, re_, im_, 96)
+    Hh, Zh = H0.copy(order="F"), Z0.copy(order="F")
+    Hd, Zd = hq.to_device(H0), hq.to_device(Z0)
+    if mode == "both_host":
+        hq.sweep(Hh, Zh, ilo, ihi, re_, im_, 96)
+        Hr, Zr = Hh, Zh
+    elif mode == "h_host":
+        hq.sweep(Hh, Zd, ilo, ihi, re_, im_, 96)
+        Hr, Zr = Hh, hq.from_device(Zd)
+    else:
+        hq.sweep(Hd, Zh, ilo, ihi, re_, im_, 96)
+        Hr, Zr = hq.from_device(Hd), Zh
+    assert np.array_equal(Hr, Hg) and np.array_equal(Zr, Zg)
+    st = hq.stats()
+    nb = n * n * 8
+    assert st["h2d_bytes"] == nb * (2 if mode == "both_host" else 1)
+    assert st["d2h_bytes"] == nb * (2 if mode == "both_host" else 1)
+
+
 def test_graph_and_direct_launch_bitwise_equal():
     H0, Z0, re_, im_ = random_case(51, 300, 32, 0, 299, z0="orth")
     Hg, Zg = gpu_sweep(H0, Z0, 0, 299, re_, im_, 64)
