@@ -447,6 +447,9 @@ struct IoPlan {
     cudaEvent_t e = io_event(zev + (size_t)s);
     CK(cudaEventRecord(e, A));
     CK(cudaStreamWaitEvent(g.cout, e, 0));
+    // columns no step touches (before ilo, after ihi) may be final before their Z chunk is up
+    if (Zh)
+      for (int64_t k = out_done / chunk; k * chunk < f; ++k) CK(cudaStreamWaitEvent(g.cout, io_event(ev + (size_t)k), 0));
     const int64_t w = f - out_done;
     if (Hh) CK(cudaMemcpyAsync(Hh + out_done * n, dH + out_done * n, col * w, cudaMemcpyDeviceToHost, g.cout));
     if (Zh) CK(cudaMemcpyAsync(Zh + out_done * n, dZ + out_done * n, col * w, cudaMemcpyDeviceToHost, g.cout));
