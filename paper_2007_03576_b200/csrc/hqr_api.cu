@@ -484,6 +484,7 @@ int enqueue_fused(CachedPlan& cp, double* H, double* Z, int64_t n, const hqr::Te
       a.win_count = P.step_begin[s + 1] - P.step_begin[s];
       a.slot_offset = (s % hqr::kQSets) * P.nchains;
     }
+    a.step = s;
     return a;
   };
   size_t ev = 0;
@@ -729,6 +730,8 @@ int sweep_impl(double* H, double* Z, int64_t n, const Blocks& blocks, const doub
       st.h2d_bytes += nn * sizeof(double);
     }
   }
+  static const bool timing = getenv("HQR_TIMING_DUMP") != nullptr;  // -DHQR_TIMING builds
+  if (timing && fused) hqr::debug_timing(0, true);
   if (overlap) {
     IoPlan io;
     io.Hh = h_dev ? nullptr : H;
@@ -784,6 +787,7 @@ int sweep_impl(double* H, double* Z, int64_t n, const Blocks& blocks, const doub
   CK(cudaEventRecord(g.ev1, g.stream));
   CK(cudaStreamSynchronize(g.stream));
   CK(cudaGetLastError());
+  if (timing && fused) hqr::debug_timing(cp->plan.nsteps, false);
   float ms = 0;
   CK(cudaEventElapsedTime(&ms, g.ev0, g.ev1));
   st.ms_total = ms;

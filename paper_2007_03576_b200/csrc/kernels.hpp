@@ -26,6 +26,7 @@ struct StepArgs {
   int QLD;                   // Q slot leading dimension = pad_ld(KP) (the update kernels' SMEM ld)
   int slot_offset;           // this step's Q slot set: window slot s lives at slot s + slot_offset
   int right_mode;            // right kernel: 0 = H rows above W and Z, 1 = H only, 2 = Z only
+  int step;                  // wavefront step index (debug timing only)
   double* wstats;            // nullable: per plan window, the executed DMMA work units of its factor
                              // (record_band); wstats[win_begin + i] for window i of the step
 };

@@ -61,6 +61,20 @@ __device__ int* g_prog;
 #define PROG(tag) do { } while (0)
 #endif
 
+#ifdef HQR_TIMING  // debugging build only: per-step critical-path timestamps (globaltimer, ns)
+__device__ unsigned long long g_tim[4096][4];  // min CTA start, min chase start, max chase end, max end
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define TIM_MIN(s, k) atomicMin(&g_tim[(s) & 4095][k], gtime())
+#define TIM_MAX(s, k) atomicMax(&g_tim[(s) & 4095][k], gtime())
+#else
+#define TIM_MIN(s, k) do { } while (0)
+#define TIM_MAX(s, k) do { } while (0)
+#endif
+
 // spin until *p >= target (acquire); the watchdog build reports a hang and traps
 __device__ __forceinline__ void spin_until(const int* p, int target, int tag) {
 #ifdef HQR_WATCHDOG
@@ -255,6 +269,7 @@ __global__ void __launch_bounds__(kStepThreads, 1)
   if (tid < NS) desc[tid].pos = -1;
   fence_proxy_async();
   __syncthreads();
+  if (tid == 0) TIM_MIN(a.step, 0);
 
   if (warp == kProducerWarp) {
     // ================================ producer / scheduler ================================
@@ -309,8 +324,10 @@ __global__ void __launch_bounds__(kStepThreads, 1)
           cwi = an.win_begin + T.win;
         }
         __syncthreads();
+        if (lane == 0) TIM_MIN(a.step, 1);
         chase_window_9w(an, cw, cwi, sm, R);
         __syncthreads();
+        if (lane == 0) TIM_MAX(a.step, 2);
         q_win = -1;
         continue;
       }
@@ -426,6 +443,7 @@ __global__ void __launch_bounds__(kStepThreads, 1)
       else if (cnt == 2) pend_rn += add;
     }
   }
+  if (lane == 0) TIM_MAX(a.step, 3);
 }
 
 template <int KP>
@@ -455,6 +473,41 @@ cudaError_t launch_step_t(const StepArgs& a, const StepArgs& an, const Task* tas
 }
 
 }  // namespace
+
+#ifdef HQR_TIMING
+void debug_timing(int nsteps, bool reset) {
+  static unsigned long long h[4096][4];
+  if (reset) {
+    for (int i = 0; i < 4096; ++i) { h[i][0] = h[i][1] = ~0ull; h[i][2] = h[i][3] = 0; }
+    cudaMemcpyToSymbol(g_tim, h, sizeof(h));
+    return;
+  }
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(h, g_tim, sizeof(h));
+  double cs = 0, ce = 0, e = 0, gap = 0;
+  int nc = 0;
+  for (int s = 0; s < nsteps && s < 4096; ++s) {
+    const double t0 = (double)h[s][0];
+    e += (h[s][3] - t0) * 1e-3;
+    if (s > 0) gap += ((double)h[s][0] - (double)h[s - 1][3]) * 1e-3;
+    if (h[s][1] != ~0ull) {
+      cs += (h[s][1] - t0) * 1e-3;
+      ce += (h[s][2] - t0) * 1e-3;
+      ++nc;
+    }
+  }
+  fprintf(stderr, "hqr timing: %d steps, mean launch %.1f us, chase start %.1f us, chase end %.1f us "
+          "(%d steps with chases), mean gap between launches %.2f us\n", nsteps, e / nsteps,
+          cs / std::max(nc, 1), ce / std::max(nc, 1), nc, gap / std::max(nsteps - 1, 1));
+  for (int s = 0; s < nsteps && s < 4096; s += std::max(1, nsteps / 12)) {
+    const double t0 = (double)h[s][0];
+    fprintf(stderr, "  step %4d: launch %.1f us, chase %.1f .. %.1f us\n", s, (h[s][3] - t0) * 1e-3,
+            h[s][1] != ~0ull ? (h[s][1] - t0) * 1e-3 : -1.0, h[s][2] ? (h[s][2] - t0) * 1e-3 : -1.0);
+  }
+}
+#else
+void debug_timing(int, bool) {}
+#endif
 
 #ifdef HQR_PROGRESS
 void debug_progress_init() {

@@ -43,5 +43,7 @@ cudaError_t launch_step(const StepArgs& a, const StepArgs& an, const Task* tasks
 // Debugging builds (-DHQR_PROGRESS): progress buffer in host-mapped memory, dumped after
 // HQR_PROGRESS_SECS seconds (then the process exits).  No-op otherwise.
 void debug_progress_init();
+// Debugging builds (-DHQR_TIMING): per-step timestamps; reset before a sweep, print after it.
+void debug_timing(int nsteps, bool reset);
 
 }  // namespace hqr
