@@ -68,6 +68,7 @@ __device__ __forceinline__ unsigned long long gtime() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
+__device__ unsigned long long g_ctim[8];  // chase: summed cycles per phase (all warps), windows
 #define TIM_MIN(s, k) atomicMin(&g_tim[(s) & 4095][k], gtime())
 #define TIM_MAX(s, k) atomicMax(&g_tim[(s) & 4095][k], gtime())
 #else
@@ -120,6 +121,12 @@ __device__ void chase_window_9w(const StepArgs& a, const WindowDesc& W, int widx
     }
   }
   __syncthreads();
+#ifdef HQR_TIMING
+  long long c_p1 = 0, c_s1 = 0, c_p2 = 0, c_s2 = 0, c_t = clock64();
+#define CTIM(acc) do { const long long _c = clock64(); acc += _c - c_t; c_t = _c; } while (0)
+#else
+#define CTIM(acc) do { } while (0)
+#endif
   const int rmaxH = ihi - w0;
   for (int t = W.t0; t <= W.t1; ++t) {
     const int rQ = min(ilo - 1 + t - w0 + 3, kw - 1);
@@ -171,7 +178,9 @@ __device__ void chase_window_9w(const StepArgs& a, const WindowDesc& W, int widx
         if (m == 3) hc[2] = fma(-tw, v2, h2);
       }
     }
+    CTIM(c_p1);
     __syncthreads();
+    CTIM(c_s1);
     for (int jj = warp; jj < nbc; jj += kStepWarps) {
       Refl r;
       r.pl = R.pl[jj];
@@ -180,8 +189,20 @@ __device__ void chase_window_9w(const StepArgs& a, const WindowDesc& W, int widx
       right_apply(Hs + (r.pl + 1) * ldh, ldh, min(r.pl + r.m + 1, rmaxH) + 1, r, lane);
       right_apply(Qs + (r.pl + 1) * ldh, ldh, rQ + 1, r, lane);
     }
+    CTIM(c_p2);
     __syncthreads();
+    CTIM(c_s2);
   }
+#ifdef HQR_TIMING
+  if (lane == 0) {
+    atomicAdd(&g_ctim[0], (unsigned long long)c_p1);
+    atomicAdd(&g_ctim[1], (unsigned long long)c_s1);
+    atomicAdd(&g_ctim[2], (unsigned long long)c_p2);
+    atomicAdd(&g_ctim[3], (unsigned long long)c_s2);
+    if (warp == 0) atomicAdd(&g_ctim[4], 1ull);
+    if (warp == 0) atomicAdd(&g_ctim[5], (unsigned long long)(W.t1 - W.t0 + 1));
+  }
+#endif
   {
     double* g = a.H + (int64_t)(w0 - a.hcol0) * n + w0;
     for (int c = warp; c < kw; c += kStepWarps) {
@@ -335,7 +356,11 @@ __global__ void __launch_bounds__(kStepThreads, 1)
       // A new window needs its Q_W.  Its first NS-1 panel tiles are issued first (their stages free
       // up as the previous tiles are released); once every earlier position has been released --
       // no tile reads the old Q_W any more -- Q_W is loaded, so the panel loads overlap the drain.
+#ifdef HQR_BENCH_NO_QSWITCH  // timing experiment only: keep the first Q_W (wrong results)
+      const bool new_q = q_win < 0;
+#else
       const bool new_q = T.win != q_win;
+#endif
       if (new_q) {
         ++qe;
         q_win = T.win;
@@ -480,6 +505,8 @@ void debug_timing(int nsteps, bool reset) {
   if (reset) {
     for (int i = 0; i < 4096; ++i) { h[i][0] = h[i][1] = ~0ull; h[i][2] = h[i][3] = 0; }
     cudaMemcpyToSymbol(g_tim, h, sizeof(h));
+    unsigned long long z[8] = {0};
+    cudaMemcpyToSymbol(g_ctim, z, sizeof(z));
     return;
   }
   cudaDeviceSynchronize();
@@ -495,6 +522,14 @@ void debug_timing(int nsteps, bool reset) {
       ce += (h[s][2] - t0) * 1e-3;
       ++nc;
     }
+  }
+  unsigned long long ct[8];
+  cudaMemcpyFromSymbol(ct, g_ctim, sizeof(ct));
+  if (ct[4]) {
+    const double w = (double)ct[4] * kStepWarps, st = (double)ct[5] / (double)ct[4];
+    fprintf(stderr, "hqr chase: %llu windows, %.1f steps each; cycles per step per warp: phase1 %.0f, "
+            "sync1 %.0f, phase2 %.0f, sync2 %.0f\n", ct[4], st, ct[0] / w / st, ct[1] / w / st,
+            ct[2] / w / st, ct[3] / w / st);
   }
   fprintf(stderr, "hqr timing: %d steps, mean launch %.1f us, chase start %.1f us, chase end %.1f us "
           "(%d steps with chases), mean gap between launches %.2f us\n", nsteps, e / nsteps,

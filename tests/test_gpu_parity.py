@@ -120,6 +120,46 @@ def test_host_buffers_overlapped_copies(mode):
     assert st["d2h_bytes"] == nb * (2 if mode == "both_host" else 1)
 
 
+def _band_units(Q, KP=96):
+    """Executed DMMA work units of one window factor, written out from the kernel's contract
+    (gemm_tile.cuh consume_tile): 8-column blocks' nonzero row ranges rounded to 4, quarters of
+    KP/32 blocks, K segments with their active blocks."""
+    kw = Q.shape[0]
+    ext = []
+    for b in range(KP // 8):
+        cols = [c for c in range(8 * b, 8 * b + 8) if c < kw]
+        rows = [r for c in cols for r in np.nonzero(Q[:, c])[0]]
+        ext.append((min(rows) // 4 * 4, (max(rows) + 4) // 4 * 4) if rows else (KP, 0))
+    nb, u = KP // 32, 0
+    for q in range(4):
+        e = ext[q * nb:(q + 1) * nb]
+        cuts = sorted({v for lo, hi in e if hi > lo for v in (lo, hi)})
+        for k0, k1 in zip(cuts, cuts[1:]):
+            act = [i for i, (lo, hi) in enumerate(e) if lo <= k0 < hi]
+            if act:
+                u += 8 * (max(act) - min(act) + 1) * (k1 - k0)
+    return u
+
+
+def test_executed_dmma_flops_match_band_model():
+    """hqr_stats.flops_dmma (the roofline numerator, recorded by the chase per window) equals the
+    executed work rebuilt from the windows' factors Q_W computed independently by the numpy
+    schedule emulator (same plan, same reflectors; exact zeros are structural)."""
+    import schedule_emulator as em
+    n, ns = 600, 60
+    H0, Z0, re_, im_ = random_case(61, n, ns, z0="orth", shift_kind="disk2")
+    gpu_sweep(H0, Z0, 0, n - 1, re_, im_, 96)
+    got = hq.stats()["flops_dmma"]
+    info, wins = hq.plan_query(n, 0, n - 1, ns, 96)
+    units = []
+    em.emulate(H0.copy(), None, 0, n - 1, re_, im_, 96, on_window=lambda nbc, Q: units.append(_band_units(Q)))
+    assert len(units) == len(wins)
+    want = sum(2.0 * u * ((n - 1 - int(w[3])) + int(w[2]) + n) for u, w in zip(units, wins))
+    assert abs(got - want) <= 1e-12 * want, (got, want)
+    dense = sum(2.0 * (int(w[3]) - int(w[2]) + 1) ** 2 * ((n - 1 - int(w[3])) + int(w[2]) + n) for w in wins)
+    assert 0.5 * dense < got < dense
+
+
 def test_graph_and_direct_launch_bitwise_equal():
     H0, Z0, re_, im_ = random_case(51, 300, 32, 0, 299, z0="orth")
     Hg, Zg = gpu_sweep(H0, Z0, 0, 299, re_, im_, 64)
