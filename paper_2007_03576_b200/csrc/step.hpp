@@ -25,7 +25,7 @@ struct StepCounters {  // per step, zeroed before the sweep
 };
 
 struct ChunkSizes {   // tiles per task, per phase
-  int left = 16, near = 8, bulk = 32;
+  int left = 16, near = 16, bulk = 32;
   int tail = 1500, tail_chunk = 8;  // the queue's last `tail` tiles in chunks of `tail_chunk`
 };
 
