@@ -68,10 +68,15 @@ struct CachedGraph {
 };
 
 struct FusedTasks {            // task queues of every step for the fused step kernel
-  std::vector<hqr::Task> tasks;
-  std::vector<int32_t> begin, nL, nRn, nLt, nRnt;
+  std::vector<hqr::Task> tasks;          // all steps, in queue order
+  std::vector<int32_t> begin;            // step g's tasks: [begin[g], begin[g+1])
+  std::vector<hqr::StepInfo> steps;
+  std::vector<hqr::WinDeps> wdeps;
   hqr::Task* d_tasks = nullptr;
-  hqr::StepCounters* d_ctr = nullptr;
+  hqr::StepInfo* d_steps = nullptr;
+  hqr::WinDeps* d_wdeps = nullptr;
+  int* d_ctr = nullptr;                  // [8 claim counters][4 per step][4 per window]
+  size_t nctr = 0;
   double flops = 0, bytes = 0;
 };
 
@@ -340,6 +345,8 @@ int get_fused(CachedPlan& cp, bool has_z, int64_t n, FusedTasks** out) {
     StepArgs a{};
     a.n = n; a.hcol0 = 0; a.lc0 = 0; a.lc1 = n; a.zrows = n; a.ldz = n; a.KP = cp.KP;
     a.Z = has_z ? reinterpret_cast<double*>(1) : nullptr;  // only tested for presence
+    const int nwin_all = (int)P.windows.size();
+    f->wdeps.assign(nwin_all, hqr::WinDeps{{-1, -1, -1}, 0, 0, 0});
     for (int g = 0; g < P.nsteps; ++g) {
       f->begin.push_back((int32_t)f->tasks.size());
       const WindowDesc* w = P.windows.data() + P.step_begin[g];
@@ -347,24 +354,49 @@ int get_fused(CachedPlan& cp, bool has_z, int64_t n, FusedTasks** out) {
       const WindowDesc* wn = (g + 1 < P.nsteps) ? P.windows.data() + P.step_begin[g + 1] : nullptr;
       const int nn = (g + 1 < P.nsteps) ? P.step_begin[g + 2] - P.step_begin[g + 1] : 0;
       int nl, nrn;
+      a.step = g;
       hqr::build_step_tasks(a, w, nw, wn, nn, sp[g], chunk_sizes(), &f->tasks, &nl, &nrn);
-      f->nL.push_back(nl);
-      f->nRn.push_back(nrn);
-      int lt = 0, rnt = 0;
-      for (int i = 0; i < nl + nrn; ++i) (i < nl ? lt : rnt) += f->tasks[f->begin.back() + i].ntiles;
-      f->nLt.push_back(lt);
-      f->nRnt.push_back(rnt);
+      hqr::StepInfo S{};
+      S.win_begin = P.step_begin[g];
+      S.win_count = nw;
+      S.slot_offset = (g % hqr::kQSets) * P.nchains;
+      S.nL = nl;
+      S.nRn = nrn;
+      for (int i = f->begin.back(); i < (int)f->tasks.size(); ++i) {
+        const hqr::Task& T = f->tasks[i];
+        if (T.type == hqr::kTaskChase) continue;
+        S.ntiles += T.ntiles;
+        if (T.idx < nl) S.nLt += T.ntiles;
+        else if (T.type == hqr::kTaskRight && T.idx < nl + nrn) S.nRnt += T.ntiles;
+        else if (T.type == hqr::kTaskRight) f->wdeps[S.win_begin + T.win].rftiles += T.ntiles;
+        else if (T.type == hqr::kTaskZ) f->wdeps[S.win_begin + T.win].ztiles += T.ntiles;
+      }
+      f->steps.push_back(S);
       for (int i = 0; i < nw; ++i) {
         const double kw = w[i].w1 - w[i].w0 + 1;
         const double rows = (double)(n - 1 - w[i].w1) + (double)w[i].w0 + (has_z ? (double)n : 0.0);
         f->flops += 2.0 * kw * kw * rows;
         f->bytes += 16.0 * kw * rows;
+        // windows of the previous step whose columns meet this one (far-right / Z ordering)
+        if (g > 0) {
+          int np = 0;
+          for (int k = P.step_begin[g - 1]; k < P.step_begin[g]; ++k)
+            if (P.windows[k].w0 <= w[i].w1 && w[i].w0 <= P.windows[k].w1) {
+              if (np == 3) return -102;  // cannot happen for planner windows (checked)
+              f->wdeps[P.step_begin[g] + i].pred[np++] = k;
+            }
+        }
       }
     }
     f->begin.push_back((int32_t)f->tasks.size());
     CK(cudaMalloc(&f->d_tasks, f->tasks.size() * sizeof(hqr::Task)));
     CK(cudaMemcpy(f->d_tasks, f->tasks.data(), f->tasks.size() * sizeof(hqr::Task), cudaMemcpyHostToDevice));
-    CK(cudaMalloc(&f->d_ctr, (size_t)P.nsteps * sizeof(hqr::StepCounters)));
+    CK(cudaMalloc(&f->d_steps, f->steps.size() * sizeof(hqr::StepInfo)));
+    CK(cudaMemcpy(f->d_steps, f->steps.data(), f->steps.size() * sizeof(hqr::StepInfo), cudaMemcpyHostToDevice));
+    CK(cudaMalloc(&f->d_wdeps, f->wdeps.size() * sizeof(hqr::WinDeps)));
+    CK(cudaMemcpy(f->d_wdeps, f->wdeps.data(), f->wdeps.size() * sizeof(hqr::WinDeps), cudaMemcpyHostToDevice));
+    f->nctr = 8 + 4 * (size_t)P.nsteps + 4 * (size_t)nwin_all;
+    CK(cudaMalloc(&f->d_ctr, f->nctr * sizeof(int)));
     slot = std::move(f);
   }
   *out = slot.get();
@@ -472,7 +504,7 @@ int enqueue_fused(CachedPlan& cp, double* H, double* Z, int64_t n, const hqr::Te
   int rc = get_fused(cp, Z != nullptr, n, &f);
   if (rc) return rc;
   cudaStream_t A = g.stream;
-  CK(cudaMemsetAsync(f->d_ctr, 0, (size_t)P.nsteps * sizeof(hqr::StepCounters), A));
+  CK(cudaMemsetAsync(f->d_ctr, 0, f->nctr * sizeof(int), A));
   auto args = [&](int s) {
     StepArgs a{};
     a.H = H; a.Z = Z; a.n = n; a.ilo = P.ilo; a.ihi = P.ihi;
@@ -502,16 +534,30 @@ int enqueue_fused(CachedPlan& cp, double* H, double* Z, int64_t n, const hqr::Te
   CK(hqr::launch_chase(args(0), P.max_kw, P.max_nbc, A));
   mark(-1);
   st->launches_chase++;
-  for (int s = 0; s < P.nsteps; ++s) {
-    const int nt = f->begin[s + 1] - f->begin[s];
-    if (io && (rc = io->before(s, A))) return rc;
+  int* step_ctr = f->d_ctr + 8;
+  int* win_ctr = step_ctr + 4 * (size_t)P.nsteps;
+  // (step 0's chases ran in their own launch: step-0 tasks do not wait for them)
+  const StepArgs base = args(0);
+  static const bool per_step = getenv("HQR_PER_STEP") != nullptr;  // A/B knob: a launch per step
+  if (!per_step && !io && !prof) {
+    // one persistent launch for the whole sweep: step g+1's work starts as soon as its own
+    // dependencies are met (no launch boundary, no end-of-step tail)
     mark(3);
-    CK(hqr::launch_step(args(s), args(s + 1), f->d_tasks + f->begin[s], nt, f->nL[s], f->nRn[s],
-                        f->nLt[s], f->nRnt[s],
-                        f->d_ctr + s, tm, P.max_kw, g.num_sms, A));
+    CK(hqr::launch_step(base, f->d_steps, P.nsteps, f->d_wdeps, f->d_tasks, (int)f->tasks.size(), f->d_ctr,
+                        step_ctr, win_ctr, tm, P.max_kw, g.num_sms, A));
     mark(-1);
-    st->launches_left++;  // one fused launch per step (counted once)
-    if (io && (rc = io->after(s, A, s + 1 == P.nsteps))) return rc;
+    st->launches_left++;
+  } else {
+    for (int s = 0; s < P.nsteps; ++s) {
+      const int nt = f->begin[s + 1] - f->begin[s];
+      if (io && (rc = io->before(s, A))) return rc;
+      mark(3);
+      CK(hqr::launch_step(base, f->d_steps, P.nsteps, f->d_wdeps, f->d_tasks + f->begin[s], nt,
+                          step_ctr + 4 * s + 3, step_ctr, win_ctr, tm, P.max_kw, g.num_sms, A));
+      mark(-1);
+      st->launches_left++;  // one fused launch per step (counted once)
+      if (io && (rc = io->after(s, A, s + 1 == P.nsteps))) return rc;
+    }
   }
   if (io) {
     st->h2d_bytes = io->h2d;
@@ -584,6 +630,8 @@ int hqr_teardown(void) {
       if (f) {
         if (f->d_tasks) cudaFree(f->d_tasks);
         if (f->d_ctr) cudaFree(f->d_ctr);
+        if (f->d_steps) cudaFree(f->d_steps);
+        if (f->d_wdeps) cudaFree(f->d_wdeps);
       }
   }
   g.plans.clear();

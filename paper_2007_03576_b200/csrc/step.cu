@@ -232,9 +232,10 @@ struct StageDesc {
   int pos;     // ring position this descriptor belongs to (see the consumer's wait)
   int kind;    // kDescTile / kDescChase / kDescExit
   int left;    // tile: LEFT (1) or RIGHT/Z (0)
-  int ctr;     // tile: 0, or 1 / 2 = add cnt_add into l_done / rn_done after the stores
   int qe;      // tile: Q_W load epoch it multiplies with
-  int cnt_add; // tile with ctr != 0: tiles of the task this group has done (this warp adds them)
+  int cnt_add; // tile with ctr: tiles of the task this group has done (this warp adds them)
+  int* ctr;    // tile: nullptr, or the counter the task's completion feeds (after the stores) ...
+  int* ctr_all;  // ... and the step's all-tiles counter
   TileRef t;
 };
 
@@ -262,11 +263,35 @@ __device__ __forceinline__ TileRef make_tile_ref(const StepArgs& a, const Window
   return t;
 }
 
+// Per-task step arguments: the sweep-wide base with the task's step fields.
+__device__ __forceinline__ StepArgs step_args(const StepArgs& base, const StepInfo* steps, int s, int nsteps) {
+  StepArgs a = base;
+  if (s < nsteps) {
+    const StepInfo S = steps[s];
+    a.win_begin = S.win_begin;
+    a.win_count = S.win_count;
+    a.slot_offset = S.slot_offset;
+  }
+  a.step = s;
+  return a;
+}
+
+// The task list may span one step (a launch per step) or the whole sweep (one persistent launch):
+// every dependency is a completion counter, so the same code serves both.  Dependencies of a task
+// of step g (all on tasks earlier in the list; all CTAs resident, so no deadlock):
+//   any GEMM task of window W    the chase of W (run while step g-1 was executing)
+//   right (near and far), chase  every left tile of step g
+//   chase (of step g+1)          every near-right tile of step g, and every tile of step g+1-kQSets
+//                                (its Q slot set is reused)
+//   far right of W               the far-right tiles of every step-(g-1) window whose columns meet W
+//   Z of W                       the Z tiles of every step-(g-1) window whose columns meet W
+// (the left update of W and the near-right updates of step g-1 are ordered through W's chase).
 template <int KP>
 __global__ void __launch_bounds__(kStepThreads, 1)
-    step_kernel(StepArgs a, StepArgs an, const Task* __restrict__ tasks, int ntasks, int nL, int nRn,
-                int nLt, int nRnt, StepCounters* ctr, const __grid_constant__ CUtensorMap tmL,
-                const __grid_constant__ CUtensorMap tmR, const __grid_constant__ CUtensorMap tmZ) {
+    step_kernel(StepArgs base, const StepInfo* __restrict__ steps, int nsteps, const WinDeps* __restrict__ wdeps,
+                const Task* __restrict__ tasks, int ntasks, int* next_ctr, int* step_ctr, int* win_ctr,
+                const __grid_constant__ CUtensorMap tmL, const __grid_constant__ CUtensorMap tmR,
+                const __grid_constant__ CUtensorMap tmZ) {
   constexpr int NS = stages_of(KP);
   constexpr int QLD = pad_ld(KP);
   constexpr int SS = Geom<KP, true>::STAGE > Geom<KP, false>::STAGE ? Geom<KP, true>::STAGE
@@ -276,6 +301,7 @@ __global__ void __launch_bounds__(kStepThreads, 1)
   __shared__ StageDesc desc[NS];
   __shared__ WindowDesc cw;
   __shared__ int cwi;  // its plan index
+  __shared__ StepArgs cargs;  // the chased window's step
   __shared__ ChaseSmem R;
   double* Qs = sm;
   double* Ps = sm + KP * QLD;
@@ -290,13 +316,12 @@ __global__ void __launch_bounds__(kStepThreads, 1)
   if (tid < NS) desc[tid].pos = -1;
   fence_proxy_async();
   __syncthreads();
-  if (tid == 0) TIM_MIN(a.step, 0);
 
   if (warp == kProducerWarp) {
     // ================================ producer / scheduler ================================
     int j = 0;          // ring positions used (tiles + markers)
     int qe = -1;        // Q_W loads so far - 1
-    int q_win = -1;     // window whose Q_W is resident (-1: none)
+    int q_win = -1;     // plan window whose Q_W is resident (-1: none)
     // Producer-side waits are done by lane 0 alone, then __syncwarp: a lane that saw the phase
     // complete may publish the next position before its sibling lanes poll again, and the
     // consumers can complete one more phase in between -- a parity wait would then never return.
@@ -319,7 +344,7 @@ __global__ void __launch_bounds__(kStepThreads, 1)
     for (;;) {
       int t = 0;
       PROG(1000000 + j);
-      if (lane == 0) t = atomicAdd(&ctr->next, 1);
+      if (lane == 0) t = atomicAdd(next_ctr, 1);
       t = __shfl_sync(0xffffffffu, t, 0);
       if (t >= ntasks) {
         marker(kDescExit);
@@ -327,43 +352,63 @@ __global__ void __launch_bounds__(kStepThreads, 1)
         break;
       }
       const Task T = tasks[t];
+      const int g = T.step;
+      const StepInfo S = steps[g];
+      int* sc = step_ctr + 4 * g;
+      const bool chase = T.type == kTaskChase;
+      const int gw = chase ? -1 : S.win_begin + T.win;  // plan index of the task's window
+      const bool far_right = T.type == kTaskRight && T.idx >= S.nL + S.nRn;
       if (lane == 0) {
-        // dependencies on earlier tasks only (per-tile, per-warp completion counts)
-        if (T.type == kTaskRight || T.type == kTaskChase) PROG(2000000 + t);
-        if (T.type == kTaskRight || T.type == kTaskChase)
-          spin_until(&ctr->l_done, 4 * nLt, 1);
-        if (T.type == kTaskChase) PROG(3000000 + t);
-        if (T.type == kTaskChase) spin_until(&ctr->rn_done, 4 * nRnt, 2);
+        PROG(2000000 + t);
+        if (!chase && g > 0) spin_until(win_ctr + 4 * gw, 1, 0);
+        if (T.type == kTaskRight || chase) spin_until(sc + 0, 4 * S.nLt, 1);
+        if (chase) {
+          spin_until(sc + 1, 4 * S.nRnt, 2);
+          const int g_old = g + 1 - kQSets;
+          if (g_old >= 0) spin_until(step_ctr + 4 * g_old + 2, 4 * steps[g_old].ntiles, 3);
+        }
+        if ((far_right || T.type == kTaskZ) && g > 0) {
+          const WinDeps D = wdeps[gw];
+          const int k = T.type == kTaskZ ? 1 : 2;
+          for (int i = 0; i < 3; ++i)
+            if (D.pred[i] >= 0)
+              spin_until(win_ctr + 4 * D.pred[i] + k, 4 * (k == 1 ? wdeps[D.pred[i]].ztiles : wdeps[D.pred[i]].rftiles), 4);
+        }
         fence_proxy_async_all();  // other SMs' generic stores before this SM's TMA reads
       }
       __syncwarp();
-      if (T.type == kTaskChase) {
+      if (chase) {
         marker(kDescChase);
         PROG(7000000 + j);
         if (lane == 0) {
-          cw = an.wins[an.win_begin + T.win];
-          cwi = an.win_begin + T.win;
+          cargs = step_args(base, steps, g + 1, nsteps);
+          cw = cargs.wins[cargs.win_begin + T.win];
+          cwi = cargs.win_begin + T.win;
         }
         __syncthreads();
-        if (lane == 0) TIM_MIN(a.step, 1);
-        chase_window_9w(an, cw, cwi, sm, R);
+        if (lane == 0) TIM_MIN(g, 1);
+        chase_window_9w(cargs, cw, cwi, sm, R);
         __syncthreads();
-        if (lane == 0) TIM_MAX(a.step, 2);
+        if (lane == 0) {
+          TIM_MAX(g, 2);
+          red_release_add(win_ctr + 4 * cwi, 1);  // the CTA's stores are ordered by the barrier
+        }
         q_win = -1;
         continue;
       }
-      const WindowDesc w = a.wins[a.win_begin + T.win];
+      const StepArgs a = step_args(base, steps, g, nsteps);
+      const WindowDesc w = a.wins[gw];
       // A new window needs its Q_W.  Its first NS-1 panel tiles are issued first (their stages free
       // up as the previous tiles are released); once every earlier position has been released --
       // no tile reads the old Q_W any more -- Q_W is loaded, so the panel loads overlap the drain.
 #ifdef HQR_BENCH_NO_QSWITCH  // timing experiment only: keep the first Q_W (wrong results)
       const bool new_q = q_win < 0;
 #else
-      const bool new_q = T.win != q_win;
+      const bool new_q = gw != q_win;
 #endif
       if (new_q) {
         ++qe;
-        q_win = T.win;
+        q_win = gw;
       }
       const int p0 = j;
       auto load_q = [&]() {
@@ -380,7 +425,9 @@ __global__ void __launch_bounds__(kStepThreads, 1)
                  chunk, &qfull);
       };
       const bool left = T.type == kTaskLeft;
-      const int cnt = left ? 1 : (T.type == kTaskRight && t < nL + nRn) ? 2 : 0;
+      // the counter the task's completion feeds (tiles x 4 warps)
+      int* cnt = left ? sc + 0 : T.type == kTaskZ ? win_ctr + 4 * gw + 1
+                      : far_right ? win_ctr + 4 * gw + 2 : sc + 1;
       const int nq_pre = new_q ? min(T.ntiles, NS - 1) : 0;  // tiles issued before the Q_W load
       for (int i = 0; i < T.ntiles; ++i, ++j) {
         if (new_q && i == nq_pre) load_q();
@@ -388,9 +435,11 @@ __global__ void __launch_bounds__(kStepThreads, 1)
         if (lane == 0) {
           StageDesc& d = desc[j % NS];
           d.pos = j; d.kind = kDescTile; d.left = left; d.qe = qe;
-          // completion count: on each group's last tile of the task, that group's tile count
+          // completion counts: on each group's last tile of the task, that group's tile count
           // (the group of tile i takes the task's tiles i, i-G, ..., i.e. i/G + 1 of them)
-          d.ctr = (cnt && i + kGroups >= T.ntiles) ? cnt : 0;
+          const bool last = i + kGroups >= T.ntiles;
+          d.ctr = last ? cnt : nullptr;
+          d.ctr_all = last ? sc + 2 : nullptr;
           d.cnt_add = i / kGroups + 1;
           if (left) {
             d.t = make_tile_ref<KP, true>(a, w, T, i);
@@ -408,18 +457,21 @@ __global__ void __launch_bounds__(kStepThreads, 1)
     // ================================ consumers ================================
     const int q = warp >> 2, i4 = warp & 3;  // group, sub-partition
     int last_qe = -1;
-    // Completion counts (tiles x 4 warps) of the tasks other tasks wait on are published with a
-    // release add.  The release waits for the warp's outstanding stores, so it is deferred: it is
-    // issued after the next tile's K loop (the earlier stores have landed by then), or at once
-    // when the warp would otherwise wait with counts pending (never sit on them: others may wait).
-    int pend_l = 0, pend_rn = 0;
+    // Completion counts (tiles x 4 warps) are published with release adds.  The release waits for
+    // the warp's outstanding stores, so it is deferred: it is issued after the next tile's K loop
+    // (the earlier stores have landed by then), or at once when the warp would otherwise wait
+    // with counts pending (never sit on them: others may wait for them).
+    int* pend_p = nullptr;
+    int* pend_all = nullptr;
+    int pend_n = 0;
     auto flush = [&]() {
       __syncwarp();
       if (lane == 0) {
-        if (pend_l) red_release_add(&ctr->l_done, pend_l);
-        if (pend_rn) red_release_add(&ctr->rn_done, pend_rn);
+        red_release_add(pend_p, pend_n);
+        red_release_add(pend_all, pend_n);
       }
-      pend_l = pend_rn = 0;
+      pend_p = nullptr;
+      pend_n = 0;
     };
     for (int j = q;; j += kGroups) {
       const int s = j % NS;
@@ -427,13 +479,13 @@ __global__ void __launch_bounds__(kStepThreads, 1)
       // The stage's previous phase belongs to the other group and may still be in flight; a parity
       // wait cannot tell phase p from p - 2, so first wait until the producer has published this
       // position (which it does only after the previous phase was consumed), then on the barrier.
-      if ((pend_l | pend_rn) && *reinterpret_cast<volatile int*>(&desc[s].pos) != j) flush();
+      if (pend_p && *reinterpret_cast<volatile int*>(&desc[s].pos) != j) flush();
       while (*reinterpret_cast<volatile int*>(&desc[s].pos) != j) {
       }
       mbar_wait(&full[s], (unsigned)(j / NS) & 1, 3000000 + j);
       const int kind = desc[s].kind;
       if (kind != kDescTile) {
-        if (pend_l | pend_rn) flush();
+        if (pend_p) flush();
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);
         if (kind == kDescExit) {
@@ -442,33 +494,37 @@ __global__ void __launch_bounds__(kStepThreads, 1)
         }
         PROG(14000000 + j);
         __syncthreads();
-        chase_window_9w(an, cw, cwi, sm, R);
+        chase_window_9w(cargs, cw, cwi, sm, R);
         __syncthreads();
         continue;
       }
-      const int qe = desc[s].qe, cnt = desc[s].ctr, add = desc[s].cnt_add;
+      const int qe = desc[s].qe, add = desc[s].cnt_add;
+      int* const cp = desc[s].ctr;
+      int* const call = desc[s].ctr_all;
       const bool left = desc[s].left;
       const TileRef t = desc[s].t;
       if (qe != last_qe) {
-        if ((pend_l | pend_rn) && !mbar_test(&qfull, (unsigned)qe & 1)) flush();
+        if (pend_p && !mbar_test(&qfull, (unsigned)qe & 1)) flush();
         PROG(12000000 + qe);
         mbar_wait(&qfull, (unsigned)qe & 1, 4000000 + qe);
         last_qe = qe;
       }
       PROG(13000000 + j);
       auto mid = [&]() {
-        if (pend_l | pend_rn) flush();
+        if (pend_p) flush();
       };
       // Q_W quarters: with two groups the warps of an SM sub-partition take opposite quarters (their
       // band shares add up to about half); otherwise the quarter rotates with the ring position
       const int qq = kGroups == 2 ? (i4 + 2 * q) & 3 : (i4 + j) & 3;
       if (left) consume_tile<KP, true>(Qs, Ps + s * SS, &empty[s], t, qq, lane, mid);
       else consume_tile<KP, false>(Qs, Ps + s * SS, &empty[s], t, qq, lane, mid);
-      if (cnt == 1) pend_l += add;
-      else if (cnt == 2) pend_rn += add;
+      if (cp) {
+        pend_p = cp;
+        pend_all = call;
+        pend_n = add;
+      }
     }
   }
-  if (lane == 0) TIM_MAX(a.step, 3);
 }
 
 template <int KP>
@@ -481,9 +537,9 @@ size_t step_smem(int max_kw) {
 }
 
 template <int KP>
-cudaError_t launch_step_t(const StepArgs& a, const StepArgs& an, const Task* tasks, int ntasks, int nL,
-                          int nRn, int nLt, int nRnt, StepCounters* ctr, const TensorMaps& tm, int max_kw, int num_sms,
-                          cudaStream_t st) {
+cudaError_t launch_step_t(const StepArgs& base, const StepInfo* steps, int nsteps, const WinDeps* wdeps,
+                          const Task* tasks, int ntasks, int* next_ctr, int* step_ctr, int* win_ctr,
+                          const TensorMaps& tm, int max_kw, int num_sms, cudaStream_t st) {
   static size_t configured = 0;
   const size_t smem = step_smem<KP>(max_kw);
   if (smem > configured) {
@@ -492,8 +548,8 @@ cudaError_t launch_step_t(const StepArgs& a, const StepArgs& an, const Task* tas
     configured = smem;
   }
   const int grid = std::max(1, std::min(ntasks, num_sms));
-  step_kernel<KP><<<grid, kStepThreads, smem, st>>>(a, an, tasks, ntasks, nL, nRn, nLt, nRnt, ctr, tm.left_H,
-                                                     tm.right_H, tm.right_Z);
+  step_kernel<KP><<<grid, kStepThreads, smem, st>>>(base, steps, nsteps, wdeps, tasks, ntasks, next_ctr,
+                                                     step_ctr, win_ctr, tm.left_H, tm.right_H, tm.right_Z);
   return cudaGetLastError();
 }
 
@@ -585,15 +641,15 @@ void debug_progress_init() {
 void debug_progress_init() {}
 #endif
 
-cudaError_t launch_step(const StepArgs& a, const StepArgs& an, const Task* tasks, int ntasks, int nL,
-                        int nRn, int nLt, int nRnt, StepCounters* ctr, const TensorMaps& tm, int max_kw, int num_sms,
-                        cudaStream_t st) {
+cudaError_t launch_step(const StepArgs& base, const StepInfo* steps, int nsteps, const WinDeps* wdeps,
+                        const Task* tasks, int ntasks, int* next_ctr, int* step_ctr, int* win_ctr,
+                        const TensorMaps& tm, int max_kw, int num_sms, cudaStream_t st) {
   if (!tm.valid) return cudaErrorNotSupported;
-  switch (a.KP) {
-    case 32: return launch_step_t<32>(a, an, tasks, ntasks, nL, nRn, nLt, nRnt, ctr, tm, max_kw, num_sms, st);
-    case 64: return launch_step_t<64>(a, an, tasks, ntasks, nL, nRn, nLt, nRnt, ctr, tm, max_kw, num_sms, st);
-    case 96: return launch_step_t<96>(a, an, tasks, ntasks, nL, nRn, nLt, nRnt, ctr, tm, max_kw, num_sms, st);
-    case 128: return launch_step_t<128>(a, an, tasks, ntasks, nL, nRn, nLt, nRnt, ctr, tm, max_kw, num_sms, st);
+  switch (base.KP) {
+    case 32: return launch_step_t<32>(base, steps, nsteps, wdeps, tasks, ntasks, next_ctr, step_ctr, win_ctr, tm, max_kw, num_sms, st);
+    case 64: return launch_step_t<64>(base, steps, nsteps, wdeps, tasks, ntasks, next_ctr, step_ctr, win_ctr, tm, max_kw, num_sms, st);
+    case 96: return launch_step_t<96>(base, steps, nsteps, wdeps, tasks, ntasks, next_ctr, step_ctr, win_ctr, tm, max_kw, num_sms, st);
+    case 128: return launch_step_t<128>(base, steps, nsteps, wdeps, tasks, ntasks, next_ctr, step_ctr, win_ctr, tm, max_kw, num_sms, st);
   }
   return cudaErrorInvalidValue;
 }
@@ -608,7 +664,7 @@ void build_step_tasks(const StepArgs& a, const WindowDesc* wins, int nwin, const
   auto add = [&](int type, int win, int64_t tiles, int64_t r_lo, int64_t r_hi, int chunk) {
     for (int64_t t0 = 0; t0 < tiles; t0 += chunk) {
       Task T{};
-      T.type = type; T.win = win; T.tile0 = (int32_t)t0;
+      T.type = type; T.win = win; T.tile0 = (int32_t)t0; T.step = a.step;
       T.ntiles = (int32_t)std::min<int64_t>(chunk, tiles - t0);
       T.r_lo = r_lo; T.r_hi = r_hi;
       out->push_back(T);
@@ -629,7 +685,7 @@ void build_step_tasks(const StepArgs& a, const WindowDesc* wins, int nwin, const
   *nRn = (int)(out->size() - rn0);
   for (int i = 0; i < nnext; ++i) {
     Task T{};
-    T.type = kTaskChase; T.win = i; T.ntiles = 0;
+    T.type = kTaskChase; T.win = i; T.ntiles = 0; T.step = a.step;
     out->push_back(T);
   }
   const size_t bulk0 = out->size();
@@ -652,6 +708,7 @@ void build_step_tasks(const StepArgs& a, const WindowDesc* wins, int nwin, const
       U.ntiles = std::min(cs.tail_chunk, T.ntiles - t0);
       out->push_back(U);
     }
+  for (size_t i = base; i < out->size(); ++i) (*out)[i].idx = (int32_t)(i - base);
 }
 
 }  // namespace hqr

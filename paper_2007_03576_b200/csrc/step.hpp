@@ -14,15 +14,30 @@ struct Task {       // one claimable unit of work of a wavefront step
   int32_t type;     // kTaskLeft / kTaskRight / kTaskZ / kTaskChase
   int32_t win;      // window index within the step (kTaskChase: within the next step)
   int32_t tile0, ntiles;
+  int32_t step;     // wavefront step
+  int32_t idx;      // index within the step's queue (L: [0, nL), Rn: [nL, nL + nRn), ...)
   int64_t r_lo, r_hi;  // kTaskRight: H rows [r_lo, r_hi), tiles of right_rows(KP) from r_lo
 };
 
-struct StepCounters {  // per step, zeroed before the sweep
-  int next;     // next task to claim
-  int l_done;   // left tiles done x 4 (one release add per consumer warp)
-  int rn_done;  // near-right tiles done x 4
-  int pad;
+struct StepInfo {   // per wavefront step (device array)
+  int32_t win_begin, win_count, slot_offset;
+  int32_t nL, nRn;          // tasks of the left / near-right phases
+  int32_t nLt, nRnt;        // their tiles
+  int32_t ntiles;           // all GEMM tiles of the step
 };
+
+struct WinDeps {    // per plan window (device array)
+  int32_t pred[3];          // windows of the previous step whose columns meet this one (-1: none)
+  int32_t ztiles, rftiles;  // its Z / far-right tiles
+  int32_t pad;
+};
+
+// Completion counters (device, zeroed per sweep):
+//   step_ctr[4 g + 0]  left tiles of step g done x 4 (one release add per consumer warp)
+//   step_ctr[4 g + 1]  near-right tiles x 4
+//   step_ctr[4 g + 2]  all GEMM tiles x 4
+//   win_ctr[4 w + 0]   chase of plan window w done (1)
+//   win_ctr[4 w + 1]   Z tiles of w x 4;  win_ctr[4 w + 2]  far-right tiles of w x 4
 
 struct ChunkSizes {   // tiles per task, per phase
   int left = 16, near = 16, bulk = 32;
@@ -34,11 +49,12 @@ void build_step_tasks(const StepArgs& a, const WindowDesc* wins, int nwin, const
                       int nnext, int64_t sp, const ChunkSizes& cs, std::vector<Task>* out, int* nL,
                       int* nRn);
 
-// One persistent launch (one CTA per SM) running the step's task queue.  Needs the TMA path.
-// nL / nRn: tasks of the L / Rn phases; nLt / nRnt: their tiles (completion is counted per tile).
-cudaError_t launch_step(const StepArgs& a, const StepArgs& an, const Task* tasks, int ntasks, int nL,
-                        int nRn, int nLt, int nRnt, StepCounters* ctr, const TensorMaps& tm, int max_kw, int num_sms,
-                        cudaStream_t st);
+// One persistent launch (one CTA per SM) running `ntasks` tasks -- one step's queue, or the whole
+// sweep's -- claimed through *next_ctr.  base: the sweep's StepArgs (per-step fields come from
+// steps[]).  Needs the TMA path.
+cudaError_t launch_step(const StepArgs& base, const StepInfo* steps, int nsteps, const WinDeps* wdeps,
+                        const Task* tasks, int ntasks, int* next_ctr, int* step_ctr, int* win_ctr,
+                        const TensorMaps& tm, int max_kw, int num_sms, cudaStream_t st);
 
 // Debugging builds (-DHQR_PROGRESS): progress buffer in host-mapped memory, dumped after
 // HQR_PROGRESS_SECS seconds (then the process exits).  No-op otherwise.
