@@ -273,7 +273,9 @@ def main():
         if ps["ms_step"] > 0:   # fused step kernels: updates of step g + chase of step g+1
             upd_ms = ps["ms_step"]
             upd_launches = ps["launches_left"]
-            kern = "fused step kernel (left/right/Z DMMA GEMM tiles + next chase), one launch per step"
+            kern = ("fused step kernel (left/right/Z DMMA GEMM tiles + the chases), one persistent launch "
+                    "per sweep" if ps["launches_left"] == 1 else
+                    "fused step kernel (left/right/Z DMMA GEMM tiles + next chase), one launch per step")
         else:
             upd_ms = ps["ms_left"] + ps["ms_right"]
             upd_launches = ps["launches_left"] + ps["launches_right"]

@@ -539,7 +539,7 @@ int enqueue_fused(CachedPlan& cp, double* H, double* Z, int64_t n, const hqr::Te
   // (step 0's chases ran in their own launch: step-0 tasks do not wait for them)
   const StepArgs base = args(0);
   static const bool per_step = getenv("HQR_PER_STEP") != nullptr;  // A/B knob: a launch per step
-  if (!per_step && !io && !prof) {
+  if (!per_step && !io) {
     // one persistent launch for the whole sweep: step g+1's work starts as soon as its own
     // dependencies are met (no launch boundary, no end-of-step tail)
     mark(3);
