@@ -33,13 +33,18 @@ FP64_PEAK_FILE = os.path.join(ROOT, "profiles", "fp64_peaks_r01.json")
 METRIC = "seconds/sweep & fp64 GFLOP/s (frac of FP64 TC peak), n=10k/20k, 1/2/4/8 B200"
 
 
-def ncu_traffic():
-    """DRAM bytes per fused-step launch from the committed ncu --set full capture (profiles/)."""
+def ncu_traffic(persistent):
+    """DRAM bytes per fused-kernel launch from the committed ncu captures (profiles/): the
+    persistent launch (one per sweep) from the launch list, or one step's launch."""
     path = os.path.join(ROOT, "profiles", "ncu_step_summary.json")
     if not os.path.exists(path):
         return None
     with open(path) as f:
         d = json.load(f)
+    if persistent:
+        if "persistent_launch" not in d:
+            return None
+        d = d["persistent_launch"]
     return {"bytes_per_launch": d["dram_bytes_read"] + d["dram_bytes_write"], "source": d["source"]}
 
 
@@ -284,7 +289,7 @@ def main():
         # actually multiply (hqr_stats.flops_dmma, recorded per window by the chase); the dense
         # 2*m*n*k count of the same GEMMs is reported beside it
         achieved = ps["flops_dmma"] / (upd_ms * 1e-3) / 1e12
-        traffic = ncu_traffic()
+        traffic = ncu_traffic(ps["launches_left"] == 1)
         roofline = {"bound": "tensor", "kernel": kern,
                     "achieved": achieved, "peak": peak_sus, "unit": "TFLOP/s", "frac": achieved / peak_sus,
                     "traffic": traffic["bytes_per_launch"] if traffic else None,

@@ -47,5 +47,12 @@ out = {
     "dmma_pipe_active_pct": val("sm__pipe_tensor_subpipe_dmma_cycles_active.avg.pct_of_peak_sustained_active"),
 }
 out["traffic_over_alg"] = (out["dram_bytes_read"] + out["dram_bytes_write"]) / alg
-json.dump(out, open("profiles/ncu_step_summary.json", "w"), indent=1)
+path = "profiles/ncu_step_summary.json"
+try:  # keep the persistent launch's launch-list numbers
+    prev = json.load(open(path))
+    if "persistent_launch" in prev:
+        out["persistent_launch"] = prev["persistent_launch"]
+except (OSError, ValueError):
+    pass
+json.dump(out, open(path, "w"), indent=1)
 print(json.dumps(out, indent=1))
