@@ -40,8 +40,8 @@ struct WinDeps {    // per plan window (device array)
 //   win_ctr[4 w + 1]   Z tiles of w x 4;  win_ctr[4 w + 2]  far-right tiles of w x 4
 
 struct ChunkSizes {   // tiles per task, per phase
-  int left = 16, near = 16, bulk = 32;
-  int tail = 1500, tail_chunk = 8;  // the queue's last `tail` tiles in chunks of `tail_chunk`
+  int left = 24, near = 16, bulk = 48;  // tuned for the persistent sweep (configs[3])
+  int tail = 0, tail_chunk = 8;  // the queue's last `tail` tiles in chunks of `tail_chunk`
 };
 
 // Tasks of one step in queue order (L, Rn, C, Z, Rf).
