@@ -100,6 +100,8 @@ struct State {
   size_t coef_cap = 0;
   double* d_q = nullptr;
   size_t q_cap = 0;
+  int* d_upflags = nullptr;      // host-buffer sweeps: per upload chunk, 1 once on the device
+  size_t upflags_cap = 0;
   double* d_wstats = nullptr;    // per plan window: executed DMMA work units (record_band)
   size_t wstats_cap = 0;
   const void* wstats_plan = nullptr;  // plan (CachedPlan) the last single-GPU sweep recorded
@@ -389,6 +391,16 @@ int get_fused(CachedPlan& cp, bool has_z, int64_t n, FusedTasks** out) {
       }
     }
     f->begin.push_back((int32_t)f->tasks.size());
+    // host-buffer sweeps: the last upload chunk (H rows / Z columns) step g's tasks and the chase
+    // of step g+1 touch: max w1 over the windows of steps g and g+1 (cumulative)
+    {
+      int64_t reach = 0;
+      for (int g2 = 0; g2 < P.nsteps; ++g2) {
+        for (int s2 = g2; s2 <= std::min(g2 + 1, P.nsteps - 1); ++s2)
+          for (int i = P.step_begin[s2]; i < P.step_begin[s2 + 1]; ++i) reach = std::max<int64_t>(reach, P.windows[i].w1);
+        f->steps[g2].up_need = (int32_t)(reach / hqr::kUploadChunk);
+      }
+    }
     CK(cudaMalloc(&f->d_tasks, f->tasks.size() * sizeof(hqr::Task)));
     CK(cudaMemcpy(f->d_tasks, f->tasks.data(), f->tasks.size() * sizeof(hqr::Task), cudaMemcpyHostToDevice));
     CK(cudaMalloc(&f->d_steps, f->steps.size() * sizeof(hqr::StepInfo)));
@@ -412,86 +424,118 @@ cudaEvent_t io_event(size_t i) {
   return g.io_events[i];
 }
 
-// Host-buffer sweep (the e2e path): the copies overlap the fused steps instead of bracketing them.
-// H goes up first (step 0's left update reads rows of every column); Z goes up in column chunks
-// behind it, and step s waits only for the Z columns its windows touch (the lowest chain reaches
-// column c after about c/s steps).  Column c of H and Z is final once every later window starts
-// below it (w0 > c: no later left, right, Z update or chase touches it), so finished column chunks
-// go down during the sweep on a second copy stream (the link is full duplex).
+// Stream memory operations (driver API, fetched through the runtime): a copy stream tells the
+// persistent kernel which chunks have arrived, and waits for the kernel's step counters before
+// copying finished columns back.
+typedef CUresult (*StreamValueFn)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+int stream_value_fns(StreamValueFn* wr, StreamValueFn* wt) {
+  static StreamValueFn w = nullptr, t = nullptr;
+  if (!w || !t) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !p)
+      return 1000 + (int)cudaErrorNotSupported;
+    w = reinterpret_cast<StreamValueFn>(p);
+    if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !p)
+      return 1000 + (int)cudaErrorNotSupported;
+    t = reinterpret_cast<StreamValueFn>(p);
+  }
+  *wr = w;
+  *wt = t;
+  return 0;
+}
+#define CU(call) do { CUresult r_ = (call); if (r_ != CUDA_SUCCESS) return 1000 + (int)cudaErrorUnknown; } while (0)
+
+// Host-buffer sweep (the e2e path): the copies overlap the persistent sweep kernel instead of
+// bracketing it.  Windows move down the diagonal, so step s touches H only in rows [0, max w1 + 1)
+// of its windows (left updates: window rows, all columns right; right updates: rows above; chase:
+// the window) and Z only in columns [0, max w1 + 1).  Chunk k (H rows and Z columns
+// [512 k, 512 k + 512)) goes up on one copy stream, then a flag is written (cuStreamWriteValue32);
+// the kernel's producer waits for the flag of the last chunk a task's step needs
+// (StepInfo::up_need).  Column c of H and Z is final once every step that touches it is done (every
+// later window starts below c), so a second copy stream waits for the steps' completion counters
+// (cuStreamWaitValue32) and copies finished column chunks down during the sweep; of H only the
+// rows [0, c + 2) of column c come back (below them the matrix is Hessenberg: zero in and out).
 struct IoPlan {
   double* Hh = nullptr;  // caller's host H (nullptr: H is device-resident)
   double* Zh = nullptr;  // caller's host Z (nullptr: device-resident or absent)
   double* dH = nullptr;
   double* dZ = nullptr;
   int64_t n = 0;
-  std::vector<int64_t> need_z;  // step s needs Z columns [0, need_z[s])
-  std::vector<int64_t> fin;     // after launch s, columns [0, fin[s]) are final
-  int64_t chunk = 512;
-  int64_t z_waited = 0, out_done = 0;
-  size_t ev = 0;
+  int* d_flags = nullptr;   // per chunk: 1 once it is on the device
+  std::vector<int64_t> fin;  // after step s (and every earlier step), columns [0, fin[s]) are final
+  int64_t chunk = hqr::kUploadChunk;
   int64_t h2d = 0, d2h = 0;
+  StreamValueFn write_value = nullptr, wait_value = nullptr;
 
+  int64_t nchunks() const { return (n + chunk - 1) / chunk; }
   void plan(const Plan& P) {
-    need_z.assign(P.nsteps, 0);
     fin.assign(P.nsteps, n);
     int64_t run = n;
     for (int s = P.nsteps - 1; s >= 0; --s) {
       fin[s] = run;  // min w0 over the windows of later steps
-      for (int i = P.step_begin[s]; i < P.step_begin[s + 1]; ++i) {
-        run = std::min<int64_t>(run, P.windows[i].w0);
-        need_z[s] = std::max<int64_t>(need_z[s], P.windows[i].w1 + 1);
-      }
+      for (int i = P.step_begin[s]; i < P.step_begin[s + 1]; ++i) run = std::min<int64_t>(run, P.windows[i].w0);
     }
   }
-  int start(cudaStream_t A) {  // before chase(0)
+  int upload(cudaStream_t A, int64_t first_rows) {  // before chase(0); A waits for its rows
+    int rc = stream_value_fns(&write_value, &wait_value);
+    if (rc) return rc;
     const size_t col = (size_t)n * sizeof(double);
     CK(cudaStreamWaitEvent(g.cin, g.ev0, 0));
-    if (Hh) {
-      CK(cudaMemcpyAsync(dH, Hh, col * n, cudaMemcpyHostToDevice, g.cin));
-      h2d += (int64_t)(col * n);
-    }
-    cudaEvent_t e = io_event(ev++);
-    CK(cudaEventRecord(e, g.cin));
-    CK(cudaStreamWaitEvent(A, e, 0));
-    if (Zh) {
-      for (int64_t c = 0; c < n; c += chunk) {
-        const int64_t w = std::min(chunk, n - c);
-        CK(cudaMemcpyAsync(dZ + c * n, Zh + c * n, col * w, cudaMemcpyHostToDevice, g.cin));
-        CK(cudaEventRecord(io_event(ev + c / chunk), g.cin));
+    CK(cudaMemsetAsync(d_flags, 0, (size_t)nchunks() * sizeof(int), g.cin));
+    for (int64_t k = 0; k < nchunks(); ++k) {
+      const int64_t c = k * chunk, w = std::min(chunk, n - c);
+      if (Hh)  // rows [c, c + w) of every column
+        CK(cudaMemcpy2DAsync(dH + c, col, Hh + c, col, (size_t)w * sizeof(double), (size_t)n,
+                             cudaMemcpyHostToDevice, g.cin));
+      if (Zh) CK(cudaMemcpyAsync(dZ + c * n, Zh + c * n, col * w, cudaMemcpyHostToDevice, g.cin));
+      CU(write_value((CUstream)g.cin, (CUdeviceptr)(d_flags + k), 1, 0));
+      if (c <= first_rows && first_rows < c + w) {  // chase(0) is a separate launch: an event
+        cudaEvent_t e = io_event(0);
+        CK(cudaEventRecord(e, g.cin));
+        CK(cudaStreamWaitEvent(A, e, 0));
       }
-      h2d += (int64_t)(col * n);
     }
+    h2d = (int64_t)(col * n) * ((Hh ? 1 : 0) + (Zh ? 1 : 0));
     return 0;
   }
-  int before(int s, cudaStream_t A) {  // before launch s
-    if (!Zh) return 0;
-    while (z_waited < need_z[s]) {
-      CK(cudaStreamWaitEvent(A, io_event(ev + z_waited / chunk), 0));
-      z_waited = std::min(n, (z_waited / chunk + 1) * chunk);
-    }
-    return 0;
-  }
-  int after(int s, cudaStream_t A, bool last) {  // after launch s
-    const int64_t f = last ? n : fin[s];
-    if (f <= out_done || (!last && f - out_done < chunk)) return 0;
+  int down(int64_t c0, int64_t c1) {  // finished columns [c0, c1) to the host (on cout)
     const size_t col = (size_t)n * sizeof(double);
-    const size_t zev = ev + (size_t)((n + chunk - 1) / chunk);
-    cudaEvent_t e = io_event(zev + (size_t)s);
-    CK(cudaEventRecord(e, A));
-    CK(cudaStreamWaitEvent(g.cout, e, 0));
-    // columns no step touches (before ilo, after ihi) may be final before their Z chunk is up
-    if (Zh)
-      for (int64_t k = out_done / chunk; k * chunk < f; ++k) CK(cudaStreamWaitEvent(g.cout, io_event(ev + (size_t)k), 0));
-    const int64_t w = f - out_done;
-    if (Hh) CK(cudaMemcpyAsync(Hh + out_done * n, dH + out_done * n, col * w, cudaMemcpyDeviceToHost, g.cout));
-    if (Zh) CK(cudaMemcpyAsync(Zh + out_done * n, dZ + out_done * n, col * w, cudaMemcpyDeviceToHost, g.cout));
-    d2h += (int64_t)(col * w) * ((Hh ? 1 : 0) + (Zh ? 1 : 0));
-    out_done = f;
-    if (last) {
-      cudaEvent_t done = io_event(zev + fin.size());
-      CK(cudaEventRecord(done, g.cout));
-      CK(cudaStreamWaitEvent(A, done, 0));
+    const int64_t rows = std::min(n, c1 + 1);  // H rows the sweep may have changed
+    const int64_t kmax = std::max((rows - 1) / chunk, (c1 - 1) / chunk);
+    CU(wait_value((CUstream)g.cout, (CUdeviceptr)(d_flags + kmax), 1, CU_STREAM_WAIT_VALUE_GEQ));
+    if (Hh)
+      CK(cudaMemcpy2DAsync(Hh + c0 * n, col, dH + c0 * n, col, (size_t)rows * sizeof(double), (size_t)(c1 - c0),
+                           cudaMemcpyDeviceToHost, g.cout));
+    if (Zh) CK(cudaMemcpyAsync(Zh + c0 * n, dZ + c0 * n, col * (c1 - c0), cudaMemcpyDeviceToHost, g.cout));
+    d2h += (int64_t)(c1 - c0) * (Hh ? rows : 0) * 8 + (Zh ? (int64_t)(col * (c1 - c0)) : 0);
+    return 0;
+  }
+  // all downloads, enqueued before the kernel finishes: chunk by chunk behind the step counters,
+  // the rest after the kernel (event `kernel_done` recorded on A)
+  int download(cudaStream_t A, const int* step_ctr, const std::vector<hqr::StepInfo>& steps,
+               cudaEvent_t kernel_done) {
+    int64_t done = 0;
+    for (size_t s = 0; s < fin.size(); ++s) {
+      if (steps[s].ntiles > 0)
+        CU(wait_value((CUstream)g.cout, (CUdeviceptr)(step_ctr + 4 * s + 2), (cuuint32_t)(4 * steps[s].ntiles),
+                      CU_STREAM_WAIT_VALUE_GEQ));
+      if (fin[s] - done >= chunk) {
+        int rc = down(done, fin[s]);
+        if (rc) return rc;
+        done = fin[s];
+      }
     }
+    CK(cudaStreamWaitEvent(g.cout, kernel_done, 0));
+    if (done < n) {
+      int rc = down(done, n);
+      if (rc) return rc;
+    }
+    cudaEvent_t e = io_event(1);
+    CK(cudaEventRecord(e, g.cout));
+    CK(cudaStreamWaitEvent(A, e, 0));
     return 0;
   }
 };
@@ -527,8 +571,9 @@ int enqueue_fused(CachedPlan& cp, double* H, double* Z, int64_t n, const hqr::Te
   };
   if (io) {
     io->plan(P);
-    rc = io->start(A);
-    if (rc) return rc;
+    int64_t first_rows = 0;
+    for (int i = P.step_begin[0]; i < P.step_begin[1]; ++i) first_rows = std::max<int64_t>(first_rows, P.windows[i].w1);
+    if ((rc = io->upload(A, first_rows))) return rc;
   }
   mark(0);
   CK(hqr::launch_chase(args(0), P.max_kw, P.max_nbc, A));
@@ -539,24 +584,27 @@ int enqueue_fused(CachedPlan& cp, double* H, double* Z, int64_t n, const hqr::Te
   // (step 0's chases ran in their own launch: step-0 tasks do not wait for them)
   const StepArgs base = args(0);
   static const bool per_step = getenv("HQR_PER_STEP") != nullptr;  // A/B knob: a launch per step
-  if (!per_step && !io) {
+  if (!per_step || io) {
     // one persistent launch for the whole sweep: step g+1's work starts as soon as its own
     // dependencies are met (no launch boundary, no end-of-step tail)
     mark(3);
     CK(hqr::launch_step(base, f->d_steps, P.nsteps, f->d_wdeps, f->d_tasks, (int)f->tasks.size(), f->d_ctr,
-                        step_ctr, win_ctr, tm, P.max_kw, g.num_sms, A));
+                        step_ctr, win_ctr, io ? io->d_flags : nullptr, tm, P.max_kw, g.num_sms, A));
     mark(-1);
     st->launches_left++;
+    if (io) {
+      cudaEvent_t kd = io_event(2);
+      CK(cudaEventRecord(kd, A));
+      if ((rc = io->download(A, step_ctr, f->steps, kd))) return rc;
+    }
   } else {
     for (int s = 0; s < P.nsteps; ++s) {
       const int nt = f->begin[s + 1] - f->begin[s];
-      if (io && (rc = io->before(s, A))) return rc;
       mark(3);
       CK(hqr::launch_step(base, f->d_steps, P.nsteps, f->d_wdeps, f->d_tasks + f->begin[s], nt,
-                          step_ctr + 4 * s + 3, step_ctr, win_ctr, tm, P.max_kw, g.num_sms, A));
+                          step_ctr + 4 * s + 3, step_ctr, win_ctr, nullptr, tm, P.max_kw, g.num_sms, A));
       mark(-1);
       st->launches_left++;  // one fused launch per step (counted once)
-      if (io && (rc = io->after(s, A, s + 1 == P.nsteps))) return rc;
     }
   }
   if (io) {
@@ -639,6 +687,9 @@ int hqr_teardown(void) {
   g.prof_events.clear();
   if (g.d_coef) cudaFree(g.d_coef);
   if (g.d_wstats) cudaFree(g.d_wstats);
+  if (g.d_upflags) cudaFree(g.d_upflags);
+  g.d_upflags = nullptr;
+  g.upflags_cap = 0;
   g.d_wstats = nullptr;
   g.wstats_cap = 0;
   g.wstats_plan = nullptr;
@@ -787,6 +838,15 @@ int sweep_impl(double* H, double* Z, int64_t n, const Blocks& blocks, const doub
     io.dH = dH;
     io.dZ = dZ;
     io.n = n;
+    const size_t nch = (size_t)((n + hqr::kUploadChunk - 1) / hqr::kUploadChunk);
+    if (g.upflags_cap < nch) {
+      if (g.d_upflags) CK(cudaFree(g.d_upflags));
+      g.d_upflags = nullptr;
+      g.upflags_cap = 0;
+      CK(cudaMalloc(&g.d_upflags, nch * sizeof(int)));
+      g.upflags_cap = nch;
+    }
+    io.d_flags = g.d_upflags;
     rc = enqueue_fused(*cp, dH, dZ, n, tmf, &st, false, nullptr, &io);
     if (rc) return rc;
   } else if (use_graph) {

@@ -290,7 +290,7 @@ template <int KP>
 __global__ void __launch_bounds__(kStepThreads, 1)
     step_kernel(StepArgs base, const StepInfo* __restrict__ steps, int nsteps, const WinDeps* __restrict__ wdeps,
                 const Task* __restrict__ tasks, int ntasks, int* next_ctr, int* step_ctr, int* win_ctr,
-                const __grid_constant__ CUtensorMap tmL, const __grid_constant__ CUtensorMap tmR,
+                const int* __restrict__ up_flags, const __grid_constant__ CUtensorMap tmL, const __grid_constant__ CUtensorMap tmR,
                 const __grid_constant__ CUtensorMap tmZ) {
   constexpr int NS = stages_of(KP);
   constexpr int QLD = pad_ld(KP);
@@ -360,6 +360,7 @@ __global__ void __launch_bounds__(kStepThreads, 1)
       const bool far_right = T.type == kTaskRight && T.idx >= S.nL + S.nRn;
       if (lane == 0) {
         PROG(2000000 + t);
+        if (up_flags) spin_until(up_flags + S.up_need, 1, 5);  // host-buffer sweep: rows / columns up
         if (!chase && g > 0) spin_until(win_ctr + 4 * gw, 1, 0);
         if (T.type == kTaskRight || chase) spin_until(sc + 0, 4 * S.nLt, 1);
         if (chase) {
@@ -539,7 +540,7 @@ size_t step_smem(int max_kw) {
 template <int KP>
 cudaError_t launch_step_t(const StepArgs& base, const StepInfo* steps, int nsteps, const WinDeps* wdeps,
                           const Task* tasks, int ntasks, int* next_ctr, int* step_ctr, int* win_ctr,
-                          const TensorMaps& tm, int max_kw, int num_sms, cudaStream_t st) {
+                          const int* up_flags, const TensorMaps& tm, int max_kw, int num_sms, cudaStream_t st) {
   static size_t configured = 0;
   const size_t smem = step_smem<KP>(max_kw);
   if (smem > configured) {
@@ -549,7 +550,7 @@ cudaError_t launch_step_t(const StepArgs& base, const StepInfo* steps, int nstep
   }
   const int grid = std::max(1, std::min(ntasks, num_sms));
   step_kernel<KP><<<grid, kStepThreads, smem, st>>>(base, steps, nsteps, wdeps, tasks, ntasks, next_ctr,
-                                                     step_ctr, win_ctr, tm.left_H, tm.right_H, tm.right_Z);
+                                                     step_ctr, win_ctr, up_flags, tm.left_H, tm.right_H, tm.right_Z);
   return cudaGetLastError();
 }
 
@@ -643,13 +644,13 @@ void debug_progress_init() {}
 
 cudaError_t launch_step(const StepArgs& base, const StepInfo* steps, int nsteps, const WinDeps* wdeps,
                         const Task* tasks, int ntasks, int* next_ctr, int* step_ctr, int* win_ctr,
-                        const TensorMaps& tm, int max_kw, int num_sms, cudaStream_t st) {
+                        const int* up_flags, const TensorMaps& tm, int max_kw, int num_sms, cudaStream_t st) {
   if (!tm.valid) return cudaErrorNotSupported;
   switch (base.KP) {
-    case 32: return launch_step_t<32>(base, steps, nsteps, wdeps, tasks, ntasks, next_ctr, step_ctr, win_ctr, tm, max_kw, num_sms, st);
-    case 64: return launch_step_t<64>(base, steps, nsteps, wdeps, tasks, ntasks, next_ctr, step_ctr, win_ctr, tm, max_kw, num_sms, st);
-    case 96: return launch_step_t<96>(base, steps, nsteps, wdeps, tasks, ntasks, next_ctr, step_ctr, win_ctr, tm, max_kw, num_sms, st);
-    case 128: return launch_step_t<128>(base, steps, nsteps, wdeps, tasks, ntasks, next_ctr, step_ctr, win_ctr, tm, max_kw, num_sms, st);
+    case 32: return launch_step_t<32>(base, steps, nsteps, wdeps, tasks, ntasks, next_ctr, step_ctr, win_ctr, up_flags, tm, max_kw, num_sms, st);
+    case 64: return launch_step_t<64>(base, steps, nsteps, wdeps, tasks, ntasks, next_ctr, step_ctr, win_ctr, up_flags, tm, max_kw, num_sms, st);
+    case 96: return launch_step_t<96>(base, steps, nsteps, wdeps, tasks, ntasks, next_ctr, step_ctr, win_ctr, up_flags, tm, max_kw, num_sms, st);
+    case 128: return launch_step_t<128>(base, steps, nsteps, wdeps, tasks, ntasks, next_ctr, step_ctr, win_ctr, up_flags, tm, max_kw, num_sms, st);
   }
   return cudaErrorInvalidValue;
 }

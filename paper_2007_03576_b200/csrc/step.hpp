@@ -24,7 +24,11 @@ struct StepInfo {   // per wavefront step (device array)
   int32_t nL, nRn;          // tasks of the left / near-right phases
   int32_t nLt, nRnt;        // their tiles
   int32_t ntiles;           // all GEMM tiles of the step
+  int32_t up_need;          // host-buffer sweeps: the last upload chunk its tasks (and the chase of
+                            // step g+1) need (chunks of kUploadChunk H rows / Z columns)
 };
+
+constexpr int kUploadChunk = 512;
 
 struct WinDeps {    // per plan window (device array)
   int32_t pred[3];          // windows of the previous step whose columns meet this one (-1: none)
@@ -52,9 +56,10 @@ void build_step_tasks(const StepArgs& a, const WindowDesc* wins, int nwin, const
 // One persistent launch (one CTA per SM) running `ntasks` tasks -- one step's queue, or the whole
 // sweep's -- claimed through *next_ctr.  base: the sweep's StepArgs (per-step fields come from
 // steps[]).  Needs the TMA path.
+// up_flags (nullable): per upload chunk, nonzero once on the device (host-buffer sweeps).
 cudaError_t launch_step(const StepArgs& base, const StepInfo* steps, int nsteps, const WinDeps* wdeps,
                         const Task* tasks, int ntasks, int* next_ctr, int* step_ctr, int* win_ctr,
-                        const TensorMaps& tm, int max_kw, int num_sms, cudaStream_t st);
+                        const int* up_flags, const TensorMaps& tm, int max_kw, int num_sms, cudaStream_t st);
 
 // Debugging builds (-DHQR_PROGRESS): progress buffer in host-mapped memory, dumped after
 // HQR_PROGRESS_SECS seconds (then the process exits).  No-op otherwise.

@@ -117,7 +117,14 @@ def test_host_buffers_overlapped_copies(mode):
     st = hq.stats()
     nb = n * n * 8
     assert st["h2d_bytes"] == nb * (2 if mode == "both_host" else 1)
-    assert st["d2h_bytes"] == nb * (2 if mode == "both_host" else 1)
+    # Z comes back whole; of H only the rows the sweep can change (rows <= c + 1 of column c: the
+    # rest of a Hessenberg matrix is zero in and out), about half
+    z_back = nb if mode != "h_host" else 0
+    h_back = st["d2h_bytes"] - z_back
+    if mode == "z_host":
+        assert h_back == 0
+    else:
+        assert 0.45 * nb < h_back <= nb
 
 
 def _band_units(Q, KP=96):
