@@ -199,8 +199,14 @@ def main():
             H.t().copy_(H0.t())
             Z.t().copy_(Z0.t())
 
-        def one():
-            hq.sweep(H, Z, prob.ilo, prob.ihi, prob.shifts_re, prob.shifts_im, args.window)
+        if len(prob.blocks) > 1:  # configs[4]: decoupled blocks swept together (hqr_sweep_multi)
+            blocks = [(b[0], b[1], b[3]) for b in prob.blocks]
+
+            def one():
+                hq.sweep_multi(H, Z, blocks, prob.shifts_re, prob.shifts_im, args.window)
+        else:
+            def one():
+                hq.sweep(H, Z, prob.ilo, prob.ihi, prob.shifts_re, prob.shifts_im, args.window)
     else:
         # sharded sweep: this rank's H column shard (+ halo) and Z row shard
         import torch.distributed as dist
@@ -258,7 +264,7 @@ def main():
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms = float(t.item())
     st = hq.stats()
-    fa = f_alg(n, prob.ilo, prob.ihi, nshifts // 2, True)
+    fa = sum(f_alg(n, b[0], b[1], b[3] // 2, True) for b in prob.blocks)
     value = fa / (ms * 1e-3) / 1e9   # one sweep (strong scaling: the same sweep on every N)
     peak_sus, peak_burst = fp64_peak()
     gflops_exec = (st["flops_update"] + st["flops_chase"]) / (ms * 1e-3) / 1e9
