@@ -124,6 +124,24 @@ __device__ __forceinline__ void named_sync(int id, int threads) {
 // Householder reflector (reading R2): P = I - tau v v^T, v = [1, v1, v2],
 // P x = beta e1 with beta = -sign(x0) ||x||, sign(0) = +1; zero tail -> identity.
 // With d = x0 - beta and r = 1 / (d * beta): v_i = x_i / d = x_i * beta * r, tau = -d / beta = -d*d*r.
+// The chase's critical path is a chain of these (one per bulge and step), so the square root and
+// the reciprocal use the hardware approximations refined by Newton steps (rounding-level
+// differences from IEEE sqrt / division, reading R10) instead of the long IEEE sequences.
+__device__ __forceinline__ double rsqrt_nr(double s) {  // 1 / sqrt(s), s > 0 normal
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(s));
+  const double hs = 0.5 * s;
+  y = y * fma(-hs * y, y, 1.5);  // Newton: ~2x the correct bits per step
+  y = y * fma(-hs * y, y, 1.5);
+  return y;
+}
+__device__ __forceinline__ double rcp_nr(double q) {  // 1 / q, q != 0 normal
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(q));
+  r = r * fma(-q, r, 2.0);
+  r = r * fma(-q, r, 2.0);
+  return fma(r, fma(-q, r, 1.0), r);  // final correction
+}
 __device__ __forceinline__ void house(double x0, double x1, double x2, double& v1, double& v2,
                                       double& tau, double& beta) {
   const double tail2 = fma(x1, x1, x2 * x2);
@@ -131,10 +149,13 @@ __device__ __forceinline__ void house(double x0, double x1, double x2, double& v
     v1 = 0.0; v2 = 0.0; tau = 0.0; beta = x0;
     return;
   }
-  const double nrm = sqrt(fma(x0, x0, tail2));
+  const double s = fma(x0, x0, tail2);
+  const double y = rsqrt_nr(s);
+  double nrm = s * y;
+  nrm = fma(0.5 * y, fma(-nrm, nrm, s), nrm);  // sqrt(s), Newton-corrected
   const double b = (x0 >= 0.0) ? -nrm : nrm;
   const double d = x0 - b;
-  const double r = 1.0 / (d * b);
+  const double r = rcp_nr(d * b);
   const double br = b * r;
   v1 = x1 * br;
   v2 = x2 * br;
