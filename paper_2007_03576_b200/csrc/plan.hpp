@@ -28,6 +28,8 @@
 
 namespace hqr {
 
+constexpr int kChainCap = 13;  // bulges per chain (= the fused step kernel's warps)
+
 struct WindowDesc {     // one diagonal window = one CTA of the chase kernel in one wavefront step
   int32_t chain;        // chain index (global over blocks; 0 = lowest chain of the first block)
   int32_t w0, w1;       // global row/col range [w0, w1] (inclusive)
@@ -80,7 +82,10 @@ inline int plan_block(int64_t ilo, int64_t ihi, int nb, int b_base, int c_base, 
     *nbc_out = nb; *s_out = (int)N; *lag_out = 1;
     return 0;
   }
-  const int nbc_cap = (int)((k - 2) / 6);
+  // at most (k-2)/6 bulges fit a window; at most kChainCap so that the fused kernel's
+  // chase runs every bulge of a step on its own warp (step.cu).  Fewer bulges per chain cost no
+  // flops: the window advances further (s = k - 3*nbc - 1), so the chains have fewer windows.
+  const int nbc_cap = std::min((int)((k - 2) / 6), kChainCap);
   const int C = (nb + nbc_cap - 1) / nbc_cap;
   const int base = nb / C, rem = nb % C;                 // remainders on the earliest chains
   const int nbc_max = base + (rem > 0 ? 1 : 0);

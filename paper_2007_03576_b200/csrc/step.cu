@@ -32,6 +32,7 @@
 #include "device_common.cuh"
 #include "gemm_tile.cuh"
 #include "kernels.hpp"
+#include "plan.hpp"
 #include "step.hpp"
 
 namespace hqr {
@@ -43,6 +44,7 @@ constexpr int kGroups = 3;  // consumer groups of 4 warps (one warp per SM sub-p
 constexpr int kProducerWarp = 4 * kGroups;
 constexpr int kStepThreads = 32 * (4 * kGroups + 1);  // consumers + 1 producer warp; all chase
 constexpr int kStepWarps = kStepThreads / 32;
+static_assert(kStepWarps >= kChainCap, "one chase warp per bulge of a chain (plan.hpp kChainCap)");
 
 __device__ __forceinline__ void fence_proxy_async_all() { asm volatile("fence.proxy.async;\n" ::: "memory"); }
 
