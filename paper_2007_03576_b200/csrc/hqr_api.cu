@@ -329,6 +329,12 @@ hqr::ChunkSizes chunk_sizes() {
       cs.left = v[0]; cs.near = v[1]; cs.bulk = v[2]; cs.tail = v[3]; cs.tail_chunk = v[4];
     }
   }
+  if (const char* e = getenv("HQR_PHASE_TAIL")) {  // tuning knob: "ltail,ntail,chunk"
+    int v[3];
+    if (sscanf(e, "%d,%d,%d", &v[0], &v[1], &v[2]) == 3 && v[0] >= 0 && v[1] >= 0 && v[2] > 0) {
+      cs.ltail = v[0]; cs.ntail = v[1]; cs.phase_chunk = v[2];
+    }
+  }
   return cs;
 }
 

@@ -70,7 +70,8 @@ __device__ __forceinline__ unsigned long long gtime() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
-__device__ unsigned long long g_ctim[8];  // chase: summed cycles per phase (all warps), windows
+__device__ unsigned long long g_ctim[8];
+__device__ unsigned long long g_wait[12];  // [0..7] producer dependency spins per tag; [8] chase, [9] CTA, [10] consumer waits, [11] consumer K+epilogue  // chase: summed cycles per phase (all warps), windows
 #define TIM_MIN(s, k) atomicMin(&g_tim[(s) & 4095][k], gtime())
 #define TIM_MAX(s, k) atomicMax(&g_tim[(s) & 4095][k], gtime())
 #else
@@ -84,7 +85,14 @@ __device__ __forceinline__ void spin_until(const int* p, int target, int tag) {
   long long it = 0;
 #endif
   int v;
+#ifdef HQR_TIMING
+  const long long w0 = clock64();
+  bool waited = false;
+#endif
   while ((v = ld_acquire(p)) < target) {
+#ifdef HQR_TIMING
+    waited = true;
+#endif
     __nanosleep(64);
 #ifdef HQR_WATCHDOG
     if (++it == (1ll << (HQR_WD_LIMIT - 2))) {
@@ -95,6 +103,9 @@ __device__ __forceinline__ void spin_until(const int* p, int target, int tag) {
     }
 #endif
   }
+#ifdef HQR_TIMING
+  if (waited) atomicAdd(&g_wait[tag & 7], (unsigned long long)(clock64() - w0));
+#endif
 }
 
 // ---- chase of one window with all of the CTA's warps (same arithmetic as chase.cu) ------------------
@@ -299,6 +310,9 @@ __global__ void __launch_bounds__(kStepThreads, 1)
   constexpr int SS = Geom<KP, true>::STAGE > Geom<KP, false>::STAGE ? Geom<KP, true>::STAGE
                                                                     : Geom<KP, false>::STAGE;
   extern __shared__ __align__(1024) double sm[];
+#ifdef HQR_TIMING
+  const long long k_start = clock64();
+#endif
   __shared__ __align__(8) uint64_t full[NS], empty[NS], qfull;
   __shared__ StageDesc desc[NS];
   __shared__ WindowDesc cw;
@@ -390,8 +404,14 @@ __global__ void __launch_bounds__(kStepThreads, 1)
         }
         __syncthreads();
         if (lane == 0) TIM_MIN(g, 1);
+#ifdef HQR_TIMING
+        const long long c_start = clock64();
+#endif
         chase_window_9w(cargs, cw, cwi, sm, R);
         __syncthreads();
+#ifdef HQR_TIMING
+        if (lane == 0) atomicAdd(&g_wait[8], (unsigned long long)(clock64() - c_start));
+#endif
         if (lane == 0) {
           TIM_MAX(g, 2);
           red_release_add(win_ctr + 4 * cwi, 1);  // the CTA's stores are ordered by the barrier
@@ -483,9 +503,15 @@ __global__ void __launch_bounds__(kStepThreads, 1)
       // wait cannot tell phase p from p - 2, so first wait until the producer has published this
       // position (which it does only after the previous phase was consumed), then on the barrier.
       if (pend_p && *reinterpret_cast<volatile int*>(&desc[s].pos) != j) flush();
+#ifdef HQR_TIMING
+      const long long cw0 = clock64();
+#endif
       while (*reinterpret_cast<volatile int*>(&desc[s].pos) != j) {
       }
       mbar_wait(&full[s], (unsigned)(j / NS) & 1, 3000000 + j);
+#ifdef HQR_TIMING
+      if (lane == 0) atomicAdd(&g_wait[10], (unsigned long long)(clock64() - cw0));
+#endif
       const int kind = desc[s].kind;
       if (kind != kDescTile) {
         if (pend_p) flush();
@@ -519,8 +545,14 @@ __global__ void __launch_bounds__(kStepThreads, 1)
       // Q_W quarters: with two groups the warps of an SM sub-partition take opposite quarters (their
       // band shares add up to about half); otherwise the quarter rotates with the ring position
       const int qq = kGroups == 2 ? (i4 + 2 * q) & 3 : (i4 + j) & 3;
+#ifdef HQR_TIMING
+      const long long ck0 = clock64();
+#endif
       if (left) consume_tile<KP, true>(Qs, Ps + s * SS, &empty[s], t, qq, lane, mid);
       else consume_tile<KP, false>(Qs, Ps + s * SS, &empty[s], t, qq, lane, mid);
+#ifdef HQR_TIMING
+      if (lane == 0) atomicAdd(&g_wait[11], (unsigned long long)(clock64() - ck0));
+#endif
       if (cp) {
         pend_p = cp;
         pend_all = call;
@@ -528,6 +560,9 @@ __global__ void __launch_bounds__(kStepThreads, 1)
       }
     }
   }
+#ifdef HQR_TIMING
+  if (threadIdx.x == 0) atomicAdd(&g_wait[9], (unsigned long long)(clock64() - k_start));
+#endif
 }
 
 template <int KP>
@@ -564,8 +599,9 @@ void debug_timing(int nsteps, bool reset) {
   if (reset) {
     for (int i = 0; i < 4096; ++i) { h[i][0] = h[i][1] = ~0ull; h[i][2] = h[i][3] = 0; }
     cudaMemcpyToSymbol(g_tim, h, sizeof(h));
-    unsigned long long z[8] = {0};
-    cudaMemcpyToSymbol(g_ctim, z, sizeof(z));
+    unsigned long long z[12] = {0};
+    cudaMemcpyToSymbol(g_ctim, z, 8 * sizeof(unsigned long long));
+    cudaMemcpyToSymbol(g_wait, z, sizeof(z));
     return;
   }
   cudaDeviceSynchronize();
@@ -582,8 +618,16 @@ void debug_timing(int nsteps, bool reset) {
       ++nc;
     }
   }
-  unsigned long long ct[8];
+  unsigned long long ct[8], wt[12];
   cudaMemcpyFromSymbol(ct, g_ctim, sizeof(ct));
+  cudaMemcpyFromSymbol(wt, g_wait, sizeof(wt));
+  if (wt[9]) {
+    const double T = (double)wt[9];  // summed CTA cycles
+    fprintf(stderr, "hqr sm-time: chase %.3f | producer dep spins: chase-done %.3f left %.3f near-right %.3f "
+            "qslot %.3f far/Z preds %.3f upload %.3f | consumer: waiting %.3f (per warp) busy %.3f (per warp)\n",
+            wt[8] / T, wt[0] / T, wt[1] / T, wt[2] / T, wt[3] / T, wt[4] / T, wt[5] / T,
+            wt[10] / T / (4.0 * kGroups), wt[11] / T / (4.0 * kGroups));
+  }
   if (ct[4]) {
     const double w = (double)ct[4] * kStepWarps, st = (double)ct[5] / (double)ct[4];
     fprintf(stderr, "hqr chase: %llu windows, %.1f steps each; cycles per step per warp: phase1 %.0f, "
@@ -673,18 +717,36 @@ void build_step_tasks(const StepArgs& a, const WindowDesc* wins, int nwin, const
       out->push_back(T);
     }
   };
+  // re-split the last `tiles` tiles of the queue from index `from` on into chunks of `chunk` (same
+  // order): the phase's end -- which the next phase waits for -- is then not one long task
+  auto resplit = [&](size_t from, int tiles, int chunk) {
+    int64_t acc = 0;
+    size_t cut = out->size();
+    while (cut > from && acc < tiles) acc += (*out)[--cut].ntiles;
+    std::vector<Task> tail(out->begin() + cut, out->end());
+    out->resize(cut);
+    for (const Task& T : tail)
+      for (int t0 = 0; t0 < T.ntiles; t0 += chunk) {
+        Task U = T;
+        U.tile0 = T.tile0 + t0;
+        U.ntiles = std::min(chunk, T.ntiles - t0);
+        out->push_back(U);
+      }
+  };
   const size_t base = out->size();
   for (int i = 0; i < nwin; ++i) {
     int64_t c, cnt;
     left_range(a, wins[i], c, cnt);
     add(kTaskLeft, i, (cnt + NT - 1) / NT, 0, 0, cs.left);
   }
+  if (cs.ltail > 0) resplit(base, cs.ltail, cs.phase_chunk);
   *nL = (int)(out->size() - base);
   const size_t rn0 = out->size();
   for (int i = 0; i < nwin; ++i) {
     const int64_t w0 = wins[i].w0;
     if (sp < w0) add(kTaskRight, i, (w0 - sp + MT - 1) / MT, sp, w0, cs.near);
   }
+  if (cs.ntail > 0) resplit(rn0, cs.ntail, cs.phase_chunk);
   *nRn = (int)(out->size() - rn0);
   for (int i = 0; i < nnext; ++i) {
     Task T{};
@@ -698,19 +760,7 @@ void build_step_tasks(const StepArgs& a, const WindowDesc* wins, int nwin, const
     const int64_t hi = std::min<int64_t>(sp, wins[i].w0);
     if (hi > 0) add(kTaskRight, i, (hi + MT - 1) / MT, 0, hi, cs.bulk);
   }
-  // re-split the queue's last cs.tail tiles into small chunks (same order)
-  int64_t acc = 0;
-  size_t cut = out->size();
-  while (cut > bulk0 && acc < cs.tail) acc += (*out)[--cut].ntiles;
-  std::vector<Task> tail(out->begin() + cut, out->end());
-  out->resize(cut);
-  for (const Task& T : tail)
-    for (int t0 = 0; t0 < T.ntiles; t0 += cs.tail_chunk) {
-      Task U = T;
-      U.tile0 = T.tile0 + t0;
-      U.ntiles = std::min(cs.tail_chunk, T.ntiles - t0);
-      out->push_back(U);
-    }
+  if (cs.tail > 0) resplit(bulk0, cs.tail, cs.tail_chunk);  // the queue's last tiles
   for (size_t i = base; i < out->size(); ++i) (*out)[i].idx = (int32_t)(i - base);
 }
 

@@ -46,6 +46,7 @@ struct WinDeps {    // per plan window (device array)
 struct ChunkSizes {   // tiles per task, per phase
   int left = 24, near = 16, bulk = 48;  // tuned for the persistent sweep (configs[3])
   int tail = 0, tail_chunk = 8;  // the queue's last `tail` tiles in chunks of `tail_chunk`
+  int ltail = 1200, ntail = 600, phase_chunk = 2;  // the left / near-right phases' last tiles in small chunks
 };
 
 // Tasks of one step in queue order (L, Rn, C, Z, Rf).
