@@ -508,9 +508,15 @@ __global__ void __launch_bounds__(kStepThreads, 1)
 #endif
       while (*reinterpret_cast<volatile int*>(&desc[s].pos) != j) {
       }
+#ifdef HQR_TIMING
+      const long long cw1 = clock64();
+#endif
       mbar_wait(&full[s], (unsigned)(j / NS) & 1, 3000000 + j);
 #ifdef HQR_TIMING
-      if (lane == 0) atomicAdd(&g_wait[10], (unsigned long long)(clock64() - cw0));
+      if (lane == 0) {
+        atomicAdd(&g_wait[10], (unsigned long long)(cw1 - cw0));
+        atomicAdd(&g_wait[5], (unsigned long long)(clock64() - cw1));
+      }
 #endif
       const int kind = desc[s].kind;
       if (kind != kDescTile) {
@@ -535,7 +541,16 @@ __global__ void __launch_bounds__(kStepThreads, 1)
       if (qe != last_qe) {
         if (pend_p && !mbar_test(&qfull, (unsigned)qe & 1)) flush();
         PROG(12000000 + qe);
+#ifdef HQR_TIMING
+        const long long cq0 = clock64();
+#endif
         mbar_wait(&qfull, (unsigned)qe & 1, 4000000 + qe);
+#ifdef HQR_TIMING
+        if (lane == 0) {
+          atomicAdd(&g_wait[7], (unsigned long long)(clock64() - cq0));
+          atomicAdd(&g_wait[6], 1ull);
+        }
+#endif
         last_qe = qe;
       }
       PROG(13000000 + j);
@@ -624,9 +639,11 @@ void debug_timing(int nsteps, bool reset) {
   if (wt[9]) {
     const double T = (double)wt[9];  // summed CTA cycles
     fprintf(stderr, "hqr sm-time: chase %.3f | producer dep spins: chase-done %.3f left %.3f near-right %.3f "
-            "qslot %.3f far/Z preds %.3f upload %.3f | consumer: waiting %.3f (per warp) busy %.3f (per warp)\n",
-            wt[8] / T, wt[0] / T, wt[1] / T, wt[2] / T, wt[3] / T, wt[4] / T, wt[5] / T,
-            wt[10] / T / (4.0 * kGroups), wt[11] / T / (4.0 * kGroups));
+            "qslot %.3f far/Z preds %.3f | consumer: pos %.3f data %.3f + Q_W %.3f (per warp, %.0f cycles "
+            "per Q_W wait) busy %.3f (per warp)\n",
+            wt[8] / T, wt[0] / T, wt[1] / T, wt[2] / T, wt[3] / T, wt[4] / T,
+            wt[10] / T / (4.0 * kGroups), wt[5] / T / (4.0 * kGroups), wt[7] / T / (4.0 * kGroups), wt[6] ? (double)wt[7] / wt[6] : 0.0,
+            wt[11] / T / (4.0 * kGroups));
   }
   if (ct[4]) {
     const double w = (double)ct[4] * kStepWarps, st = (double)ct[5] / (double)ct[4];
