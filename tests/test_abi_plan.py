@@ -66,15 +66,18 @@ def test_plan_invariants(n, ns, ilo, ihi, win):
     k = info["k"]
     assert k == min(win, N, hq.MAX_WINDOW)
     nb = ns // 2
-    # chains partition the bulges (remainders on the earliest chains), <= (k-2)/6 each
+    # chains partition the bulges (remainders on the earliest chains), <= (k-2)/6 each (P:383-385)
+    # and <= 13 (the fused kernel's chase runs one warp per bulge, R5)
     chains = {}
     for w in W:
         chains.setdefault(int(w[1]), (int(w[6]), int(w[7])))
     b = 0
     for c in sorted(chains):
         b0, nbc = chains[c]
-        assert b0 == b and (N <= k or nbc <= (k - 2) // 6)
+        assert b0 == b and (N <= k or nbc <= min((k - 2) // 6, 13))
         b += nbc
+    if N > k:  # as few chains as the cap allows
+        assert len(chains) == -(-nb // min((k - 2) // 6, 13))
     assert b == nb
     sizes = [chains[c][1] for c in sorted(chains)]
     assert sizes == sorted(sizes, reverse=True) and max(sizes) - min(sizes) <= 1
