@@ -16,8 +16,7 @@ namespace hqr {
 // stays resident next to a ring of stages_of(KP) panel tiles.  KP = 96: 32-wide tiles, five stages
 // (76.8 + 5 x 27.6 KB): with three consumer groups a group's next tile is loaded about two thirds
 // of a tile time ahead (measured: 40-wide x 4 stages 153.4 ms, 32 x 5 146.1 ms, 24 x 6 153.9 ms).
-__host__ __device__ constexpr int left_cols(int KP) { return KP <= 64 ? 64 : 32; }
-__host__ __device__ constexpr int right_rows(int KP) { return KP <= 64 ? 64 : 32; }
+// (left_cols / right_rows: kernels.hpp)
 __host__ __device__ constexpr int stages_of(int KP) { return KP <= 64 ? 4 : KP == 96 ? 5 : 2; }
 // Panel leading dimension: an m8n8k4 fragment load (per half-warp: 4 consecutive doubles x 4 strided
 // rows) is conflict-free iff the stride is an odd multiple of 4 doubles: smallest such ld >= x.

@@ -354,16 +354,54 @@ int get_fused(CachedPlan& cp, bool has_z, int64_t n, FusedTasks** out) {
     a.n = n; a.hcol0 = 0; a.lc0 = 0; a.lc1 = n; a.zrows = n; a.ldz = n; a.KP = cp.KP;
     a.Z = has_z ? reinterpret_cast<double*>(1) : nullptr;  // only tested for presence
     const int nwin_all = (int)P.windows.size();
-    f->wdeps.assign(nwin_all, hqr::WinDeps{{-1, -1, -1}, 0, 0, 0});
+    f->wdeps.assign(nwin_all, hqr::WinDeps{{-1, -1, -1}, 0, 0, 0, 0, -1, -1, -1, {0, 0}});
+    const int NT = hqr::left_cols(cp.KP);
     for (int g = 0; g < P.nsteps; ++g) {
       f->begin.push_back((int32_t)f->tasks.size());
-      const WindowDesc* w = P.windows.data() + P.step_begin[g];
-      const int nw = P.step_begin[g + 1] - P.step_begin[g];
+      const int b0 = P.step_begin[g];
+      const WindowDesc* w = P.windows.data() + b0;
+      const int nw = P.step_begin[g + 1] - b0;
       const WindowDesc* wn = (g + 1 < P.nsteps) ? P.windows.data() + P.step_begin[g + 1] : nullptr;
       const int nn = (g + 1 < P.nsteps) ? P.step_begin[g + 2] - P.step_begin[g + 1] : 0;
+      // near tasks (step.hpp): for every window W' of step g+1, the step-g windows meeting it
+      std::vector<int64_t> xcol(nw), rnear(nw, INT64_MAX);
+      std::vector<int> lnear(nw, 0);
+      for (int i = 0; i < nw; ++i) xcol[i] = w[i].w1;
+      for (int j = 0; j < nn; ++j) {
+        const WindowDesc& W2 = wn[j];
+        hqr::WinDeps& D2 = f->wdeps[P.step_begin[g + 1] + j];
+        for (int i = 0; i < nw; ++i) {
+          if (!(w[i].w0 <= W2.w1 && W2.w0 <= w[i].w1)) continue;
+          if (w[i].w0 <= W2.w0) {
+            if (D2.c_pred >= 0) return -103;
+            D2.c_pred = b0 + i;
+            xcol[i] = std::max<int64_t>(xcol[i], W2.w1);
+          } else {
+            if (D2.c_below >= 0) return -103;
+            D2.c_below = b0 + i;
+            rnear[i] = std::min<int64_t>(rnear[i], std::max<int64_t>((int64_t)W2.w0 & ~(int64_t)1, sp[g]));
+          }
+        }
+      }
+      for (int i = 0; i < nw; ++i) {
+        if (rnear[i] >= w[i].w0) continue;
+        for (int k = 0; k < nw; ++k)  // the window whose rows meet the RightNear rows
+          if (k != i && w[k].w0 < w[i].w0 && w[k].w1 >= rnear[i]) {
+            if (f->wdeps[b0 + i].rn_over >= 0) return -103;
+            f->wdeps[b0 + i].rn_over = b0 + k;
+            xcol[k] = std::max<int64_t>(xcol[k], w[i].w1);
+          }
+      }
+      for (int i = 0; i < nw; ++i) {
+        int64_t c, cnt;
+        hqr::left_range(a, w[i], c, cnt);
+        const int64_t tiles = (cnt + NT - 1) / NT;
+        lnear[i] = (int)std::min<int64_t>(tiles, (xcol[i] - w[i].w1 + NT - 1) / NT);
+      }
       int nl, nrn;
       a.step = g;
-      hqr::build_step_tasks(a, w, nw, wn, nn, sp[g], chunk_sizes(), &f->tasks, &nl, &nrn);
+      hqr::build_step_tasks(a, w, nw, wn, nn, sp[g], chunk_sizes(), lnear.data(), rnear.data(), &f->tasks,
+                            &nl, &nrn);
       hqr::StepInfo S{};
       S.win_begin = P.step_begin[g];
       S.win_count = nw;
@@ -373,11 +411,14 @@ int get_fused(CachedPlan& cp, bool has_z, int64_t n, FusedTasks** out) {
       for (int i = f->begin.back(); i < (int)f->tasks.size(); ++i) {
         const hqr::Task& T = f->tasks[i];
         if (T.type == hqr::kTaskChase) continue;
+        hqr::WinDeps& D = f->wdeps[S.win_begin + T.win];
         S.ntiles += T.ntiles;
-        if (T.idx < nl) S.nLt += T.ntiles;
-        else if (T.type == hqr::kTaskRight && T.idx < nl + nrn) S.nRnt += T.ntiles;
-        else if (T.type == hqr::kTaskRight) f->wdeps[S.win_begin + T.win].rftiles += T.ntiles;
-        else if (T.type == hqr::kTaskZ) f->wdeps[S.win_begin + T.win].ztiles += T.ntiles;
+        if (T.type == hqr::kTaskLeft || T.type == hqr::kTaskLeftNear) S.nLt += T.ntiles;
+        if (T.type == hqr::kTaskRight || T.type == hqr::kTaskRightNear) S.nRnt += T.ntiles;
+        if (T.type == hqr::kTaskLeftNear) D.lnear += T.ntiles;
+        if (T.type == hqr::kTaskRightNear) D.rnear += T.ntiles;
+        if (T.type == hqr::kTaskRightFar) D.rftiles += T.ntiles;
+        if (T.type == hqr::kTaskZ) D.ztiles += T.ntiles;
       }
       f->steps.push_back(S);
       for (int i = 0; i < nw; ++i) {
@@ -413,7 +454,7 @@ int get_fused(CachedPlan& cp, bool has_z, int64_t n, FusedTasks** out) {
     CK(cudaMemcpy(f->d_steps, f->steps.data(), f->steps.size() * sizeof(hqr::StepInfo), cudaMemcpyHostToDevice));
     CK(cudaMalloc(&f->d_wdeps, f->wdeps.size() * sizeof(hqr::WinDeps)));
     CK(cudaMemcpy(f->d_wdeps, f->wdeps.data(), f->wdeps.size() * sizeof(hqr::WinDeps), cudaMemcpyHostToDevice));
-    f->nctr = 8 + 4 * (size_t)P.nsteps + 4 * (size_t)nwin_all;
+    f->nctr = 8 + 4 * (size_t)P.nsteps + hqr::kWinCtr * (size_t)nwin_all;
     CK(cudaMalloc(&f->d_ctr, f->nctr * sizeof(int)));
     slot = std::move(f);
   }

@@ -71,6 +71,10 @@ constexpr int kQSets = 4;
 // Largest window side whose chase fits in SMEM (H window + Q_W both resident).
 constexpr int kMaxWindow = 112;
 
+// Panel tile width (LEFT: H columns) / height (RIGHT: H or Z rows) of the TMA-path update tiles.
+__host__ __device__ constexpr int left_cols(int KP) { return KP <= 64 ? 64 : 32; }
+__host__ __device__ constexpr int right_rows(int KP) { return KP <= 64 ? 64 : 32; }
+
 inline int padded_kp(int kw) { return kw <= 32 ? 32 : kw <= 64 ? 64 : kw <= 96 ? 96 : 128; }
 
 // SMEM leading dimension = 4 (mod 16) doubles: conflict-free mma.m8n8k4 fragment loads

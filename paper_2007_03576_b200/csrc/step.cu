@@ -248,6 +248,7 @@ struct StageDesc {
   int qe;      // tile: Q_W load epoch it multiplies with
   int cnt_add; // tile with ctr: tiles of the task this group has done (this warp adds them)
   int* ctr;    // tile: nullptr, or the counter the task's completion feeds (after the stores) ...
+  int* ctr2;   // ... a second one (near tasks: their phase's step counter) or nullptr ...
   int* ctr_all;  // ... and the step's all-tiles counter
   TileRef t;
 };
@@ -373,14 +374,31 @@ __global__ void __launch_bounds__(kStepThreads, 1)
       int* sc = step_ctr + 4 * g;
       const bool chase = T.type == kTaskChase;
       const int gw = chase ? -1 : S.win_begin + T.win;  // plan index of the task's window
-      const bool far_right = T.type == kTaskRight && T.idx >= S.nL + S.nRn;
+      const bool far_right = T.type == kTaskRightFar;
       if (lane == 0) {
         PROG(2000000 + t);
         if (up_flags) spin_until(up_flags + S.up_need, 1, 5);  // host-buffer sweep: rows / columns up
-        if (!chase && g > 0) spin_until(win_ctr + 4 * gw, 1, 0);
-        if (T.type == kTaskRight || chase) spin_until(sc + 0, 4 * S.nLt, 1);
+        // (dependency rules: step.hpp)
+        if ((T.type == kTaskLeft || T.type == kTaskLeftNear || T.type == kTaskRightNear || chase) && g > 0) {
+          spin_until(sc - 4 + 0, 4 * steps[g - 1].nLt, 6);   // step g-1's left phase
+          spin_until(sc - 4 + 1, 4 * steps[g - 1].nRnt, 6);  // and near-right phase
+        }
+        if (!chase && g > 0) spin_until(win_ctr + kWinCtr * gw, 1, 0);
+        if (T.type == kTaskRight || far_right) spin_until(sc + 0, 4 * S.nLt, 1);
+        if (T.type == kTaskRightNear) {
+          const int k = wdeps[gw].rn_over;
+          if (k >= 0) spin_until(win_ctr + kWinCtr * k + 3, 4 * wdeps[k].lnear, 7);
+        }
         if (chase) {
-          spin_until(sc + 1, 4 * S.nRnt, 2);
+          const WinDeps D = wdeps[steps[g + 1].win_begin + T.win];
+          if (D.c_pred >= 0) {
+            if (g > 0) spin_until(win_ctr + kWinCtr * D.c_pred, 1, 2);
+            spin_until(win_ctr + kWinCtr * D.c_pred + 3, 4 * wdeps[D.c_pred].lnear, 2);
+          }
+          if (D.c_below >= 0) {
+            if (g > 0) spin_until(win_ctr + kWinCtr * D.c_below, 1, 2);
+            spin_until(win_ctr + kWinCtr * D.c_below + 4, 4 * wdeps[D.c_below].rnear, 2);
+          }
           const int g_old = g + 1 - kQSets;
           if (g_old >= 0) spin_until(step_ctr + 4 * g_old + 2, 4 * steps[g_old].ntiles, 3);
         }
@@ -389,7 +407,7 @@ __global__ void __launch_bounds__(kStepThreads, 1)
           const int k = T.type == kTaskZ ? 1 : 2;
           for (int i = 0; i < 3; ++i)
             if (D.pred[i] >= 0)
-              spin_until(win_ctr + 4 * D.pred[i] + k, 4 * (k == 1 ? wdeps[D.pred[i]].ztiles : wdeps[D.pred[i]].rftiles), 4);
+              spin_until(win_ctr + kWinCtr * D.pred[i] + k, 4 * (k == 1 ? wdeps[D.pred[i]].ztiles : wdeps[D.pred[i]].rftiles), 4);
         }
         fence_proxy_async_all();  // other SMs' generic stores before this SM's TMA reads
       }
@@ -414,7 +432,7 @@ __global__ void __launch_bounds__(kStepThreads, 1)
 #endif
         if (lane == 0) {
           TIM_MAX(g, 2);
-          red_release_add(win_ctr + 4 * cwi, 1);  // the CTA's stores are ordered by the barrier
+          red_release_add(win_ctr + kWinCtr * cwi, 1);  // the CTA's stores are ordered by the barrier
         }
         q_win = -1;
         continue;
@@ -447,10 +465,12 @@ __global__ void __launch_bounds__(kStepThreads, 1)
         bulk_g2s(reinterpret_cast<char*>(Qs) + lane * chunk, reinterpret_cast<const char*>(Q) + lane * chunk,
                  chunk, &qfull);
       };
-      const bool left = T.type == kTaskLeft;
-      // the counter the task's completion feeds (tiles x 4 warps)
-      int* cnt = left ? sc + 0 : T.type == kTaskZ ? win_ctr + 4 * gw + 1
-                      : far_right ? win_ctr + 4 * gw + 2 : sc + 1;
+      const bool left = T.type == kTaskLeft || T.type == kTaskLeftNear;
+      // the counters the task's completion feeds (tiles x 4 warps)
+      int* const wc = win_ctr + kWinCtr * gw;
+      int* cnt = T.type == kTaskLeft ? sc + 0 : T.type == kTaskLeftNear ? wc + 3 : T.type == kTaskZ ? wc + 1
+               : far_right ? wc + 2 : T.type == kTaskRightNear ? wc + 4 : sc + 1;
+      int* cnt2 = T.type == kTaskLeftNear ? sc + 0 : T.type == kTaskRightNear ? sc + 1 : nullptr;
       const int nq_pre = new_q ? min(T.ntiles, NS - 1) : 0;  // tiles issued before the Q_W load
       for (int i = 0; i < T.ntiles; ++i, ++j) {
         if (new_q && i == nq_pre) load_q();
@@ -462,6 +482,7 @@ __global__ void __launch_bounds__(kStepThreads, 1)
           // (the group of tile i takes the task's tiles i, i-G, ..., i.e. i/G + 1 of them)
           const bool last = i + kGroups >= T.ntiles;
           d.ctr = last ? cnt : nullptr;
+          d.ctr2 = last ? cnt2 : nullptr;
           d.ctr_all = last ? sc + 2 : nullptr;
           d.cnt_add = i / kGroups + 1;
           if (left) {
@@ -485,12 +506,14 @@ __global__ void __launch_bounds__(kStepThreads, 1)
     // (the earlier stores have landed by then), or at once when the warp would otherwise wait
     // with counts pending (never sit on them: others may wait for them).
     int* pend_p = nullptr;
+    int* pend_p2 = nullptr;
     int* pend_all = nullptr;
     int pend_n = 0;
     auto flush = [&]() {
       __syncwarp();
       if (lane == 0) {
         red_release_add(pend_p, pend_n);
+        if (pend_p2) red_release_add(pend_p2, pend_n);
         red_release_add(pend_all, pend_n);
       }
       pend_p = nullptr;
@@ -535,6 +558,7 @@ __global__ void __launch_bounds__(kStepThreads, 1)
       }
       const int qe = desc[s].qe, add = desc[s].cnt_add;
       int* const cp = desc[s].ctr;
+      int* const cp2 = desc[s].ctr2;
       int* const call = desc[s].ctr_all;
       const bool left = desc[s].left;
       const TileRef t = desc[s].t;
@@ -570,6 +594,7 @@ __global__ void __launch_bounds__(kStepThreads, 1)
 #endif
       if (cp) {
         pend_p = cp;
+        pend_p2 = cp2;
         pend_all = call;
         pend_n = add;
       }
@@ -722,14 +747,15 @@ cudaError_t launch_step(const StepArgs& base, const StepInfo* steps, int nsteps,
 // cs.left, cs.near for L / Rn (they gate the next chase: small), cs.bulk for Z / Rf; the last
 // cs.tail tiles of the queue use chunks of cs.tail_chunk so the CTAs finish together.
 void build_step_tasks(const StepArgs& a, const WindowDesc* wins, int nwin, const WindowDesc* next_wins,
-                      int nnext, int64_t sp, const ChunkSizes& cs, std::vector<Task>* out, int* nL,
-                      int* nRn) {
+                      int nnext, int64_t sp, const ChunkSizes& cs, const int* lnear, const int64_t* rnear,
+                      std::vector<Task>* out, int* nL, int* nRn) {
   const int NT = left_cols(a.KP), MT = right_rows(a.KP);
-  auto add = [&](int type, int win, int64_t tiles, int64_t r_lo, int64_t r_hi, int chunk) {
-    for (int64_t t0 = 0; t0 < tiles; t0 += chunk) {
+  // tiles [t_begin, t_end) of window `win` in tasks of `chunk` tiles
+  auto add = [&](int type, int win, int64_t t_begin, int64_t t_end, int64_t r_lo, int64_t r_hi, int chunk) {
+    for (int64_t t0 = t_begin; t0 < t_end; t0 += chunk) {
       Task T{};
       T.type = type; T.win = win; T.tile0 = (int32_t)t0; T.step = a.step;
-      T.ntiles = (int32_t)std::min<int64_t>(chunk, tiles - t0);
+      T.ntiles = (int32_t)std::min<int64_t>(chunk, t_end - t0);
       T.r_lo = r_lo; T.r_hi = r_hi;
       out->push_back(T);
     }
@@ -751,31 +777,42 @@ void build_step_tasks(const StepArgs& a, const WindowDesc* wins, int nwin, const
       }
   };
   const size_t base = out->size();
-  for (int i = 0; i < nwin; ++i) {
-    int64_t c, cnt;
-    left_range(a, wins[i], c, cnt);
-    add(kTaskLeft, i, (cnt + NT - 1) / NT, 0, 0, cs.left);
-  }
-  if (cs.ltail > 0) resplit(base, cs.ltail, cs.phase_chunk);
-  *nL = (int)(out->size() - base);
-  const size_t rn0 = out->size();
+  // what the next step's chases read first: LeftNear, RightNear, then the chases themselves
+  for (int i = 0; i < nwin; ++i) add(kTaskLeftNear, i, 0, lnear[i], 0, 0, cs.left);
   for (int i = 0; i < nwin; ++i) {
     const int64_t w0 = wins[i].w0;
-    if (sp < w0) add(kTaskRight, i, (w0 - sp + MT - 1) / MT, sp, w0, cs.near);
+    if (rnear[i] < w0) add(kTaskRightNear, i, 0, (w0 - rnear[i] + MT - 1) / MT, rnear[i], w0, cs.near);
   }
-  if (cs.ntail > 0) resplit(rn0, cs.ntail, cs.phase_chunk);
-  *nRn = (int)(out->size() - rn0);
   for (int i = 0; i < nnext; ++i) {
     Task T{};
     T.type = kTaskChase; T.win = i; T.ntiles = 0; T.step = a.step;
     out->push_back(T);
   }
+  const size_t l0 = out->size();
+  for (int i = 0; i < nwin; ++i) {
+    int64_t c, cnt;
+    left_range(a, wins[i], c, cnt);
+    add(kTaskLeft, i, lnear[i], (cnt + NT - 1) / NT, 0, 0, cs.left);
+  }
+  if (cs.ltail > 0) resplit(l0, cs.ltail, cs.phase_chunk);
+  const size_t rn0 = out->size();
+  for (int i = 0; i < nwin; ++i) {
+    const int64_t hi = std::min<int64_t>(wins[i].w0, rnear[i]);
+    if (sp < hi) add(kTaskRight, i, 0, (hi - sp + MT - 1) / MT, sp, hi, cs.near);
+  }
+  if (cs.ntail > 0) resplit(rn0, cs.ntail, cs.phase_chunk);
+  *nL = *nRn = 0;
+  for (size_t i = base; i < out->size(); ++i) {
+    const int ty = (*out)[i].type;
+    *nL += ty == kTaskLeft || ty == kTaskLeftNear;
+    *nRn += ty == kTaskRight || ty == kTaskRightNear;
+  }
   const size_t bulk0 = out->size();
   if (a.Z)
-    for (int i = 0; i < nwin; ++i) add(kTaskZ, i, (a.zrows + MT - 1) / MT, 0, 0, cs.bulk);
+    for (int i = 0; i < nwin; ++i) add(kTaskZ, i, 0, (a.zrows + MT - 1) / MT, 0, 0, cs.bulk);
   for (int i = 0; i < nwin; ++i) {
     const int64_t hi = std::min<int64_t>(sp, wins[i].w0);
-    if (hi > 0) add(kTaskRight, i, (hi + MT - 1) / MT, 0, hi, cs.bulk);
+    if (hi > 0) add(kTaskRightFar, i, 0, (hi + MT - 1) / MT, 0, hi, cs.bulk);
   }
   if (cs.tail > 0) resplit(bulk0, cs.tail, cs.tail_chunk);  // the queue's last tiles
   for (size_t i = base; i < out->size(); ++i) (*out)[i].idx = (int32_t)(i - base);

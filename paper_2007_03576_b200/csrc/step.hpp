@@ -7,21 +7,24 @@
 
 namespace hqr {
 
-constexpr int kTaskLeft = 0, kTaskRight = 1, kTaskZ = 2, kTaskChase = 3;
+// Task types.  Left / RightNear-rest / RightFar / Z: GEMM tiles of one window; Chase: the chase of a
+// window of the next step.  LeftNear / RightNear: the few tiles the next step's chases read (below).
+constexpr int kTaskLeft = 0, kTaskRight = 1, kTaskZ = 2, kTaskChase = 3, kTaskLeftNear = 4,
+              kTaskRightNear = 5, kTaskRightFar = 6;
 constexpr int kMaxChaseBulges = 64;  // bulges per window the fused chase handles
 
 struct Task {       // one claimable unit of work of a wavefront step
-  int32_t type;     // kTaskLeft / kTaskRight / kTaskZ / kTaskChase
+  int32_t type;     // kTask*
   int32_t win;      // window index within the step (kTaskChase: within the next step)
   int32_t tile0, ntiles;
   int32_t step;     // wavefront step
-  int32_t idx;      // index within the step's queue (L: [0, nL), Rn: [nL, nL + nRn), ...)
-  int64_t r_lo, r_hi;  // kTaskRight: H rows [r_lo, r_hi), tiles of right_rows(KP) from r_lo
+  int32_t idx;      // index within the step's queue
+  int64_t r_lo, r_hi;  // right tasks: H rows [r_lo, r_hi), tiles of right_rows(KP) from r_lo
 };
 
 struct StepInfo {   // per wavefront step (device array)
   int32_t win_begin, win_count, slot_offset;
-  int32_t nL, nRn;          // tasks of the left / near-right phases
+  int32_t nL, nRn;          // tasks of the left / near-right phases (near parts included)
   int32_t nLt, nRnt;        // their tiles
   int32_t ntiles;           // all GEMM tiles of the step
   int32_t up_need;          // host-buffer sweeps: the last upload chunk its tasks (and the chase of
@@ -33,15 +36,30 @@ constexpr int kUploadChunk = 512;
 struct WinDeps {    // per plan window (device array)
   int32_t pred[3];          // windows of the previous step whose columns meet this one (-1: none)
   int32_t ztiles, rftiles;  // its Z / far-right tiles
-  int32_t pad;
+  int32_t lnear, rnear;     // its LeftNear / RightNear tiles
+  int32_t rn_over;          // RightNear: the window of its step whose rows meet those rows (-1: none)
+  int32_t c_pred, c_below;  // its chase: the previous step's windows meeting it from above / below
+  int32_t pad[2];
 };
+
+// The chase of window W' (step g+1) reads H(W', W'); at step g only these tasks write there: the
+// chases of the step-g windows meeting W' -- the predecessor X (w0_X <= w0') and the window Y
+// below -- X's left tiles on columns (w1_X, w1'] and Y's right tiles on rows [w0', w0_Y).  Those
+// tiles form the LeftNear task of X and the RightNear task of Y; the chase waits for them (and for
+// step g-1's left / near-right phases) instead of for the whole left / near-right phases of step g,
+// so it overlaps them.  A RightNear task of Y also waits for the LeftNear task of the window whose
+// rows meet its rows (they update the same block H(rows, Y) from the two sides); LeftNear covers
+// those columns too.  Every left / near-right task of step g waits for step g-1's left and
+// near-right phases (previously implied by waiting for the chase).
 
 // Completion counters (device, zeroed per sweep):
 //   step_ctr[4 g + 0]  left tiles of step g done x 4 (one release add per consumer warp)
 //   step_ctr[4 g + 1]  near-right tiles x 4
 //   step_ctr[4 g + 2]  all GEMM tiles x 4
-//   win_ctr[4 w + 0]   chase of plan window w done (1)
-//   win_ctr[4 w + 1]   Z tiles of w x 4;  win_ctr[4 w + 2]  far-right tiles of w x 4
+//   win_ctr[kWinCtr w + 0]   chase of plan window w done (1)
+//   win_ctr[kWinCtr w + 1]   Z tiles of w x 4;  + 2  far-right tiles of w x 4
+//   win_ctr[kWinCtr w + 3]   LeftNear tiles of w x 4;  + 4  RightNear tiles of w x 4
+constexpr int kWinCtr = 8;
 
 struct ChunkSizes {   // tiles per task, per phase
   int left = 24, near = 16, bulk = 48;  // tuned for the persistent sweep (configs[3])
@@ -49,10 +67,11 @@ struct ChunkSizes {   // tiles per task, per phase
   int ltail = 1200, ntail = 600, phase_chunk = 2;  // the left / near-right phases' last tiles in small chunks
 };
 
-// Tasks of one step in queue order (L, Rn, C, Z, Rf).
+// Tasks of one step in queue order (LeftNear, RightNear, C, L, Rn, Z, Rf).
+// lnear[i]: LeftNear tiles of window i; rnear[i]: first row of its RightNear rows (>= w0: none).
 void build_step_tasks(const StepArgs& a, const WindowDesc* wins, int nwin, const WindowDesc* next_wins,
-                      int nnext, int64_t sp, const ChunkSizes& cs, std::vector<Task>* out, int* nL,
-                      int* nRn);
+                      int nnext, int64_t sp, const ChunkSizes& cs, const int* lnear, const int64_t* rnear,
+                      std::vector<Task>* out, int* nL, int* nRn);
 
 // One persistent launch (one CTA per SM) running `ntasks` tasks -- one step's queue, or the whole
 // sweep's -- claimed through *next_ctr.  base: the sweep's StepArgs (per-step fields come from
