@@ -165,7 +165,8 @@ __global__ void __launch_bounds__(kChaseThreads, 1) chase_kernel(StepArgs a) {
       for (int jj = qw; jj < nbc; jj += kQWarps) {
         const Refl R = ring[slot][jj];
         if (R.pl == INT_MIN) continue;
-        right_apply(Qs + (R.pl + 1) * ldh, ldh, rQ + 1, R, lane);
+        const int q0 = q_first_row(W, jj);
+        right_apply(Qs + (R.pl + 1) * ldh + q0, ldh, rQ + 1 - q0, R, lane);
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[slot]);

@@ -168,6 +168,18 @@ struct Refl {      // one reflector in the ring: P = I - tau v v^T acting on loc
 };
 
 
+// First Q_W row bulge jj of window W can reach.  Q_W starts as I at the window's first step; a
+// row's support then grows only through the reflectors that touch it, and its right end follows
+// the deepest bulge that ever touched it (a deeper bulge starts 3 columns further right and is
+// never reached).  Rows above bulge jj's first reflector (local columns pf+1..pf+3) belong to
+// bulges above it, so they stay zero in bulge jj's columns; a bulge introduced in this window
+// (pf = ilo-1) can reach every row.
+__device__ __forceinline__ int q_first_row(const WindowDesc& W, int jj) {
+  const int tf = max(W.t0, 3 * jj);  // bulge jj's first step in this window (p >= ilo - 1)
+  const int pf = W.ilo - 1 + tf - 3 * jj;
+  return pf <= W.ilo - 1 ? 0 : pf - W.w0 + 1;
+}
+
 // Apply reflector r from the right to `rows` rows of three (two) consecutive SMEM columns starting
 // at c1 (ld = ldh); lanes across rows.
 __device__ __forceinline__ void right_apply(double* c1, int ldh, int rows, const Refl& r, int lane) {

@@ -200,7 +200,8 @@ __device__ void chase_window_9w(const StepArgs& a, const WindowDesc& W, int widx
       if (r.pl == INT_MIN) continue;
       r.v1 = R.v1[jj]; r.v2 = R.v2[jj]; r.tau = R.tau[jj]; r.m = R.m[jj];
       right_apply(Hs + (r.pl + 1) * ldh, ldh, min(r.pl + r.m + 1, rmaxH) + 1, r, lane);
-      right_apply(Qs + (r.pl + 1) * ldh, ldh, rQ + 1, r, lane);
+      const int q0 = q_first_row(W, jj);
+      right_apply(Qs + (r.pl + 1) * ldh + q0, ldh, rQ + 1 - q0, r, lane);
     }
     CTIM(c_p2);
     __syncthreads();
