@@ -713,10 +713,10 @@ void debug_progress_init() {
     fprintf(stderr, "hqr progress dump (%s): blocks whose producer did not exit, last events per warp\n",
             cudaGetErrorString(err));
     for (int b = 0; b < 148; ++b) {
-      const int* pw = h + (b * 16 + 8) * 65;
+      const int* pw = h + (b * 16 + kProducerWarp) * 65;
       const int last = pw[1 + ((pw[0] - 1) & 63)];
       if (last / 1000000 == 8) continue;
-      for (int w = 0; w < 9; ++w) {
+      for (int w = 0; w < kStepWarps; ++w) {
         const int* r = h + (b * 16 + w) * 65;
         fprintf(stderr, "b%d w%d n=%d:", b, w, r[0]);
         for (int k = r[0] > 40 ? r[0] - 40 : 0; k < r[0]; ++k) fprintf(stderr, " %d", r[1 + (k & 63)]);
