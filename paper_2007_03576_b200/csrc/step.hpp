@@ -62,7 +62,7 @@ struct WinDeps {    // per plan window (device array)
 constexpr int kWinCtr = 8;
 
 struct ChunkSizes {   // tiles per task, per phase
-  int left = 24, near = 16, bulk = 48;  // tuned for the persistent sweep (configs[3])
+  int left = 24, near = 48, bulk = 48;  // tuned for the persistent sweep (configs[3], tools/tune_chunks.sh)
   int tail = 0, tail_chunk = 8;  // the queue's last `tail` tiles in chunks of `tail_chunk`
   int ltail = 300, ntail = 0, phase_chunk = 2;  // the left phase's last tiles in small chunks (tools/tune_phase_tail.sh)
 };
