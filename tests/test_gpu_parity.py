@@ -71,6 +71,9 @@ CASES = [
     (12, 333, 50, 0, 332, 112, "orth"), (13, 400, 80, 0, 399, 96, "eye"), (14, 150, 100, 0, 149, 40, "eye"),
     (15, 120, 24, 0, 119, 112, "orth"), (16, 511, 64, 100, 400, 48, "eye"), (17, 97, 2, 0, 96, 9, "eye"),
     (18, 250, 248, 0, 249, 112, "eye"), (19, 401, 30, 1, 399, 100, "orth"),
+    # many chains over many wavefront steps: the next step's chases wait only for the near tiles of
+    # the windows meeting them, so chain-to-chain interactions matter here
+    (20, 1500, 200, 0, 1499, 48, "orth"), (21, 2000, 300, 7, 1990, 96, "eye"),
 ]
 
 
