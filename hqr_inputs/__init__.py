@@ -52,8 +52,13 @@ CONFIGS = {
 }
 
 
-def hessenberg(n: int, upper: str, cfg: int, blocks: int = 1, col_chunk: int = 512) -> np.ndarray:
-    """Random upper-Hessenberg H (Fortran order).  blocks > 1 zeroes h[b*n/blocks, b*n/blocks - 1]."""
+def hessenberg(n: int, upper: str, cfg: int, blocks: int = 1, col_chunk: int = 512,
+               subdiag: str = "u0515") -> np.ndarray:
+    """Random upper-Hessenberg H (Fortran order).  blocks > 1 zeroes h[b*n/blocks, b*n/blocks - 1].
+    subdiag: "u0515" = U[0.5, 1.5] (BASELINE configs) or "chi2" = the paper's hess_n recipe
+    (after Braman et al.): h_{i+1,i}^2 ~ chi^2(n - i) (1-based i), i.e.
+    h[i+1, i] = sqrt(chi^2(n - 1 - i)) 0-based -- graded from ~sqrt(n) at the top to ~1 at the
+    bottom (the Hessenberg form of a Ginibre matrix)."""
     H = np.zeros((n, n), dtype=np.float64, order="F")
     g = rng(cfg, 0)
     for c0 in range(0, n, col_chunk):
@@ -69,7 +74,12 @@ def hessenberg(n: int, upper: str, cfg: int, blocks: int = 1, col_chunk: int = 5
         for j in range(c0, c1):
             H[: j + 1, j] = vals[off: off + j + 1]
             off += j + 1
-    sub = rng(cfg, 1).uniform(0.5, 1.5, max(n - 1, 0))
+    if subdiag == "u0515":
+        sub = rng(cfg, 1).uniform(0.5, 1.5, max(n - 1, 0))
+    elif subdiag == "chi2":
+        sub = np.sqrt(rng(cfg, 1).chisquare(np.arange(n - 1, 0, -1, dtype=np.float64)))
+    else:
+        raise ValueError(subdiag)
     idx = np.arange(n - 1)
     H[idx + 1, idx] = sub
     if blocks > 1:
@@ -114,6 +124,29 @@ def shifts(kind: str, nshifts: int, cfg: int, stream_offset: int = 0) -> tuple[n
                 re[2 * j: 2 * j + 2] = a
                 im[2 * j], im[2 * j + 1] = b, -b
                 j += 1
+    elif kind == "ring68":
+        # conjugate pairs on the annulus 6 <= |lambda| <= 8, upper half plane (angle U(0, pi)):
+        # well outside the spectrum of the configs[2..4] matrices (spectral radius ~4), so no
+        # subdiagonal converges during the sweep and the reflectors stay well conditioned -- the
+        # full-size parity case whose rounding floor sits far below 1e-10 (R14)
+        for j in range(npairs):
+            r, t = g.uniform(6.0, 8.0), g.uniform(0.0, np.pi)
+            b = r * np.sin(t)
+            if b <= 0.0:
+                b = 1e-3 * r
+            re[2 * j: 2 * j + 2] = r * np.cos(t)
+            im[2 * j], im[2 * j + 1] = b, -b
+    elif kind.startswith("disk"):
+        # "disk<R>": conjugate pairs uniform on the upper half disk of radius R (rejection), e.g.
+        # hess_n shifts drawn from the region its spectrum fills (radius sqrt(n), Ginibre-like)
+        R = float(kind[4:])
+        j = 0
+        while j < npairs:
+            a, b = g.uniform(-R, R), g.uniform(0.0, R)
+            if a * a + b * b <= R * R and b > 0.0:
+                re[2 * j: 2 * j + 2] = a
+                im[2 * j], im[2 * j + 1] = b, -b
+                j += 1
     else:
         raise ValueError(kind)
     return re, im
@@ -131,14 +164,16 @@ class Problem:
     blocks: list  # [(ilo, ihi, shift slice start, shift count)]
 
 
-def make(cfg_idx: int, z_device: str = "cpu", n_override: int | None = None) -> Problem:
-    """Materialise BASELINE.json configs[cfg_idx] (optionally at a smaller n for tests)."""
+def make(cfg_idx: int, z_device: str = "cpu", n_override: int | None = None,
+         shift_kind: str | None = None) -> Problem:
+    """Materialise BASELINE.json configs[cfg_idx] (optionally at a smaller n for tests, or with
+    another shift distribution: shift_kind, e.g. "ring68")."""
     c = CONFIGS[cfg_idx]
     n = n_override or c.n
     H = hessenberg(n, c.upper, c.idx, blocks=c.blocks)
     Z = np.asfortranarray(np.eye(n)) if c.z0 == "eye" else orthogonal(n, c.idx, z_device)
     if c.blocks == 1:
-        re, im = shifts(c.shifts, c.nshifts, c.idx)
+        re, im = shifts(shift_kind or c.shifts, c.nshifts, c.idx)
         return Problem(H, Z, 0, n - 1, re, im, c.window, [(0, n - 1, 0, c.nshifts)])
     bs = n // c.blocks
     res, ims, blocks = [], [], []
@@ -148,6 +183,19 @@ def make(cfg_idx: int, z_device: str = "cpu", n_override: int | None = None) -> 
         ims.append(im)
         blocks.append((b * bs, b * bs + bs - 1, b * c.nshifts, c.nshifts))
     return Problem(H, Z, 0, n - 1, np.concatenate(res), np.concatenate(ims), c.window, blocks)
+
+
+HESS_CFG = 5  # seed-space id of the hess_n workload
+
+
+def make_hess(n: int, nshifts: int, z0: str = "eye", z_device: str = "cpu") -> Problem:
+    """hess_n: N(0,1) upper entries, sqrt(chi^2(n-i)) subdiagonal; shifts =
+    conjugate pairs uniform on the upper half disk of radius sqrt(n) (the region a Ginibre-like
+    spectrum fills: the shifts an AED window would return lie there); one sweep ilo=0, ihi=n-1."""
+    H = hessenberg(n, "n01", HESS_CFG, subdiag="chi2")
+    Z = np.asfortranarray(np.eye(n)) if z0 == "eye" else orthogonal(n, HESS_CFG, z_device)
+    re, im = shifts("disk%.6g" % np.sqrt(n), nshifts, HESS_CFG)
+    return Problem(H, Z, 0, n - 1, re, im, None, [(0, n - 1, 0, nshifts)])
 
 
 def random_case(seed: int, n: int, nshifts: int, ilo: int = 0, ihi: int | None = None,

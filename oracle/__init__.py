@@ -7,10 +7,12 @@ fp64, OpenMP over independent rows/columns only), this module only marshals argu
 
 Functions and the passages they follow (PAPER.md line numbers, see hqr_oracle.c):
   house(x)                 -- 3x3 / 2x2 Householder reflector, P:200 (reading R2 in DESIGN.md)
-  first_column(H, ilo, ..) -- first column of (H - s I)(H - s' I), P:200 (reading R1)
+  first_column(H, ilo, ..) -- first column of (H - s I)(H - s' I), P:200 (reading R1), scaled
+                              by a power of two (reading R15)
   sweep(H, Z, ...)         -- nshifts/2 sequential Francis double steps on the full matrix,
                               P:146-151, P:198-206, P:227-233
   flops(...)               -- F_alg, the work of applying every reflector directly
+  subdiag_scan(H, ...)     -- the aftermath subdiagonal scan, P:379-381 (reading R16)
 
 Parity pins for every function are in tests/test_oracle.py (none is "parity unpinned").
 """
@@ -47,7 +49,8 @@ def _load():
         lib.oracle_house.argtypes = [ctypes.c_int, dp, dp, dp, dp]
         lib.oracle_house.restype = None
         lib.oracle_first_column.argtypes = [dp, ctypes.c_int64, ctypes.c_int64, ctypes.c_double,
-                                            ctypes.c_double, dp]
+                                            ctypes.c_double, ctypes.c_double, ctypes.c_double, dp,
+                                            ctypes.POINTER(ctypes.c_int)]
         lib.oracle_first_column.restype = None
         lib.oracle_sweep.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64,
                                      ctypes.c_int64, dp, dp, ctypes.c_int, ctypes.c_int, ctypes.c_int,
@@ -56,6 +59,9 @@ def _load():
         lib.oracle_flops.argtypes = [ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int,
                                      ctypes.c_int]
         lib.oracle_flops.restype = ctypes.c_double
+        lib.oracle_subdiag_scan.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64,
+                                            ctypes.c_int64, ctypes.c_void_p]
+        lib.oracle_subdiag_scan.restype = None
         _lib = lib
     return _lib
 
@@ -75,11 +81,16 @@ def house(x):
     return v, tau.value, beta.value
 
 
-def first_column(H: np.ndarray, ilo: int, sigma: float, pi: float) -> np.ndarray:
+def first_column(H: np.ndarray, ilo: int, re_pair, im_pair=(0.0, 0.0)):
+    """(x, e2): the first column of (H - s I)(H - s' I) at rows ilo..ilo+2 is x * 2**e2 (x is
+    computed on inputs scaled by a power of two, reading R15).  re_pair / im_pair: the shift pair
+    (s, s') as real and imaginary parts."""
     H = _as_colmajor(H)
     x = np.zeros(3)
-    _load().oracle_first_column(_dptr(H), H.shape[0], ilo, sigma, pi, _dptr(x))
-    return x
+    e2 = ctypes.c_int()
+    _load().oracle_first_column(_dptr(H), H.shape[0], ilo, float(re_pair[0]), float(re_pair[1]),
+                                float(im_pair[0]), float(im_pair[1]), _dptr(x), ctypes.byref(e2))
+    return x, e2.value
 
 
 def _as_colmajor(a: np.ndarray) -> np.ndarray:
@@ -112,3 +123,14 @@ def sweep(H: np.ndarray, Z: np.ndarray | None, ilo: int, ihi: int, shifts_re, sh
 
 def flops(n: int, ilo: int, ihi: int, nbulges: int, with_z: bool = True) -> float:
     return _load().oracle_flops(n, ilo, ihi, nbulges, 1 if with_z else 0)
+
+
+def subdiag_scan(H: np.ndarray, blocks) -> np.ndarray:
+    """Aftermath flags (int8, n entries) of H for the active blocks [(ilo, ihi), ...]: 2 exact
+    zero, 1 negligible (|h| <= 2^-52 (|h_ii| + |h_i+1,i+1|)), 0 otherwise, -1 not scanned."""
+    H = _as_colmajor(H)
+    n = H.shape[0]
+    flags = np.full(n, -1, dtype=np.int8)
+    for ilo, ihi in blocks:
+        _load().oracle_subdiag_scan(H.ctypes.data, n, ilo, ihi, flags.ctypes.data)
+    return flags

@@ -20,6 +20,8 @@
  *      v = [1, x1/(x0-beta), ...]; zero tail => tau = 0, beta = x0 (identity).
  *   R3 shift pairs: consecutive (2j, 2j+1); sigma = s+s', pi = s*s' (= re*re' - im*im').
  *   R6 no vigilant deflation during the sweep.  R9 annihilated entries stored as exact 0.0.
+ *   R15 the reflector and bulge vectors are computed on inputs scaled by a power of two (exact:
+ *      bit-identical where the unscaled formulas stay finite, finite where they would not).
  *
  * Layout: column-major doubles, leading dimension n (element (i,j) at i + j*n).
  */
@@ -31,42 +33,64 @@
 
 #define EL(A, i, j, ld) (A)[(size_t)(i) + (size_t)(j) * (size_t)(ld)]
 
+/* Scaling by a power of two (reading R15): for amax = m 2^e with m in [0.5, 1),
+ * returns e; x * 2^-e is exact (no rounding) whenever it is a normal number, so the scaled
+ * formulas below give bit-identical results to the unscaled ones wherever those do not overflow or
+ * underflow, and stay finite where they would (|H| up to ~1e300, down to ~1e-300).  Any nonzero
+ * scaling of x gives the same reflector (SURVEY §8(c) reading 1). */
+static int pow2_exponent(double amax) {
+  int e;
+  (void)frexp(amax, &e);
+  return e;
+}
+
 /* R2: Householder reflector of length m (2 or 3) mapping x to beta*e1 ("generate a 3-by-3
- * Householder reflector Q1 such that Q1^T v is a multiple of e1").  P = I - tau v v^T. */
+ * Householder reflector Q1 such that Q1^T v is a multiple of e1").  P = I - tau v v^T.
+ * Computed on x scaled by 2^-e (R15); beta is scaled back. */
 void oracle_house(int m, const double* x, double* v, double* tau, double* beta) {
-  double alpha = x[0];
-  double tail2 = 0.0;
-  for (int i = 1; i < m; ++i) tail2 += x[i] * x[i];
+  double amax = 0.0;
+  for (int i = 0; i < m; ++i) amax = fmax(amax, fabs(x[i]));
   v[0] = 1.0;
-  if (tail2 == 0.0) {
-    for (int i = 1; i < m; ++i) v[i] = 0.0;
-    *tau = 0.0;
-    *beta = alpha;
-    return;
-  }
+  for (int i = 1; i < m; ++i) v[i] = 0.0;
+  *tau = 0.0;
+  *beta = x[0];
+  if (amax == 0.0) return;
+  const int e = pow2_exponent(amax);
+  double xs[3];
+  for (int i = 0; i < m; ++i) xs[i] = ldexp(x[i], -e);
+  double alpha = xs[0];
+  double tail2 = 0.0;
+  for (int i = 1; i < m; ++i) tail2 += xs[i] * xs[i];
+  if (tail2 == 0.0) return; /* zero tail: P = I, beta = x0 */
   double norm = sqrt(alpha * alpha + tail2);
   double b = (alpha >= 0.0) ? -norm : norm; /* sign(0) = +1 */
   *tau = (b - alpha) / b;
-  for (int i = 1; i < m; ++i) v[i] = x[i] / (alpha - b);
-  *beta = b;
+  for (int i = 1; i < m; ++i) v[i] = xs[i] / (alpha - b);
+  *beta = ldexp(b, e);
 }
 
 /* R1: x = (H - s I)(H - s' I) e_ilo restricted to rows ilo..ilo+2, in real arithmetic
- * ("v = (H - l1 I)(H - l2 I) e1").  sigma = s + s', pi = s s'. */
-void oracle_first_column(const double* H, int64_t n, int64_t ilo, double sigma, double pi,
-                         double* x) {
+ * ("v = (H - l1 I)(H - l2 I) e1"), with sigma = s + s' and pi = s s' = re re' - im im'
+ * (R3).  Returned scaled (R15): the true vector is x * 2^(*e2); every input is multiplied by the
+ * same 2^-e first, so x = 2^-2e times the unscaled expression, rounding for rounding. */
+void oracle_first_column(const double* H, int64_t n, int64_t ilo, double re0, double re1,
+                         double im0, double im1, double* x, int* e2) {
   double h00 = EL(H, ilo, ilo, n), h01 = EL(H, ilo, ilo + 1, n);
   double h10 = EL(H, ilo + 1, ilo, n), h11 = EL(H, ilo + 1, ilo + 1, n);
   double h21 = EL(H, ilo + 2, ilo + 1, n);
+  const double all[9] = {h00, h01, h10, h11, h21, re0, re1, im0, im1};
+  double amax = 0.0;
+  for (int i = 0; i < 9; ++i) amax = fmax(amax, fabs(all[i]));
+  const int e = amax == 0.0 ? 0 : pow2_exponent(amax);
+  h00 = ldexp(h00, -e); h01 = ldexp(h01, -e); h10 = ldexp(h10, -e);
+  h11 = ldexp(h11, -e); h21 = ldexp(h21, -e);
+  re0 = ldexp(re0, -e); re1 = ldexp(re1, -e); im0 = ldexp(im0, -e); im1 = ldexp(im1, -e);
+  const double sigma = re0 + re1;
+  const double pi = re0 * re1 - im0 * im1;
   x[0] = h00 * (h00 - sigma) + h01 * h10 + pi;
   x[1] = h10 * (h00 + h11 - sigma);
   x[2] = h10 * h21;
-}
-
-/* R3: the shift pair of bulge j. */
-static void pair_coeffs(const double* sr, const double* si, int j, double* sigma, double* pi) {
-  *sigma = sr[2 * j] + sr[2 * j + 1];
-  *pi = sr[2 * j] * sr[2 * j + 1] - si[2 * j] * si[2 * j + 1];
+  *e2 = 2 * e;
 }
 
 /* Apply the reflector of bulge j at position p (acting on rows/cols p+1..p+m) to the full H and Z,
@@ -74,11 +98,12 @@ static void pair_coeffs(const double* sr, const double* si, int j, double* sigma
  * rows p+1..p+m (all columns to the right), store beta / exact zeros in column p, apply from the
  * right to columns p+1..p+m (all rows above the bulge), and accumulate into Z (all n rows). */
 static void apply_one(double* H, double* Z, int64_t n, int64_t ilo, int64_t ihi, int64_t p,
-                      double sigma, double pi) {
+                      const double* sr, const double* si, int j) {
   int m = (p <= ihi - 3) ? 3 : 2;
   double x[3], v[3], tau, beta;
-  if (p == ilo - 1) {
-    oracle_first_column(H, n, ilo, sigma, pi, x);
+  if (p == ilo - 1) { /* bulge j: shifts (2j, 2j+1), R3 */
+    int e2;
+    oracle_first_column(H, n, ilo, sr[2 * j], sr[2 * j + 1], si[2 * j], si[2 * j + 1], x, &e2);
   } else {
     for (int i = 0; i < m; ++i) x[i] = EL(H, p + 1 + i, p, n);
   }
@@ -128,11 +153,8 @@ int oracle_sweep(double* H, double* Z, int64_t n, int64_t ilo, int64_t ihi, cons
                  const double* si, int nshifts, int order, int j0, int j1) {
   (void)nshifts;
   if (order == 0) {
-    for (int j = j0; j < j1; ++j) {
-      double sigma, pi;
-      pair_coeffs(sr, si, j, &sigma, &pi);
-      for (int64_t p = ilo - 1; p <= ihi - 2; ++p) apply_one(H, Z, n, ilo, ihi, p, sigma, pi);
-    }
+    for (int j = j0; j < j1; ++j)
+      for (int64_t p = ilo - 1; p <= ihi - 2; ++p) apply_one(H, Z, n, ilo, ihi, p, sr, si, j);
   } else {
     int nb = j1 - j0;
     int64_t last = (ihi - 2) - (ilo - 1) + 3 * (int64_t)(nb - 1);
@@ -140,9 +162,7 @@ int oracle_sweep(double* H, double* Z, int64_t n, int64_t ilo, int64_t ihi, cons
       for (int jj = 0; jj < nb; ++jj) { /* lowest (earliest introduced) first */
         int64_t p = ilo - 1 + t - 3 * (int64_t)jj;
         if (p < ilo - 1 || p > ihi - 2) continue;
-        double sigma, pi;
-        pair_coeffs(sr, si, j0 + jj, &sigma, &pi);
-        apply_one(H, Z, n, ilo, ihi, p, sigma, pi);
+        apply_one(H, Z, n, ilo, ihi, p, sr, si, j0 + jj);
       }
     }
   }
@@ -161,4 +181,20 @@ double oracle_flops(int64_t n, int64_t ilo, int64_t ihi, int nbulges, int with_z
     f += per * ((double)(n - c0) + (double)(r1 + 1) + (with_z ? (double)n : 0.0));
   }
   return f * nbulges;
+}
+
+/* Subdiagonal scan (check only; "scanning the sub-diagonal entries in order to identify
+ * any unreduced blocks that were decoupled during the bulge chasing step ... stored to a special
+ * aftermath vector that has an entry for each row of the matrix"), reading R16: for every row i
+ * with ilo-1 <= i <= ihi (and 0 <= i <= n-2), h = H[i+1, i], d = |H[i,i]| + |H[i+1,i+1]|:
+ *   flags[i] = 2 if h == 0 (decoupled), 1 if |h| <= 2^-52 d (negligible by the standard
+ *   criterion), else 0.  Other entries are left as they are (the caller initialises them). */
+void oracle_subdiag_scan(const double* H, int64_t n, int64_t ilo, int64_t ihi, signed char* flags) {
+  int64_t i0 = ilo - 1 < 0 ? 0 : ilo - 1;
+  int64_t i1 = ihi < n - 2 ? ihi : n - 2;
+  for (int64_t i = i0; i <= i1; ++i) {
+    double h = EL(H, i + 1, i, n);
+    double d = fabs(EL(H, i, i, n)) + fabs(EL(H, i + 1, i + 1, n));
+    flags[i] = (h == 0.0) ? 2 : (fabs(h) <= 0x1p-52 * d) ? 1 : 0;
+  }
 }

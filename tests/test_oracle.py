@@ -53,6 +53,20 @@ def test_house_34_and_sign_of_zero():
     assert beta == -5.0 and tau == 1.0
 
 
+@pytest.mark.parametrize("k", [600, -600, 1000, -1000])
+def test_house_scaled_extremes(k):
+    # R15: |x| ~ 2^k (1e180 .. 1e-300): the unscaled x0^2 + tail^2 would overflow / underflow; the
+    # reflector is the one of x = (1, 2, 2) exactly (tau, v identical; beta scaled by 2^k)
+    v, tau, beta = oracle.house(np.ldexp([1.0, 2.0, 2.0], k))
+    v0, tau0, beta0 = oracle.house([1.0, 2.0, 2.0])
+    assert np.array_equal(v, v0) and tau == tau0 and beta == np.ldexp(beta0, k)
+    v, tau, beta = oracle.house(np.ldexp([3.0, 4.0], k))
+    assert beta == np.ldexp(-5.0, k) and np.isfinite(tau)
+    # a tail far below the head but representable: still a (tiny) rotation, not the identity
+    v, tau, beta = oracle.house([np.ldexp(1.0, k), np.ldexp(1.0, k - 200), 0.0])
+    assert beta == -np.ldexp(1.0, k) and tau == 0.0 or abs(v[1]) <= 2.0 ** -199
+
+
 @pytest.mark.parametrize("seed", range(20))
 def test_house_random_maps_to_beta_e1(seed):
     g = np.random.default_rng(seed)
@@ -91,9 +105,24 @@ def test_first_column_matches_explicit_product(seed):
     # the active block starts at ilo: (B - s1 I)(B - s2 I) e1 with B = H[ilo:, ilo:]
     Bq = [[Fraction(int(Hi[i, j])) for j in range(ilo, n)] for i in range(ilo, n)]
     exact = _shifted_first_col_exact(Bq, s1, s2, 0)
-    x = oracle.first_column(np.asfortranarray(Hi), ilo, float(s1 + s2), float(s1 * s2))
-    assert all(Fraction(x[i]) == exact[i] for i in range(3))
+    x, e2 = oracle.first_column(np.asfortranarray(Hi), ilo, (float(s1), float(s2)))
+    assert all(Fraction(x[i]) * Fraction(2) ** e2 == exact[i] for i in range(3))
     assert all(v == 0 for v in exact[3:])
+    # scale invariance (R15): H and the shifts times 2^k give the same scaled vector, e2 + 2k; at
+    # k = +-600 the unscaled products would overflow / underflow (|H| ~ 1e180 / 1e-180)
+    for k in (600, -600, 7):
+        xs, e2s = oracle.first_column(np.asfortranarray(np.ldexp(Hi, k)), ilo,
+                                      (float(np.ldexp(float(s1), k)), float(np.ldexp(float(s2), k))))
+        assert np.array_equal(xs, x) and e2s == e2 + 2 * k
+    # a conjugate pair (a +- bi): pi = a^2 + b^2, sigma = 2a
+    a, b = Fraction(int(g.integers(-3, 4)), 2), Fraction(int(g.integers(1, 4)), 2)
+    Bc = [[Fraction(int(Hi[i, j])) for j in range(ilo, n)] for i in range(ilo, n)]
+    e1 = [Fraction(int(i == 0)) for i in range(n - ilo)]
+    mv = lambda v: [sum(Bc[i][k] * v[k] for k in range(n - ilo)) for i in range(n - ilo)]
+    Hv, HHv = mv(e1), mv(mv(e1))
+    exact_c = [HHv[i] - 2 * a * Hv[i] + (a * a + b * b) * e1[i] for i in range(n - ilo)]
+    x, e2 = oracle.first_column(np.asfortranarray(Hi), ilo, (float(a), float(a)), (float(b), float(-b)))
+    assert all(Fraction(x[i]) * Fraction(2) ** e2 == exact_c[i] for i in range(3))
 
 
 # --------------------------------------------------------------------------------------------
@@ -109,10 +138,10 @@ def test_worked_example_6x6_exact_values():
     g = _gold()
     H0 = np.asfortranarray(np.array(g["H_rows"], dtype=float))
     H, Z = H0.copy(order="F"), np.asfortranarray(np.eye(6))
-    x = oracle.first_column(H0, 0, 3.0, 2.0)
-    assert [Fraction(t) for t in x] == [F(s) for s in g["first_column"]]
-    v, tau, beta = oracle.house(x)
-    assert Fraction(beta) == F(g["house_beta"]) and abs(tau - float(F(g["house_tau"]))) <= 2 * U
+    x, e2 = oracle.first_column(H0, 0, (1.0, 2.0))   # shifts 1, 2: sigma = 3, pi = 2
+    assert [Fraction(t) * Fraction(2) ** e2 for t in x] == [F(s) for s in g["first_column"]]
+    v, tau, beta = oracle.house(x)   # the reflector of the scaled vector; beta scales back by 2^e2
+    assert Fraction(beta) * Fraction(2) ** e2 == F(g["house_beta"]) and abs(tau - float(F(g["house_tau"]))) <= 2 * U
     oracle.sweep(H, Z, 0, 5, g["shifts_re"], g["shifts_im"])
     assert abs(H[0, 0] - float(F(g["Hp00"]))) <= 8 * U * 4
     assert np.allclose(Z[:, 0], [float(F(s)) for s in g["Zp_col0"]], atol=4 * U, rtol=0)
@@ -304,3 +333,64 @@ def test_flops_formula_small():
         tot += (10 if m == 3 else 6) * (cols + rows + n)
     assert oracle.flops(n, ilo, ihi, 1) == tot
     assert oracle.flops(n, ilo, ihi, 3) == 3 * tot
+
+
+def test_flops_match_survey_table():
+    # F_alg of the BASELINE configs as tabulated in SURVEY.md §8(d) (derived there independently
+    # of this code, 4 significant digits): catches a wrong term count or range in oracle_flops
+    table = {0: (256, [(0, 255, 8)], 5.255e6), 1: (4000, [(0, 3999, 100)], 1.600e10),
+             2: (10000, [(0, 9999, 256)], 2.560e11), 3: (20000, [(0, 19999, 512)], 2.048e12),
+             4: (40000, [(b * 10000, b * 10000 + 9999, 512) for b in range(4)], 8.191e12)}
+    for cfg, (n, blocks, want) in table.items():
+        got = sum(oracle.flops(n, lo, hi, ns // 2) for lo, hi, ns in blocks)
+        assert abs(got - want) <= 0.0005 * want, (cfg, got, want)
+
+
+@pytest.mark.parametrize("k", [600, -600])
+def test_sweep_scale_equivariance(k):
+    # R15: scaling H and the shifts by 2^k scales H' by 2^k bit for bit and leaves Z' unchanged
+    # (every step is linear in H or scale invariant); at k = +-600 the unscaled bulge vector
+    # (~|H|^2) would overflow / underflow, so this also pins the scaled first column and house
+    n, ns = 60, 10
+    H0, Z0, re, im = random_case(91, n, ns, z0="orth", shift_kind="disk2")
+    H, Z = H0.copy(order="F"), Z0.copy(order="F")
+    oracle.sweep(H, Z, 0, n - 1, re, im)
+    Hs, Zs = np.asfortranarray(np.ldexp(H0, k)), Z0.copy(order="F")
+    oracle.sweep(Hs, Zs, 0, n - 1, np.ldexp(re, k), np.ldexp(im, k))
+    assert np.all(np.isfinite(Hs)) and np.array_equal(Hs, np.ldexp(H, k)) and np.array_equal(Zs, Z)
+
+
+def test_hess_n_workload_sweep_invariants():
+    # NEXT-3 workload: graded chi^2 subdiagonal, shifts in the disk of radius sqrt(n)
+    from hqr_inputs import make_hess
+    p = make_hess(300, 40, z0="orth")
+    sub = np.diag(p.H, -1)
+    assert sub[0] > 10.0 and np.all(sub > 0) and np.all(np.tril(p.H, -2) == 0)
+    H, Z = p.H.copy(order="F"), p.Z.copy(order="F")
+    oracle.sweep(H, Z, 0, 299, p.shifts_re, p.shifts_im)
+    n, hn = 300, np.linalg.norm(p.H)
+    assert np.all(np.tril(H, -2) == 0.0)
+    assert np.linalg.norm(Z.T @ Z - np.eye(n)) <= 1e-13 * n
+    assert np.linalg.norm(Z @ H @ Z.T - p.Z @ p.H @ p.Z.T) / hn <= 1e-13 * n
+
+
+# --------------------------------------------------------------------------------------------
+# Subdiagonal scan (aftermath vector; reading R16)
+# --------------------------------------------------------------------------------------------
+
+def test_subdiag_scan_closed_cases():
+    n = 10
+    H = np.asfortranarray(np.triu(np.ones((n, n)), -1) * 2.0)
+    H[3, 2] = 0.0                     # exact zero -> 2
+    H[6, 5] = 2.0 ** -52 * 4.0        # = eps (|h55| + |h66|) exactly -> 1 (boundary included)
+    H[8, 7] = np.nextafter(2.0 ** -52 * 4.0, 1.0)   # one ulp above -> 0
+    f = oracle.subdiag_scan(H, [(0, n - 1)])
+    want = np.zeros(n, dtype=np.int8)
+    want[2], want[5], want[9] = 2, 1, -1  # row n-1 has no subdiagonal entry
+    assert np.array_equal(f, want)
+    # only rows ilo-1 .. ihi of each block are scanned; ilo-1 / ihi are the decoupling zeros
+    H[4, 3] = 0.0
+    f = oracle.subdiag_scan(H, [(4, 6)])
+    assert list(f) == [-1, -1, -1, 2, 0, 1, 0, -1, -1, -1]
+    f = oracle.subdiag_scan(H, [(0, 2), (3, 3 + 2)])
+    assert list(f[:6]) == [0, 0, 2, 2, 0, 1]

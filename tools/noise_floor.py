@@ -12,8 +12,8 @@ import oracle  # noqa: E402
 from hqr_inputs import make  # noqa: E402
 
 
-def main(cfg):
-    p = make(cfg)
+def main(cfg, shift_kind=None):
+    p = make(cfg, shift_kind=shift_kind)
     n = p.H.shape[0]
     t0 = time.time()
     Hs, Zs = p.H.copy(order="F"), p.Z.copy(order="F")
@@ -25,7 +25,7 @@ def main(cfg):
     dH = Hs - Hp
     i, j = np.unravel_index(np.argmax(np.abs(dH)), dH.shape)
     sub = np.abs(np.diag(Hs, -1))
-    out = {"cfg": cfg, "n": n, "nshifts": len(p.shifts_re),
+    out = {"cfg": cfg, "shifts": shift_kind or "config", "n": n, "nshifts": len(p.shifts_re),
            "dH_rel_fro": float(np.linalg.norm(dH) / np.linalg.norm(p.H)),
            "dZ_fro_over_sqrt_n": float(np.linalg.norm(Zs - Zp) / np.sqrt(n)),
            "dH_max": float(np.abs(dH).max()), "dH_argmax": [int(i), int(j)],
@@ -35,5 +35,7 @@ def main(cfg):
 
 
 if __name__ == "__main__":
+    # arguments: "3" (configs[3] as specified) or "3:ring68" (configs[3] with another shift set)
     for c in sys.argv[1:]:
-        main(int(c))
+        cfg, _, kind = c.partition(":")
+        main(int(cfg), kind or None)
