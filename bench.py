@@ -54,6 +54,12 @@ def fp64_peak():
     return d["dmma_sustained_tflops"], d["dmma_burst_tflops"]
 
 
+def dgemm_peak():
+    with open(FP64_PEAK_FILE) as f:
+        d = json.load(f)
+    return d.get("cublas_dgemm_8192_sustained_tflops")
+
+
 class Clocks:
     """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
 
@@ -95,6 +101,21 @@ class Clocks:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def host_info():
+    """CPU model, OpenMP threads and affinity of the host the oracle runs on."""
+    model = None
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    aff = sorted(os.sched_getaffinity(0))
+    return {"cpu_model": model, "omp_num_threads": os.environ.get("OMP_NUM_THREADS"),
+            "affinity_cpus": len(aff), "nproc": os.cpu_count()}
+
+
 def cpu_baseline(prob, bulges, n, ilo, ihi):
     """The oracle as it stands on this host's cores, on a bounded sample: the first `bulges`
     shift pairs on the full matrix (F_alg per pair is the same for every pair)."""
@@ -109,7 +130,8 @@ def cpu_baseline(prob, bulges, n, ilo, ihi):
     return {"value": f / dt / 1e9, "unit": "GFLOP/s", "cores": cores, "kind": "oracle",
             "sample": f"first {bulges} of {len(prob.shifts_re) // 2} shift pairs on the full "
                       f"n={n} matrix ({dt:.1f} s; F_alg {f:.3e})",
-            "seconds_per_sweep_extrapolated": dt * (len(prob.shifts_re) // 2) / bulges}
+            "seconds_per_sweep_extrapolated": dt * (len(prob.shifts_re) // 2) / bulges,
+            "host": host_info()}
 
 
 def f_alg(n, ilo, ihi, nb, with_z):
@@ -163,6 +185,11 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--n", type=int, default=None, help="override n (debug)")
+    ap.add_argument("--sweeps", type=int, default=1,
+                    help="NEXT-1: this many overlapped sweeps per step (hqr_sweeps), shift set 0 = the "
+                         "config's, the others drawn from the same distribution")
+    ap.add_argument("--workload", default="config", choices=["config", "hess"],
+                    help="hess: the paper's hess_n matrix (NEXT-3) at --n (default 10000), 256 shifts")
     args = ap.parse_args()
 
     if args.impl == "reference":
@@ -183,10 +210,23 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
 
     t0 = time.time()
-    prob = make(args.config, z_device="cuda" if torch.cuda.is_available() else "cpu", n_override=args.n)
+    if args.workload == "hess":
+        from hqr_inputs import make_hess
+        prob = make_hess(args.n or 10000, 256, z0="orth", z_device="cuda" if torch.cuda.is_available() else "cpu")
+        workload = f"hess_n (P:1061-1068), n={prob.H.shape[0]}, 256 shifts (NEXT-3)"
+    else:
+        prob = make(args.config, z_device="cuda" if torch.cuda.is_available() else "cpu", n_override=args.n)
+        workload = f"configs[{args.config}]"
     n = prob.H.shape[0]
     gen_s = time.time() - t0
     nshifts = len(prob.shifts_re)
+    shift_sets = None
+    if args.sweeps > 1:  # NEXT-1: further shift sets from the same distribution (stream offsets)
+        from hqr_inputs import CONFIGS, shifts as draw_shifts
+        c = CONFIGS[args.config]
+        shift_sets = [(prob.shifts_re, prob.shifts_im)] + [
+            draw_shifts(c.shifts, c.nshifts, c.idx, stream_offset=i) for i in range(1, args.sweeps)]
+        workload += f" x {args.sweeps} overlapped sweeps (hqr_sweeps, NEXT-1)"
 
     if world == 1:
         hq.setup(local)
@@ -202,11 +242,17 @@ def main():
         if len(prob.blocks) > 1:  # configs[4]: decoupled blocks swept together (hqr_sweep_multi)
             blocks = [(b[0], b[1], b[3]) for b in prob.blocks]
 
-            def one():
-                hq.sweep_multi(H, Z, blocks, prob.shifts_re, prob.shifts_im, args.window)
+            def call(Hx, Zx):
+                hq.sweep_multi(Hx, Zx, blocks, prob.shifts_re, prob.shifts_im, args.window)
+        elif shift_sets is not None:
+            def call(Hx, Zx):
+                hq.sweeps(Hx, Zx, prob.ilo, prob.ihi, shift_sets, args.window)
         else:
-            def one():
-                hq.sweep(H, Z, prob.ilo, prob.ihi, prob.shifts_re, prob.shifts_im, args.window)
+            def call(Hx, Zx):
+                hq.sweep(Hx, Zx, prob.ilo, prob.ihi, prob.shifts_re, prob.shifts_im, args.window)
+
+        def one():
+            call(H, Z)
     else:
         # sharded sweep: this rank's H column shard (+ halo) and Z row shard
         import torch.distributed as dist
@@ -264,7 +310,20 @@ def main():
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms = float(t.item())
     st = hq.stats()
-    fa = sum(f_alg(n, b[0], b[1], b[3] // 2, True) for b in prob.blocks)
+    fa = sum(f_alg(n, b[0], b[1], b[3] // 2, True) for b in prob.blocks) * max(1, args.sweeps)
+    sequential_ms = None
+    if shift_sets is not None and world == 1:
+        # the same shift sets as separate hqr_sweep calls (device-timed), for the overlap's gain
+        seq = []
+        for _ in range(2):
+            restore()
+            torch.cuda.synchronize()
+            tot = 0.0
+            for sre, sim in shift_sets:
+                hq.sweep(H, Z, prob.ilo, prob.ihi, sre, sim, args.window)
+                tot += hq.stats()["ms_total"]
+            seq.append(tot)
+        sequential_ms = min(seq)
     value = fa / (ms * 1e-3) / 1e9   # one sweep (strong scaling: the same sweep on every N)
     peak_sus, peak_burst = fp64_peak()
     gflops_exec = (st["flops_update"] + st["flops_chase"]) / (ms * 1e-3) / 1e9
@@ -296,8 +355,10 @@ def main():
         # 2*m*n*k count of the same GEMMs is reported beside it
         achieved = ps["flops_dmma"] / (upd_ms * 1e-3) / 1e12
         traffic = ncu_traffic(ps["launches_left"] == 1)
+        dg = dgemm_peak()
         roofline = {"bound": "tensor", "kernel": kern,
                     "achieved": achieved, "peak": peak_sus, "unit": "TFLOP/s", "frac": achieved / peak_sus,
+                    "frac_of_cublas_dgemm": achieved / dg if dg else None, "cublas_dgemm_tflops": dg,
                     "traffic": traffic["bytes_per_launch"] if traffic else None,
                     "traffic_source": traffic["source"] if traffic else None,
                     "achieved_what": "executed FP64 DMMA flops (band-trimmed update GEMMs) per launch / "
@@ -331,18 +392,15 @@ def main():
             Hh.copy_(torch.from_numpy(Hp.T.copy()))
             Zh.copy_(torch.from_numpy(np.ascontiguousarray(prob.Z.T)))
             rc_t = time.perf_counter()
-            rc = hq.sweep_raw(Hh.data_ptr(), Zh.data_ptr(), n, prob.ilo, prob.ihi,
-                              np.ascontiguousarray(prob.shifts_re).ctypes.data,
-                              np.ascontiguousarray(prob.shifts_im).ctypes.data, nshifts, args.window)
+            call(Hh.t(), Zh.t())   # pinned HOST buffers: the library stages them (copies in the call)
             dt = time.perf_counter() - rc_t
-            assert rc == 0, rc
             e2e_t.append(dt)
         st2 = hq.stats()
         hq.teardown()
         e2e = {"value": fa / min(e2e_t) / 1e9, "unit": "GFLOP/s",
                "seconds_per_sweep": min(e2e_t),
                "h2d_bytes_per_step": st2["h2d_bytes"], "d2h_bytes_per_step": st2["d2h_bytes"],
-               "how": "hqr_sweep with pinned host H and Z (wall clock around the C-ABI call)"}
+               "how": "the same C-ABI call with pinned host H and Z (wall clock around it)"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -354,8 +412,10 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, BASELINE.json configs)",
-            "config": {"workload": f"configs[{args.config}]", "n": n, "nshifts": nshifts,
-                       "window": st["window_eff"], "z": "random orthogonal" if args.config in (1, 3) else "identity",
+            "config": {"workload": workload, "n": n, "nshifts": nshifts,
+                       "sweeps_per_step": args.sweeps,
+                       "window": st["window_eff"],
+                       "z": "random orthogonal" if (args.config in (1, 3) or args.workload == "hess") else "identity",
                        "parallelism": (f"{world} GPUs: H block-column (sqrt-balanced), Z block-row, "
                                        "per-window Q ncclBroadcast, lent slabs") if world > 1 else "1 GPU",
                        "l2": "inputs (2 x %.1f GB) larger than L2" % (n * n * 8 / 1e9),
@@ -370,6 +430,7 @@ def main():
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
             "gpu_launches": launches, "steps_per_sweep": st["steps"], "windows_per_sweep": st["windows"],
             "input_gen_s": gen_s,
+            "sequential_sweeps_ms": sequential_ms,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

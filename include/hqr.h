@@ -46,6 +46,16 @@ typedef struct hqr_config {
                         /* bit 1: HQR_FLAG_PROFILE  -- time every launch with CUDA events         */
                         /* bit 2: HQR_FLAG_NO_FUSE  -- separate chase / left / right launches     */
                         /*        instead of the fused step kernel                                */
+  /* Shard boundaries (world > 1): NULL = the sqrt-balanced default of
+   * hqr_dist_layout for every n.  Otherwise both arrays hold world + 1 entries for n = n_max:
+   * col_bounds[r] .. col_bounds[r+1] are rank r's H columns, row_bounds[..] its Z rows; 0 = b[0] <
+   * ... < b[world] = n_max, even, H shards >= HQR_MAX_WINDOW + 8 columns (else hqr_setup returns -1;
+   * a sweep with another n returns -11).  The arrays are copied; the caller keeps ownership. */
+  const int64_t* col_bounds;
+  const int64_t* row_bounds;
+  int window_max;       /* largest window side this setup will use (0 = HQR_MAX_WINDOW; must be   */
+                        /* <= HQR_MAX_WINDOW, else -1): the effective side is min(window, N,      */
+                        /* window_max)                                                            */
 } hqr_config;
 
 #define HQR_FLAG_NO_GRAPH 1
@@ -53,8 +63,9 @@ typedef struct hqr_config {
 #define HQR_FLAG_NO_FUSE 4
 
 /* Initialise the library on cfg->device: streams, events, workspace, NCCL communicator (world > 1).
- * Returns 0, -1 (cfg NULL or inconsistent rank/world/nccl_id), -101 (no usable sm_100 device),
- * 1000+cudaError_t, 2000+ncclResult_t.  Calling it again re-initialises (tears down first). */
+ * Returns 0, -1 (cfg NULL or inconsistent rank/world/nccl_id/bounds/window_max), -101 (no usable
+ * sm_100 device), 1000+cudaError_t, 2000+ncclResult_t.  Calling it again re-initialises (tears
+ * down first). */
 int hqr_setup(const hqr_config* cfg);
 
 /*
@@ -71,14 +82,19 @@ int hqr_setup(const hqr_config* cfg);
  *                      any two reals.
  *   nshifts   even, 2 <= nshifts <= N
  *   window    diagonal-window side k (performance knob only; never changes the mathematical result):
- *             the effective side is min(window, N, HQR_MAX_WINDOW); it must be >= 8 unless it
- *             covers the whole block (window >= N).
+ *             the effective side is min(window, N, window_max); window <= 0 is -9; a window
+ *             smaller than the block must be >= 8 (-9); window >= N is accepted and means one
+ *             window holding the whole block (SURVEY §8(b) lists "> N" as -9; we accept it
+ *             because N < 8 blocks -- valid sweeps -- have no other legal window; R5).
  * Returns 0 or: -1 H NULL; -3 n < 1; -4 ilo < 0 or ilo > ihi; -5 ihi >= n or N < 3;
  *   -6 non-finite shift; -7 conjugate partner not exact / mixed real-complex pair;
  *   -8 nshifts odd, < 2 or > N; -9 window out of range; -10 block not decoupled
  *   (H[ilo,ilo-1] != 0 or H[ihi+1,ihi] != 0); -100 not set up; 1000+cudaError_t; 2000+ncclResult_t.
- * Matrix entries are assumed finite (no NaN/Inf scan).  With world > 1 it is a collective called by
- * every rank with identical scalars and shifts (multi-GPU layout: see DESIGN.md §Multi-GPU).
+ * Matrix entries are assumed finite (no NaN/Inf scan).  Entry: the library's stream waits for work
+ * queued on the legacy default stream (so H / Z writes issued there before the call are seen).
+ * With world > 1 (hqr_setup) it is a collective called by every rank with identical scalars and
+ * shifts, H and Z being this rank's LOCAL shards in the hqr_dist_layout layout (exactly
+ * hqr_sweep_dist; host pointers are not accepted there).
  */
 int hqr_sweep(double* H, double* Z, int64_t n, int64_t ilo, int64_t ihi, const double* shifts_re,
               const double* shifts_im, int nshifts, int window);
@@ -95,6 +111,19 @@ int hqr_sweep(double* H, double* Z, int64_t n, int64_t ilo, int64_t ihi, const d
 int hqr_sweep_multi(double* H, double* Z, int64_t n, int nblocks, const int64_t* ilo,
                     const int64_t* ihi, const double* shifts_re, const double* shifts_im,
                     const int* nshifts, int window);
+
+/*
+ * Several sweeps of one active block, overlapped ("two
+ * bulge chasing steps can be overlapped"): sweep i uses nshifts[i] shifts, taken
+ * consecutively from shifts_re / shifts_im (sweep 0 first), and is applied after sweep i-1 -- the
+ * result is hqr_sweep called nsweeps times in order.  The shift sets are inputs here (known up
+ * front), so sweep i+1's bulge chains enter the wavefront right behind sweep i's last chain and
+ * its introduction and chase run while sweep i's right / Z updates drain.  Single GPU.  Codes as
+ * hqr_sweep (each sweep's shifts validated as there), -8 also for nsweeps < 1 or nshifts NULL,
+ * -1 after a world > 1 setup.
+ */
+int hqr_sweeps(double* H, double* Z, int64_t n, int64_t ilo, int64_t ihi, int nsweeps,
+               const double* shifts_re, const double* shifts_im, const int* nshifts, int window);
 
 /*
  * ---- Sharded sweep over several GPUs -------------------------------------------
@@ -137,12 +166,26 @@ int hqr_sweep_virtual(double* H, double* Z, int64_t n, int64_t ilo, int64_t ihi,
                       const double* shifts_re, const double* shifts_im, int nshifts, int window,
                       int vworld);
 
+/*
+ * Aftermath vector of the last successful single-GPU sweep (hqr_sweep / hqr_sweep_multi /
+ * hqr_sweeps: the push-bulges tasks of the last bulge
+ * chain scan the subdiagonal for blocks decoupled during the sweep).  Check only: H is not
+ * modified.  flags[i] (host array of n int8) for row i:
+ *    2  h(i+1, i) == 0 exactly (decoupled)
+ *    1  0 < |h(i+1, i)| <= 2^-52 (|h(i,i)| + |h(i+1,i+1)|)  (negligible: deflatable)
+ *    0  otherwise
+ *   -1  not scanned (outside [ilo-1, ihi] of every active block, or i = n-1)
+ * computed by the chases of each block's last (topmost) chain from the final entries.
+ * Returns 0, -1 (flags NULL), -3 (n differs from the last sweep's n), -100 (no sweep yet).
+ */
+int hqr_get_aftermath(signed char* flags, int64_t n);
+
 /* Release everything hqr_setup acquired.  Returns 0 (also when not set up) or 1000+cudaError_t. */
 int hqr_teardown(void);
 
 /* Largest effective window side the chase kernel supports (SMEM-resident window + factor). */
 #define HQR_MAX_WINDOW 112
-/* Library default window side used when window <= 0 is passed to hqr_plan_query / bench. */
+/* Library default window side (the bench's and the Python binding's default argument). */
 #define HQR_DEFAULT_WINDOW 96
 
 /*
@@ -158,6 +201,9 @@ int hqr_plan_query(int64_t n, int64_t ilo, int64_t ihi, int nshifts, int window,
 int hqr_plan_query_multi(int64_t n, int nblocks, const int64_t* ilo, const int64_t* ihi,
                          const int* nshifts, int window, int32_t* info, int32_t* windows,
                          int64_t cap);
+
+int hqr_plan_query_sweeps(int64_t n, int64_t ilo, int64_t ihi, int nsweeps, const int* nshifts,
+                          int window, int32_t* info, int32_t* windows, int64_t cap);
 
 /* Statistics of the last successful hqr_sweep on this process. */
 typedef struct hqr_stats {

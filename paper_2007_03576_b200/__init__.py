@@ -46,7 +46,9 @@ class HQRError(RuntimeError):
 
 class _Config(ctypes.Structure):
     _fields_ = [("device", ctypes.c_int), ("rank", ctypes.c_int), ("world", ctypes.c_int),
-                ("nccl_id", ctypes.c_void_p), ("n_max", ctypes.c_int64), ("flags", ctypes.c_int)]
+                ("nccl_id", ctypes.c_void_p), ("n_max", ctypes.c_int64), ("flags", ctypes.c_int),
+                ("col_bounds", ctypes.c_void_p), ("row_bounds", ctypes.c_void_p),
+                ("window_max", ctypes.c_int)]
 
 
 class Stats(ctypes.Structure):
@@ -66,7 +68,8 @@ class Stats(ctypes.Structure):
 
 SYMBOLS = ["hqr_setup", "hqr_sweep", "hqr_sweep_multi", "hqr_teardown", "hqr_plan_query",
            "hqr_plan_query_multi", "hqr_get_stats", "hqr_error_string", "hqr_dist_layout",
-           "hqr_dist_query", "hqr_nccl_unique_id", "hqr_sweep_dist", "hqr_sweep_virtual"]
+           "hqr_dist_query", "hqr_nccl_unique_id", "hqr_sweep_dist", "hqr_sweep_virtual",
+           "hqr_get_aftermath", "hqr_sweeps", "hqr_plan_query_sweeps"]
 
 
 def lib():
@@ -115,6 +118,16 @@ def lib():
         L.hqr_plan_query.argtypes = [ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int,
                                      ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64]
         L.hqr_plan_query.restype = ctypes.c_int
+        L.hqr_sweeps.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64,
+                                 ctypes.c_int64, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p,
+                                 ctypes.c_void_p, ctypes.c_int]
+        L.hqr_sweeps.restype = ctypes.c_int
+        L.hqr_plan_query_sweeps.argtypes = [ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int,
+                                            ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p,
+                                            ctypes.c_void_p, ctypes.c_int64]
+        L.hqr_plan_query_sweeps.restype = ctypes.c_int
+        L.hqr_get_aftermath.argtypes = [ctypes.c_void_p, ctypes.c_int64]
+        L.hqr_get_aftermath.restype = ctypes.c_int
         L.hqr_get_stats.argtypes = [ctypes.POINTER(Stats)]
         L.hqr_get_stats.restype = ctypes.c_int
         L.hqr_error_string.argtypes = [ctypes.c_int]
@@ -124,12 +137,19 @@ def lib():
 
 
 def setup(device: int = 0, flags: int = 0, rank: int = 0, world: int = 1, nccl_id: bytes | None = None,
-          n_max: int = 0) -> None:
+          n_max: int = 0, col_bounds=None, row_bounds=None, window_max: int = 0) -> None:
     buf = None
-    cfg = _Config(device, rank, world, None, n_max, flags)
+    cfg = _Config(device, rank, world, None, n_max, flags, None, None, window_max)
     if nccl_id is not None:
         buf = ctypes.create_string_buffer(bytes(nccl_id), len(nccl_id))
         cfg.nccl_id = ctypes.cast(buf, ctypes.c_void_p)
+    cbs = rbs = None
+    if col_bounds is not None:
+        cbs = np.ascontiguousarray(col_bounds, dtype=np.int64)
+        cfg.col_bounds = cbs.ctypes.data
+    if row_bounds is not None:
+        rbs = np.ascontiguousarray(row_bounds, dtype=np.int64)
+        cfg.row_bounds = rbs.ctypes.data
     rc = lib().hqr_setup(ctypes.byref(cfg))
     if rc:
         raise HQRError(rc, "hqr_setup")
@@ -196,6 +216,43 @@ def sweep_multi(H, Z, blocks, shifts_re, shifts_im, window: int = DEFAULT_WINDOW
                                sr.ctypes.data, si.ctypes.data, ns.ctypes.data, int(window))
     if rc:
         raise HQRError(rc, "hqr_sweep_multi")
+
+
+def sweeps(H, Z, ilo: int, ihi: int, shift_sets, window: int = DEFAULT_WINDOW) -> None:
+    """Several sweeps of one block, overlapped (hqr_sweeps): shift_sets = [(re, im), ...], applied
+    in order; the result is sweep() called once per set."""
+    hp, n = _ptr_n(H)
+    zp, nz = _ptr_n(Z)
+    if hp is None:
+        raise HQRError(-1, "hqr_sweeps")
+    if zp is not None and nz != n:
+        raise ValueError("H and Z must have the same order")
+    sr = np.ascontiguousarray(np.concatenate([np.asarray(r, dtype=np.float64) for r, _ in shift_sets]))
+    si = np.ascontiguousarray(np.concatenate([np.asarray(i, dtype=np.float64) for _, i in shift_sets]))
+    ns = np.array([len(r) for r, _ in shift_sets], dtype=np.int32)
+    if sr.shape != si.shape:
+        raise ValueError("re / im lengths differ")
+    rc = lib().hqr_sweeps(hp, zp, n, ilo, ihi, len(shift_sets), sr.ctypes.data, si.ctypes.data,
+                          ns.ctypes.data, int(window))
+    if rc:
+        raise HQRError(rc, "hqr_sweeps")
+
+
+def plan_query_sweeps(n: int, ilo: int, ihi: int, nshifts_list, window: int):
+    """plan_query for hqr_sweeps: (info dict, windows int32 [nw, 12])."""
+    ns = np.array(nshifts_list, dtype=np.int32)
+    info = np.zeros(10, dtype=np.int32)
+    args = (n, ilo, ihi, len(ns), ns.ctypes.data, window)
+    rc = lib().hqr_plan_query_sweeps(*args, info.ctypes.data, None, 0)
+    if rc:
+        raise HQRError(rc, "hqr_plan_query_sweeps")
+    nw = int(info[6])
+    wins = np.zeros((nw, 12), dtype=np.int32)
+    rc = lib().hqr_plan_query_sweeps(*args, info.ctypes.data, wins.ctypes.data, nw)
+    if rc:
+        raise HQRError(rc, "hqr_plan_query_sweeps")
+    keys = ["k", "nbc_max", "s", "lag", "nchains", "nsteps", "nwindows", "max_kw", "max_nbc", "nb"]
+    return dict(zip(keys, (int(v) for v in info))), wins
 
 
 def dist_layout(n: int, world: int):
@@ -279,6 +336,16 @@ def plan_query_multi(n: int, blocks, window: int):
         raise HQRError(rc, "hqr_plan_query_multi")
     keys = ["k", "nbc_max", "s", "lag", "nchains", "nsteps", "nwindows", "max_kw", "max_nbc", "nb"]
     return dict(zip(keys, (int(v) for v in info))), wins
+
+
+def aftermath(n: int) -> np.ndarray:
+    """Aftermath flags (int8 per row) of the last single-GPU sweep (include/hqr.h
+    hqr_get_aftermath): 2 exact zero subdiagonal, 1 negligible, 0 not small, -1 not scanned."""
+    out = np.empty(n, dtype=np.int8)
+    rc = lib().hqr_get_aftermath(out.ctypes.data, n)
+    if rc:
+        raise HQRError(rc, "hqr_get_aftermath")
+    return out
 
 
 def stats() -> dict:

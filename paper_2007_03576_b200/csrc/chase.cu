@@ -96,12 +96,7 @@ __global__ void __launch_bounds__(kChaseThreads, 1) chase_kernel(StepArgs a) {
           const int m = (p <= ihi - 3) ? 3 : 2;
           double x0, x1, x2;
           if (p == ilo - 1) {  // bulge introduction; the window starts at ilo
-            const int jb = W.b0 + jj;
-            const double sigma = a.coef[2 * jb], pi = a.coef[2 * jb + 1];
-            const double h00 = Hs[0], h10 = Hs[1], h01 = Hs[ldh], h11 = Hs[1 + ldh], h21 = Hs[2 + ldh];
-            x0 = h00 * (h00 - sigma) + h01 * h10 + pi;
-            x1 = h10 * (h00 + h11 - sigma);
-            x2 = h10 * h21;
+            intro_vector(Hs, ldh, a.coef + 4 * (W.b0 + jj), x0, x1, x2);
           } else {
             const double* col = Hs + pl * ldh + pl;
             x0 = col[1];
@@ -174,6 +169,7 @@ __global__ void __launch_bounds__(kChaseThreads, 1) chase_kernel(StepArgs a) {
     }
   }
   __syncthreads();
+  aftermath_scan(Hs, ldh, W, a, threadIdx.x, kChaseThreads);  // a9 (check only)
 
   // write back the window; store Q_W column-major with ld = QLD (= the update kernels' SMEM
   // layout), zero padded to KP x QLD

@@ -40,11 +40,12 @@ typedef std::vector<int64_t> PlanKey;
 struct Blocks {
   std::vector<int64_t> ilo, ihi;
   std::vector<int> nshifts;
+  bool sweeps = false;  // entries are successive sweeps of ONE block (hqr_sweeps), not disjoint blocks
   int count() const { return (int)ilo.size(); }
 };
 
 PlanKey plan_key(int64_t n, const Blocks& b, int window) {
-  PlanKey k{n, window};
+  PlanKey k{n, window, b.sweeps ? -1 : 0};
   for (int i = 0; i < b.count(); ++i) {
     k.push_back(b.ilo[i]);
     k.push_back(b.ihi[i]);
@@ -94,10 +95,17 @@ struct State {
   cudaStream_t stream = nullptr;   // stream A: chase -> left -> right (high priority)
   cudaStream_t zstream = nullptr;  // stream B: Z updates (low priority)
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  cudaEvent_t ev_in = nullptr;     // entry: the library stream waits for the caller's legacy stream
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   cudaEvent_t ev_q[hqr::kQSets] = {}, ev_z[hqr::kQSets] = {};
   double* d_coef = nullptr;
   size_t coef_cap = 0;
+  double* d_aft = nullptr;       // aftermath flags of the last single-GPU sweep (int8 per row)
+  size_t aft_cap = 0;            // (in doubles)
+  int64_t aft_n = 0;             // n of the sweep that wrote them (0: none)
+  std::vector<int64_t> user_cb, user_rb;  // hqr_config shard bounds (empty: sqrt-balanced default)
+  int64_t user_n = 0;            // the n they are for
+  int window_max = 0;            // hqr_config window cap (0: HQR_MAX_WINDOW)
   double* d_q = nullptr;
   size_t q_cap = 0;
   int* d_upflags = nullptr;      // host-buffer sweeps: per upload chunk, 1 once on the device
@@ -165,7 +173,7 @@ int validate_blocks(int64_t n, const Blocks& b, const double* sr, const double* 
   if (b.count() < 1) return -4;
   int64_t off = 0;
   for (int i = 0; i < b.count(); ++i) {
-    if (i > 0 && b.ilo[i] <= b.ihi[i - 1]) return -4;  // ascending, disjoint
+    if (i > 0 && !b.sweeps && b.ilo[i] <= b.ihi[i - 1]) return -4;  // ascending, disjoint
     int rc = validate_block(n, b.ilo[i], b.ihi[i], sr ? sr + off : nullptr, si ? si + off : nullptr,
                             b.nshifts[i], check_shifts);
     if (rc) return rc;
@@ -180,8 +188,11 @@ int get_plan(int64_t n, const Blocks& b, int window, CachedPlan** out, bool uplo
   auto it = g.plans.find(key);
   if (it == g.plans.end()) {
     auto cp = std::make_unique<CachedPlan>();
-    int rc = hqr::make_plan_multi(n, b.count(), b.ilo.data(), b.ihi.data(), b.nshifts.data(), window,
-                                  hqr::kMaxWindow, &cp->plan);
+    const int kmax = g.window_max > 0 ? g.window_max : hqr::kMaxWindow;
+    int rc = b.sweeps ? hqr::make_plan_sweeps(n, b.ilo[0], b.ihi[0], b.count(), b.nshifts.data(), window,
+                                              kmax, &cp->plan)
+                      : hqr::make_plan_multi(n, b.count(), b.ilo.data(), b.ihi.data(), b.nshifts.data(),
+                                             window, kmax, &cp->plan);
     if (rc) return rc;
     cp->KP = hqr::padded_kp(cp->plan.max_kw);
     it = g.plans.emplace(key, std::move(cp)).first;
@@ -221,6 +232,30 @@ int ensure(double** p, size_t* cap, size_t count) {
   return 0;
 }
 
+// a1: the shift pairs go to the device as they are -- coef[4j..4j+3] = (re_2j, re_2j+1, im_2j,
+// im_2j+1); the chase forms sigma = s + s' and pi = s s' from them on scaled inputs (R1, R3, R15)
+int upload_coef(const double* sr, const double* si, int nb) {
+  std::vector<double> coef(4 * (size_t)nb);
+  for (int j = 0; j < nb; ++j) {
+    coef[4 * j] = sr[2 * j];
+    coef[4 * j + 1] = sr[2 * j + 1];
+    coef[4 * j + 2] = si[2 * j];
+    coef[4 * j + 3] = si[2 * j + 1];
+  }
+  int rc = ensure(&g.d_coef, &g.coef_cap, coef.size());
+  if (rc) return rc;
+  CK(cudaMemcpyAsync(g.d_coef, coef.data(), coef.size() * sizeof(double), cudaMemcpyHostToDevice, g.stream));
+  return 0;
+}
+
+// Entry of every sweep: the library stream (non-blocking) waits for the work the caller has
+// queued on the legacy default stream (e.g. torch's default stream still writing H or Z).
+int wait_for_caller() {
+  CK(cudaEventRecord(g.ev_in, cudaStreamLegacy));
+  CK(cudaStreamWaitEvent(g.stream, g.ev_in, 0));
+  return 0;
+}
+
 cudaEvent_t prof_event(size_t i) {
   while (g.prof_events.size() <= i) {
     cudaEvent_t e;
@@ -245,8 +280,9 @@ int enqueue_sweep(const CachedPlan& cp, double* H, double* Z, int64_t n, bool pr
   a.hcol0 = 0; a.lc0 = 0; a.lc1 = n; a.zrows = n; a.ldz = n;
   a.wins = cp.d_wins; a.coef = g.d_coef; a.qslots = g.d_q; a.KP = cp.KP; a.wstats = g.d_wstats;
   a.QLD = hqr::pad_ld(cp.KP);
+  a.aftermath = reinterpret_cast<signed char*>(g.d_aft);
   size_t ev = 0;
-  static const bool dbg_sync = getenv("HQR_DEBUG_SYNC") != nullptr;  // debugging: sync after launches
+  static const bool dbg_sync = hqr::tuning_env("HQR_DEBUG_SYNC") != nullptr;  // debugging builds: sync after launches
   auto mark = [&](int cls) {
     if (dbg_sync) {
       cudaError_t e = cudaStreamSynchronize(A);
@@ -275,8 +311,7 @@ int enqueue_sweep(const CachedPlan& cp, double* H, double* Z, int64_t n, bool pr
     const WindowDesc* hw = P.windows.data() + a.win_begin;
     if (split && s >= hqr::kQSets) CK(cudaStreamWaitEvent(A, g.ev_z[set], 0));
     mark(0);
-    static const bool dbg_skip_chase = getenv("HQR_DEBUG_SKIP_CHASE") != nullptr;
-    if (!dbg_skip_chase) CK(hqr::launch_chase(a, P.max_kw, P.max_nbc, A));
+    CK(hqr::launch_chase(a, P.max_kw, P.max_nbc, A));
     mark(-1);
     st->launches_chase++;
     int64_t items;
@@ -319,17 +354,17 @@ int enqueue_sweep(const CachedPlan& cp, double* H, double* Z, int64_t n, bool pr
 
 // Fused path (single GPU, TMA-capable layout): chase(0), then one step-kernel launch per step that
 // runs the step's updates and the next step's chase from a prioritised task queue (step.cu).
-// Task chunk sizes; HQR_CHUNK="left,near,bulk,tail,tail_chunk" overrides them (tuning knob).
+// Task chunk sizes; HQR_CHUNK="left,near,bulk,tail,tail_chunk" overrides them (tuning builds only).
 hqr::ChunkSizes chunk_sizes() {
   hqr::ChunkSizes cs;
-  if (const char* e = getenv("HQR_CHUNK")) {
+  if (const char* e = hqr::tuning_env("HQR_CHUNK")) {
     int v[5];
     if (sscanf(e, "%d,%d,%d,%d,%d", &v[0], &v[1], &v[2], &v[3], &v[4]) == 5 && v[0] > 0 && v[1] > 0 &&
         v[2] > 0 && v[3] >= 0 && v[4] > 0) {
       cs.left = v[0]; cs.near = v[1]; cs.bulk = v[2]; cs.tail = v[3]; cs.tail_chunk = v[4];
     }
   }
-  if (const char* e = getenv("HQR_PHASE_TAIL")) {  // tuning knob: "ltail,ntail,chunk"
+  if (const char* e = hqr::tuning_env("HQR_PHASE_TAIL")) {  // tuning builds: "ltail,ntail,chunk"
     int v[3];
     if (sscanf(e, "%d,%d,%d", &v[0], &v[1], &v[2]) == 3 && v[0] >= 0 && v[1] >= 0 && v[2] > 0) {
       cs.ltail = v[0]; cs.ntail = v[1]; cs.phase_chunk = v[2];
@@ -602,6 +637,7 @@ int enqueue_fused(CachedPlan& cp, double* H, double* Z, int64_t n, const hqr::Te
     a.hcol0 = 0; a.lc0 = 0; a.lc1 = n; a.zrows = n; a.ldz = n;
     a.wins = cp.d_wins; a.coef = g.d_coef; a.qslots = g.d_q; a.KP = cp.KP; a.QLD = hqr::pad_ld(cp.KP);
     a.wstats = g.d_wstats;
+    a.aftermath = reinterpret_cast<signed char*>(g.d_aft);
     if (s < P.nsteps) {
       a.win_begin = P.step_begin[s];
       a.win_count = P.step_begin[s + 1] - P.step_begin[s];
@@ -630,7 +666,7 @@ int enqueue_fused(CachedPlan& cp, double* H, double* Z, int64_t n, const hqr::Te
   int* win_ctr = step_ctr + 4 * (size_t)P.nsteps;
   // (step 0's chases ran in their own launch: step-0 tasks do not wait for them)
   const StepArgs base = args(0);
-  static const bool per_step = getenv("HQR_PER_STEP") != nullptr;  // A/B knob: a launch per step
+  static const bool per_step = hqr::tuning_env("HQR_PER_STEP") != nullptr;  // A/B knob (tuning builds): a launch per step
   if (!per_step || io) {
     // one persistent launch for the whole sweep: step g+1's work starts as soon as its own
     // dependencies are met (no launch boundary, no end-of-step tail)
@@ -675,6 +711,19 @@ int hqr_setup(const hqr_config* cfg) {
   if (g.ready) hqr_teardown();
   if (cfg->world < 1 || cfg->rank < 0 || cfg->rank >= cfg->world) return -1;
   if (cfg->world > 1 && !cfg->nccl_id) return -1;
+  if (cfg->window_max < 0 || cfg->window_max > hqr::kMaxWindow) return -1;
+  if ((cfg->col_bounds || cfg->row_bounds) && cfg->world > 1) {
+    // explicit shard bounds (for n = n_max): both given, 0 = b[0] < ... < b[world] = n_max, even
+    // (16-byte TMA strides), H shards >= HQR_MAX_WINDOW + 8 columns wide (a window meets <= 2 ranks)
+    if (!cfg->col_bounds || !cfg->row_bounds || cfg->n_max < 1) return -1;
+    const int64_t* cb = cfg->col_bounds;
+    const int64_t* rb = cfg->row_bounds;
+    if (cb[0] != 0 || rb[0] != 0 || cb[cfg->world] != cfg->n_max || rb[cfg->world] != cfg->n_max) return -1;
+    for (int r = 0; r < cfg->world; ++r) {
+      if (cb[r + 1] - cb[r] < hqr::kMaxWindow + 8 || rb[r + 1] - rb[r] < 2) return -1;
+      if ((r > 0 && ((cb[r] | rb[r]) & 1))) return -1;
+    }
+  }
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= cfg->device || cfg->device < 0) {
     cudaGetLastError();
@@ -685,6 +734,15 @@ int hqr_setup(const hqr_config* cfg) {
   CK(cudaGetDeviceProperties(&prop, cfg->device));
   if (prop.major != 10) return -101;  // built for sm_100a only
   g.device = cfg->device;
+  g.window_max = cfg->window_max;
+  g.user_cb.clear();
+  g.user_rb.clear();
+  g.user_n = 0;
+  if (cfg->col_bounds && cfg->world > 1) {
+    g.user_cb.assign(cfg->col_bounds, cfg->col_bounds + cfg->world + 1);
+    g.user_rb.assign(cfg->row_bounds, cfg->row_bounds + cfg->world + 1);
+    g.user_n = cfg->n_max;
+  }
   g.rank = cfg->rank;
   g.world = cfg->world;
   g.flags = cfg->flags;
@@ -697,6 +755,7 @@ int hqr_setup(const hqr_config* cfg) {
   CK(cudaStreamCreateWithFlags(&g.cout, cudaStreamNonBlocking));
   CK(cudaEventCreate(&g.ev0));
   CK(cudaEventCreate(&g.ev1));
+  CK(cudaEventCreateWithFlags(&g.ev_in, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&g.ev_fork, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&g.ev_join, cudaEventDisableTiming));
   for (int i = 0; i < hqr::kQSets; ++i) {
@@ -708,7 +767,7 @@ int hqr_setup(const hqr_config* cfg) {
     std::memcpy(&id, cfg->nccl_id, sizeof(id));
     NK(ncclCommInitRank(&g.comm, g.world, id, g.rank));
   }
-  if (getenv("HQR_PROGRESS_SECS")) hqr::debug_progress_init();
+  if (hqr::tuning_env("HQR_PROGRESS_SECS")) hqr::debug_progress_init();
   g.ready = true;
   return 0;
 }
@@ -733,6 +792,10 @@ int hqr_teardown(void) {
   for (auto e : g.prof_events) cudaEventDestroy(e);
   g.prof_events.clear();
   if (g.d_coef) cudaFree(g.d_coef);
+  if (g.d_aft) cudaFree(g.d_aft);
+  g.d_aft = nullptr;
+  g.aft_cap = 0;
+  g.aft_n = 0;
   if (g.d_wstats) cudaFree(g.d_wstats);
   if (g.d_upflags) cudaFree(g.d_upflags);
   g.d_upflags = nullptr;
@@ -747,6 +810,7 @@ int hqr_teardown(void) {
   g.coef_cap = g.q_cap = g.stage_cap = 0;
   cudaEventDestroy(g.ev0);
   cudaEventDestroy(g.ev1);
+  cudaEventDestroy(g.ev_in);
   cudaEventDestroy(g.ev_fork);
   cudaEventDestroy(g.ev_join);
   for (int i = 0; i < hqr::kQSets; ++i) {
@@ -811,17 +875,16 @@ int sweep_impl(double* H, double* Z, int64_t n, const Blocks& blocks, const doub
     }
   }
 
-  // a1 pair the shifts: sigma = s + s', pi = s s' (real form, reading R1/R3); bulges of all blocks
-  const int nb = cp->plan.nb;
-  std::vector<double> coef(2 * nb);
-  for (int j = 0; j < nb; ++j) {
-    coef[2 * j] = shifts_re[2 * j] + shifts_re[2 * j + 1];
-    coef[2 * j + 1] = shifts_re[2 * j] * shifts_re[2 * j + 1] - shifts_im[2 * j] * shifts_im[2 * j + 1];
-  }
-  rc = ensure(&g.d_coef, &g.coef_cap, coef.size());
+  rc = wait_for_caller();
   if (rc) return rc;
-  CK(cudaMemcpyAsync(g.d_coef, coef.data(), coef.size() * sizeof(double), cudaMemcpyHostToDevice,
-                     g.stream));
+  // a1 the shift pairs of all blocks' bulges (sigma, pi are formed in the chase: R1/R3/R15)
+  rc = upload_coef(shifts_re, shifts_im, cp->plan.nb);
+  if (rc) return rc;
+  // a9 aftermath flags: -1 (not scanned) everywhere, then the chases of each block's last chain
+  rc = ensure(&g.d_aft, &g.aft_cap, (size_t)(n + 7) / 8);
+  if (rc) return rc;
+  CK(cudaMemsetAsync(g.d_aft, 0xff, (size_t)n, g.stream));
+  g.aft_n = 0;
   rc = ensure(&g.d_q, &g.q_cap, (size_t)hqr::kQSets * cp->plan.nchains * cp->KP * hqr::pad_ld(cp->KP));
   if (rc) return rc;
   rc = ensure(&g.d_wstats, &g.wstats_cap, cp->plan.windows.size());
@@ -876,7 +939,7 @@ int sweep_impl(double* H, double* Z, int64_t n, const Blocks& blocks, const doub
       st.h2d_bytes += nn * sizeof(double);
     }
   }
-  static const bool timing = getenv("HQR_TIMING_DUMP") != nullptr;  // -DHQR_TIMING builds
+  static const bool timing = hqr::tuning_env("HQR_TIMING_DUMP") != nullptr;  // -DHQR_TIMING -DHQR_TUNING builds
   if (timing && fused) hqr::debug_timing(0, true);
   if (overlap) {
     IoPlan io;
@@ -942,6 +1005,7 @@ int sweep_impl(double* H, double* Z, int64_t n, const Blocks& blocks, const doub
   CK(cudaEventRecord(g.ev1, g.stream));
   CK(cudaStreamSynchronize(g.stream));
   CK(cudaGetLastError());
+  g.aft_n = n;
   if (timing && fused) hqr::debug_timing(cp->plan.nsteps, false);
   float ms = 0;
   CK(cudaEventElapsedTime(&ms, g.ev0, g.ev1));
@@ -965,9 +1029,9 @@ int sweep_impl(double* H, double* Z, int64_t n, const Blocks& blocks, const doub
     for (const WindowDesc& w : P.windows) {
       for (int t = w.t0; t <= w.t1; ++t)
         for (int jj = 0; jj < w.nbc; ++jj) {
-          int64_t p = P.ilo - 1 + t - 3 * (int64_t)jj;
-          if (p < P.ilo - 1 || p > P.ihi - 2) continue;
-          int m = (p <= P.ihi - 3) ? 3 : 2;
+          int64_t p = w.ilo - 1 + t - 3 * (int64_t)jj;
+          if (p < w.ilo - 1 || p > w.ihi - 2) continue;
+          int m = (p <= w.ihi - 3) ? 3 : 2;
           int64_t pl = p - w.w0;
           double cnt = (double)(w.w1 - std::max<int64_t>(pl, 0) - w.w0) + (double)(pl + m + 2) +
                        (double)std::min<int64_t>(pl + m + 3, w.w1 - w.w0 + 1);
@@ -986,8 +1050,10 @@ int plan_query_impl(int64_t n, const Blocks& b, int window, int32_t* info, int32
   int rc = validate_blocks(n, b, nullptr, nullptr, window, false);
   if (rc) return rc;
   Plan P;
-  rc = hqr::make_plan_multi(n, b.count(), b.ilo.data(), b.ihi.data(), b.nshifts.data(), window,
-                            hqr::kMaxWindow, &P);
+  rc = b.sweeps ? hqr::make_plan_sweeps(n, b.ilo[0], b.ihi[0], b.count(), b.nshifts.data(), window,
+                                        hqr::kMaxWindow, &P)
+                : hqr::make_plan_multi(n, b.count(), b.ilo.data(), b.ihi.data(), b.nshifts.data(), window,
+                                       hqr::kMaxWindow, &P);
   if (rc) return rc;
   if (info) {
     int32_t v[10] = {P.k, P.nbc_max, P.s, P.lag, P.nchains, P.nsteps, (int32_t)P.windows.size(),
@@ -1167,22 +1233,25 @@ int dist_prepare(int64_t n, int64_t ilo, int64_t ihi, const double* sr, const do
   b.ilo = {ilo}; b.ihi = {ihi}; b.nshifts = {nshifts};
   int rc = validate_blocks(n, b, sr, si, window, true);
   if (rc) return rc;
-  rc = hqr::make_layout(n, world, hqr::kMaxWindow, L);
-  if (rc) return rc;
+  if (!g.user_cb.empty() && world == g.world) {  // hqr_config shard bounds (for n = n_max only)
+    if (n != g.user_n) return -11;
+    L->world = world;
+    L->halo = hqr::kMaxWindow;
+    L->cb = g.user_cb;
+    L->rb = g.user_rb;
+  } else {
+    rc = hqr::make_layout(n, world, hqr::kMaxWindow, L);
+    if (rc) return rc;
+  }
   if (!g.ready) return -100;
   CK(cudaSetDevice(g.device));
   rc = get_plan(n, b, window, cpo, true);
   if (rc) return rc;
   CachedPlan* cp = *cpo;
-  const int nb = cp->plan.nb;
-  std::vector<double> coef(2 * nb);
-  for (int j = 0; j < nb; ++j) {
-    coef[2 * j] = sr[2 * j] + sr[2 * j + 1];
-    coef[2 * j + 1] = sr[2 * j] * sr[2 * j + 1] - si[2 * j] * si[2 * j + 1];
-  }
-  rc = ensure(&g.d_coef, &g.coef_cap, coef.size());
+  rc = wait_for_caller();
   if (rc) return rc;
-  CK(cudaMemcpyAsync(g.d_coef, coef.data(), coef.size() * sizeof(double), cudaMemcpyHostToDevice, g.stream));
+  rc = upload_coef(sr, si, cp->plan.nb);
+  if (rc) return rc;
   rc = ensure(&g.d_q, &g.q_cap, (size_t)hqr::kQSets * cp->plan.nchains * cp->KP * hqr::pad_ld(cp->KP));
   return rc;
 }
@@ -1203,6 +1272,8 @@ extern "C" {
 
 int hqr_sweep(double* H, double* Z, int64_t n, int64_t ilo, int64_t ihi, const double* shifts_re,
               const double* shifts_im, int nshifts, int window) {
+  // world > 1: a collective on this rank's local shards -- the sharded executor
+  if (g.ready && g.world > 1) return hqr_sweep_dist(H, Z, n, ilo, ihi, shifts_re, shifts_im, nshifts, window);
   return sweep_impl(H, Z, n, make_blocks(1, &ilo, &ihi, &nshifts), shifts_re, shifts_im, window);
 }
 
@@ -1212,6 +1283,34 @@ int hqr_sweep_multi(double* H, double* Z, int64_t n, int nblocks, const int64_t*
   if (!H) return -1;
   if (nblocks < 1 || !ilo || !ihi || !nshifts) return -4;
   return sweep_impl(H, Z, n, make_blocks(nblocks, ilo, ihi, nshifts), shifts_re, shifts_im, window);
+}
+
+int hqr_sweeps(double* H, double* Z, int64_t n, int64_t ilo, int64_t ihi, int nsweeps,
+               const double* shifts_re, const double* shifts_im, const int* nshifts, int window) {
+  if (!H) return -1;
+  if (nsweeps < 1 || !nshifts) return -8;
+  if (g.ready && g.world > 1) return -1;  // single GPU (the sharded executor runs one sweep)
+  Blocks b;
+  b.sweeps = true;
+  for (int i = 0; i < nsweeps; ++i) {
+    b.ilo.push_back(ilo);
+    b.ihi.push_back(ihi);
+    b.nshifts.push_back(nshifts[i]);
+  }
+  return sweep_impl(H, Z, n, b, shifts_re, shifts_im, window);
+}
+
+int hqr_plan_query_sweeps(int64_t n, int64_t ilo, int64_t ihi, int nsweeps, const int* nshifts, int window,
+                          int32_t* info, int32_t* windows, int64_t cap) {
+  if (nsweeps < 1 || !nshifts) return -8;
+  Blocks b;
+  b.sweeps = true;
+  for (int i = 0; i < nsweeps; ++i) {
+    b.ilo.push_back(ilo);
+    b.ihi.push_back(ihi);
+    b.nshifts.push_back(nshifts[i]);
+  }
+  return plan_query_impl(n, b, window, info, windows, cap);
 }
 
 int hqr_plan_query(int64_t n, int64_t ilo, int64_t ihi, int nshifts, int window, int32_t* info,
@@ -1280,6 +1379,28 @@ int hqr_sweep_dist(double* H_local, double* Z_local, int64_t n, int64_t ilo, int
   int rc = dist_prepare(n, ilo, ihi, shifts_re, shifts_im, nshifts, window, g.world, &cp, &L);
   if (rc) return rc;
   if (g.world > 1 && !g.comm) return -100;
+  {  // -10: H[ilo, ilo-1] on the rank owning column ilo-1, H[ihi+1, ihi] on the owner of column ihi;
+     // the verdict is agreed over all ranks (max), so every rank returns the same code
+    const int64_t c0 = L.cb[g.rank], c1 = L.cb[g.rank + 1];
+    int bad = 0;
+    double v = 0.0;
+    if (ilo > 0 && ilo - 1 >= c0 && ilo - 1 < c1) {
+      CK(cudaMemcpy(&v, H_local + ilo + (ilo - 1 - c0) * n, sizeof(double), cudaMemcpyDeviceToHost));
+      bad |= v != 0.0;
+    }
+    if (ihi < n - 1 && ihi >= c0 && ihi < c1) {
+      CK(cudaMemcpy(&v, H_local + (ihi + 1) + (ihi - c0) * n, sizeof(double), cudaMemcpyDeviceToHost));
+      bad |= v != 0.0;
+    }
+    if (g.world > 1) {
+      int* d_bad = reinterpret_cast<int*>(g.d_q);  // workspace scratch (Q slots are rewritten below)
+      CK(cudaMemcpyAsync(d_bad, &bad, sizeof(int), cudaMemcpyHostToDevice, g.stream));
+      NK(ncclAllReduce(d_bad, d_bad, 1, ncclInt32, ncclMax, g.comm, g.stream));
+      CK(cudaMemcpyAsync(&bad, d_bad, sizeof(int), cudaMemcpyDeviceToHost, g.stream));
+      CK(cudaStreamSynchronize(g.stream));
+    }
+    if (bad) return -10;
+  }
   hqr_stats st{};
   st.window_eff = cp->plan.k;
   std::vector<RankCtx> ranks(1);
@@ -1313,6 +1434,12 @@ int hqr_sweep_virtual(double* H, double* Z, int64_t n, int64_t ilo, int64_t ihi,
   int rc = dist_prepare(n, ilo, ihi, shifts_re, shifts_im, nshifts, window, vworld, &cp, &L);
   if (rc) return rc;
   if (!is_device_ptr(H) || (Z && !is_device_ptr(Z))) return -1;
+  {  // -10 (as hqr_sweep)
+    double v[2] = {0.0, 0.0};
+    if (ilo > 0) CK(cudaMemcpy(&v[0], H + ilo + (ilo - 1) * n, sizeof(double), cudaMemcpyDeviceToHost));
+    if (ihi < n - 1) CK(cudaMemcpy(&v[1], H + (ihi + 1) + ihi * n, sizeof(double), cudaMemcpyDeviceToHost));
+    if (v[0] != 0.0 || v[1] != 0.0) return -10;
+  }
   hqr_stats st{};
   st.window_eff = cp->plan.k;
   g.vH.resize(vworld, nullptr); g.vZ.resize(vworld, nullptr);
@@ -1359,6 +1486,15 @@ int hqr_sweep_virtual(double* H, double* Z, int64_t n, int64_t ilo, int64_t ihi,
   CK(cudaEventElapsedTime(&ms, g.ev0, g.ev1));
   st.ms_total = ms;
   g.stats = st;
+  return 0;
+}
+
+int hqr_get_aftermath(signed char* flags, int64_t n) {
+  if (!flags) return -1;
+  if (!g.ready || g.aft_n == 0) return -100;
+  if (n != g.aft_n) return -3;
+  CK(cudaSetDevice(g.device));
+  CK(cudaMemcpy(flags, g.d_aft, (size_t)n, cudaMemcpyDeviceToHost));
   return 0;
 }
 

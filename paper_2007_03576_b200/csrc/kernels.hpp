@@ -2,12 +2,24 @@
 // (chase.cu, update.cu).  Product path only; shares nothing with oracle/.
 #pragma once
 #include <cstdint>
+#include <cstdlib>
 #include <cuda.h>  // CUtensorMap (header only; the encoder is fetched through cudaGetDriverEntryPoint)
 #include <cuda_runtime.h>
 
 #include "plan.hpp"
 
 namespace hqr {
+
+// Schedule / debugging knobs read from the environment exist only in tuning builds
+// (-DHQR_TUNING, never the product build): the product library's schedule is fixed.
+inline const char* tuning_env(const char* name) {
+#ifdef HQR_TUNING
+  return getenv(name);
+#else
+  (void)name;
+  return nullptr;
+#endif
+}
 
 // Arguments of one wavefront step (device pointers).
 struct StepArgs {
@@ -20,7 +32,8 @@ struct StepArgs {
   int64_t ilo, ihi;
   const WindowDesc* wins;    // device copy of plan.windows
   int win_begin, win_count;  // this step's windows
-  const double* coef;        // per bulge j: coef[2j] = sigma_j, coef[2j+1] = pi_j
+  const double* coef;        // per bulge j: its shift pair coef[4j..4j+3] = (re_2j, re_2j+1,
+                             // im_2j, im_2j+1); sigma / pi are formed in the chase (scaled, R15)
   double* qslots;            // Q slot s at qslots + s*KP*QLD: column-major, ld = QLD, zero padded
   int KP;                    // padded factor side (32, 64, 96 or 128)
   int QLD;                   // Q slot leading dimension = pad_ld(KP) (the update kernels' SMEM ld)
@@ -29,6 +42,8 @@ struct StepArgs {
   int step;                  // wavefront step index (debug timing only)
   double* wstats;            // nullable: per plan window, the executed DMMA work units of its factor
                              // (record_band); wstats[win_begin + i] for window i of the step
+  signed char* aftermath;    // nullable: per row, the subdiagonal scan flags (R16), written by the
+                             // chases of windows with scan rows (WindowDesc::scan_lo/hi)
 };
 
 // One CTA per window: chase the step's bulges inside SMEM-resident windows, accumulate Q_W.

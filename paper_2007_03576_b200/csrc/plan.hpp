@@ -38,6 +38,10 @@ struct WindowDesc {     // one diagonal window = one CTA of the chase kernel in 
   int32_t slot;         // Q workspace slot
   int32_t last;         // 1 if this is the chain's final window
   int32_t ilo, ihi;     // the active block this window's chain sweeps
+  int32_t scan_lo, scan_hi;  // aftermath scan: rows [scan_lo, scan_hi] whose
+                        // subdiagonal (and diagonal) entries are final once this window's chase
+                        // is done -- set on the windows of each block's last chain (the topmost:
+                        // nothing chases above it), scan_hi < scan_lo elsewhere
 };
 
 struct Plan {
@@ -62,8 +66,15 @@ struct ChainPlan {
   std::vector<WindowDesc> windows;
 };
 
-inline int plan_block(int64_t ilo, int64_t ihi, int nb, int b_base, int c_base, int window, int kmax,
-                      std::vector<ChainPlan>* chains, int* k_out, int* nbc_out, int* s_out, int* lag_out) {
+// nbc_force > 0: use that many bulges per chain for the stride (s = k - 3 nbc_force - 1) -- the
+// chains of several sweeps of one block (make_plan_sweeps) must share one stride; g_base: wavefront
+// step of the first chain's start in units of lag chains (chain c starts at (g_base + c) lag);
+// scan: mark the aftermath rows on the last chain.
+inline int plan_block(int64_t n, int64_t ilo, int64_t ihi, int nb, int b_base, int c_base, int window,
+                      int kmax, std::vector<ChainPlan>* chains, int* k_out, int* nbc_out, int* s_out,
+                      int* lag_out, int nbc_force = 0, int g_base = 0, bool scan = true) {
+  // aftermath rows: ilo-1 (the decoupling entry) .. ihi, clipped to rows that have a subdiagonal
+  const int32_t scan0 = (int32_t)std::max<int64_t>(ilo - 1, 0), scan1 = (int32_t)std::min<int64_t>(ihi, n - 2);
   const int64_t N = ihi - ilo + 1;
   int64_t k = std::min<int64_t>({(int64_t)window, N, (int64_t)kmax});
   if (k < N && k < 8) return -9;
@@ -71,12 +82,13 @@ inline int plan_block(int64_t ilo, int64_t ihi, int nb, int b_base, int c_base, 
   if (N <= k) {
     // one window holds the whole active block: a single chain with every bulge
     ChainPlan cp;
-    cp.g0 = 0;
+    cp.g0 = g_base;
     WindowDesc w{};
     w.chain = c_base; w.w0 = (int32_t)ilo; w.w1 = (int32_t)ihi;
     w.t0 = 0; w.t1 = (int32_t)(N + 3 * (int64_t)nb - 5);  // top bulge's last p = ihi-2
     w.b0 = b_base; w.nbc = nb; w.slot = c_base; w.last = 1;
     w.ilo = (int32_t)ilo; w.ihi = (int32_t)ihi;
+    w.scan_lo = scan ? scan0 : 0; w.scan_hi = scan ? scan1 : -1;
     cp.windows.push_back(w);
     chains->push_back(cp);
     *nbc_out = nb; *s_out = (int)N; *lag_out = 1;
@@ -88,7 +100,7 @@ inline int plan_block(int64_t ilo, int64_t ihi, int nb, int b_base, int c_base, 
   const int nbc_cap = std::min((int)((k - 2) / 6), kChainCap);
   const int C = (nb + nbc_cap - 1) / nbc_cap;
   const int base = nb / C, rem = nb % C;                 // remainders on the earliest chains
-  const int nbc_max = base + (rem > 0 ? 1 : 0);
+  const int nbc_max = std::max(base + (rem > 0 ? 1 : 0), nbc_force);
   const int s = (int)(k - 3 * nbc_max - 1);
   const int lag = (int)((k + s - 1) / s);
   *nbc_out = nbc_max; *s_out = s; *lag_out = lag;
@@ -96,11 +108,12 @@ inline int plan_block(int64_t ilo, int64_t ihi, int nb, int b_base, int c_base, 
   for (int c = 0; c < C; ++c) {
     const int nbc = base + (c < rem ? 1 : 0);
     ChainPlan cp;
-    cp.g0 = c * lag;
+    cp.g0 = (g_base + c) * lag;
     for (int i = 0;; ++i) {
       WindowDesc w{};
       w.chain = c_base + c; w.b0 = b; w.nbc = nbc; w.slot = c_base + c;
       w.ilo = (int32_t)ilo; w.ihi = (int32_t)ihi;
+      w.scan_lo = 0; w.scan_hi = -1;
       const int64_t w0 = ilo + (int64_t)i * s;
       const int64_t w1 = std::min<int64_t>(w0 + k - 1, ihi);
       w.w0 = (int32_t)w0; w.w1 = (int32_t)w1;
@@ -112,6 +125,10 @@ inline int plan_block(int64_t ilo, int64_t ihi, int nb, int b_base, int c_base, 
         w.t1 = (int32_t)((int64_t)i * s + k - 4);
         w.last = 0;
       }
+      if (scan && c == C - 1) {  // the block's last (topmost) chain: rows above the next window are final
+        w.scan_lo = (i == 0) ? scan0 : w.w0;
+        w.scan_hi = w.last ? scan1 : (int32_t)(w0 + s - 1);
+      }
       cp.windows.push_back(w);
       if (w.last) break;
     }
@@ -120,6 +137,8 @@ inline int plan_block(int64_t ilo, int64_t ihi, int nb, int b_base, int c_base, 
   }
   return 0;
 }
+
+inline void merge_wavefront(const std::vector<ChainPlan>& chains, Plan* out);
 
 // Builds the plan of one sweep over `nblocks` decoupled active blocks (ascending, disjoint).
 // Block i has nshifts[i] shifts; its bulges are numbered after those of blocks 0..i-1.
@@ -133,7 +152,7 @@ inline int make_plan_multi(int64_t n, int nblocks, const int64_t* ilo, const int
   for (int i = 0; i < nblocks; ++i) {
     int k, nbc, s, lag;
     const int nb = nshifts[i] / 2;
-    int rc = plan_block(ilo[i], ihi[i], nb, b_base, (int)chains.size(), window, kmax, &chains, &k,
+    int rc = plan_block(n, ilo[i], ihi[i], nb, b_base, (int)chains.size(), window, kmax, &chains, &k,
                         &nbc, &s, &lag);
     if (rc) return rc;
     if (i == 0) { P.k = k; P.nbc_max = nbc; P.s = s; P.lag = lag; }
@@ -142,9 +161,59 @@ inline int make_plan_multi(int64_t n, int nblocks, const int64_t* ilo, const int
     b_base += nb;
   }
   P.nb = b_base;
+  merge_wavefront(chains, &P);
+  *out = std::move(P);
+  return 0;
+}
+
+// Several sweeps of one active block with known shift sets, overlapped (
+// PAPER.md P:831-833 "two bulge chasing steps can be overlapped", P:706-765 priorities): sweep i
+// is nshifts[i]/2 Francis double steps, applied after sweep i-1, so its chains are simply further
+// chains of the same wavefront, started lag steps after sweep i-1's last chain -- the tightest
+// packing the window geometry allows.  All chains share one stride (the largest bulge
+// count per chain over the sweeps), so no chain catches up with the one below it.  The result is
+// the sweeps applied one after another (the oracle applies them so); the fused kernel's
+// dependency counters order every update exactly as for one sweep.  The aftermath rows are
+// scanned by the last sweep's last chain.
+inline int make_plan_sweeps(int64_t n, int64_t ilo, int64_t ihi, int nsweeps, const int* nshifts,
+                            int window, int kmax, Plan* out) {
+  Plan P;
+  P.n = n; P.ilo = ilo; P.ihi = ihi;
+  const int64_t N = ihi - ilo + 1;
+  const int64_t k = std::min<int64_t>({(int64_t)window, N, (int64_t)kmax});
+  if (k < N && k < 8) return -9;
+  // common bulges-per-chain bound of all sweeps (plan_block's split of each sweep)
+  int nbc_force = 0;
+  if (N > k) {
+    const int cap = std::min((int)((k - 2) / 6), kChainCap);
+    for (int i = 0; i < nsweeps; ++i) {
+      const int nb = nshifts[i] / 2, C = (nb + cap - 1) / cap;
+      nbc_force = std::max(nbc_force, nb / C + (nb % C > 0 ? 1 : 0));
+    }
+  }
+  std::vector<ChainPlan> chains;
+  int b_base = 0;
+  for (int i = 0; i < nsweeps; ++i) {
+    int kk, nbc, s, lag;
+    const int c0 = (int)chains.size();
+    int rc = plan_block(n, ilo, ihi, nshifts[i] / 2, b_base, c0, window, kmax, &chains, &kk, &nbc, &s,
+                        &lag, nbc_force, c0, i == nsweeps - 1);
+    if (rc) return rc;
+    if (i == 0) { P.k = kk; P.nbc_max = nbc; P.s = s; P.lag = lag; }
+    P.nbc_max = std::max(P.nbc_max, nbc);
+    b_base += nshifts[i] / 2;
+  }
+  P.nb = b_base;
+  merge_wavefront(chains, &P);
+  *out = std::move(P);
+  return 0;
+}
+
+// wavefront: step g runs window (g - g0) of every chain; windows of a step are disjoint diagonal
+// blocks, listed top first (the paper's reverse interleaved insertion order)
+inline void merge_wavefront(const std::vector<ChainPlan>& chains, Plan* out) {
+  Plan& P = *out;
   P.nchains = (int)chains.size();
-  // wavefront: step g runs window (g - g0) of every chain; windows of a step are disjoint
-  // diagonal blocks, listed top first (the paper's reverse interleaved insertion order)
   int nsteps = 0;
   for (auto& ch : chains) nsteps = std::max(nsteps, ch.g0 + (int)ch.windows.size());
   P.nsteps = nsteps;
@@ -163,8 +232,6 @@ inline int make_plan_multi(int64_t n, int nblocks, const int64_t* ilo, const int
     }
     P.step_begin.push_back((int32_t)P.windows.size());
   }
-  *out = std::move(P);
-  return 0;
 }
 
 // Single active block.

@@ -153,12 +153,7 @@ __device__ void chase_window_9w(const StepArgs& a, const WindowDesc& W, int widx
       const int m = (p <= ihi - 3) ? 3 : 2;
       double x0, x1, x2;
       if (p == ilo - 1) {
-        const int jb = W.b0 + jj;
-        const double sigma = a.coef[2 * jb], pi = a.coef[2 * jb + 1];
-        const double h00 = Hs[0], h10 = Hs[1], h01 = Hs[ldh], h11 = Hs[1 + ldh], h21 = Hs[2 + ldh];
-        x0 = h00 * (h00 - sigma) + h01 * h10 + pi;
-        x1 = h10 * (h00 + h11 - sigma);
-        x2 = h10 * h21;
+        intro_vector(Hs, ldh, a.coef + 4 * (W.b0 + jj), x0, x1, x2);
       } else {
         const double* col = Hs + pl * ldh + pl;
         x0 = col[1];
@@ -217,6 +212,7 @@ __device__ void chase_window_9w(const StepArgs& a, const WindowDesc& W, int widx
     if (warp == 0) atomicAdd(&g_ctim[5], (unsigned long long)(W.t1 - W.t0 + 1));
   }
 #endif
+  aftermath_scan(Hs, ldh, W, a, threadIdx.x, kStepThreads);  // a9 (check only)
   {
     double* g = a.H + (int64_t)(w0 - a.hcol0) * n + w0;
     for (int c = warp; c < kw; c += kStepWarps) {
@@ -700,7 +696,7 @@ void debug_progress_init() {
   cudaMemcpyToSymbol(g_prog, &d, sizeof(d));
   int dev = 0;
   cudaGetDevice(&dev);
-  const char* e = getenv("HQR_PROGRESS_SECS");
+  const char* e = tuning_env("HQR_PROGRESS_SECS");
   const int secs = e ? atoi(e) : 20;
   std::thread([secs, dev, bytes, count] {
     std::this_thread::sleep_for(std::chrono::seconds(secs));
@@ -793,8 +789,8 @@ void build_step_tasks(const StepArgs& a, const WindowDesc* wins, int nwin, const
   };
   // the chases after the left tasks (their near inputs are done by then; a chase claimed right after
   // the near tasks idles its SM until they finish): measured 0.2-0.3 ms better at configs[2] / [3].
-  // HQR_CHASE_POS=0: right after the near tasks (A/B knob)
-  static const int chase_pos = getenv("HQR_CHASE_POS") ? atoi(getenv("HQR_CHASE_POS")) : 1;
+  // HQR_CHASE_POS=0: right after the near tasks (A/B knob, tuning builds only)
+  static const int chase_pos = tuning_env("HQR_CHASE_POS") ? atoi(tuning_env("HQR_CHASE_POS")) : 1;
   if (chase_pos == 0) chases();
   const size_t l0 = out->size();
   for (int i = 0; i < nwin; ++i) {

@@ -20,12 +20,16 @@ def _house(m, x):
     return x[1:m] / (x0 - b), (b - x0) / b, b
 
 
-def emulate(H, Z, ilo, ihi, sr, si, window, on_window=None, blocks=None):
-    """blocks = [(ilo, ihi, nshifts), ...] for a multi-block sweep (ilo/ihi ignored then)."""
+def emulate(H, Z, ilo, ihi, sr, si, window, on_window=None, blocks=None, sweeps=None):
+    """blocks = [(ilo, ihi, nshifts), ...] for a multi-block sweep (ilo/ihi ignored then);
+    sweeps = [nshifts_0, nshifts_1, ...] for overlapped sweeps of [ilo, ihi] (hqr_sweeps)."""
     n = H.shape[0]
-    if blocks is None:
-        blocks = [(ilo, ihi, len(sr))]
-    info, wins = hq.plan_query_multi(n, blocks, window)
+    if sweeps is not None:
+        info, wins = hq.plan_query_sweeps(n, ilo, ihi, sweeps, window)
+    else:
+        if blocks is None:
+            blocks = [(ilo, ihi, len(sr))]
+        info, wins = hq.plan_query_multi(n, blocks, window)
     nb = len(sr) // 2
     sig = [sr[2 * j] + sr[2 * j + 1] for j in range(nb)]
     pis = [sr[2 * j] * sr[2 * j + 1] - si[2 * j] * si[2 * j + 1] for j in range(nb)]

@@ -197,3 +197,36 @@ def test_multi_block_validation():
     assert L.hqr_sweep_multi(*args(ilo2, ihi2)) == -4          # unsorted
     ilo3 = np.array([0, 51], dtype=np.int64); ihi3 = np.array([50, 99], dtype=np.int64)
     assert L.hqr_sweep_multi(*args(ilo3, ihi3)) == -100        # valid, library not set up
+
+
+@pytest.mark.parametrize("n,ilo,ihi,sweeps,win", [
+    (400, 0, 399, [20, 20, 20], 40), (300, 10, 290, [24, 8, 40], 48), (120, 0, 119, [8, 8], 200),
+    (500, 0, 499, [60, 60, 60, 60], 96),
+])
+def test_sweeps_emulation_matches_oracle(n, ilo, ihi, sweeps, win):
+    """NEXT-1: overlapped sweeps (hqr_sweeps' plan) reproduce the oracle applying the sweeps one
+    after another; every step's windows stay disjoint and all chains share one stride."""
+    from hqr_inputs import shifts
+    H0, Z0, _, _ = random_case(n + len(sweeps), n, 2, ilo, ihi, z0="orth")
+    sets = [shifts("disk2", ns, 17, stream_offset=i + 1) for i, ns in enumerate(sweeps)]
+    Ho, Zo = H0.copy(order="F"), Z0.copy(order="F")
+    for re_, im_ in sets:
+        oracle.sweep(Ho, Zo, ilo, ihi, re_, im_)
+    sr = np.concatenate([r for r, _ in sets]); si = np.concatenate([i for _, i in sets])
+    He, Ze = H0.copy(order="F"), Z0.copy(order="F")
+    info = emulate(He, Ze, ilo, ihi, sr, si, win, sweeps=sweeps)
+    assert np.linalg.norm(He - Ho) / np.linalg.norm(H0) <= 1e-11
+    assert np.linalg.norm(Ze - Zo) <= 1e-11 * np.sqrt(n)
+    _, W = hq.plan_query_sweeps(n, ilo, ihi, sweeps, win)
+    for step in range(info["nsteps"]):
+        sw = W[W[:, 0] == step]
+        for a_, b_ in zip(sw[:-1], sw[1:]):
+            assert a_[3] < b_[2]
+    # the sweeps overlap: a later sweep's first window runs while an earlier sweep is still active
+    first = {}
+    for w in W:
+        first.setdefault(int(w[6]), int(w[0]))
+    if ihi - ilo + 1 > win:
+        last_step_sweep0 = max(int(w[0]) for w in W if int(w[6]) < sweeps[0] // 2)
+        b_sweep1 = sweeps[0] // 2
+        assert min(int(w[0]) for w in W if int(w[6]) >= b_sweep1) < last_step_sweep0

@@ -257,33 +257,66 @@ def _gpu_invariants(Hd, Zd, H0d, Z0d, n):
     return orth, sim
 
 
-@pytest.mark.parametrize("cfg", [2, 3])
-def test_full_size_parity_against_oracle(cfg):
-    """BASELINE configs[2] (n = 10000) and configs[3] (n = 20000) in the bench's launch
-    configuration (default window), element by element against the oracle run on the host cores,
-    plus the invariants computed on the GPU.
+def _record_parity(key, rec):
+    """Append one full-size parity record to gpurun_out/parity_r02.json (copied to profiles/)."""
+    import json
+    import os
+    out = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "gpurun_out")
+    os.makedirs(out, exist_ok=True)
+    path = os.path.join(out, "parity_r02.json")
+    d = json.load(open(path)) if os.path.exists(path) else {}
+    d[key] = rec
+    with open(path, "w") as f:
+        json.dump(d, f, indent=1)
 
-    Tolerance (reading R14): max(1e-10, 2 x the oracle's own two-order noise floor).
-    At configs[3] two valid orders of the oracle itself differ by 5.3e-10 (H) / 3.7e-10 (Z)
-    (tests/golden/noise_floor.json, written by tools/noise_floor.py from oracle/ only): the 512
-    shifts lie inside the spectrum, a subdiagonal converges to 1e-11 during the sweep and bulges
-    crossing it lose accuracy locally, so 1e-10 is below the rounding floor of the problem."""
-    import torch
-    p = make(cfg, z_device="cuda")
+
+def _floor(key):
+    import json
+    import os
+    floor = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "noise_floor.json")))
+    return floor["configs"].get(key)
+
+
+FULL = [  # (record key, BASELINE config, shift kind override, tolerance rule)
+    ("2", 2, None, "1e-10"),
+    ("3", 3, None, "R14"),
+    ("3:ring68", 3, "ring68", "1e-10"),
+]
+
+
+@pytest.mark.parametrize("key,cfg,kind,rule", FULL, ids=[f[0] for f in FULL])
+def test_full_size_parity_against_oracle(key, cfg, kind, rule):
+    """BASELINE configs[2] (n = 10000) and configs[3] (n = 20000, 512 shifts) in the bench's launch
+    configuration (default window), element by element against the oracle run on the host cores,
+    plus the invariants computed on the GPU.  The measured differences and the oracle's own
+    two-order noise floor are recorded (gpurun_out/parity_r02.json -> profiles/).
+
+    Tolerance: the north_star's 1e-10, except configs[3] with its own shifts (rule R14):
+    there two valid orders of the oracle itself differ by 5.3e-10 (tests/golden/noise_floor.json,
+    tools/noise_floor.py, oracle/ only) -- the 512 shifts lie inside the spectrum, a subdiagonal
+    converges to 1e-11 during the sweep and bulges crossing it lose accuracy locally -- so there
+    the GPU must sit within 1.2 x that floor.  The same matrix with shifts outside the spectrum
+    ("3:ring68", floor far below 1e-10) is held at 1e-10."""
+    p = make(cfg, z_device="cuda", shift_kind=kind)
     n = p.H.shape[0]
     H0d, Z0d = hq.to_device(p.H), hq.to_device(p.Z)
     Hd = hq.to_device(p.H)
     Zd = hq.to_device(p.Z)
     hq.sweep(Hd, Zd, p.ilo, p.ihi, p.shifts_re, p.shifts_im, hq.DEFAULT_WINDOW)
-    _gpu_invariants(Hd, Zd, H0d, Z0d, n)
+    orth, sim = _gpu_invariants(Hd, Zd, H0d, Z0d, n)
     Hg, Zg = hq.from_device(Hd), hq.from_device(Zd)
     del Hd, Zd, H0d, Z0d
     Ho, Zo = oracle_sweep(p.H, p.Z, p.ilo, p.ihi, p.shifts_re, p.shifts_im)
-    import json
-    import os
-    floor = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "noise_floor.json")))
-    fl = floor["configs"][str(cfg)]
-    tol = max(TOL, 2.0 * max(fl["dH_rel_fro"], fl["dZ_fro_over_sqrt_n"]))
+    dh = float(np.linalg.norm(Hg - Ho) / np.linalg.norm(p.H))
+    dz = float(np.linalg.norm(Zg - Zo) / np.sqrt(n))
+    fl = _floor(key)
+    floor = max(fl["dH_rel_fro"], fl["dZ_fro_over_sqrt_n"]) if fl else None
+    tol = TOL if rule == "1e-10" else max(TOL, 1.2 * floor)
+    _record_parity(key, {"n": n, "nshifts": len(p.shifts_re), "window": hq.DEFAULT_WINDOW,
+                         "dH_rel_fro": dh, "dZ_fro_over_sqrt_n": dz, "dH_max": float(np.abs(Hg - Ho).max()),
+                         "oracle_floor": fl, "tolerance": tol, "rule": rule,
+                         "orth_ZtZ_minus_I": orth, "similarity_rel": sim,
+                         "min_abs_subdiag_gpu": float(np.abs(np.diag(Hg, -1)).min())})
     check(Hg, Zg, Ho, Zo, p.H, p.ilo, p.ihi, tol=tol)
 
 
@@ -318,3 +351,186 @@ def test_fused_step_kernel_matches_separate_launches(case):
         hq.teardown()
         hq.setup(0)
     assert np.array_equal(Hf, Hs) and np.array_equal(Zf, Zs)
+
+
+# ------------------------------------------------------------------------------------------------
+# round 2: aftermath scan (a9), scaled inputs (R15), degenerate reflectors, hess_n, entry ordering
+# ------------------------------------------------------------------------------------------------
+
+@pytest.mark.parametrize("case", [(80, 500, 40, 0, 499, 64), (81, 700, 60, 30, 650, 96),
+                                  (82, 60, 8, 5, 50, 112)])
+def test_aftermath_scan_bit_exact(case):
+    """a9: the flags the last chain's chases compute equal the oracle's scan of the
+    GPU's own H' bit for bit (same criterion, same precision), and the scan of the oracle's H'."""
+    seed, n, ns, ilo, ihi, win = case
+    H0, Z0, re_, im_ = random_case(seed, n, ns, ilo, ihi, z0="orth", shift_kind="disk2")
+    Hg, Zg = gpu_sweep(H0, Z0, ilo, ihi, re_, im_, win)
+    f = hq.aftermath(n)
+    assert np.array_equal(f, oracle.subdiag_scan(Hg, [(ilo, ihi)]))
+    Ho, _ = oracle_sweep(H0, Z0, ilo, ihi, re_, im_)
+    assert np.array_equal(f, oracle.subdiag_scan(Ho, [(ilo, ihi)]))
+    if ilo > 0:
+        assert f[ilo - 1] == 2 and np.all(f[:ilo - 1] == -1)
+    if ihi < n - 1:
+        assert f[ihi] == 2 and np.all(f[ihi + 1:] == -1)
+
+
+def test_aftermath_multi_block_and_small_entries():
+    """Several blocks: the decoupling zeros between them are flagged 2; an entry made negligible
+    (but nonzero) in a block that is not swept is left unscanned (-1), one right at a block edge
+    is scanned."""
+    H0, Z0, blocks, re_, im_ = _multi_case(600, [150, 150, 300], [16, 16, 40], 12)
+    Hd, Zd = hq.to_device(H0), hq.to_device(Z0)
+    hq.sweep_multi(Hd, Zd, blocks, re_, im_, 48)
+    Hg = hq.from_device(Hd)
+    f = hq.aftermath(600)
+    want = oracle.subdiag_scan(Hg, [(lo, hi) for lo, hi, _ in blocks])
+    assert np.array_equal(f, want)
+    assert f[149] == 2 and f[299] == 2 and f[599] == -1
+
+
+@pytest.mark.parametrize("k", [600, -600])
+def test_scaled_matrix_parity_and_equivariance(k):
+    """R15: H and the shifts times 2^k (|H| ~ 1e180 / 1e-180: the unscaled bulge vector and
+    house() would overflow / underflow): finite, equal to 2^k times the unscaled GPU sweep bit for
+    bit (every kernel step is linear in H or scale invariant), and within tolerance of the oracle."""
+    n, ns, win = 400, 40, 64
+    H0, Z0, re_, im_ = random_case(85, n, ns, z0="orth", shift_kind="disk2")
+    Hg, Zg = gpu_sweep(H0, Z0, 0, n - 1, re_, im_, win)
+    Hs0 = np.asfortranarray(np.ldexp(H0, k))
+    Hgs, Zgs = gpu_sweep(Hs0, Z0, 0, n - 1, np.ldexp(re_, k), np.ldexp(im_, k), win)
+    assert np.all(np.isfinite(Hgs))
+    assert np.array_equal(Hgs, np.ldexp(Hg, k)) and np.array_equal(Zgs, Zg)
+    Ho, Zo = oracle_sweep(Hs0, Z0, 0, n - 1, np.ldexp(re_, k), np.ldexp(im_, k))
+    # norms of 2^+-600-sized entries over/underflow: compare scaled back (exact)
+    check(np.ldexp(Hgs, -k), Zgs, np.ldexp(Ho, -k), Zo, H0, 0, n - 1)
+
+
+def test_decimal_extreme_scales():
+    """|H| ~ 1e200 and 1e-200 (not powers of two): the sweep stays finite and matches the oracle."""
+    n, ns = 300, 24
+    H0, Z0, re_, im_ = random_case(86, n, ns, z0="orth", shift_kind="disk2")
+    for sc in (1e200, 1e-200):
+        Hs0 = np.asfortranarray(H0 * sc)
+        Hg, Zg = gpu_sweep(Hs0, Z0, 0, n - 1, re_ * sc, im_ * sc, 48)
+        Ho, Zo = oracle_sweep(Hs0, Z0, 0, n - 1, re_ * sc, im_ * sc)
+        assert np.all(np.isfinite(Hg)) and np.all(np.isfinite(Zg))
+        check(Hg / sc, Zg, Ho / sc, Zo, Hs0 / sc, 0, n - 1)   # norms of 1e+-200 entries over/underflow
+
+
+@pytest.mark.parametrize("n,win", [(40, 16), (300, 64)])
+def test_zero_tail_reflectors_identity(n, win):
+    """tau = 0 path (R2: zero tail -> identity): with h(ilo+1, ilo) = 0 every bulge vector has a
+    zero tail (x1 = h10 (...), x2 = h10 h21) and every later reflector acts on an exactly zero
+    column, so the sweep is the identity -- bitwise, on H and Z, as in the oracle."""
+    H0, Z0, re_, im_ = random_case(87, n, 8, z0="orth", shift_kind="disk2")
+    H0[1, 0] = 0.0
+    Hg, Zg = gpu_sweep(H0, Z0, 0, n - 1, re_, im_, win)
+    Ho, Zo = oracle_sweep(H0, Z0, 0, n - 1, re_, im_)
+    assert np.array_equal(Ho, H0) and np.array_equal(Zo, Z0)
+    assert np.array_equal(Hg, H0) and np.array_equal(Zg, Z0)
+    assert hq.aftermath(n)[0] == 2
+
+
+@pytest.mark.parametrize("n,ns,win", [(8, 2, 8), (12, 4, 12), (24, 4, 10), (30, 2, 8)])
+def test_perfect_shifts(n, ns, win):
+    """Shifts = exact eigenvalues (conjugate pairs exact): the trailing m x m block (m = ns)
+    decouples on the GPU as in the oracle (small n only: over long chases the bulges lose the
+    shift information -- forward instability -- and the oracle itself decouples only to ~1e-2 at
+    n = 150; windows smaller than n make the chase cross windows).  Its internal basis is then fixed only by rounding (the
+    last reflectors act on a collapsed bulge), so there the two are compared through invariants --
+    the spectrum of the trailing block, the subspace of the last m columns of Z, the row norms of
+    the coupling block -- and everything else element by element."""
+    H0, Z0, _, _ = random_case(88 + n, n, 2, z0="orth")
+    lam = np.linalg.eigvals(H0)   # test infrastructure: the shifts are inputs
+    cpx = sorted([z for z in lam if z.imag > 1e-9], key=lambda z: -abs(z))[: ns // 2]
+    rl = sorted([z.real for z in lam if abs(z.imag) <= 1e-9], key=lambda x: -abs(x))
+    re_, im_ = [], []
+    for z in cpx:
+        re_ += [z.real, z.real]
+        im_ += [abs(z.imag), -abs(z.imag)]
+    while len(re_) < ns and len(rl) >= 2:   # not enough conjugate pairs: real pairs
+        re_ += [rl.pop(0), rl.pop(0)]
+        im_ += [0.0, 0.0]
+    assert len(re_) == ns
+    re_, im_ = np.array(re_), np.array(im_)
+    Hg, Zg = gpu_sweep(H0, Z0, 0, n - 1, re_, im_, win)
+    Ho, Zo = oracle_sweep(H0, Z0, 0, n - 1, re_, im_)
+    m, hn = ns, np.linalg.norm(H0)
+    assert abs(Hg[n - m, n - m - 1]) <= 1e-9 * hn and abs(Ho[n - m, n - m - 1]) <= 1e-9 * hn
+    assert np.all(np.tril(Hg, -2) == 0.0)
+    k = n - m
+    assert np.linalg.norm(Hg[:k, :k] - Ho[:k, :k]) <= TOL * hn
+    assert np.linalg.norm(Zg[:, :k] - Zo[:, :k]) <= TOL * np.sqrt(n)
+    assert np.allclose(np.linalg.norm(Hg[:k, k:], axis=1), np.linalg.norm(Ho[:k, k:], axis=1),
+                       rtol=0, atol=1e-10 * hn)
+    Pg, Po = Zg[:, k:] @ Zg[:, k:].T, Zo[:, k:] @ Zo[:, k:].T
+    assert np.linalg.norm(Pg - Po) <= 1e-10 * np.sqrt(n)
+    eg = np.sort_complex(np.linalg.eigvals(Hg[k:, k:]))
+    eo = np.sort_complex(np.linalg.eigvals(Ho[k:, k:]))
+    assert np.allclose(eg, eo, rtol=0, atol=1e-9 * hn)
+    assert np.allclose(np.sort_complex(re_ + 1j * im_), eg, rtol=0, atol=1e-7 * hn)
+
+
+@pytest.mark.parametrize("n,ns", [(1000, 100), (4000, 200)])
+def test_hess_n_parity(n, ns):
+    """NEXT-3 workload hess_n: graded chi^2 subdiagonal, shifts in the disk of
+    radius sqrt(n), random orthogonal Z."""
+    from hqr_inputs import make_hess
+    p = make_hess(n, ns, z0="orth")
+    Hg, Zg = gpu_sweep(p.H, p.Z, 0, n - 1, p.shifts_re, p.shifts_im, hq.DEFAULT_WINDOW)
+    Ho, Zo = oracle_sweep(p.H, p.Z, 0, n - 1, p.shifts_re, p.shifts_im)
+    check(Hg, Zg, Ho, Zo, p.H, 0, n - 1)
+
+
+def test_entry_waits_for_default_stream():
+    """the sweep must see H / Z writes the caller queued on the default stream just
+    before the call (the library stream waits for the legacy stream at entry)."""
+    import torch
+    n = 1200
+    H0, Z0, re_, im_ = random_case(89, n, 40, z0="orth", shift_kind="disk2")
+    Href, Zref = gpu_sweep(H0, Z0, 0, n - 1, re_, im_, 96)
+    src_h, src_z = hq.to_device(H0), hq.to_device(Z0)
+    Hd = torch.zeros_like(src_h.t()).t()
+    Zd = torch.zeros_like(src_z.t()).t()
+    torch.cuda.synchronize()
+    torch.cuda._sleep(200_000_000)   # ~0.1 s of queued work ahead of the copies
+    Hd.t().copy_(src_h.t())
+    Zd.t().copy_(src_z.t())
+    hq.sweep(Hd, Zd, 0, n - 1, re_, im_, 96)
+    assert np.array_equal(hq.from_device(Hd), Href) and np.array_equal(hq.from_device(Zd), Zref)
+
+
+def test_window_max_config():
+    """hqr_config.window_max caps the effective window (SURVEY §8(b) "max window")."""
+    n = 500
+    H0, Z0, re_, im_ = random_case(90, n, 40, z0="orth", shift_kind="disk2")
+    hq.teardown()
+    hq.setup(0, window_max=48)
+    try:
+        Hg, Zg = gpu_sweep(H0, Z0, 0, n - 1, re_, im_, 96)
+        assert hq.stats()["window_eff"] == 48
+    finally:
+        hq.teardown()
+        hq.setup(0)
+    Ho, Zo = oracle_sweep(H0, Z0, 0, n - 1, re_, im_)
+    check(Hg, Zg, Ho, Zo, H0, 0, n - 1)
+
+
+@pytest.mark.parametrize("n,ilo,ihi,sweeps,win", [(1500, 0, 1499, [100, 100, 100], 96),
+                                                  (900, 20, 880, [40, 16, 64], 64),
+                                                  (100, 0, 99, [8, 8], 112)])
+def test_overlapped_sweeps_parity(n, ilo, ihi, sweeps, win):
+    """NEXT-1 (P:831-833): hqr_sweeps equals the oracle applying the sweeps one after another;
+    the aftermath scan of the last sweep matches the oracle's scan of the GPU's H'."""
+    from hqr_inputs import shifts
+    H0, Z0, _, _ = random_case(95, n, 2, ilo, ihi, z0="orth")
+    sets = [shifts("disk2", ns, 18, stream_offset=i + 1) for i, ns in enumerate(sweeps)]
+    Hd, Zd = hq.to_device(H0), hq.to_device(Z0)
+    hq.sweeps(Hd, Zd, ilo, ihi, sets, win)
+    Hg, Zg = hq.from_device(Hd), hq.from_device(Zd)
+    Ho, Zo = H0.copy(order="F"), Z0.copy(order="F")
+    for re_, im_ in sets:
+        oracle.sweep(Ho, Zo, ilo, ihi, re_, im_)
+    check(Hg, Zg, Ho, Zo, H0, ilo, ihi)
+    assert np.array_equal(hq.aftermath(n), oracle.subdiag_scan(Hg, [(ilo, ihi)]))
