@@ -198,6 +198,51 @@ def make_hess(n: int, nshifts: int, z0: str = "eye", z_device: str = "cpu") -> P
     return Problem(H, Z, 0, n - 1, re, im, None, [(0, n - 1, 0, nshifts)])
 
 
+QZ_CFG = 6  # seed-space id of the generalized (QZ) workload
+
+
+def triangular(n: int, cfg: int) -> np.ndarray:
+    """Random upper-triangular T (Fortran order) for the QZ workload: diagonal U[1, 2], strictly
+    upper entries N(0, 1/n) drawn column by column (stream 4) -- nonsingular and well conditioned,
+    so the pair has finite generalized eigenvalues near those of H (no infinite eigenvalues: the
+    paper's push-infinities task, is out of scope)."""
+    T = np.zeros((n, n), dtype=np.float64, order="F")
+    g = rng(cfg, 4)
+    for j in range(n):
+        T[:j, j] = g.standard_normal(j) / np.sqrt(n)
+    T[np.arange(n), np.arange(n)] = rng(cfg, 5).uniform(1.0, 2.0, n)
+    return T
+
+
+@dataclass
+class QZProblem:
+    H: np.ndarray
+    T: np.ndarray
+    Q: np.ndarray
+    Z: np.ndarray
+    ilo: int
+    ihi: int
+    shifts_re: np.ndarray
+    shifts_im: np.ndarray
+
+
+def make_qz(n: int, nshifts: int, q0: str = "eye", seed: int = 0, upper: str = "n01",
+            shift_kind: str = "disk2") -> QZProblem:
+    """Hessenberg-triangular pair (H as BASELINE configs[2..4]: N(0,1) upper, U[0.5,1.5]
+    subdiagonal; T = triangular()), Q0 = Z0 = I or random orthogonal, conjugate-pair shifts."""
+    cfg = QZ_CFG * 1000 + seed
+    H = hessenberg(n, upper, cfg)
+    T = triangular(n, cfg)
+    if q0 == "eye":
+        Q = np.asfortranarray(np.eye(n))
+        Z = np.asfortranarray(np.eye(n))
+    else:
+        Q = orthogonal(n, cfg)
+        Z = orthogonal(n, cfg + 500)
+    re, im = shifts(shift_kind, nshifts, cfg)
+    return QZProblem(H, T, Q, Z, 0, n - 1, re, im)
+
+
 def random_case(seed: int, n: int, nshifts: int, ilo: int = 0, ihi: int | None = None,
                 upper: str = "n01", z0: str = "eye", shift_kind: str = "mixed"):
     """Small random case for property tests: H decoupled at ilo/ihi, Z0 identity or orthogonal."""

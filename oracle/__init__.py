@@ -13,6 +13,9 @@ Functions and the passages they follow (PAPER.md line numbers, see hqr_oracle.c)
                               P:146-151, P:198-206, P:227-233
   flops(...)               -- F_alg, the work of applying every reflector directly
   subdiag_scan(H, ...)     -- the aftermath subdiagonal scan, P:379-381 (reading R16)
+  rhs_house(r)             -- right-hand side reflector r P = beta e_m^T (reading R18)
+  qz_first_column(H, T ..) -- (H T^-1 - s I)(H T^-1 - s' I) e1, P:209 (reading R17)
+  qz_sweep(H, T, Q, Z, ..) -- nshifts/2 sequential double-shift QZ steps
 
 Parity pins for every function are in tests/test_oracle.py (none is "parity unpinned").
 """
@@ -62,6 +65,14 @@ def _load():
         lib.oracle_subdiag_scan.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64,
                                             ctypes.c_int64, ctypes.c_void_p]
         lib.oracle_subdiag_scan.restype = None
+        lib.oracle_rhs_house.argtypes = [ctypes.c_int, dp, dp, dp, dp]
+        lib.oracle_rhs_house.restype = None
+        lib.oracle_qz_first_column.argtypes = [dp, dp, ctypes.c_int64, ctypes.c_int64, ctypes.c_double,
+                                               ctypes.c_double, ctypes.c_double, ctypes.c_double, dp]
+        lib.oracle_qz_first_column.restype = None
+        lib.oracle_qz_sweep.argtypes = [ctypes.c_void_p] * 4 + [ctypes.c_int64] * 3 + [dp, dp, ctypes.c_int,
+                                                                                       ctypes.c_int]
+        lib.oracle_qz_sweep.restype = ctypes.c_int
         _lib = lib
     return _lib
 
@@ -134,3 +145,37 @@ def subdiag_scan(H: np.ndarray, blocks) -> np.ndarray:
     for ilo, ihi in blocks:
         _load().oracle_subdiag_scan(H.ctypes.data, n, ilo, ihi, flags.ctypes.data)
     return flags
+
+
+def rhs_house(r):
+    """(u, tau, beta) with r (I - tau u u^T) = beta e_m^T, u[m-1] = 1 (reading R18)."""
+    r = np.ascontiguousarray(r, dtype=np.float64)
+    m = r.shape[0]
+    u = np.zeros(m)
+    tau = ctypes.c_double()
+    beta = ctypes.c_double()
+    _load().oracle_rhs_house(m, _dptr(r), _dptr(u), ctypes.byref(tau), ctypes.byref(beta))
+    return u, tau.value, beta.value
+
+
+def qz_first_column(H, T, ilo, re_pair, im_pair=(0.0, 0.0)):
+    H, T = _as_colmajor(H), _as_colmajor(T)
+    x = np.zeros(3)
+    _load().oracle_qz_first_column(_dptr(H), _dptr(T), H.shape[0], ilo, float(re_pair[0]),
+                                   float(re_pair[1]), float(im_pair[0]), float(im_pair[1]), _dptr(x))
+    return x
+
+
+def qz_sweep(H, T, Q, Z, ilo, ihi, shifts_re, shifts_im, bulges=None):
+    """In place: (H, T) <- Q_s^T (H, T) Z_s, Q <- Q Q_s, Z <- Z Z_s for one multishift QZ sweep
+    (Q / Z may be None).  Column-major float64 arrays."""
+    H, T = _as_colmajor(H), _as_colmajor(T)
+    n = H.shape[0]
+    for A in (Q, Z):
+        if A is not None:
+            _as_colmajor(A)
+    sr = np.ascontiguousarray(shifts_re, dtype=np.float64)
+    si = np.ascontiguousarray(shifts_im, dtype=np.float64)
+    j0, j1 = bulges if bulges is not None else (0, sr.shape[0] // 2)
+    _load().oracle_qz_sweep(H.ctypes.data, T.ctypes.data, None if Q is None else Q.ctypes.data,
+                            None if Z is None else Z.ctypes.data, n, ilo, ihi, _dptr(sr), _dptr(si), j0, j1)

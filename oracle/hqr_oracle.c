@@ -198,3 +198,107 @@ void oracle_subdiag_scan(const double* H, int64_t n, int64_t ilo, int64_t ihi, s
     flags[i] = (h == 0.0) ? 2 : (fabs(h) <= 0x1p-52 * d) ? 1 : 0;
   }
 }
+
+/* ===================================================================================================
+ * Generalized (QZ) sweep -- SURVEY §8(f) NEXT-4; PAPER.md P:208-213 (the generalized double-shift
+ * step) and P:412-439 (push bulges on a Hessenberg-triangular pair).  Test infrastructure like the
+ * rest of this file.
+ *
+ * One multishift QZ sweep on a Hessenberg-triangular pair (H, T): (H, T) <- Q^T (H, T) Z,
+ * Qacc <- Qacc Q, Zacc <- Zacc Z, the product of nshifts/2 sequential double-shift QZ steps (pair 0
+ * first).  Per step (P:209-211 and the textbook QZ step it cites, Moler-Stewart): the bulge vector
+ * v = (H T^-1 - s I)(H T^-1 - s' I) e_ilo (reading R17), a 3x3 Householder reflector from the left,
+ * then, at every position p, a left reflector from H's column p (rows p+1..p+m) and two "right-hand
+ * side" reflectors from the right that return T to triangular form: the first from T's row p+3
+ * (columns p+1..p+3, zeroing T[p+3, p+1..p+2]), the second from T's row p+2 (columns p+1..p+2,
+ * zeroing T[p+2, p+1]); at the last position (m = 2) a single 2-element right reflector.
+ * =================================================================================================== */
+
+/* Right-hand side reflector (reading R18): for a row vector r of length m (2 or 3) returns u
+ * (u[m-1] = 1) and tau with r (I - tau u u^T) = beta e_m^T -- the R2 reflector of the reversed
+ * vector (r[m-1], ..., r[0]), reversed. */
+void oracle_rhs_house(int m, const double* r, double* u, double* tau, double* beta) {
+  double x[3], v[3];
+  for (int i = 0; i < m; ++i) x[i] = r[m - 1 - i];
+  oracle_house(m, x, v, tau, beta);
+  for (int i = 0; i < m; ++i) u[i] = v[m - 1 - i];
+}
+
+/* R17: v = (M - s I)(M - s' I) e_1 at rows ilo..ilo+2, M = H T^-1 on the active block, with
+ * sigma = s + s', pi = s s' (R3).  M e1 = (h00/t00, h10/t00, 0); y = T^-1 M e1 has y1 = h10/(t00 t11)
+ * and y0 = (h00/t00 - t01 y1)/t00; M^2 e1 = H y. */
+void oracle_qz_first_column(const double* H, const double* T, int64_t n, int64_t ilo, double re0,
+                            double re1, double im0, double im1, double* x) {
+  const double h00 = EL(H, ilo, ilo, n), h01 = EL(H, ilo, ilo + 1, n);
+  const double h10 = EL(H, ilo + 1, ilo, n), h11 = EL(H, ilo + 1, ilo + 1, n);
+  const double h21 = EL(H, ilo + 2, ilo + 1, n);
+  const double t00 = EL(T, ilo, ilo, n), t01 = EL(T, ilo, ilo + 1, n), t11 = EL(T, ilo + 1, ilo + 1, n);
+  const double sigma = re0 + re1, pi = re0 * re1 - im0 * im1;
+  const double a = h00 / t00, b = h10 / t00;
+  const double y1 = b / t11;
+  const double y0 = (a - t01 * y1) / t00;
+  x[0] = h00 * y0 + h01 * y1 - sigma * a + pi;
+  x[1] = h10 * y0 + h11 * y1 - sigma * b;
+  x[2] = h21 * y1;
+}
+
+static void left_rows(double* A, int64_t n, int64_t r0, int m, int64_t c0, int64_t c1, const double* v,
+                      double tau) { /* A(r0..r0+m-1, c0..c1-1) -= tau v (v^T A) */
+#pragma omp parallel for schedule(static) if (c1 - c0 > 2048)
+  for (int64_t c = c0; c < c1; ++c) {
+    double w = 0.0;
+    for (int i = 0; i < m; ++i) w += v[i] * EL(A, r0 + i, c, n);
+    for (int i = 0; i < m; ++i) EL(A, r0 + i, c, n) -= tau * v[i] * w;
+  }
+}
+
+static void right_cols(double* A, int64_t n, int64_t c0, int m, int64_t r1, const double* u, double tau) {
+  /* A(0..r1, c0..c0+m-1) -= tau (A u) u^T */
+#pragma omp parallel for schedule(static) if (r1 > 2048)
+  for (int64_t r = 0; r <= r1; ++r) {
+    double w = 0.0;
+    for (int i = 0; i < m; ++i) w += EL(A, r, c0 + i, n) * u[i];
+    for (int i = 0; i < m; ++i) EL(A, r, c0 + i, n) -= tau * w * u[i];
+  }
+}
+
+static void qz_apply_one(double* H, double* T, double* Qa, double* Za, int64_t n, int64_t ilo, int64_t ihi,
+                         int64_t p, const double* sr, const double* si, int j) {
+  const int m = (p <= ihi - 3) ? 3 : 2;
+  double x[3], v[3], tau, beta;
+  if (p == ilo - 1)
+    oracle_qz_first_column(H, T, n, ilo, sr[2 * j], sr[2 * j + 1], si[2 * j], si[2 * j + 1], x);
+  else
+    for (int i = 0; i < m; ++i) x[i] = EL(H, p + 1 + i, p, n);
+  oracle_house(m, x, v, &tau, &beta);
+  /* left: rows p+1..p+m of H (columns from ilo / p+1) and T (columns from p+1), Qacc columns */
+  left_rows(H, n, p + 1, m, (p == ilo - 1) ? ilo : p + 1, n, v, tau);
+  if (p >= ilo) {
+    EL(H, p + 1, p, n) = beta;
+    for (int i = 1; i < m; ++i) EL(H, p + 1 + i, p, n) = 0.0;
+  }
+  left_rows(T, n, p + 1, m, p + 1, n, v, tau);
+  if (Qa) right_cols(Qa, n, p + 1, m, n - 1, v, tau);
+  /* right: restore T's triangular form, last row of the block first */
+  const int64_t hr = (p + 4 < ihi) ? p + 4 : ihi;
+  for (int mm = m; mm >= 2; --mm) {
+    const int64_t row = p + mm; /* T row whose entries left of the diagonal are zeroed */
+    double r[3], u[3], tz, bz;
+    for (int i = 0; i < mm; ++i) r[i] = EL(T, row, p + 1 + i, n);
+    oracle_rhs_house(mm, r, u, &tz, &bz);
+    right_cols(H, n, p + 1, mm, hr, u, tz);
+    right_cols(T, n, p + 1, mm, row, u, tz);
+    for (int i = 0; i < mm - 1; ++i) EL(T, row, p + 1 + i, n) = 0.0; /* R9: exact zeros */
+    EL(T, row, row, n) = bz;
+    if (Za) right_cols(Za, n, p + 1, mm, n - 1, u, tz);
+  }
+}
+
+/* The QZ oracle: nshifts/2 sequential double-shift QZ steps, bulges j0 .. j1-1.  Qa / Za may be
+ * NULL.  No argument validation. */
+int oracle_qz_sweep(double* H, double* T, double* Qa, double* Za, int64_t n, int64_t ilo, int64_t ihi,
+                    const double* sr, const double* si, int j0, int j1) {
+  for (int j = j0; j < j1; ++j)
+    for (int64_t p = ilo - 1; p <= ihi - 2; ++p) qz_apply_one(H, T, Qa, Za, n, ilo, ihi, p, sr, si, j);
+  return 0;
+}
