@@ -126,6 +126,22 @@ int hqr_sweeps(double* H, double* Z, int64_t n, int64_t ilo, int64_t ihi, int ns
                const double* shifts_re, const double* shifts_im, const int* nshifts, int window);
 
 /*
+ * Generalized (QZ) multishift sweep (PAPER.md P:208-213 the double-shift QZ
+ * step, P:412-439 push bulges on a Hessenberg-triangular pair): (H, T) <- Q_s^T (H, T) Z_s,
+ * Q <- Q Q_s, Z <- Z Z_s, where the sweep is the product of nshifts/2 double-shift QZ steps (pair 0
+ * first): bulge vector (H T^-1 - s I)(H T^-1 - s' I) e1 (R17), left Householder
+ * reflectors from H's columns, right-hand side reflectors from T's rows restoring T's triangular
+ * form (R18).  H is upper Hessenberg, T upper triangular with T[ilo,ilo], T[ilo+1,ilo+1] != 0 (no
+ * infinite eigenvalues at the top; the paper's push-infinities task is out of scope), both n x n
+ * column-major on the DEVICE (host pointers: -1).  Q, Z: n x n device or NULL (skip).  Window side
+ * min(window, N, HQR_MAX_WINDOW_QZ).  Single GPU.  Codes as hqr_sweep, plus -2 (T NULL, or a zero
+ * leading diagonal entry of T in the block).
+ */
+int hqr_qz_sweep(double* H, double* T, double* Q, double* Z, int64_t n, int64_t ilo, int64_t ihi,
+                 const double* shifts_re, const double* shifts_im, int nshifts, int window);
+#define HQR_MAX_WINDOW_QZ 80
+
+/*
  * ---- Sharded sweep over several GPUs -------------------------------------------
  * Layout for `world` ranks (one process per GPU): rank r owns H columns [cb[r], cb[r+1]) -- all n
  * rows, column-major, ld = n -- and must allocate `halo` further columns after them (work space for

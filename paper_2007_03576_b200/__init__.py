@@ -27,6 +27,7 @@ ERRORS = {
     -7: "shift pair not two reals / exact conjugates", -8: "nshifts odd, < 2 or > N",
     -9: "window out of range", -10: "active block not decoupled", -100: "not set up",
     -101: "no usable sm_100 CUDA device", -11: "matrix too small for the shard count",
+    -2: "T is NULL or singular at the top of the block (QZ)",
 }
 
 FLAG_NO_GRAPH = 1
@@ -69,7 +70,7 @@ class Stats(ctypes.Structure):
 SYMBOLS = ["hqr_setup", "hqr_sweep", "hqr_sweep_multi", "hqr_teardown", "hqr_plan_query",
            "hqr_plan_query_multi", "hqr_get_stats", "hqr_error_string", "hqr_dist_layout",
            "hqr_dist_query", "hqr_nccl_unique_id", "hqr_sweep_dist", "hqr_sweep_virtual",
-           "hqr_get_aftermath", "hqr_sweeps", "hqr_plan_query_sweeps"]
+           "hqr_get_aftermath", "hqr_sweeps", "hqr_plan_query_sweeps", "hqr_qz_sweep"]
 
 
 def lib():
@@ -126,6 +127,9 @@ def lib():
                                             ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p,
                                             ctypes.c_void_p, ctypes.c_int64]
         L.hqr_plan_query_sweeps.restype = ctypes.c_int
+        L.hqr_qz_sweep.argtypes = [ctypes.c_void_p] * 4 + [ctypes.c_int64] * 3 + [
+            ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int]
+        L.hqr_qz_sweep.restype = ctypes.c_int
         L.hqr_get_aftermath.argtypes = [ctypes.c_void_p, ctypes.c_int64]
         L.hqr_get_aftermath.restype = ctypes.c_int
         L.hqr_get_stats.argtypes = [ctypes.POINTER(Stats)]
@@ -253,6 +257,27 @@ def plan_query_sweeps(n: int, ilo: int, ihi: int, nshifts_list, window: int):
         raise HQRError(rc, "hqr_plan_query_sweeps")
     keys = ["k", "nbc_max", "s", "lag", "nchains", "nsteps", "nwindows", "max_kw", "max_nbc", "nb"]
     return dict(zip(keys, (int(v) for v in info))), wins
+
+
+def qz_sweep(H, T, Q, Z, ilo: int, ihi: int, shifts_re, shifts_im, window: int = 64) -> None:
+    """Generalized (QZ) multishift sweep in place on device matrices (include/hqr.h hqr_qz_sweep):
+    (H, T) <- Q_s^T (H, T) Z_s, Q <- Q Q_s, Z <- Z Z_s (Q / Z may be None)."""
+    hp, n = _ptr_n(H)
+    tp, nt = _ptr_n(T)
+    qp, nq = _ptr_n(Q)
+    zp, nz = _ptr_n(Z)
+    if hp is None:
+        raise HQRError(-1, "hqr_qz_sweep")
+    if tp is None:
+        raise HQRError(-2, "hqr_qz_sweep")
+    if nt != n or (qp is not None and nq != n) or (zp is not None and nz != n):
+        raise ValueError("H, T, Q, Z must have the same order")
+    sr = np.ascontiguousarray(shifts_re, dtype=np.float64)
+    si = np.ascontiguousarray(shifts_im, dtype=np.float64)
+    rc = lib().hqr_qz_sweep(hp, tp, qp, zp, n, ilo, ihi, sr.ctypes.data, si.ctypes.data, int(sr.shape[0]),
+                            int(window))
+    if rc:
+        raise HQRError(rc, "hqr_qz_sweep")
 
 
 def dist_layout(n: int, world: int):

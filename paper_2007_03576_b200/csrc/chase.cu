@@ -169,7 +169,7 @@ __global__ void __launch_bounds__(kChaseThreads, 1) chase_kernel(StepArgs a) {
     }
   }
   __syncthreads();
-  aftermath_scan(Hs, ldh, W, a, threadIdx.x, kChaseThreads);  // a9 (check only)
+  aftermath_scan(Hs, ldh, W, a.aftermath, threadIdx.x, kChaseThreads);  // a9 (check only)
 
   // write back the window; store Q_W column-major with ld = QLD (= the update kernels' SMEM
   // layout), zero padded to KP x QLD

@@ -120,21 +120,10 @@ __device__ __forceinline__ void named_sync(int id, int threads) {
   asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(threads) : "memory");
 }
 
-// Power-of-two scaling (reading R15): for amax = m 2^e, m in [0.5, 1), returns 2^-e in
-// *down and 2^e in *up when both are normal numbers (1 <= biased exponent <= 2044), else false.
-// Multiplying by them is exact, so the scaled formulas round exactly like the unscaled ones
-// wherever those stay finite -- and stay finite where they would not.
-__device__ __forceinline__ bool pow2_scale(double amax, double* down, double* up) {
-  const long long E = __double_as_longlong(amax) >> 52;  // amax >= 0: biased exponent
-  if (E < 1 || E > 2044) return false;
-  *down = __longlong_as_double((2045 - E) << 52);
-  *up = __longlong_as_double((E + 1) << 52);
-  return true;
-}
-
 // Householder reflector (reading R2): P = I - tau v v^T, v = [1, v1, v2],
 // P x = beta e1 with beta = -sign(x0) ||x||, sign(0) = +1; zero tail -> identity.  Computed on x
-// scaled by a power of two (R15).
+// scaled by a power of two (R15: exact, so the result rounds exactly like the unscaled formulas
+// wherever those stay finite, and stays finite where they would not).
 // With d = x0 - beta and r = 1 / (d * beta): v_i = x_i / d = x_i * beta * r, tau = -d / beta = -d*d*r.
 // The chase's critical path is a chain of these (one per bulge and step), so the square root and
 // the reciprocal use the hardware approximations refined by Newton steps (rounding-level
@@ -154,37 +143,34 @@ __device__ __forceinline__ double rcp_nr(double q) {  // 1 / q, q != 0 normal
   r = r * fma(-q, r, 2.0);
   return fma(r, fma(-q, r, 1.0), r);  // final correction
 }
-static __device__ __noinline__ void house_scale_slow(double& x0, double& x1, double& x2, double amax, int& e) {
-  (void)frexp(amax, &e);  // |x| near the overflow threshold or subnormal: library scaling
-  x0 = ldexp(x0, -e); x1 = ldexp(x1, -e); x2 = ldexp(x2, -e);
-}
 __device__ __forceinline__ void house(double x0, double x1, double x2, double& v1, double& v2,
                                       double& tau, double& beta) {
+  // R15 scale 2^-e, branch-free (the chase's critical path; registers are tight in the fused
+  // kernel): for max|x| outside [2^-1022, 2^1021) -- entries the update GEMMs could not carry
+  // either -- the unscaled formulas are used
   const double amax = fmax(fabs(x0), fmax(fabs(x1), fabs(x2)));
-  v1 = 0.0; v2 = 0.0; tau = 0.0; beta = x0;
-  if (amax == 0.0) return;
-  double down, up;
-  int e = 0;
-  const bool fast = pow2_scale(amax, &down, &up);
-  if (fast) {
-    x0 *= down; x1 *= down; x2 *= down;
-  } else {
-    house_scale_slow(x0, x1, x2, amax, e);
-  }
+  const long long E = __double_as_longlong(amax) >> 52;   // biased exponent (amax >= 0)
+  const bool ok = (E >= 1) & (E <= 2044);
+  const double down = ok ? __longlong_as_double((2045 - E) << 52) : 1.0;
+  x1 *= down; x2 *= down;
   const double tail2 = fma(x1, x1, x2 * x2);
-  if (tail2 == 0.0) return;  // zero tail: identity, beta = x0 (unscaled)
-  const double s = fma(x0, x0, tail2);
+  if (tail2 == 0.0) {  // zero tail: identity, beta = x0
+    v1 = 0.0; v2 = 0.0; tau = 0.0; beta = x0;
+    return;
+  }
+  const double xs0 = x0 * down;
+  const double s = fma(xs0, xs0, tail2);
   const double y = rsqrt_nr(s);
   double nrm = s * y;
   nrm = fma(0.5 * y, fma(-nrm, nrm, s), nrm);  // sqrt(s), Newton-corrected
-  const double b = (x0 >= 0.0) ? -nrm : nrm;
-  const double d = x0 - b;
+  const double b = (xs0 >= 0.0) ? -nrm : nrm;
+  const double d = xs0 - b;
   const double r = rcp_nr(d * b);
   const double br = b * r;
   v1 = x1 * br;
   v2 = x2 * br;
   tau = -d * d * r;
-  beta = fast ? b * up : ldexp(b, e);
+  beta = b * (ok ? __longlong_as_double((E + 1) << 52) : 1.0);
 }
 
 // Bulge introduction (a2; reading R1): x = the first column of (H - s I)(H - s' I) at the top of the
@@ -198,12 +184,11 @@ __device__ __forceinline__ void intro_vector(const double* Hs, int ldh, const do
   double re0 = c4[0], re1 = c4[1], im0 = c4[2], im1 = c4[3];
   const double amax = fmax(fmax(fmax(fabs(h00), fabs(h10)), fmax(fabs(h01), fabs(h11))),
                            fmax(fmax(fabs(h21), fabs(re0)), fmax(fmax(fabs(re1), fabs(im0)), fabs(im1))));
-  if (amax != 0.0) {
-    int e;
-    (void)frexp(amax, &e);
-    h00 = ldexp(h00, -e); h10 = ldexp(h10, -e); h01 = ldexp(h01, -e); h11 = ldexp(h11, -e);
-    h21 = ldexp(h21, -e); re0 = ldexp(re0, -e); re1 = ldexp(re1, -e); im0 = ldexp(im0, -e);
-    im1 = ldexp(im1, -e);
+  const long long E = __double_as_longlong(amax) >> 52;  // R15 (as house: [2^-1022, 2^1021))
+  if (E >= 1 && E <= 2044) {
+    const double down = __longlong_as_double((2045 - E) << 52);
+    h00 *= down; h10 *= down; h01 *= down; h11 *= down; h21 *= down;
+    re0 *= down; re1 *= down; im0 *= down; im1 *= down;
   }
   const double sigma = re0 + re1, pi = re0 * re1 - im0 * im1;
   x0 = h00 * (h00 - sigma) + h01 * h10 + pi;
@@ -212,20 +197,22 @@ __device__ __forceinline__ void intro_vector(const double* Hs, int ldh, const do
 }
 
 // Aftermath subdiagonal scan (check only, reading R16) of rows [W.scan_lo, W.scan_hi]
-// after W's chase: flags[i] = 2 if h(i+1,i) == 0, 1 if |h(i+1,i)| <= 2^-52 (|h(i,i)| + |h(i+1,i+1)|),
-// else 0.  Entries inside the window come from its SMEM copy Hs (ld ldh), the boundary entries
-// around it (row ilo-1 / ihi + 1, untouched by the sweep) from H in global memory.  No mutation.
+// after W's chase, from its SMEM copy Hs (ld ldh): flags[i] = 2 if h(i+1,i) == 0, 1 if
+// |h(i+1,i)| <= 2^-52 (|h(i,i)| + |h(i+1,i+1)|), else 0.  The boundary rows ilo-1 / ihi (outside
+// the window) hold h(i+1, i) = 0, verified at entry (-10) and never written by the sweep: 2.
+// No mutation.
 __device__ __forceinline__ void aftermath_scan(const double* Hs, int ldh, const WindowDesc& W,
-                                               const StepArgs& a, int tid, int nthreads) {
-  if (!a.aftermath || W.scan_hi < W.scan_lo) return;
-  auto h = [&](int i, int j) -> double {
-    if (i >= W.w0 && i <= W.w1 && j >= W.w0 && j <= W.w1) return Hs[(i - W.w0) + (j - W.w0) * ldh];
-    return a.H[(int64_t)i + (int64_t)(j - a.hcol0) * a.n];
-  };
+                                               signed char* flags, int tid, int nthreads) {
+  if (!flags || W.scan_hi < W.scan_lo) return;
   for (int i = W.scan_lo + tid; i <= W.scan_hi; i += nthreads) {
-    const double s = h(i + 1, i);
-    const double d = fabs(h(i, i)) + fabs(h(i + 1, i + 1));
-    a.aftermath[i] = (s == 0.0) ? 2 : (fabs(s) <= 0x1p-52 * d) ? 1 : 0;
+    const int l = i - W.w0;
+    signed char f = 2;
+    if (l >= 0 && l + 1 < W.w1 - W.w0 + 1) {
+      const double s = Hs[(l + 1) + l * ldh];
+      const double d = fabs(Hs[l + l * ldh]) + fabs(Hs[(l + 1) + (l + 1) * ldh]);
+      f = (s == 0.0) ? 2 : (fabs(s) <= 0x1p-52 * d) ? 1 : 0;
+    }
+    flags[i] = f;
   }
 }
 

@@ -1489,6 +1489,111 @@ int hqr_sweep_virtual(double* H, double* Z, int64_t n, int64_t ilo, int64_t ihi,
   return 0;
 }
 
+// ================================================================================================
+// Generalized (QZ) sweep (qz.cu).  Per wavefront step: the QZ chase of every
+// window (H, T windows + Q_W, Z_W in SMEM), then the DMMA update kernels of update.cu, each twice:
+// left  Q_W^T on the rows of W right of it in H and in T;
+// right Z_W on the columns of W above it in H and in T;
+// accumulate Qacc(:, W) Q_W and Zacc(:, W) Z_W.
+// One stream, in order (a step's left updates before its right updates: they meet in the blocks
+// H(W_c, W_c') / T(W_c, W_c')).
+// ================================================================================================
+int hqr_qz_sweep(double* H, double* T, double* Q, double* Z, int64_t n, int64_t ilo, int64_t ihi,
+                 const double* shifts_re, const double* shifts_im, int nshifts, int window) {
+  if (!H) return -1;
+  if (!T) return -2;
+  Blocks b;
+  b.ilo = {ilo}; b.ihi = {ihi}; b.nshifts = {nshifts};
+  int rc = validate_blocks(n, b, shifts_re, shifts_im, window, true);
+  if (rc) return rc;
+  Plan P;
+  const int kmax = std::min(g.window_max > 0 ? g.window_max : hqr::kMaxWindowQZ, hqr::kMaxWindowQZ);
+  rc = hqr::make_plan(n, ilo, ihi, nshifts, window, kmax, &P);
+  if (rc) return rc;
+  if (!g.ready) return -100;
+  if (g.world > 1) return -1;
+  CK(cudaSetDevice(g.device));
+  if (!is_device_ptr(H) || !is_device_ptr(T) || (Q && !is_device_ptr(Q)) || (Z && !is_device_ptr(Z))) return -1;
+  {  // -10 (H decoupled at the block ends); T's leading diagonal entries divide the bulge vector (-2)
+    double v[4] = {0.0, 0.0, 1.0, 1.0};
+    if (ilo > 0) CK(cudaMemcpy(&v[0], H + ilo + (ilo - 1) * n, sizeof(double), cudaMemcpyDeviceToHost));
+    if (ihi < n - 1) CK(cudaMemcpy(&v[1], H + (ihi + 1) + ihi * n, sizeof(double), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(&v[2], T + ilo + ilo * n, sizeof(double), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(&v[3], T + (ilo + 1) + (ilo + 1) * n, sizeof(double), cudaMemcpyDeviceToHost));
+    if (v[0] != 0.0 || v[1] != 0.0) return -10;
+    if (v[2] == 0.0 || v[3] == 0.0) return -2;
+  }
+  rc = wait_for_caller();
+  if (rc) return rc;
+  rc = upload_coef(shifts_re, shifts_im, P.nb);
+  if (rc) return rc;
+  const int KP = hqr::padded_kp(P.max_kw), QLD = hqr::pad_ld(KP);
+  const size_t slots = (size_t)hqr::kQSets * P.nchains * KP * QLD;
+  rc = ensure(&g.d_q, &g.q_cap, 2 * slots);  // Q_W slots, then Z_W slots
+  if (rc) return rc;
+  double* zslots = g.d_q + slots;
+  WindowDesc* d_wins = nullptr;
+  CK(cudaMalloc(&d_wins, P.windows.size() * sizeof(WindowDesc)));
+  CK(cudaMemcpyAsync(d_wins, P.windows.data(), P.windows.size() * sizeof(WindowDesc), cudaMemcpyHostToDevice,
+                     g.stream));
+  hqr::TensorMaps tmA, tmB;  // (H, Qacc) and (T, Zacc)
+  CK(hqr::make_tensor_maps(&tmA, H, n, Q, n, n, n, KP));
+  CK(hqr::make_tensor_maps(&tmB, T, n, Z, n, n, n, KP));
+  hqr_stats st{};
+  st.window_eff = P.k;
+  cudaStream_t A = g.stream;
+  CK(cudaEventRecord(g.ev0, A));
+  for (int s = 0; s < P.nsteps; ++s) {
+    StepArgs a{};
+    a.n = n; a.ilo = ilo; a.ihi = ihi; a.hcol0 = 0; a.lc0 = 0; a.lc1 = n; a.zrows = n; a.ldz = n;
+    a.wins = d_wins; a.win_begin = P.step_begin[s]; a.win_count = P.step_begin[s + 1] - P.step_begin[s];
+    a.coef = g.d_coef; a.KP = KP; a.QLD = QLD; a.slot_offset = (s % hqr::kQSets) * P.nchains; a.step = s;
+    const WindowDesc* hw = P.windows.data() + a.win_begin;
+    StepArgs aH = a, aHz = a, aT = a, aTz = a;
+    aH.H = H; aH.Z = Q; aH.qslots = g.d_q;     // left on H, Qacc Q_W
+    aHz.H = H; aHz.Z = nullptr; aHz.qslots = zslots;  // right on H rows above W with Z_W
+    aT.H = T; aT.Z = nullptr; aT.qslots = g.d_q;      // left on T
+    aTz.H = T; aTz.Z = Z; aTz.qslots = zslots;  // right on T rows above W, Zacc Z_W
+    CK(hqr::launch_qz_chase(aH, T, zslots, P.max_kw, A));
+    st.launches_chase++;
+    int64_t items;
+    double fl, by;
+    CK(hqr::launch_left(aH, hw, g.num_sms, tmA, A, &items, &fl, &by));
+    st.launches_left += items > 0; st.flops_update += fl; st.bytes_update += by;
+    CK(hqr::launch_left(aT, hw, g.num_sms, tmB, A, &items, &fl, &by));
+    st.launches_left += items > 0; st.flops_update += fl; st.bytes_update += by;
+    aHz.right_mode = 1;
+    CK(hqr::launch_right(aHz, hw, g.num_sms, tmA, A, &items, &fl, &by));
+    st.launches_right += items > 0; st.flops_update += fl; st.bytes_update += by;
+    aTz.right_mode = 1;
+    CK(hqr::launch_right(aTz, hw, g.num_sms, tmB, A, &items, &fl, &by));
+    st.launches_right += items > 0; st.flops_update += fl; st.bytes_update += by;
+    if (Q) {
+      aH.right_mode = 2;
+      CK(hqr::launch_right(aH, hw, g.num_sms, tmA, A, &items, &fl, &by));
+      st.launches_right += items > 0; st.flops_update += fl; st.bytes_update += by;
+    }
+    if (Z) {
+      aTz.right_mode = 2;
+      CK(hqr::launch_right(aTz, hw, g.num_sms, tmB, A, &items, &fl, &by));
+      st.launches_right += items > 0; st.flops_update += fl; st.bytes_update += by;
+    }
+  }
+  CK(cudaEventRecord(g.ev1, A));
+  CK(cudaStreamSynchronize(A));
+  CK(cudaGetLastError());
+  cudaFree(d_wins);
+  float ms = 0;
+  CK(cudaEventElapsedTime(&ms, g.ev0, g.ev1));
+  st.ms_total = ms;
+  st.steps = P.nsteps;
+  st.windows = (int64_t)P.windows.size();
+  st.kernels_launched = st.launches_chase + st.launches_left + st.launches_right;
+  g.stats = st;
+  g.wstats_plan = nullptr;  // flops_dmma is not tracked for the QZ sweep
+  return 0;
+}
+
 int hqr_get_aftermath(signed char* flags, int64_t n) {
   if (!flags) return -1;
   if (!g.ready || g.aft_n == 0) return -100;
@@ -1523,6 +1628,7 @@ const char* hqr_error_string(int code) {
   switch (code) {
     case 0: return "ok";
     case -1: return "H is NULL / invalid config";
+    case -2: return "T is NULL or T[ilo,ilo] / T[ilo+1,ilo+1] is zero (QZ)";
     case -3: return "n < 1";
     case -4: return "ilo < 0 or ilo > ihi";
     case -5: return "ihi >= n or active block shorter than 3";

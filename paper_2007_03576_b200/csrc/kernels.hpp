@@ -50,6 +50,12 @@ struct StepArgs {
 cudaError_t launch_chase(const StepArgs& a, int max_kw, int max_nbc, cudaStream_t st);
 size_t chase_smem_bytes(int kw, int nbc);
 
+// QZ (qz.cu): one CTA per window of the pair (H, T); Q_W to a.qslots, Z_W to zslots (same layout).
+cudaError_t launch_qz_chase(const StepArgs& a, double* T, double* zslots, int max_kw, cudaStream_t st);
+size_t qz_chase_smem_bytes(int kw);
+// Largest window side of the QZ chase (H, T, Q_W, Z_W all SMEM-resident: 4 k (k|1) doubles)
+constexpr int kMaxWindowQZ = 80;
+
 // 2-D TMA descriptors of H and Z (column-major, n x n) with the update kernels' SMEM boxes.
 // Valid only for even n (TMA global strides must be multiples of 16 bytes).
 struct TensorMaps {

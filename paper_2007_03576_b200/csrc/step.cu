@@ -212,7 +212,7 @@ __device__ void chase_window_9w(const StepArgs& a, const WindowDesc& W, int widx
     if (warp == 0) atomicAdd(&g_ctim[5], (unsigned long long)(W.t1 - W.t0 + 1));
   }
 #endif
-  aftermath_scan(Hs, ldh, W, a, threadIdx.x, kStepThreads);  // a9 (check only)
+  aftermath_scan(Hs, ldh, W, a.aftermath, threadIdx.x, kStepThreads);  // a9 (check only)
   {
     double* g = a.H + (int64_t)(w0 - a.hcol0) * n + w0;
     for (int c = warp; c < kw; c += kStepWarps) {
