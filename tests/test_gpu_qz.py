@@ -97,3 +97,15 @@ def test_qz_error_codes():
     with pytest.raises(hq.HQRError) as e:
         hq.qz_sweep(H, hq.to_device(T0), None, None, 0, n - 1, p.shifts_re, p.shifts_im, 16)
     assert e.value.code == -2
+
+
+def test_qz_parity_large():
+    """n = 4000, 100 shifts, window 80 (the bench's QZ window): many chains and wavefront steps."""
+    n = 4000
+    p, ilo, ihi = _case(n, 100, 11)
+    Hg, Tg, Qg, Zg = _run(p, ilo, ihi, 80)
+    Ho, To, Qo, Zo = _oracle(p, ilo, ihi)
+    assert np.linalg.norm(Hg - Ho) / np.linalg.norm(p.H) <= TOL
+    assert np.linalg.norm(Tg - To) / np.linalg.norm(p.T) <= TOL
+    assert np.linalg.norm(Qg - Qo) <= TOL * np.sqrt(n) and np.linalg.norm(Zg - Zo) <= TOL * np.sqrt(n)
+    assert np.all(np.tril(Hg, -2) == 0.0) and np.all(np.tril(Tg, -1) == 0.0)
