@@ -114,26 +114,7 @@ __global__ void __launch_bounds__(kChaseThreads, 1) chase_kernel(StepArgs a) {
           }
           if (tau != 0.0) {
             R.v1 = v1; R.v2 = v2; R.tau = tau; R.pl = pl; R.m = m;
-            const int c0 = (p == ilo - 1) ? 0 : pl + 1;
-            double* hrow = Hs + (pl + 1);
-            if (m == 3) {
-              for (int c = c0 + lane; c < kw; c += 32) {
-                double* hc = hrow + c * ldh;
-                const double h0 = hc[0], h1 = hc[1], h2 = hc[2];
-                const double tw = tau * fma(v2, h2, fma(v1, h1, h0));
-                hc[0] = h0 - tw;
-                hc[1] = fma(-tw, v1, h1);
-                hc[2] = fma(-tw, v2, h2);
-              }
-            } else {
-              for (int c = c0 + lane; c < kw; c += 32) {
-                double* hc = hrow + c * ldh;
-                const double h0 = hc[0], h1 = hc[1];
-                const double tw = tau * fma(v1, h1, h0);
-                hc[0] = h0 - tw;
-                hc[1] = fma(-tw, v1, h1);
-              }
-            }
+            left_apply(Hs + (pl + 1), ldh, (p == ilo - 1) ? 0 : pl + 1, kw, m, v1, v2, tau, lane);
           }
         }
         if (lane == 0) ring[slot][jj] = R;

@@ -145,6 +145,10 @@ __device__ __forceinline__ double rcp_nr(double q) {  // 1 / q, q != 0 normal
 }
 __device__ __forceinline__ void house(double x0, double x1, double x2, double& v1, double& v2,
                                       double& tau, double& beta) {
+#ifdef HQR_EXP_CHEAPHOUSE  // timing experiment only (wrong results): no reflector arithmetic
+  v1 = x1 * 0.5; v2 = x2 * 0.5; tau = (x1 != 0.0) ? 0.25 : 0.0; beta = x0;
+  return;
+#endif
   // R15 scale 2^-e, branch-free (the chase's critical path; registers are tight in the fused
   // kernel): for max|x| outside [2^-1022, 2^1021) -- entries the update GEMMs could not carry
   // either -- the unscaled formulas are used
@@ -235,8 +239,12 @@ __device__ __forceinline__ int q_first_row(const WindowDesc& W, int jj) {
 }
 
 // Apply reflector r from the right to `rows` rows of three (two) consecutive SMEM columns starting
-// at c1 (ld = ldh); lanes across rows.
+// at c1 (ld = ldh); lanes across rows.  (Batching two rows per lane before updating measured no
+// faster: phase 2 1232 vs 1141 cycles per step.)
 __device__ __forceinline__ void right_apply(double* c1, int ldh, int rows, const Refl& r, int lane) {
+#ifdef HQR_EXP_NOQ
+  if (rows > 64) return;  // timing experiment only (wrong results): skip long (Q_W) applications
+#endif
   if (r.m == 3) {
     for (int i = lane; i < rows; i += 32) {
       double* x = c1 + i;
@@ -257,6 +265,32 @@ __device__ __forceinline__ void right_apply(double* c1, int ldh, int rows, const
   }
 }
 
+// Apply reflector (v1, v2, tau; m = 3 or 2 rows) from the left to rows hrow[0..m-1] of the SMEM
+// columns c0..kw-1 (column-major, ld = ldh); lanes across columns.
+__device__ __forceinline__ void left_apply(double* hrow, int ldh, int c0, int kw, int m, double v1, double v2,
+                                           double tau, int lane) {
+#ifdef HQR_EXP_NOLEFT
+  return;  // timing experiment only (wrong results)
+#endif
+  if (m == 3) {
+    for (int c = c0 + lane; c < kw; c += 32) {
+      double* hc = hrow + c * ldh;
+      const double h0 = hc[0], h1 = hc[1], h2 = hc[2];
+      const double tw = tau * fma(v2, h2, fma(v1, h1, h0));
+      hc[0] = h0 - tw;
+      hc[1] = fma(-tw, v1, h1);
+      hc[2] = fma(-tw, v2, h2);
+    }
+  } else {
+    for (int c = c0 + lane; c < kw; c += 32) {
+      double* hc = hrow + c * ldh;
+      const double h0 = hc[0], h1 = hc[1];
+      const double tw = tau * fma(v1, h1, h0);
+      hc[0] = h0 - tw;
+      hc[1] = fma(-tw, v1, h1);
+    }
+  }
+}
 
 // Store the accumulated factor Q_W (kw x kw in SMEM, Qs[r + c*ldq]) into its workspace slot
 // (KP x QLD doubles, column-major, ld = QLD, zero padded), and record the support of every block of

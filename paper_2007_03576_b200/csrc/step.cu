@@ -135,7 +135,7 @@ __device__ void chase_window_9w(const StepArgs& a, const WindowDesc& W, int widx
   }
   __syncthreads();
 #ifdef HQR_TIMING
-  long long c_p1 = 0, c_s1 = 0, c_p2 = 0, c_s2 = 0, c_t = clock64();
+  long long c_p1 = 0, c_s1 = 0, c_p2 = 0, c_s2 = 0, c_pa = 0, c_pb = 0, c_t = clock64();
 #define CTIM(acc) do { const long long _c = clock64(); acc += _c - c_t; c_t = _c; } while (0)
 #else
 #define CTIM(acc) do { } while (0)
@@ -143,10 +143,14 @@ __device__ void chase_window_9w(const StepArgs& a, const WindowDesc& W, int widx
   const int rmaxH = ihi - w0;
   for (int t = W.t0; t <= W.t1; ++t) {
     const int rQ = min(ilo - 1 + t - w0 + 3, kw - 1);
+    // A warp's first bulge (jj = warp; every bulge when nbc <= kStepWarps, i.e. every multi-window
+    // chain) keeps its reflector in registers across the barrier; further bulges of a warp (a block
+    // that fits one window holds up to N/2 bulges) go through SMEM.
+    double rv1 = 0.0, rv2 = 0.0, rtau = 0.0;  // the first bulge's reflector (tau = 0: none)
     for (int jj = warp; jj < nbc; jj += kStepWarps) {
       const int p = ilo - 1 + t - 3 * jj;
       if (p < ilo - 1 || p > ihi - 2) {
-        if (lane == 0) R.pl[jj] = INT_MIN;
+        if (jj >= kStepWarps && lane == 0) R.pl[jj] = INT_MIN;
         continue;
       }
       const int pl = p - w0;
@@ -162,38 +166,33 @@ __device__ void chase_window_9w(const StepArgs& a, const WindowDesc& W, int widx
       }
       double v1, v2, tau, beta;
       house(x0, x1, x2, v1, v2, tau, beta);
+      CTIM(c_pa);
       __syncwarp();
-      if (lane == 0) {
-        if (p >= ilo) {
-          double* col = Hs + pl * ldh + pl;
-          col[1] = beta;
-          col[2] = 0.0;
-          if (m == 3) col[3] = 0.0;
-        }
-        R.v1[jj] = v1; R.v2[jj] = v2; R.tau[jj] = tau;
-        R.pl[jj] = (tau == 0.0) ? INT_MIN : pl;
-        R.m[jj] = m;
+      if (p >= ilo && lane < m) Hs[pl * ldh + pl + 1 + lane] = (lane == 0) ? beta : 0.0;  // beta, exact zeros
+      if (jj < kStepWarps) {
+        rv1 = v1; rv2 = v2; rtau = tau;
+      } else if (lane == 0) {
+        R.v1[jj] = v1; R.v2[jj] = v2; R.tau[jj] = tau; R.pl[jj] = (tau == 0.0) ? INT_MIN : pl; R.m[jj] = m;
       }
+      CTIM(c_pb);
       if (tau == 0.0) continue;
-      const int c0 = (p == ilo - 1) ? 0 : pl + 1;
-      double* hrow = Hs + (pl + 1);
-      for (int c = c0 + lane; c < kw; c += 32) {
-        double* hc = hrow + c * ldh;
-        const double h0 = hc[0], h1 = hc[1], h2 = (m == 3) ? hc[2] : 0.0;
-        const double tw = tau * fma(v2, h2, fma(v1, h1, h0));
-        hc[0] = h0 - tw;
-        hc[1] = fma(-tw, v1, h1);
-        if (m == 3) hc[2] = fma(-tw, v2, h2);
-      }
+      left_apply(Hs + (pl + 1), ldh, (p == ilo - 1) ? 0 : pl + 1, kw, m, v1, v2, tau, lane);
     }
     CTIM(c_p1);
     __syncthreads();
     CTIM(c_s1);
     for (int jj = warp; jj < nbc; jj += kStepWarps) {
       Refl r;
-      r.pl = R.pl[jj];
+      if (jj < kStepWarps) {
+        const int p = ilo - 1 + t - 3 * jj;
+        r.pl = (rtau == 0.0 || p < ilo - 1 || p > ihi - 2) ? INT_MIN : p - w0;
+        r.m = (p <= ihi - 3) ? 3 : 2;
+        r.v1 = rv1; r.v2 = rv2; r.tau = rtau;
+      } else {
+        r.pl = R.pl[jj];
+        r.v1 = R.v1[jj]; r.v2 = R.v2[jj]; r.tau = R.tau[jj]; r.m = R.m[jj];
+      }
       if (r.pl == INT_MIN) continue;
-      r.v1 = R.v1[jj]; r.v2 = R.v2[jj]; r.tau = R.tau[jj]; r.m = R.m[jj];
       right_apply(Hs + (r.pl + 1) * ldh, ldh, min(r.pl + r.m + 1, rmaxH) + 1, r, lane);
       const int q0 = q_first_row(W, jj);
       right_apply(Qs + (r.pl + 1) * ldh + q0, ldh, rQ + 1 - q0, r, lane);
@@ -208,6 +207,8 @@ __device__ void chase_window_9w(const StepArgs& a, const WindowDesc& W, int widx
     atomicAdd(&g_ctim[1], (unsigned long long)c_s1);
     atomicAdd(&g_ctim[2], (unsigned long long)c_p2);
     atomicAdd(&g_ctim[3], (unsigned long long)c_s2);
+    atomicAdd(&g_ctim[6], (unsigned long long)c_pa);
+    atomicAdd(&g_ctim[7], (unsigned long long)c_pb);
     if (warp == 0) atomicAdd(&g_ctim[4], 1ull);
     if (warp == 0) atomicAdd(&g_ctim[5], (unsigned long long)(W.t1 - W.t0 + 1));
   }
@@ -669,9 +670,10 @@ void debug_timing(int nsteps, bool reset) {
   }
   if (ct[4]) {
     const double w = (double)ct[4] * kStepWarps, st = (double)ct[5] / (double)ct[4];
-    fprintf(stderr, "hqr chase: %llu windows, %.1f steps each; cycles per step per warp: phase1 %.0f, "
-            "sync1 %.0f, phase2 %.0f, sync2 %.0f\n", ct[4], st, ct[0] / w / st, ct[1] / w / st,
-            ct[2] / w / st, ct[3] / w / st);
+    fprintf(stderr, "hqr chase: %llu windows, %.1f steps each; cycles per step per warp: phase1 %.0f "
+            "(vector load + house %.0f, beta / reflector stores %.0f, left application %.0f), "
+            "sync1 %.0f, phase2 %.0f, sync2 %.0f\n", ct[4], st, (ct[0] + ct[6] + ct[7]) / w / st,
+            ct[6] / w / st, ct[7] / w / st, ct[0] / w / st, ct[1] / w / st, ct[2] / w / st, ct[3] / w / st);
   }
   fprintf(stderr, "hqr timing: %d steps, mean launch %.1f us, chase start %.1f us, chase end %.1f us "
           "(%d steps with chases), mean gap between launches %.2f us\n", nsteps, e / nsteps,
