@@ -142,6 +142,25 @@ int hqr_qz_sweep(double* H, double* T, double* Q, double* Z, int64_t n, int64_t 
 #define HQR_MAX_WINDOW_QZ 80
 
 /*
+ * QR iteration around the sweep (partial: shift generation and deflation
+ * without the paper's AED window, R21):
+ * repeatedly (a) take the bottom unreduced block [l, hi] of [ilo, ihi] (h(l, l-1) = 0); (b) if it has
+ * at most nmin rows, compute its eigenvalues with the one-CTA Francis double-shift QR solver and
+ * continue above it; (c) else sweep it (hqr_sweep's fused path, window `window`) with the
+ * eigenvalues of its trailing nshifts x nshifts block as shifts (complex pairs first, then reals
+ * paired), then set every subdiagonal entry with |h(k,k-1)| <= 2^-52 (|h(k-1,k-1)| + |h(k,k)|) to
+ * zero (deflation).  H, Z (Z may be NULL) are n x n device matrices updated by every sweep, so on
+ * return Z^T H0 Z = H (Z0 = I) with H reduced to blocks of at most nmin rows.  wr, wi: host arrays of
+ * n doubles receiving the eigenvalues of rows ilo..ihi (conjugate pairs adjacent).  *sweeps_out
+ * (nullable): sweeps run.  Returns 0; > 0 = ihi' + 1 when max_sweeps was reached with rows
+ * ilo..ihi' unfinished (LAPACK INFO style); -1 H NULL / host pointer / world > 1; -3 n; -4 ilo;
+ * -5 ihi; -6 nshifts odd, < 2 or > 128; -7 window < 1; -8 nmin < 2 or > 128; -10 wr / wi NULL;
+ * -100 not set up; 1000+cudaError_t.
+ */
+int hqr_qr_iterate(double* H, double* Z, int64_t n, int64_t ilo, int64_t ihi, int nshifts, int window,
+                   int nmin, int max_sweeps, double* wr, double* wi, int* sweeps_out);
+
+/*
  * ---- Sharded sweep over several GPUs -------------------------------------------
  * Layout for `world` ranks (one process per GPU): rank r owns H columns [cb[r], cb[r+1]) -- all n
  * rows, column-major, ld = n -- and must allocate `halo` further columns after them (work space for

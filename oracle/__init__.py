@@ -16,6 +16,10 @@ Functions and the passages they follow (PAPER.md line numbers, see hqr_oracle.c)
   rhs_house(r)             -- right-hand side reflector r P = beta e_m^T (reading R18)
   qz_first_column(H, T ..) -- (H T^-1 - s I)(H T^-1 - s' I) e1, P:209 (reading R17)
   qz_sweep(H, T, Q, Z, ..) -- nshifts/2 sequential double-shift QZ steps
+  small_eig(A)             -- eigenvalues of a small Hessenberg matrix, Francis double-shift QR
+                              (the small Schur task's role; reading R21)
+  qr_iterate(H, Z, ..)     -- repeated sweeps with shifts from the trailing block and deflation
+                              (NEXT-2 without AED; reading R21)
 
 Parity pins for every function are in tests/test_oracle.py (none is "parity unpinned").
 """
@@ -73,6 +77,12 @@ def _load():
         lib.oracle_qz_sweep.argtypes = [ctypes.c_void_p] * 4 + [ctypes.c_int64] * 3 + [dp, dp, ctypes.c_int,
                                                                                        ctypes.c_int]
         lib.oracle_qz_sweep.restype = ctypes.c_int
+        lib.oracle_small_eig.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, dp, dp]
+        lib.oracle_small_eig.restype = ctypes.c_int
+        lib.oracle_qr_iterate.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64,
+                                          ctypes.c_int64, ctypes.c_int, ctypes.c_int64, ctypes.c_int, dp, dp,
+                                          ctypes.POINTER(ctypes.c_int)]
+        lib.oracle_qr_iterate.restype = ctypes.c_int
         _lib = lib
     return _lib
 
@@ -179,3 +189,23 @@ def qz_sweep(H, T, Q, Z, ilo, ihi, shifts_re, shifts_im, bulges=None):
     j0, j1 = bulges if bulges is not None else (0, sr.shape[0] // 2)
     _load().oracle_qz_sweep(H.ctypes.data, T.ctypes.data, None if Q is None else Q.ctypes.data,
                             None if Z is None else Z.ctypes.data, n, ilo, ihi, _dptr(sr), _dptr(si), j0, j1)
+
+
+def small_eig(A):
+    """Eigenvalues (wr, wi, info) of the small upper-Hessenberg matrix A (not modified)."""
+    B = np.asfortranarray(np.array(A, dtype=np.float64))
+    m = B.shape[0]
+    wr, wi = np.zeros(m), np.zeros(m)
+    info = _load().oracle_small_eig(B.ctypes.data, m, m, _dptr(wr), _dptr(wi))
+    return wr, wi, info
+
+
+def qr_iterate(H, Z, ilo, ihi, nshifts, nmin=64, max_sweeps=1000):
+    """In place: the QR iteration of R21 on H (and Z).  Returns (wr, wi, rc, sweeps)."""
+    H = _as_colmajor(H)
+    n = H.shape[0]
+    wr, wi = np.zeros(n), np.zeros(n)
+    sw = ctypes.c_int()
+    rc = _load().oracle_qr_iterate(H.ctypes.data, None if Z is None else _as_colmajor(Z).ctypes.data, n, ilo,
+                                   ihi, nshifts, nmin, max_sweeps, _dptr(wr), _dptr(wi), ctypes.byref(sw))
+    return wr, wi, rc, sw.value

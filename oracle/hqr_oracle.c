@@ -302,3 +302,187 @@ int oracle_qz_sweep(double* H, double* T, double* Qa, double* Za, int64_t n, int
     for (int64_t p = ilo - 1; p <= ihi - 2; ++p) qz_apply_one(H, T, Qa, Za, n, ilo, ihi, p, sr, si, j);
   return 0;
 }
+
+/* ===================================================================================================
+ * QR iteration (partial; PAPER.md P:270-297 shifts, P:370-381 deflation,
+ * P:1142-1189 deflation criteria): repeated sweeps whose shifts are the eigenvalues of the trailing
+ * nshifts x nshifts block of the active block, with the small-subdiagonal deflation test after every
+ * sweep.  (The paper's AED -- deflating eigenvalues of the trailing window through the spike and
+ * reordering -- is not reproduced: reading R21.)  Test infrastructure like the rest of this file.
+ * =================================================================================================== */
+
+/* Eigenvalues of a 2x2 block [[a, b], [c, d]] (reading R21): tr/2 +- sqrt((a-d)^2/4 + bc); a
+ * real pair is returned larger-magnitude root first computed as tr/2 + sign(tr/2) sqrt(disc) and
+ * the other as det / that root (no cancellation); a complex pair as re +- i im. */
+static void eig2(double a, double b, double c, double d, double* wr1, double* wi1, double* wr2, double* wi2) {
+  const double h = 0.5 * (a + d);
+  const double q = 0.5 * (a - d);
+  const double disc = q * q + b * c;
+  if (disc >= 0.0) {
+    const double r = sqrt(disc);
+    const double l1 = (h >= 0.0) ? h + r : h - r;
+    const double det = a * d - b * c;
+    const double l2 = (l1 != 0.0) ? det / l1 : h - (l1 - h);
+    *wr1 = l1; *wi1 = 0.0; *wr2 = l2; *wi2 = 0.0;
+  } else {
+    const double im = sqrt(-disc);
+    *wr1 = h; *wi1 = im; *wr2 = h; *wi2 = -im;
+  }
+}
+
+/* Eigenvalues of the m x m upper-Hessenberg matrix A (column-major, ld lda; overwritten) by the
+ * textbook Francis double-shift QR iteration with deflation (Golub & Van Loan Alg. 7.5.2, the
+ * paper's small Schur task P:367-372 uses LAPACK's DHSEQR for this), eigenvalues only: reflectors
+ * act on the active block [l, i] only.  Deflation test R16 (|h(k,k-1)| <= 2^-52 (|h(k-1,k-1)| +
+ * |h(k,k)|) -> 0); exceptional shifts after 10 and 20 iterations without deflation.
+ * Returns 0, or the number of eigenvalues not found (iteration limit 30 m). */
+int oracle_small_eig(double* A, int64_t m, int64_t lda, double* wr, double* wi) {
+#define A_(r, c) A[(size_t)(r) + (size_t)(c) * (size_t)lda]
+  int64_t i = m - 1;
+  int64_t total = 0;
+  while (i >= 0) {
+    int its = 0;
+    int64_t l = 0;
+    for (;;) {
+      /* deflation: the lowest negligible subdiagonal of the active part */
+      for (l = i; l > 0; --l) {
+        const double s = fabs(A_(l - 1, l - 1)) + fabs(A_(l, l));
+        if (fabs(A_(l, l - 1)) <= 0x1p-52 * s) {
+          A_(l, l - 1) = 0.0;
+          break;
+        }
+      }
+      if (l >= i - 1) break;
+      if (++total > 30 * m) return (int)(i + 1);
+      ++its;
+      double sigma, pi;
+      if (its == 10 || its == 20) { /* exceptional shift (as LAPACK's dlahqr) */
+        const double s = fabs(A_(i, i - 1)) + fabs(A_(i - 1, i - 2));
+        const double h11 = 0.75 * s + A_(i, i);
+        sigma = 2.0 * h11;
+        pi = h11 * h11 + 0.4375 * s * s;
+      } else { /* the trailing 2x2 block's eigenvalues (Francis) */
+        const double a = A_(i - 1, i - 1), b = A_(i - 1, i), c = A_(i, i - 1), d = A_(i, i);
+        sigma = a + d;
+        pi = a * d - b * c;
+      }
+      /* double-shift sweep on [l, i] */
+      for (int64_t p = l - 1; p <= i - 2; ++p) {
+        const int mm = (p <= i - 3) ? 3 : 2;
+        double x[3], v[3], tau, beta;
+        if (p == l - 1) {
+          const double h00 = A_(l, l), h01 = A_(l, l + 1), h10 = A_(l + 1, l), h11 = A_(l + 1, l + 1);
+          const double h21 = A_(l + 2, l + 1);
+          x[0] = h00 * (h00 - sigma) + h01 * h10 + pi;
+          x[1] = h10 * (h00 + h11 - sigma);
+          x[2] = h10 * h21;
+        } else {
+          for (int k = 0; k < mm; ++k) x[k] = A_(p + 1 + k, p);
+        }
+        oracle_house(mm, x, v, &tau, &beta);
+        const int64_t c0 = (p == l - 1) ? l : p + 1;
+        for (int64_t c = c0; c <= i; ++c) {
+          double w = 0.0;
+          for (int k = 0; k < mm; ++k) w += v[k] * A_(p + 1 + k, c);
+          for (int k = 0; k < mm; ++k) A_(p + 1 + k, c) -= tau * v[k] * w;
+        }
+        if (p >= l) {
+          A_(p + 1, p) = beta;
+          for (int k = 1; k < mm; ++k) A_(p + 1 + k, p) = 0.0;
+        }
+        const int64_t r1 = (p + mm + 1 < i) ? p + mm + 1 : i;
+        for (int64_t r = l; r <= r1; ++r) {
+          double w = 0.0;
+          for (int k = 0; k < mm; ++k) w += A_(r, p + 1 + k) * v[k];
+          for (int k = 0; k < mm; ++k) A_(r, p + 1 + k) -= tau * w * v[k];
+        }
+      }
+    }
+    if (l == i) {
+      wr[i] = A_(i, i);
+      wi[i] = 0.0;
+      i -= 1;
+    } else {
+      eig2(A_(i - 1, i - 1), A_(i - 1, i), A_(i, i - 1), A_(i, i), &wr[i - 1], &wi[i - 1], &wr[i], &wi[i]);
+      i -= 2;
+    }
+  }
+#undef A_
+  return 0;
+}
+
+/* Shifts from m eigenvalues (R21): the complex pairs in the order found (positive imaginary part
+ * first, its exact conjugate next), then the real ones paired in the order found; at most ns
+ * (even).  Returns the number of shifts written (even). */
+static int make_shifts(const double* wr, const double* wi, int64_t m, int ns, double* sr, double* si) {
+  int k = 0;
+  /* complex pairs as they appear (wi > 0 followed by its conjugate), then reals in pairs */
+  for (int64_t j = 0; j < m && k + 1 < ns; ++j)
+    if (wi[j] > 0.0) {
+      sr[k] = wr[j]; si[k] = wi[j]; sr[k + 1] = wr[j]; si[k + 1] = -wi[j];
+      k += 2;
+    }
+  int64_t pending = -1;
+  for (int64_t j = 0; j < m && k + 1 < ns; ++j)
+    if (wi[j] == 0.0) {
+      if (pending < 0) {
+        pending = j;
+      } else {
+        sr[k] = wr[pending]; si[k] = 0.0; sr[k + 1] = wr[j]; si[k + 1] = 0.0;
+        k += 2;
+        pending = -1;
+      }
+    }
+  return k;
+}
+
+/* The QR iteration on H (n x n, active block [ilo, ihi]) with Z: until every unreduced block is at
+ * most nmin long, sweep the bottom unreduced block [l, hi] with the eigenvalues of its trailing
+ * nshifts x nshifts block as shifts (oracle_sweep), then set negligible subdiagonals (R16) to zero;
+ * the eigenvalues of the remaining small blocks by oracle_small_eig.  wr / wi: n entries (rows
+ * outside [ilo, ihi] untouched).  Returns 0, or -(sweeps) when max_sweeps was reached. */
+int oracle_qr_iterate(double* H, double* Z, int64_t n, int64_t ilo, int64_t ihi, int nshifts, int64_t nmin,
+                      int max_sweeps, double* wr, double* wi, int* sweeps_out) {
+  int sweeps = 0;
+  int64_t hi = ihi;
+  double* work = (double*)malloc(sizeof(double) * (size_t)(nshifts * nshifts + 4 * nshifts + nmin * nmin + 8));
+  while (hi >= ilo) {
+    int64_t l = hi;
+    while (l > ilo && EL(H, l, l - 1, n) != 0.0) --l;
+    const int64_t N = hi - l + 1;
+    if (N <= nmin) {
+      double* B = work;
+      for (int64_t c = 0; c < N; ++c)
+        for (int64_t r = 0; r < N; ++r) B[r + c * N] = EL(H, l + r, l + c, n);
+      oracle_small_eig(B, N, N, wr + l, wi + l);
+      hi = l - 1;
+      continue;
+    }
+    if (sweeps >= max_sweeps) {
+      free(work);
+      *sweeps_out = sweeps;
+      return -sweeps;
+    }
+    int ns = nshifts;
+    if (ns > N - 2) ns = (int)((N - 2) & ~(int64_t)1);
+    if (ns < 2) ns = 2;
+    double* B = work;
+    double* ewr = B + (size_t)ns * ns;
+    double* ewi = ewr + ns;
+    double* sr = ewi + ns;
+    double* si = sr + ns;
+    for (int c = 0; c < ns; ++c)
+      for (int r = 0; r < ns; ++r) B[r + c * ns] = EL(H, hi - ns + 1 + r, hi - ns + 1 + c, n);
+    oracle_small_eig(B, ns, ns, ewr, ewi);
+    const int k = make_shifts(ewr, ewi, ns, ns, sr, si);
+    oracle_sweep(H, Z, n, l, hi, sr, si, k, 0, 0, k / 2);
+    ++sweeps;
+    for (int64_t r = l + 1; r <= hi; ++r) { /* deflation (R16 criterion), after the sweep */
+      const double s = fabs(EL(H, r - 1, r - 1, n)) + fabs(EL(H, r, r, n));
+      if (fabs(EL(H, r, r - 1, n)) <= 0x1p-52 * s) EL(H, r, r - 1, n) = 0.0;
+    }
+  }
+  free(work);
+  *sweeps_out = sweeps;
+  return 0;
+}

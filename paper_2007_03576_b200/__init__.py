@@ -70,7 +70,7 @@ class Stats(ctypes.Structure):
 SYMBOLS = ["hqr_setup", "hqr_sweep", "hqr_sweep_multi", "hqr_teardown", "hqr_plan_query",
            "hqr_plan_query_multi", "hqr_get_stats", "hqr_error_string", "hqr_dist_layout",
            "hqr_dist_query", "hqr_nccl_unique_id", "hqr_sweep_dist", "hqr_sweep_virtual",
-           "hqr_get_aftermath", "hqr_sweeps", "hqr_plan_query_sweeps", "hqr_qz_sweep"]
+           "hqr_get_aftermath", "hqr_sweeps", "hqr_plan_query_sweeps", "hqr_qz_sweep", "hqr_qr_iterate"]
 
 
 def lib():
@@ -130,6 +130,10 @@ def lib():
         L.hqr_qz_sweep.argtypes = [ctypes.c_void_p] * 4 + [ctypes.c_int64] * 3 + [
             ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int]
         L.hqr_qz_sweep.restype = ctypes.c_int
+        L.hqr_qr_iterate.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64,
+                                     ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                     ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
+        L.hqr_qr_iterate.restype = ctypes.c_int
         L.hqr_get_aftermath.argtypes = [ctypes.c_void_p, ctypes.c_int64]
         L.hqr_get_aftermath.restype = ctypes.c_int
         L.hqr_get_stats.argtypes = [ctypes.POINTER(Stats)]
@@ -278,6 +282,21 @@ def qz_sweep(H, T, Q, Z, ilo: int, ihi: int, shifts_re, shifts_im, window: int =
                             int(window))
     if rc:
         raise HQRError(rc, "hqr_qz_sweep")
+
+
+def qr_iterate(H, Z, ilo: int, ihi: int, nshifts: int = 32, window: int = DEFAULT_WINDOW, nmin: int = 64,
+               max_sweeps: int = 10000):
+    """QR iteration (include/hqr.h hqr_qr_iterate) on device H (and Z): returns (wr, wi, info,
+    sweeps) with the eigenvalues of rows ilo..ihi in wr / wi."""
+    hp, n = _ptr_n(H)
+    zp, _ = _ptr_n(Z)
+    wr, wi = np.zeros(n), np.zeros(n)
+    sw = ctypes.c_int()
+    rc = lib().hqr_qr_iterate(hp, zp, n, ilo, ihi, int(nshifts), int(window), int(nmin), int(max_sweeps),
+                              wr.ctypes.data, wi.ctypes.data, ctypes.byref(sw))
+    if rc < 0:
+        raise HQRError(rc, "hqr_qr_iterate")
+    return wr, wi, rc, sw.value
 
 
 def dist_layout(n: int, world: int):

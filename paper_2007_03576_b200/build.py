@@ -9,7 +9,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libhqr_b200.so")
-SOURCES = ["hqr_api.cu", "chase.cu", "update.cu", "step.cu", "qz.cu"]
+SOURCES = ["hqr_api.cu", "chase.cu", "update.cu", "step.cu", "qz.cu", "qriter.cu"]
 HEADERS = ["plan.hpp", "kernels.hpp", "dist.hpp", "device_common.cuh", "gemm_tile.cuh", "step.hpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 

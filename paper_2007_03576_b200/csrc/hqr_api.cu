@@ -1594,6 +1594,108 @@ int hqr_qz_sweep(double* H, double* T, double* Q, double* Z, int64_t n, int64_t 
   return 0;
 }
 
+// ================================================================================================
+// QR iteration (partial, reading R21): sweeps of the bottom unreduced block
+// with the eigenvalues of its trailing nshifts x nshifts block as shifts, deflation after each
+// sweep, small blocks solved by the one-CTA Francis QR (qriter.cu).  The sweep is hqr_sweep's
+// product path (fused persistent kernel).  The host only orchestrates (finds the block from the
+// subdiagonal, pairs the shifts, loops).
+// ================================================================================================
+namespace {
+int make_shifts_host(const double* wr, const double* wi, int m, int ns, double* sr, double* si) {
+  int k = 0;  // complex pairs in the order found, then the reals paired in the order found (R21)
+  for (int j = 0; j < m && k + 1 < ns; ++j)
+    if (wi[j] > 0.0) {
+      sr[k] = wr[j]; si[k] = wi[j]; sr[k + 1] = wr[j]; si[k + 1] = -wi[j];
+      k += 2;
+    }
+  int pending = -1;
+  for (int j = 0; j < m && k + 1 < ns; ++j)
+    if (wi[j] == 0.0) {
+      if (pending < 0) {
+        pending = j;
+      } else {
+        sr[k] = wr[pending]; si[k] = 0.0; sr[k + 1] = wr[j]; si[k + 1] = 0.0;
+        k += 2;
+        pending = -1;
+      }
+    }
+  return k;
+}
+}  // namespace
+
+int hqr_qr_iterate(double* H, double* Z, int64_t n, int64_t ilo, int64_t ihi, int nshifts, int window,
+                   int nmin, int max_sweeps, double* wr, double* wi, int* sweeps_out) {
+  if (!H) return -1;
+  if (n < 1) return -3;
+  if (ilo < 0 || ilo > ihi) return -4;
+  if (ihi >= n) return -5;
+  if (nshifts < 2 || (nshifts & 1) || nshifts > hqr::small_eig_max()) return -6;
+  if (window < 1) return -7;
+  if (nmin < 2 || nmin > hqr::small_eig_max()) return -8;
+  if (!wr || !wi) return -10;
+  if (!g.ready) return -100;
+  if (g.world > 1) return -1;
+  CK(cudaSetDevice(g.device));
+  if (!is_device_ptr(H) || (Z && !is_device_ptr(Z))) return -1;
+  double* d_w = nullptr;  // 2 * small_eig_max() eigenvalue scratch + info / counters
+  CK(cudaMalloc(&d_w, (2 * (size_t)hqr::small_eig_max() + 2) * sizeof(double)));
+  int* d_info = reinterpret_cast<int*>(d_w + 2 * hqr::small_eig_max());
+  std::vector<double> sub((size_t)std::max<int64_t>(n - 1, 1)), ewr(nshifts), ewi(nshifts), sr(nshifts), si(nshifts);
+  int sweeps = 0, rc = 0;
+  int64_t hi = ihi;
+  auto fail = [&](int code) { cudaFree(d_w); return code; };
+  while (hi >= ilo) {
+    // the bottom unreduced block [l, hi]: the subdiagonal h(k, k-1), k = ilo+1 .. hi (stride n+1)
+    int64_t l = hi;
+    if (hi > ilo) {
+      const int64_t cnt = hi - ilo;
+      cudaError_t e = cudaMemcpy2D(sub.data(), sizeof(double), H + (ilo + 1) + ilo * n, (n + 1) * sizeof(double),
+                                   sizeof(double), (size_t)cnt, cudaMemcpyDeviceToHost);
+      if (e != cudaSuccess) return fail(cuerr(e));
+      while (l > ilo && sub[(size_t)(l - 1 - ilo)] != 0.0) --l;
+    }
+    const int64_t N = hi - l + 1;
+    if (N <= nmin) {  // small block: its eigenvalues directly
+      cudaError_t e = hqr::launch_small_eig(H, n, l, (int)N, d_w, d_w + hqr::small_eig_max(), d_info, g.stream);
+      if (e == cudaSuccess) e = cudaMemcpyAsync(wr + l, d_w, N * sizeof(double), cudaMemcpyDeviceToHost, g.stream);
+      if (e == cudaSuccess)
+        e = cudaMemcpyAsync(wi + l, d_w + hqr::small_eig_max(), N * sizeof(double), cudaMemcpyDeviceToHost, g.stream);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(g.stream);
+      if (e != cudaSuccess) return fail(cuerr(e));
+      hi = l - 1;
+      continue;
+    }
+    if (sweeps >= max_sweeps) {
+      rc = (int)(hi + 1);  // LAPACK-style: the eigenvalues of rows ilo..hi were not found
+      break;
+    }
+    int ns = (int)std::min<int64_t>(nshifts, (N - 2) & ~(int64_t)1);
+    if (ns < 2) ns = 2;
+    cudaError_t e = hqr::launch_small_eig(H, n, hi - ns + 1, ns, d_w, d_w + hqr::small_eig_max(), d_info, g.stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(ewr.data(), d_w, ns * sizeof(double), cudaMemcpyDeviceToHost, g.stream);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(ewi.data(), d_w + hqr::small_eig_max(), ns * sizeof(double), cudaMemcpyDeviceToHost, g.stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(g.stream);
+    if (e != cudaSuccess) return fail(cuerr(e));
+    const int k = make_shifts_host(ewr.data(), ewi.data(), ns, ns, sr.data(), si.data());
+    if (k < 2) {
+      rc = (int)(hi + 1);
+      break;
+    }
+    const int src = sweep_impl(H, Z, n, make_blocks(1, &l, &hi, &k), sr.data(), si.data(), window);
+    if (src) return fail(src);
+    ++sweeps;
+    CK(cudaMemsetAsync(d_info + 1, 0, sizeof(int), g.stream));
+    e = hqr::launch_deflate(H, n, l, hi, d_info + 1, g.stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(g.stream);
+    if (e != cudaSuccess) return fail(cuerr(e));
+  }
+  cudaFree(d_w);
+  if (sweeps_out) *sweeps_out = sweeps;
+  return rc;
+}
+
 int hqr_get_aftermath(signed char* flags, int64_t n) {
   if (!flags) return -1;
   if (!g.ready || g.aft_n == 0) return -100;

@@ -56,6 +56,13 @@ size_t qz_chase_smem_bytes(int kw);
 // Largest window side of the QZ chase (H, T, Q_W, Z_W all SMEM-resident: 4 k (k|1) doubles)
 constexpr int kMaxWindowQZ = 80;
 
+// QR iteration pieces (qriter.cu): eigenvalues of a small Hessenberg block H(r0:r0+m, r0:r0+m)
+// (one CTA, m <= small_eig_max(); *info = 0 or the number not found) and the deflation step.
+int small_eig_max();
+cudaError_t launch_small_eig(const double* H, int64_t n, int64_t r0, int m, double* wr, double* wi, int* info,
+                             cudaStream_t st);
+cudaError_t launch_deflate(double* H, int64_t n, int64_t lo, int64_t hi, int* count, cudaStream_t st);
+
 // 2-D TMA descriptors of H and Z (column-major, n x n) with the update kernels' SMEM boxes.
 // Valid only for even n (TMA global strides must be multiples of 16 bytes).
 struct TensorMaps {
