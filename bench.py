@@ -221,6 +221,56 @@ def run_qz(args):
     print(json.dumps(line), flush=True)
 
 
+def run_qriter(args):
+    """--workload qriter: hqr_qr_iterate to all eigenvalues (one call per step), single GPU."""
+    import torch
+    import paper_2007_03576_b200 as hq
+    from hqr_inputs import hessenberg, orthogonal
+    n = args.n or 4000
+    ns, nmin = 64, 96
+    H0 = hessenberg(n, "n01", 7)
+    Z0 = np.asfortranarray(np.eye(n))
+    hq.setup(0)
+    src = [hq.to_device(A) for A in (H0, Z0)]
+    work = [torch.empty_like(A.t()).t() for A in src]
+
+    def restore():
+        for w, s0 in zip(work, src):
+            w.t().copy_(s0.t())
+
+    for _ in range(args.warmup):
+        restore()
+        hq.qr_iterate(work[0], work[1], 0, n - 1, nshifts=ns, window=args.window, nmin=nmin)
+    torch.cuda.synchronize()
+    clk = Clocks(0)
+    wall, dev, sweeps, falg = [], [], [], []
+    for _ in range(args.steps):
+        restore()
+        torch.cuda.synchronize()
+        t = time.perf_counter()
+        wr, wi, rc, sw = hq.qr_iterate(work[0], work[1], 0, n - 1, nshifts=ns, window=args.window, nmin=nmin)
+        wall.append(time.perf_counter() - t)
+        st = hq.stats()
+        dev.append(st["ms_total"])
+        sweeps.append(sw)
+        falg.append(st["flops_alg"])
+        assert rc == 0
+    clocks = clk.stop()
+    hq.teardown()
+    ms = float(np.mean(dev))
+    line = {"metric": METRIC, "value": float(np.mean(falg)) / (ms * 1e-3) / 1e9, "unit": "GFLOP/s", "n_gpus": 1,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded N(0,1) upper Hessenberg, U[0.5,1.5] subdiagonal)",
+            "config": {"workload": f"QR iteration (NEXT-2 without AED) to all eigenvalues, n={n}, {ns} shifts per "
+                                   f"sweep, blocks <= {nmin} by the one-CTA solver", "n": n, "nshifts": ns,
+                       "window": args.window, "parallelism": "1 GPU"},
+            "seconds_to_eigenvalues_wall": float(np.mean(wall)), "sweeps": float(np.mean(sweeps)),
+            "gflops_alg_over_sweeps": float(np.mean(falg)) / (ms * 1e-3) / 1e9,
+            "roofline": None, "clocks": clocks, "cpu_baseline": None, "e2e": None, "gpu_launches": None}
+    print(json.dumps(line), flush=True)
+
+
 def run_reference(args, cfg_idx):
     """--impl reference: the oracle timed as it stands on the host cores."""
     rank = int(os.environ.get("RANK", "0"))
@@ -263,10 +313,12 @@ def main():
     ap.add_argument("--sweeps", type=int, default=1,
                     help="NEXT-1: this many overlapped sweeps per step (hqr_sweeps), shift set 0 = the "
                          "config's, the others drawn from the same distribution")
-    ap.add_argument("--workload", default="config", choices=["config", "hess", "qz"],
+    ap.add_argument("--workload", default="config", choices=["config", "hess", "qz", "qriter"],
                     help="hess: the paper's hess_n matrix (NEXT-3) at --n (default 10000), 256 shifts; "
                          "qz: the generalized sweep (NEXT-4) on a Hessenberg-triangular pair at --n "
-                         "(default 10000), 256 shifts, window 80")
+                         "(default 10000), 256 shifts, window 80; qriter: the QR iteration (NEXT-2 without AED) "
+                         "to all eigenvalues of a random Hessenberg matrix at --n (default 4000), 64 shifts "
+                         "per sweep")
     args = ap.parse_args()
 
     if args.impl == "reference":
@@ -279,6 +331,9 @@ def main():
 
     if args.workload == "qz":
         run_qz(args)
+        return
+    if args.workload == "qriter":
+        run_qriter(args)
         return
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

@@ -259,6 +259,9 @@ typedef struct hqr_stats {
   double flops_dmma;          /* executed FP64 tensor-core flops of the last single-GPU sweep: the
                                  update GEMMs restricted to the band extents the kernels multiply
                                  (computed on demand by hqr_get_stats; 0 if unavailable)           */
+  double flops_alg;           /* design-independent F_alg (every reflector applied directly, SURVEY
+                                 Appendix B) of the last call's sweeps; hqr_qr_iterate: summed over
+                                 its sweeps                                                          */
 } hqr_stats;
 
 int hqr_get_stats(hqr_stats* out);

@@ -839,6 +839,19 @@ int hqr_teardown(void) {
 
 namespace {
 
+// F_alg of nb bulges on [ilo, ihi]: per reflector 10 (6 for the final 2-reflector)
+// x (left columns + right rows + n Z rows)
+double falg_block(int64_t n, int64_t ilo, int64_t ihi, int nb, bool with_z) {
+  double f = 0.0;
+  for (int64_t p = ilo - 1; p <= ihi - 2; ++p) {
+    const int m = (p <= ihi - 3) ? 3 : 2;
+    const int64_t c0 = (p == ilo - 1) ? ilo : p + 1;
+    const int64_t r1 = std::min<int64_t>(p + m + 1, ihi);
+    f += (m == 3 ? 10.0 : 6.0) * ((double)(n - c0) + (double)(r1 + 1) + (with_z ? (double)n : 0.0));
+  }
+  return f * nb;
+}
+
 int sweep_impl(double* H, double* Z, int64_t n, const Blocks& blocks, const double* shifts_re,
                const double* shifts_im, int window) {
   if (!H) return -1;
@@ -1041,6 +1054,8 @@ int sweep_impl(double* H, double* Z, int64_t n, const Blocks& blocks, const doub
     cp->flops_chase = f;
   }
   st.flops_chase = cp->flops_chase;
+  st.flops_alg = 0.0;  // F_alg of every block of this call
+  for (int i = 0; i < blocks.count(); ++i) st.flops_alg += falg_block(n, blocks.ilo[i], blocks.ihi[i], blocks.nshifts[i] / 2, Z != nullptr);
   g.stats = st;
   return 0;
 }
@@ -1644,7 +1659,12 @@ int hqr_qr_iterate(double* H, double* Z, int64_t n, int64_t ilo, int64_t ihi, in
   std::vector<double> sub((size_t)std::max<int64_t>(n - 1, 1)), ewr(nshifts), ewi(nshifts), sr(nshifts), si(nshifts);
   int sweeps = 0, rc = 0;
   int64_t hi = ihi;
-  auto fail = [&](int code) { cudaFree(d_w); return code; };
+  double falg = 0.0;
+  cudaEvent_t t0 = nullptr, t1 = nullptr;
+  CK(cudaEventCreate(&t0));
+  CK(cudaEventCreate(&t1));
+  CK(cudaEventRecord(t0, g.stream));
+  auto fail = [&](int code) { cudaFree(d_w); cudaEventDestroy(t0); cudaEventDestroy(t1); return code; };
   while (hi >= ilo) {
     // the bottom unreduced block [l, hi]: the subdiagonal h(k, k-1), k = ilo+1 .. hi (stride n+1)
     int64_t l = hi;
@@ -1685,13 +1705,23 @@ int hqr_qr_iterate(double* H, double* Z, int64_t n, int64_t ilo, int64_t ihi, in
     }
     const int src = sweep_impl(H, Z, n, make_blocks(1, &l, &hi, &k), sr.data(), si.data(), window);
     if (src) return fail(src);
+    falg += g.stats.flops_alg;
     ++sweeps;
     CK(cudaMemsetAsync(d_info + 1, 0, sizeof(int), g.stream));
     e = hqr::launch_deflate(H, n, l, hi, d_info + 1, g.stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(g.stream);
     if (e != cudaSuccess) return fail(cuerr(e));
   }
+  CK(cudaEventRecord(t1, g.stream));
+  CK(cudaEventSynchronize(t1));
+  float ms = 0.0f;
+  cudaEventElapsedTime(&ms, t0, t1);
   cudaFree(d_w);
+  cudaEventDestroy(t0);
+  cudaEventDestroy(t1);
+  g.stats.ms_total = ms;  // the whole iteration (device time of the library stream)
+  g.stats.flops_alg = falg;
+  g.stats.steps = sweeps;
   if (sweeps_out) *sweeps_out = sweeps;
   return rc;
 }
