@@ -407,9 +407,16 @@ def main():
             H.copy_(H0)
             Z.copy_(Z0)
 
-        def one():
-            hq.sweep_dist(H.data_ptr(), Z.data_ptr(), n, prob.ilo, prob.ihi, prob.shifts_re,
-                          prob.shifts_im, args.window)
+        if len(prob.blocks) > 1:  # configs[4]: decoupled blocks, sharded (hqr_sweep_dist_multi)
+            blocks = [(b[0], b[1], b[3]) for b in prob.blocks]
+
+            def one():
+                hq.sweep_dist_multi(H.data_ptr(), Z.data_ptr(), n, blocks, prob.shifts_re, prob.shifts_im,
+                                    args.window)
+        else:
+            def one():
+                hq.sweep_dist(H.data_ptr(), Z.data_ptr(), n, prob.ilo, prob.ihi, prob.shifts_re,
+                              prob.shifts_im, args.window)
 
     for _ in range(args.warmup):
         restore()

@@ -190,6 +190,13 @@ int hqr_nccl_unique_id(void* out);
 int hqr_sweep_dist(double* H_local, double* Z_local, int64_t n, int64_t ilo, int64_t ihi,
                    const double* shifts_re, const double* shifts_im, int nshifts, int window);
 
+/* hqr_sweep_dist over several decoupled blocks (as hqr_sweep_multi; BASELINE configs[4] sharded):
+ * every block's windows share the wavefront steps and the shard roles.  Codes as hqr_sweep_multi
+ * plus -11. */
+int hqr_sweep_dist_multi(double* H_local, double* Z_local, int64_t n, int nblocks, const int64_t* ilo,
+                         const int64_t* ihi, const double* shifts_re, const double* shifts_im,
+                         const int* nshifts, int window);
+
 /*
  * The sharded algorithm with `vworld` virtual ranks on this one GPU (test / single-GPU check of the
  * multi-GPU path): H, Z are full device matrices (as in hqr_sweep); the library scatters them into
@@ -214,6 +221,11 @@ int hqr_sweep_virtual(double* H, double* Z, int64_t n, int64_t ilo, int64_t ihi,
  * Returns 0, -1 (flags NULL), -3 (n differs from the last sweep's n), -100 (no sweep yet).
  */
 int hqr_get_aftermath(signed char* flags, int64_t n);
+
+/* hqr_sweep_virtual over several decoupled blocks (hqr_sweep_dist_multi's kernel sequence). */
+int hqr_sweep_virtual_multi(double* H, double* Z, int64_t n, int nblocks, const int64_t* ilo,
+                            const int64_t* ihi, const double* shifts_re, const double* shifts_im,
+                            const int* nshifts, int window, int vworld);
 
 /* Release everything hqr_setup acquired.  Returns 0 (also when not set up) or 1000+cudaError_t. */
 int hqr_teardown(void);

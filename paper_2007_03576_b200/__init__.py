@@ -70,7 +70,8 @@ class Stats(ctypes.Structure):
 SYMBOLS = ["hqr_setup", "hqr_sweep", "hqr_sweep_multi", "hqr_teardown", "hqr_plan_query",
            "hqr_plan_query_multi", "hqr_get_stats", "hqr_error_string", "hqr_dist_layout",
            "hqr_dist_query", "hqr_nccl_unique_id", "hqr_sweep_dist", "hqr_sweep_virtual",
-           "hqr_get_aftermath", "hqr_sweeps", "hqr_plan_query_sweeps", "hqr_qz_sweep", "hqr_qr_iterate"]
+           "hqr_get_aftermath", "hqr_sweeps", "hqr_plan_query_sweeps", "hqr_qz_sweep", "hqr_qr_iterate",
+           "hqr_sweep_dist_multi", "hqr_sweep_virtual_multi"]
 
 
 def lib():
@@ -134,6 +135,12 @@ def lib():
                                      ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                      ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
         L.hqr_qr_iterate.restype = ctypes.c_int
+        for nm in ("hqr_sweep_dist_multi", "hqr_sweep_virtual_multi"):
+            fn = getattr(L, nm)
+            fn.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_void_p,
+                           ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int] + (
+                [ctypes.c_int] if nm.endswith("virtual_multi") else [])
+            fn.restype = ctypes.c_int
         L.hqr_get_aftermath.argtypes = [ctypes.c_void_p, ctypes.c_int64]
         L.hqr_get_aftermath.restype = ctypes.c_int
         L.hqr_get_stats.argtypes = [ctypes.POINTER(Stats)]
@@ -350,6 +357,34 @@ def sweep_virtual(H, Z, ilo, ihi, shifts_re, shifts_im, window, vworld: int) -> 
                                  int(window), int(vworld))
     if rc:
         raise HQRError(rc, "hqr_sweep_virtual")
+
+
+def sweep_virtual_multi(H, Z, blocks, shifts_re, shifts_im, window, vworld: int) -> None:
+    """The sharded algorithm over several decoupled blocks with vworld virtual ranks on one GPU."""
+    hp, n = _ptr_n(H)
+    zp, _ = _ptr_n(Z)
+    ilo = np.array([b[0] for b in blocks], dtype=np.int64)
+    ihi = np.array([b[1] for b in blocks], dtype=np.int64)
+    ns = np.array([b[2] for b in blocks], dtype=np.int32)
+    sr = np.ascontiguousarray(shifts_re, dtype=np.float64)
+    si = np.ascontiguousarray(shifts_im, dtype=np.float64)
+    rc = lib().hqr_sweep_virtual_multi(hp, zp, n, len(blocks), ilo.ctypes.data, ihi.ctypes.data, sr.ctypes.data,
+                                       si.ctypes.data, ns.ctypes.data, int(window), int(vworld))
+    if rc:
+        raise HQRError(rc, "hqr_sweep_virtual_multi")
+
+
+def sweep_dist_multi(H_local_ptr: int, Z_local_ptr, n, blocks, shifts_re, shifts_im, window) -> None:
+    """Collective sharded sweep over several decoupled blocks on this rank's shards."""
+    ilo = np.array([b[0] for b in blocks], dtype=np.int64)
+    ihi = np.array([b[1] for b in blocks], dtype=np.int64)
+    ns = np.array([b[2] for b in blocks], dtype=np.int32)
+    sr = np.ascontiguousarray(shifts_re, dtype=np.float64)
+    si = np.ascontiguousarray(shifts_im, dtype=np.float64)
+    rc = lib().hqr_sweep_dist_multi(H_local_ptr, Z_local_ptr, n, len(blocks), ilo.ctypes.data, ihi.ctypes.data,
+                                    sr.ctypes.data, si.ctypes.data, ns.ctypes.data, int(window))
+    if rc:
+        raise HQRError(rc, "hqr_sweep_dist_multi")
 
 
 def sweep_raw(H_ptr, Z_ptr, n, ilo, ihi, sr_ptr, si_ptr, nshifts, window) -> int:

@@ -34,6 +34,10 @@ using hqr::WindowDesc;
 
 namespace {
 
+// Q slot sets of the sharded sweep: its deferred far-right / Z updates (low-priority stream) may
+// trail the chases by up to kQSetsDist - 1 steps
+constexpr int kQSetsDist = 32;
+
 // (n, window, then ilo, ihi, nshifts of every block)
 typedef std::vector<int64_t> PlanKey;
 
@@ -98,6 +102,8 @@ struct State {
   cudaEvent_t ev_in = nullptr;     // entry: the library stream waits for the caller's legacy stream
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   cudaEvent_t ev_q[hqr::kQSets] = {}, ev_z[hqr::kQSets] = {};
+  cudaStream_t cstream = nullptr;  // sharded sweep: NCCL broadcasts (comm stream)
+  cudaEvent_t dev_chase[kQSetsDist] = {}, dev_bc[kQSetsDist] = {}, dev_bulk[kQSetsDist] = {};
   double* d_coef = nullptr;
   size_t coef_cap = 0;
   double* d_aft = nullptr;       // aftermath flags of the last single-GPU sweep (int8 per row)
@@ -758,6 +764,12 @@ int hqr_setup(const hqr_config* cfg) {
   CK(cudaEventCreateWithFlags(&g.ev_in, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&g.ev_fork, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&g.ev_join, cudaEventDisableTiming));
+  CK(cudaStreamCreateWithPriority(&g.cstream, cudaStreamNonBlocking, prio_hi));
+  for (int i = 0; i < kQSetsDist; ++i) {
+    CK(cudaEventCreateWithFlags(&g.dev_chase[i], cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&g.dev_bc[i], cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&g.dev_bulk[i], cudaEventDisableTiming));
+  }
   for (int i = 0; i < hqr::kQSets; ++i) {
     CK(cudaEventCreateWithFlags(&g.ev_q[i], cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&g.ev_z[i], cudaEventDisableTiming));
@@ -813,6 +825,13 @@ int hqr_teardown(void) {
   cudaEventDestroy(g.ev_in);
   cudaEventDestroy(g.ev_fork);
   cudaEventDestroy(g.ev_join);
+  for (int i = 0; i < kQSetsDist; ++i) {
+    cudaEventDestroy(g.dev_chase[i]);
+    cudaEventDestroy(g.dev_bc[i]);
+    cudaEventDestroy(g.dev_bulk[i]);
+  }
+  if (g.cstream) cudaStreamDestroy(g.cstream);
+  g.cstream = nullptr;
   for (int i = 0; i < hqr::kQSets; ++i) {
     cudaEventDestroy(g.ev_q[i]);
     cudaEventDestroy(g.ev_z[i]);
@@ -1132,14 +1151,59 @@ int run_dist(const CachedPlan& cp, const hqr::DistLayout& L, std::vector<RankCtx
              hqr_stats* st) {
   const Plan& P = cp.plan;
   const int64_t n = P.n;
-  cudaStream_t A = g.stream;
+  // A (high priority): lend, chase, left updates, near-right updates, return -- the chain that
+  //   feeds the next chases; C: the grouped broadcast of each step's factors (NCCL);
+  // B (low priority): the updates nothing later in the sweep reads before they are done -- Z(local
+  //   rows, W) Q_W for every window and the far-right rows [0, sp) of the owned windows (P:713,
+  //   P:758-765) -- trailing A by up to kQSetsDist - 1 steps (the Q slot sets rotate).
+  // sp(s) = the smallest first row of any later window, even: later left / near-right / chase work
+  // touches only rows >= sp(s), so the far-right rows never meet it.  Straddling windows keep their
+  // far-right on A (their lent columns go back at the end of the step), and a rank drains B before
+  // it lends or borrows columns (B may still be updating the lent ones; the borrower's whole right
+  // update of the straddling window must follow its earlier deferred far-right rows).
+  cudaStream_t A = g.stream, B = g.zstream, C = nccl ? g.cstream : g.stream;
   for (auto& rc : ranks) {
     CK(hqr::make_tensor_maps(&rc.tm, rc.H, rc.hcols, rc.Z, rc.zrows, rc.zrows, n, cp.KP));
   }
+  std::vector<int64_t> sp(P.nsteps, 0);
+  {
+    int64_t run = n;
+    for (int s = P.nsteps - 1; s >= 0; --s) {
+      sp[s] = run & ~(int64_t)1;
+      for (int i = P.step_begin[s]; i < P.step_begin[s + 1]; ++i) run = std::min<int64_t>(run, P.windows[i].w0);
+    }
+  }
+  CK(cudaEventRecord(g.ev_fork, A));
+  CK(cudaStreamWaitEvent(B, g.ev_fork, 0));
+  if (nccl) CK(cudaStreamWaitEvent(C, g.ev_fork, 0));
   const size_t qsz = (size_t)cp.KP * hqr::pad_ld(cp.KP);
+  auto args = [&](const RankCtx& rc, int s, int so) {
+    StepArgs a{};
+    a.H = rc.H; a.Z = rc.Z; a.n = n; a.hcol0 = L.cb[rc.rank];
+    a.lc0 = rc.steps[s].lc0; a.lc1 = rc.steps[s].lc1; a.zrows = rc.zrows; a.ldz = rc.zrows;
+    a.wins = cp.d_wins; a.win_begin = P.step_begin[s]; a.win_count = P.step_begin[s + 1] - P.step_begin[s];
+    a.coef = g.d_coef; a.qslots = g.d_q; a.KP = cp.KP; a.QLD = hqr::pad_ld(cp.KP); a.slot_offset = so;
+    a.step = s;
+    return a;
+  };
+  auto account = [&](int64_t items, double fl, double by, int* launches) {
+    if (items) (*launches)++;
+    st->flops_update += fl;
+    st->bytes_update += by;
+  };
   for (int s = 0; s < P.nsteps; ++s) {
-    const int so = (s % hqr::kQSets) * P.nchains;
-    // (1) lend: rank r+1's leading columns -> rank r's halo
+    const int set = s % kQSetsDist;
+    const int so = set * P.nchains;
+    if (s >= kQSetsDist) CK(cudaStreamWaitEvent(A, g.dev_bulk[set], 0));  // B is done with this slot set
+    // (1) lend: rank r+1's leading columns -> rank r's halo (the lender's B drained first)
+    // (the borrower applies its straddling window's whole right update on A: after its earlier
+    // deferred far-right rows on those columns)
+    bool lends = false;
+    for (auto& rc : ranks) lends |= rc.steps[s].lend_out > 0 || rc.steps[s].lend_in > 0;
+    if (lends && s > 0) {
+      CK(cudaEventRecord(g.ev_join, B));
+      CK(cudaStreamWaitEvent(A, g.ev_join, 0));
+    }
     if (nccl) {
       RankCtx& rc = ranks[0];
       const hqr::RankStep& rs = rc.steps[s];
@@ -1163,57 +1227,75 @@ int run_dist(const CachedPlan& cp, const hqr::DistLayout& L, std::vector<RankCtx
     for (auto& rc : ranks) {
       const int nown = rc.owned_begin[s + 1] - rc.owned_begin[s];
       if (!nown) continue;
-      StepArgs a{};
-      a.H = rc.H; a.Z = rc.Z; a.n = n; a.hcol0 = L.cb[rc.rank];
-      a.lc0 = rc.steps[s].lc0; a.lc1 = rc.steps[s].lc1; a.zrows = rc.zrows; a.ldz = rc.zrows;
+      StepArgs a = args(rc, s, so);
       a.wins = rc.d_owned; a.win_begin = rc.owned_begin[s]; a.win_count = nown;
-      a.coef = g.d_coef; a.qslots = g.d_q; a.KP = cp.KP; a.QLD = hqr::pad_ld(cp.KP); a.slot_offset = so;
       CK(hqr::launch_chase(a, P.max_kw, P.max_nbc, A));
       st->launches_chase++;
     }
-    // (3) broadcast every window's factor from its owner
+    CK(cudaEventRecord(g.dev_chase[set], A));
+    // (3) broadcast every window's factor from its owner (comm stream), A and B wait for it
+    cudaEvent_t qready = g.dev_chase[set];
     if (nccl) {
+      CK(cudaStreamWaitEvent(C, g.dev_chase[set], 0));
       NK(ncclGroupStart());
       for (int i = P.step_begin[s]; i < P.step_begin[s + 1]; ++i) {
         const WindowDesc& w = P.windows[i];
         double* q = g.d_q + (size_t)(w.slot + so) * qsz;
-        NK(ncclBroadcast(q, q, qsz, ncclDouble, hqr::owner_of_col(L, w.w0), g.comm, A));
+        NK(ncclBroadcast(q, q, qsz, ncclDouble, hqr::owner_of_col(L, w.w0), g.comm, C));
       }
       NK(ncclGroupEnd());
+      CK(cudaEventRecord(g.dev_bc[set], C));
+      CK(cudaStreamWaitEvent(A, g.dev_bc[set], 0));
+      qready = g.dev_bc[set];
     }
-    // (4) left update of every window on the held columns; (5) right (owned) and Z (all)
+    (void)qready;
+    // (4) A: left update of every window on the held columns
     for (auto& rc : ranks) {
-      StepArgs a{};
-      a.H = rc.H; a.Z = rc.Z; a.n = n; a.hcol0 = L.cb[rc.rank];
-      a.lc0 = rc.steps[s].lc0; a.lc1 = rc.steps[s].lc1; a.zrows = rc.zrows; a.ldz = rc.zrows;
-      a.wins = cp.d_wins; a.win_begin = P.step_begin[s]; a.win_count = P.step_begin[s + 1] - P.step_begin[s];
-      a.coef = g.d_coef; a.qslots = g.d_q; a.KP = cp.KP; a.QLD = hqr::pad_ld(cp.KP); a.slot_offset = so;
+      StepArgs a = args(rc, s, so);
       const WindowDesc* hw = P.windows.data() + a.win_begin;
       int64_t items;
       double fl, by;
       CK(hqr::launch_left(a, hw, g.num_sms, rc.tm, A, &items, &fl, &by));
-      if (items) st->launches_left++;
-      st->flops_update += fl;
-      st->bytes_update += by;
+      account(items, fl, by, &st->launches_left);
+    }
+    // B starts the step's deferred work only after the step's left updates: the far-right rows
+    // of a window meet the left update of a window above it in the same step (rows < sp) -- the
+    // two commute but must not run concurrently
+    CK(cudaEventRecord(g.dev_chase[set], A));
+    CK(cudaStreamWaitEvent(B, g.dev_chase[set], 0));
+    // (4) A: near-right of the owned windows (all rows if the rank straddles: its lent columns
+    //     return below); (5) B: their far-right rows [0, sp) and Z(local rows, W) Q_W
+    for (auto& rc : ranks) {
+      StepArgs a = args(rc, s, so);
+      const WindowDesc* hw = P.windows.data() + a.win_begin;
+      int64_t items;
+      double fl, by;
       const int nown = rc.owned_begin[s + 1] - rc.owned_begin[s];
       if (nown) {
         StepArgs ar = a;
         ar.wins = rc.d_owned; ar.win_begin = rc.owned_begin[s]; ar.win_count = nown;
         ar.right_mode = 1;
+        const bool straddle = rc.steps[s].lend_in > 0;
+        ar.rrow_lo = straddle ? 0 : sp[s];
+        ar.rrow_hi = n;  // rows [rrow_lo, w0)
         CK(hqr::launch_right(ar, rc.owned.data() + rc.owned_begin[s], g.num_sms, rc.tm, A, &items, &fl, &by));
-        if (items) st->launches_right++;
-        st->flops_update += fl;
-        st->bytes_update += by;
+        account(items, fl, by, &st->launches_right);
+        if (!straddle && sp[s] > 0) {
+          StepArgs af = ar;
+          af.rrow_lo = 0;
+          af.rrow_hi = sp[s];
+          CK(hqr::launch_right(af, rc.owned.data() + rc.owned_begin[s], g.num_sms, rc.tm, B, &items, &fl, &by));
+          account(items, fl, by, &st->launches_right);
+        }
       }
       if (rc.Z) {
         StepArgs az = a;
         az.right_mode = 2;
-        CK(hqr::launch_right(az, hw, g.num_sms, rc.tm, A, &items, &fl, &by));
-        if (items) st->launches_right++;
-        st->flops_update += fl;
-        st->bytes_update += by;
+        CK(hqr::launch_right(az, hw, g.num_sms, rc.tm, B, &items, &fl, &by));
+        account(items, fl, by, &st->launches_right);
       }
     }
+    CK(cudaEventRecord(g.dev_bulk[set], B));
     // (6) return the lent slabs
     if (nccl) {
       RankCtx& rc = ranks[0];
@@ -1235,6 +1317,12 @@ int run_dist(const CachedPlan& cp, const hqr::DistLayout& L, std::vector<RankCtx
       }
     }
   }
+  CK(cudaEventRecord(g.ev_join, B));
+  CK(cudaStreamWaitEvent(A, g.ev_join, 0));
+  if (nccl) {
+    CK(cudaEventRecord(g.ev_join, C));
+    CK(cudaStreamWaitEvent(A, g.ev_join, 0));
+  }
   st->steps = P.nsteps;
   st->windows = (int64_t)P.windows.size();
   st->kernels_launched = st->launches_chase + st->launches_left + st->launches_right;
@@ -1242,10 +1330,8 @@ int run_dist(const CachedPlan& cp, const hqr::DistLayout& L, std::vector<RankCtx
 }
 
 // common validation + shift upload for the sharded entry points
-int dist_prepare(int64_t n, int64_t ilo, int64_t ihi, const double* sr, const double* si, int nshifts,
-                 int window, int world, CachedPlan** cpo, hqr::DistLayout* L) {
-  Blocks b;
-  b.ilo = {ilo}; b.ihi = {ihi}; b.nshifts = {nshifts};
+int dist_prepare(int64_t n, const Blocks& b, const double* sr, const double* si, int window, int world,
+                 CachedPlan** cpo, hqr::DistLayout* L) {
   int rc = validate_blocks(n, b, sr, si, window, true);
   if (rc) return rc;
   if (!g.user_cb.empty() && world == g.world) {  // hqr_config shard bounds (for n = n_max only)
@@ -1267,7 +1353,7 @@ int dist_prepare(int64_t n, int64_t ilo, int64_t ihi, const double* sr, const do
   if (rc) return rc;
   rc = upload_coef(sr, si, cp->plan.nb);
   if (rc) return rc;
-  rc = ensure(&g.d_q, &g.q_cap, (size_t)hqr::kQSets * cp->plan.nchains * cp->KP * hqr::pad_ld(cp->KP));
+  rc = ensure(&g.d_q, &g.q_cap, (size_t)kQSetsDist * cp->plan.nchains * cp->KP * hqr::pad_ld(cp->KP));
   return rc;
 }
 
@@ -1297,6 +1383,8 @@ int hqr_sweep_multi(double* H, double* Z, int64_t n, int nblocks, const int64_t*
                     const int* nshifts, int window) {
   if (!H) return -1;
   if (nblocks < 1 || !ilo || !ihi || !nshifts) return -4;
+  if (g.ready && g.world > 1)  // world > 1: the collective on local shards (as hqr_sweep)
+    return hqr_sweep_dist_multi(H, Z, n, nblocks, ilo, ihi, shifts_re, shifts_im, nshifts, window);
   return sweep_impl(H, Z, n, make_blocks(nblocks, ilo, ihi, nshifts), shifts_re, shifts_im, window);
 }
 
@@ -1386,26 +1474,29 @@ int hqr_nccl_unique_id(void* out) {
   return 0;
 }
 
-int hqr_sweep_dist(double* H_local, double* Z_local, int64_t n, int64_t ilo, int64_t ihi,
-                   const double* shifts_re, const double* shifts_im, int nshifts, int window) {
+static int dist_impl(double* H_local, double* Z_local, int64_t n, const Blocks& blocks, const double* shifts_re,
+                     const double* shifts_im, int window) {
   if (!H_local) return -1;
   CachedPlan* cp = nullptr;
   hqr::DistLayout L;
-  int rc = dist_prepare(n, ilo, ihi, shifts_re, shifts_im, nshifts, window, g.world, &cp, &L);
+  int rc = dist_prepare(n, blocks, shifts_re, shifts_im, window, g.world, &cp, &L);
   if (rc) return rc;
   if (g.world > 1 && !g.comm) return -100;
-  {  // -10: H[ilo, ilo-1] on the rank owning column ilo-1, H[ihi+1, ihi] on the owner of column ihi;
-     // the verdict is agreed over all ranks (max), so every rank returns the same code
+  {  // -10: H[ilo, ilo-1] on the rank owning column ilo-1, H[ihi+1, ihi] on the owner of column ihi,
+     // every block; the verdict is agreed over all ranks (max), so every rank returns the same code
     const int64_t c0 = L.cb[g.rank], c1 = L.cb[g.rank + 1];
     int bad = 0;
     double v = 0.0;
-    if (ilo > 0 && ilo - 1 >= c0 && ilo - 1 < c1) {
-      CK(cudaMemcpy(&v, H_local + ilo + (ilo - 1 - c0) * n, sizeof(double), cudaMemcpyDeviceToHost));
-      bad |= v != 0.0;
-    }
-    if (ihi < n - 1 && ihi >= c0 && ihi < c1) {
-      CK(cudaMemcpy(&v, H_local + (ihi + 1) + (ihi - c0) * n, sizeof(double), cudaMemcpyDeviceToHost));
-      bad |= v != 0.0;
+    for (int i = 0; i < blocks.count(); ++i) {
+      const int64_t ilo = blocks.ilo[i], ihi = blocks.ihi[i];
+      if (ilo > 0 && ilo - 1 >= c0 && ilo - 1 < c1) {
+        CK(cudaMemcpy(&v, H_local + ilo + (ilo - 1 - c0) * n, sizeof(double), cudaMemcpyDeviceToHost));
+        bad |= v != 0.0;
+      }
+      if (ihi < n - 1 && ihi >= c0 && ihi < c1) {
+        CK(cudaMemcpy(&v, H_local + (ihi + 1) + (ihi - c0) * n, sizeof(double), cudaMemcpyDeviceToHost));
+        bad |= v != 0.0;
+      }
     }
     if (g.world > 1) {
       int* d_bad = reinterpret_cast<int*>(g.d_q);  // workspace scratch (Q slots are rewritten below)
@@ -1440,16 +1531,17 @@ int hqr_sweep_dist(double* H_local, double* Z_local, int64_t n, int64_t ilo, int
   return 0;
 }
 
-int hqr_sweep_virtual(double* H, double* Z, int64_t n, int64_t ilo, int64_t ihi, const double* shifts_re,
-                      const double* shifts_im, int nshifts, int window, int vworld) {
+static int virtual_impl(double* H, double* Z, int64_t n, const Blocks& blocks, const double* shifts_re,
+                        const double* shifts_im, int window, int vworld) {
   if (!H) return -1;
   if (vworld < 1) return -10;
   CachedPlan* cp = nullptr;
   hqr::DistLayout L;
-  int rc = dist_prepare(n, ilo, ihi, shifts_re, shifts_im, nshifts, window, vworld, &cp, &L);
+  int rc = dist_prepare(n, blocks, shifts_re, shifts_im, window, vworld, &cp, &L);
   if (rc) return rc;
   if (!is_device_ptr(H) || (Z && !is_device_ptr(Z))) return -1;
-  {  // -10 (as hqr_sweep)
+  for (int i = 0; i < blocks.count(); ++i) {  // -10 (as hqr_sweep)
+    const int64_t ilo = blocks.ilo[i], ihi = blocks.ihi[i];
     double v[2] = {0.0, 0.0};
     if (ilo > 0) CK(cudaMemcpy(&v[0], H + ilo + (ilo - 1) * n, sizeof(double), cudaMemcpyDeviceToHost));
     if (ihi < n - 1) CK(cudaMemcpy(&v[1], H + (ihi + 1) + ihi * n, sizeof(double), cudaMemcpyDeviceToHost));
@@ -1733,6 +1825,32 @@ int hqr_get_aftermath(signed char* flags, int64_t n) {
   CK(cudaSetDevice(g.device));
   CK(cudaMemcpy(flags, g.d_aft, (size_t)n, cudaMemcpyDeviceToHost));
   return 0;
+}
+
+int hqr_sweep_dist(double* H_local, double* Z_local, int64_t n, int64_t ilo, int64_t ihi,
+                   const double* shifts_re, const double* shifts_im, int nshifts, int window) {
+  return dist_impl(H_local, Z_local, n, make_blocks(1, &ilo, &ihi, &nshifts), shifts_re, shifts_im, window);
+}
+
+int hqr_sweep_dist_multi(double* H_local, double* Z_local, int64_t n, int nblocks, const int64_t* ilo,
+                         const int64_t* ihi, const double* shifts_re, const double* shifts_im,
+                         const int* nshifts, int window) {
+  if (!H_local) return -1;
+  if (nblocks < 1 || !ilo || !ihi || !nshifts) return -4;
+  return dist_impl(H_local, Z_local, n, make_blocks(nblocks, ilo, ihi, nshifts), shifts_re, shifts_im, window);
+}
+
+int hqr_sweep_virtual(double* H, double* Z, int64_t n, int64_t ilo, int64_t ihi, const double* shifts_re,
+                      const double* shifts_im, int nshifts, int window, int vworld) {
+  return virtual_impl(H, Z, n, make_blocks(1, &ilo, &ihi, &nshifts), shifts_re, shifts_im, window, vworld);
+}
+
+int hqr_sweep_virtual_multi(double* H, double* Z, int64_t n, int nblocks, const int64_t* ilo,
+                            const int64_t* ihi, const double* shifts_re, const double* shifts_im,
+                            const int* nshifts, int window, int vworld) {
+  if (!H) return -1;
+  if (nblocks < 1 || !ilo || !ihi || !nshifts) return -4;
+  return virtual_impl(H, Z, n, make_blocks(nblocks, ilo, ihi, nshifts), shifts_re, shifts_im, window, vworld);
 }
 
 int hqr_get_stats(hqr_stats* out) {

@@ -44,7 +44,21 @@ struct StepArgs {
                              // (record_band); wstats[win_begin + i] for window i of the step
   signed char* aftermath;    // nullable: per row, the subdiagonal scan flags (R16), written by the
                              // chases of windows with scan rows (WindowDesc::scan_lo/hi)
+  int64_t rrow_lo, rrow_hi;  // right kernel, H rows: rrow_hi <= 0 -> [0, w0) (default); else
+                             // [rrow_lo, min(rrow_hi, w0)), rrow_lo even (sharded near / far split)
 };
+
+// H rows [lo, hi) of window w's right update (update.cu; see StepArgs::rrow_lo / rrow_hi)
+__host__ __device__ inline void right_row_range(const StepArgs& a, const WindowDesc& w, int64_t& lo,
+                                                int64_t& hi) {
+  lo = 0;
+  hi = w.w0;
+  if (a.rrow_hi > 0) {
+    lo = a.rrow_lo;
+    if (a.rrow_hi < hi) hi = a.rrow_hi;
+  }
+  if (hi < lo) hi = lo;
+}
 
 // One CTA per window: chase the step's bulges inside SMEM-resident windows, accumulate Q_W.
 cudaError_t launch_chase(const StepArgs& a, int max_kw, int max_nbc, cudaStream_t st);

@@ -108,7 +108,9 @@ __global__ void __launch_bounds__(kThreadsBulk, 1)
         si.rt[i] = c;  // LEFT: first column of the window's range
         si.pre[i + 1] = si.pre[i] + (cnt + NT - 1) / NT;
       } else {
-        si.rt[i] = (a.right_mode == 2) ? 0 : ((int64_t)w.w0 + MT - 1) / MT;
+        int64_t lo, hi;
+        right_row_range(a, w, lo, hi);
+        si.rt[i] = (a.right_mode == 2) ? 0 : (hi - lo + MT - 1) / MT;
         si.pre[i + 1] = si.pre[i] + si.rt[i] + ztiles;
       }
     }
@@ -134,7 +136,9 @@ __global__ void __launch_bounds__(kThreadsBulk, 1)
       t.M = a.H; t.c0 = si.rt[wi] + tile * NT; t.lc1 = a.lc1; t.ld = n; t.cb = a.hcol0; t.isZ = false;
       t.r0 = t.r1 = 0;
     } else if (tile < si.rt[wi]) {
-      t.M = a.H; t.r0 = tile * MT; t.r1 = w.w0; t.ld = n; t.cb = a.hcol0; t.isZ = false;
+      int64_t lo, hi;
+      right_row_range(a, w, lo, hi);
+      t.M = a.H; t.r0 = lo + tile * MT; t.r1 = hi; t.ld = n; t.cb = a.hcol0; t.isZ = false;
       t.c0 = t.lc1 = 0;
     } else {
       t.M = a.Z; t.r0 = (tile - si.rt[wi]) * MT; t.r1 = a.zrows; t.ld = a.ldz; t.cb = 0; t.isZ = true;
@@ -342,7 +346,9 @@ __global__ void __launch_bounds__(kThreadsGeneric, 1) right_generic_kernel(StepA
     for (int i = 0; i < nw; ++i) {
       WindowDesc w = a.wins[a.win_begin + i];
       si.w[i] = w;
-      si.rt[i] = (a.right_mode == 2) ? 0 : ((int64_t)w.w0 + MT - 1) / MT;
+      int64_t lo, hi;
+      right_row_range(a, w, lo, hi);
+      si.rt[i] = (a.right_mode == 2) ? 0 : (hi - lo + MT - 1) / MT;
       si.pre[i + 1] = si.pre[i] + si.rt[i] + ztiles;
     }
   }
@@ -352,7 +358,9 @@ __global__ void __launch_bounds__(kThreadsGeneric, 1) right_generic_kernel(StepA
   auto panel = [&](int wi, int64_t tile, double*& M, int64_t& r0, int64_t& r1, int64_t& ld,
                    int64_t& cb) {
     if (tile < si.rt[wi]) {
-      M = a.H; r0 = tile * MT; r1 = si.w[wi].w0; ld = n; cb = a.hcol0;
+      int64_t lo, hi;
+      right_row_range(a, si.w[wi], lo, hi);
+      M = a.H; r0 = lo + tile * MT; r1 = hi; ld = n; cb = a.hcol0;
     } else {
       M = a.Z; r0 = (tile - si.rt[wi]) * MT; r1 = a.zrows; ld = a.ldz; cb = 0;
     }
@@ -570,8 +578,10 @@ cudaError_t launch_right(const StepArgs& a, const WindowDesc* hw, int num_sms, c
   const int64_t zt = do_z ? (a.zrows + MT - 1) / MT : 0;
   for (int i = 0; i < a.win_count; ++i) {
     int64_t kw = hw[i].w1 - hw[i].w0 + 1;
-    items += (do_h ? (hw[i].w0 + MT - 1) / MT : 0) + zt;
-    double rows = (do_h ? (double)hw[i].w0 : 0.0) + (do_z ? (double)a.zrows : 0.0);
+    int64_t lo, hi;
+    right_row_range(a, hw[i], lo, hi);
+    items += (do_h ? (hi - lo + MT - 1) / MT : 0) + zt;
+    double rows = (do_h ? (double)(hi - lo) : 0.0) + (do_z ? (double)a.zrows : 0.0);
     f += 2.0 * kw * kw * rows;
     b += 16.0 * kw * rows;
   }

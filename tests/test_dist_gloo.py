@@ -3,9 +3,12 @@
 per-step role from the C++ library (hqr_dist_layout / hqr_dist_query / hqr_plan_query: ownership,
 lent column slabs, left-update column range), and executes the protocol of hqr_sweep_dist in numpy
 with gloo in place of NCCL:
-  (1) lend straddling slabs (send/recv of whole columns), (2) chase owned windows,
-  (3) broadcast every window's factor from its owner, (4) left update on the held columns,
-  (5) right update of owned windows + Z update of the local rows, (6) return the slabs.
+  (1) lend straddling slabs (send/recv of whole columns; the lender first drains its deferred
+  work), (2) chase owned windows, (3) broadcast every window's factor from its owner, (4) left
+  update on the held columns and near-right update (rows [sp, w0)) of the owned windows, (5) the
+  deferred work -- far-right rows [0, sp) of the owned windows (straddling ones: at once) and the
+  Z update of the local rows -- queued and applied up to LAG steps late, as the low-priority
+  stream of hqr_sweep_dist may, (6) return the slabs.
 Rank 0 gathers the result and compares it with the CPU oracle."""
 import os
 import socket
@@ -28,6 +31,20 @@ def _free_port():
     p = s.getsockname()[1]
     s.close()
     return p
+
+
+LAG = 7  # deferred (far-right / Z) work applied this many steps late
+
+
+def _split_rows(W, nsteps, n):
+    """sp(s): the smallest first row of any window of a later step, rounded down to even (the
+    library's near / far split of the right updates)."""
+    sp = [0] * nsteps
+    run = n
+    for s in range(nsteps - 1, -1, -1):
+        sp[s] = run & ~1
+        run = min(run, int(W[W[:, 0] == s][:, 2].min()))
+    return sp
 
 
 def _worker(rank, world, port, case, q):
@@ -54,10 +71,23 @@ def _worker(rank, world, port, case, q):
         def cols(j0, j1):  # local view of global columns [j0, j1)
             return Hl[:, j0 - c0:j1 - c0]
 
+        sp = _split_rows(W, info["nsteps"], n)
+        deferred = []  # (step, fn) of the low-priority work, applied in order
+
+        def drain(upto):
+            while deferred and deferred[0][0] <= upto:
+                deferred.pop(0)[1]()
+
         for s in range(info["nsteps"]):
             _, lend_out, lend_in, lc0, lc1, nown = (int(v) for v in roles[s])
             sw = W[W[:, 0] == s]
+            drain(s - LAG)
             # (1) lend: my leading lend_out columns -> rank-1's halo; rank+1's -> my halo
+            if lend_out or lend_in:
+                # the lender's deferred work may still touch the lent columns; the borrower applies
+                # its straddling window's whole right update at once, after its earlier deferred
+                # far-right rows on the same columns
+                drain(s)
             if lend_out:
                 dist.send(torch.from_numpy(np.ascontiguousarray(cols(c0, c0 + lend_out))), rank - 1)
             if lend_in:
@@ -86,14 +116,19 @@ def _worker(rank, world, port, case, q):
                 if a < lc1:
                     blk = cols(a, lc1)
                     blk[w0:w1 + 1] = Q[w0].T @ blk[w0:w1 + 1]
-            # (5) right update of owned windows, Z update of every window
+            # (4) near-right rows [sp, w0) of the owned windows (all rows if the rank straddles)
             for w in owned:
                 w0, w1 = int(w[2]), int(w[3])
                 blk = cols(w0, w1 + 1)
-                blk[:w0] = blk[:w0] @ Q[w0]
-            for w in sw:
+                lo = 0 if lend_in else min(sp[s], w0)
+                blk[lo:w0] = blk[lo:w0] @ Q[w0]
+                if not lend_in and lo > 0:  # (5) far-right rows [0, sp), deferred
+                    deferred.append((s, lambda w0=w0, w1=w1, lo=lo, Qw=Q[w0]:
+                                     cols(w0, w1 + 1).__setitem__(slice(0, lo), cols(w0, w1 + 1)[:lo] @ Qw)))
+            for w in sw:  # (5) Z of the local rows, deferred
                 w0, w1 = int(w[2]), int(w[3])
-                Zl[:, w0:w1 + 1] = Zl[:, w0:w1 + 1] @ Q[w0]
+                deferred.append((s, lambda w0=w0, w1=w1, Qw=Q[w0]:
+                                 Zl.__setitem__((slice(None), slice(w0, w1 + 1)), Zl[:, w0:w1 + 1] @ Qw)))
             # (6) return the lent slabs
             if lend_in:
                 dist.send(torch.from_numpy(np.ascontiguousarray(cols(c1, c1 + lend_in))), rank + 1)
@@ -101,6 +136,7 @@ def _worker(rank, world, port, case, q):
                 buf = torch.empty((n, lend_out), dtype=torch.float64)
                 dist.recv(buf, rank - 1)
                 cols(c0, c0 + lend_out)[:] = buf.numpy()
+        drain(info["nsteps"])
         # gather on rank 0
         Hs = [torch.empty((n, int(cb[r + 1] - cb[r])), dtype=torch.float64) for r in range(world)]
         Zs = [torch.empty((int(rb[r + 1] - rb[r]), n), dtype=torch.float64) for r in range(world)]

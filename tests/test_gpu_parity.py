@@ -335,6 +335,37 @@ def test_sharded_virtual_ranks(vworld, case):
     check(Hg, Zg, Ho, Zo, H0, 0, n - 1)
 
 
+@pytest.mark.parametrize("vworld,sizes,ns_each,win", [(2, [600, 600], [40, 40], 96),
+                                                      (4, [1000, 1000, 1000, 1000], [60, 60, 60, 60], 96),
+                                                      (8, [1500, 1500], [80, 60], 64)])
+def test_sharded_virtual_multi_block(vworld, sizes, ns_each, win):
+    """BASELINE configs[4] in miniature on the sharded path: several decoupled blocks, every
+    block's windows sharing the steps and the shard roles (hqr_sweep_virtual_multi)."""
+    n = sum(sizes)
+    H0, Z0, blocks, re_, im_ = _multi_case(n, sizes, ns_each, 13)
+    Hd, Zd = hq.to_device(H0), hq.to_device(Z0)
+    hq.sweep_virtual_multi(Hd, Zd, blocks, re_, im_, win, vworld)
+    Hg, Zg = hq.from_device(Hd), hq.from_device(Zd)
+    Ho, Zo = H0.copy(order="F"), Z0.copy(order="F")
+    off = 0
+    for lo, hi, ns in blocks:
+        oracle.sweep(Ho, Zo, lo, hi, re_[off:off + ns], im_[off:off + ns])
+        off += ns
+    check(Hg, Zg, Ho, Zo, H0, 0, n - 1)
+
+
+def test_sharded_virtual_deferred_long_lag():
+    """Many chains crossing every boundary of 8 virtual ranks: the deferred far-right / Z work
+    (low-priority stream) trails the chases by many steps and is drained at every lend."""
+    seed, n, ns, win = 65, 3000, 200, 96
+    H0, Z0, re_, im_ = random_case(seed, n, ns, z0="orth", shift_kind="disk2")
+    Hd, Zd = hq.to_device(H0), hq.to_device(Z0)
+    hq.sweep_virtual(Hd, Zd, 0, n - 1, re_, im_, win, 8)
+    Hg, Zg = hq.from_device(Hd), hq.from_device(Zd)
+    Ho, Zo = oracle_sweep(H0, Z0, 0, n - 1, re_, im_)
+    check(Hg, Zg, Ho, Zo, H0, 0, n - 1)
+
+
 @pytest.mark.parametrize("case", [(70, 600, 60, 96), (71, 1000, 100, 64), (72, 400, 40, 112)])
 def test_fused_step_kernel_matches_separate_launches(case):
     """The fused step kernel (prioritised task queue, chase of step g+1 inside step g's launch) and
