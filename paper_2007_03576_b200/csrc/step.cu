@@ -251,6 +251,12 @@ struct StageDesc {
   TileRef t;
 };
 
+// One release fence, then relaxed adds: the release pattern for several counters at the cost of one
+// membar (red.release costs a full MEMBAR.GPU + ERRBAR each).
+__device__ __forceinline__ void fence_release_gpu() { asm volatile("fence.acq_rel.gpu;\n" ::: "memory"); }
+__device__ __forceinline__ void red_relaxed_add(int* p, int v) {
+  asm volatile("red.relaxed.gpu.global.add.s32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
+}
 __device__ __forceinline__ void red_release_add(int* p, int v) {
   asm volatile("red.release.gpu.global.add.s32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
 }
@@ -510,9 +516,10 @@ __global__ void __launch_bounds__(kStepThreads, 1)
     auto flush = [&]() {
       __syncwarp();
       if (lane == 0) {
-        red_release_add(pend_p, pend_n);
-        if (pend_p2) red_release_add(pend_p2, pend_n);
-        red_release_add(pend_all, pend_n);
+        fence_release_gpu();  // the warp's stores (ordered by __syncwarp) before the three counts
+        red_relaxed_add(pend_p, pend_n);
+        if (pend_p2) red_relaxed_add(pend_p2, pend_n);
+        red_relaxed_add(pend_all, pend_n);
       }
       pend_p = nullptr;
       pend_n = 0;
