@@ -46,6 +46,9 @@ typedef struct hqr_config {
                         /* bit 1: HQR_FLAG_PROFILE  -- time every launch with CUDA events         */
                         /* bit 2: HQR_FLAG_NO_FUSE  -- separate chase / left / right launches     */
                         /*        instead of the fused step kernel                                */
+                        /* bit 3: HQR_FLAG_NCCL_SELF -- world == 1 only: create a one-rank NCCL   */
+                        /*        communicator, so hqr_sweep_dist runs its NCCL transport (the     */
+                        /*        grouped broadcasts on the comm stream) on one GPU (tests)       */
   /* Shard boundaries (world > 1): NULL = the sqrt-balanced default of
    * hqr_dist_layout for every n.  Otherwise both arrays hold world + 1 entries for n = n_max:
    * col_bounds[r] .. col_bounds[r+1] are rank r's H columns, row_bounds[..] its Z rows; 0 = b[0] <
@@ -61,6 +64,7 @@ typedef struct hqr_config {
 #define HQR_FLAG_NO_GRAPH 1
 #define HQR_FLAG_PROFILE 2
 #define HQR_FLAG_NO_FUSE 4
+#define HQR_FLAG_NCCL_SELF 8
 
 /* Initialise the library on cfg->device: streams, events, workspace, NCCL communicator (world > 1).
  * Returns 0, -1 (cfg NULL or inconsistent rank/world/nccl_id/bounds/window_max), -101 (no usable

@@ -33,6 +33,7 @@ ERRORS = {
 FLAG_NO_GRAPH = 1
 FLAG_PROFILE = 2
 FLAG_NO_FUSE = 4
+FLAG_NCCL_SELF = 8
 MAX_WINDOW = 112
 DEFAULT_WINDOW = 96
 

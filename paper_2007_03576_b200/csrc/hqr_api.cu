@@ -778,6 +778,10 @@ int hqr_setup(const hqr_config* cfg) {
     ncclUniqueId id;
     std::memcpy(&id, cfg->nccl_id, sizeof(id));
     NK(ncclCommInitRank(&g.comm, g.world, id, g.rank));
+  } else if (g.flags & HQR_FLAG_NCCL_SELF) {  // one-rank communicator: the NCCL transport on one GPU
+    ncclUniqueId id;
+    NK(ncclGetUniqueId(&id));
+    NK(ncclCommInitRank(&g.comm, 1, id, 0));
   }
   if (hqr::tuning_env("HQR_PROGRESS_SECS")) hqr::debug_progress_init();
   g.ready = true;
@@ -1519,7 +1523,7 @@ static int dist_impl(double* H_local, double* Z_local, int64_t n, const Blocks& 
   rc = prepare_rank(*cp, L, &r);
   if (rc) return rc;
   CK(cudaEventRecord(g.ev0, g.stream));
-  rc = run_dist(*cp, L, ranks, g.world > 1, &st);
+  rc = run_dist(*cp, L, ranks, g.comm != nullptr, &st);
   if (rc) return rc;
   CK(cudaEventRecord(g.ev1, g.stream));
   CK(cudaStreamSynchronize(g.stream));

@@ -354,6 +354,31 @@ def test_sharded_virtual_multi_block(vworld, sizes, ns_each, win):
     check(Hg, Zg, Ho, Zo, H0, 0, n - 1)
 
 
+def test_sharded_nccl_transport_one_rank():
+    """hqr_sweep_dist with its NCCL transport executed (HQR_FLAG_NCCL_SELF: a one-rank communicator
+    on this GPU): the grouped ncclBroadcast of every step's factors on the comm stream, the event
+    gating of the two compute streams -- against the oracle, on the local shard (= the matrix)."""
+    import torch
+    n, ns, win = 1200, 80, 96
+    H0, Z0, re_, im_ = random_case(66, n, ns, z0="orth", shift_kind="disk2")
+    cb, rb, halo = hq.dist_layout(n, 1)
+    hq.teardown()
+    hq.setup(0, flags=hq.FLAG_NCCL_SELF)
+    try:
+        Hl = torch.zeros((n + halo, n), dtype=torch.float64, device="cuda")   # rows = local columns
+        Hl[:n].copy_(torch.from_numpy(np.ascontiguousarray(H0.T)))
+        Zl = torch.from_numpy(np.ascontiguousarray(Z0.T)).cuda()
+        hq.sweep_dist(Hl.data_ptr(), Zl.data_ptr(), n, 0, n - 1, re_, im_, win)
+        torch.cuda.synchronize()
+        Hg = np.asfortranarray(Hl[:n].cpu().numpy().T)
+        Zg = np.asfortranarray(Zl.cpu().numpy().T)
+    finally:
+        hq.teardown()
+        hq.setup(0)
+    Ho, Zo = oracle_sweep(H0, Z0, 0, n - 1, re_, im_)
+    check(Hg, Zg, Ho, Zo, H0, 0, n - 1)
+
+
 def test_sharded_virtual_deferred_long_lag():
     """Many chains crossing every boundary of 8 virtual ranks: the deferred far-right / Z work
     (low-priority stream) trails the chases by many steps and is drained at every lend."""
