@@ -1617,9 +1617,9 @@ int hqr_qz_sweep(double* H, double* T, double* Q, double* Z, int64_t n, int64_t 
   b.ilo = {ilo}; b.ihi = {ihi}; b.nshifts = {nshifts};
   int rc = validate_blocks(n, b, shifts_re, shifts_im, window, true);
   if (rc) return rc;
-  Plan P;
   const int kmax = std::min(g.window_max > 0 ? g.window_max : hqr::kMaxWindowQZ, hqr::kMaxWindowQZ);
-  rc = hqr::make_plan(n, ilo, ihi, nshifts, window, kmax, &P);
+  Plan P0;
+  rc = hqr::make_plan(n, ilo, ihi, nshifts, window, kmax, &P0);  // validates the window (-9)
   if (rc) return rc;
   if (!g.ready) return -100;
   if (g.world > 1) return -1;
@@ -1634,72 +1634,122 @@ int hqr_qz_sweep(double* H, double* T, double* Q, double* Z, int64_t n, int64_t 
     if (v[0] != 0.0 || v[1] != 0.0) return -10;
     if (v[2] == 0.0 || v[3] == 0.0) return -2;
   }
+  // the plan (cached like the QR sweep's, key marked as QZ: its window cap differs)
+  PlanKey key = plan_key(n, b, window);
+  key.push_back(-2);
+  key.push_back(kmax);
+  auto it = g.plans.find(key);
+  if (it == g.plans.end()) {
+    auto cp = std::make_unique<CachedPlan>();
+    cp->plan = std::move(P0);
+    cp->KP = hqr::padded_kp(cp->plan.max_kw);
+    it = g.plans.emplace(key, std::move(cp)).first;
+  }
+  CachedPlan* cp = it->second.get();
+  const Plan& P = cp->plan;
+  if (!cp->d_wins) {
+    CK(cudaMalloc(&cp->d_wins, P.windows.size() * sizeof(WindowDesc)));
+    CK(cudaMemcpy(cp->d_wins, P.windows.data(), P.windows.size() * sizeof(WindowDesc), cudaMemcpyHostToDevice));
+  }
   rc = wait_for_caller();
   if (rc) return rc;
   rc = upload_coef(shifts_re, shifts_im, P.nb);
   if (rc) return rc;
-  const int KP = hqr::padded_kp(P.max_kw), QLD = hqr::pad_ld(KP);
+  const int KP = cp->KP, QLD = hqr::pad_ld(KP);
   const size_t slots = (size_t)hqr::kQSets * P.nchains * KP * QLD;
   rc = ensure(&g.d_q, &g.q_cap, 2 * slots);  // Q_W slots, then Z_W slots
   if (rc) return rc;
   double* zslots = g.d_q + slots;
-  WindowDesc* d_wins = nullptr;
-  CK(cudaMalloc(&d_wins, P.windows.size() * sizeof(WindowDesc)));
-  CK(cudaMemcpyAsync(d_wins, P.windows.data(), P.windows.size() * sizeof(WindowDesc), cudaMemcpyHostToDevice,
-                     g.stream));
   hqr::TensorMaps tmA, tmB;  // (H, Qacc) and (T, Zacc)
   CK(hqr::make_tensor_maps(&tmA, H, n, Q, n, n, n, KP));
   CK(hqr::make_tensor_maps(&tmB, T, n, Z, n, n, n, KP));
   hqr_stats st{};
   st.window_eff = P.k;
-  cudaStream_t A = g.stream;
-  CK(cudaEventRecord(g.ev0, A));
-  for (int s = 0; s < P.nsteps; ++s) {
-    StepArgs a{};
-    a.n = n; a.ilo = ilo; a.ihi = ihi; a.hcol0 = 0; a.lc0 = 0; a.lc1 = n; a.zrows = n; a.ldz = n;
-    a.wins = d_wins; a.win_begin = P.step_begin[s]; a.win_count = P.step_begin[s + 1] - P.step_begin[s];
-    a.coef = g.d_coef; a.KP = KP; a.QLD = QLD; a.slot_offset = (s % hqr::kQSets) * P.nchains; a.step = s;
-    const WindowDesc* hw = P.windows.data() + a.win_begin;
-    StepArgs aH = a, aHz = a, aT = a, aTz = a;
-    aH.H = H; aH.Z = Q; aH.qslots = g.d_q;     // left on H, Qacc Q_W
-    aHz.H = H; aHz.Z = nullptr; aHz.qslots = zslots;  // right on H rows above W with Z_W
-    aT.H = T; aT.Z = nullptr; aT.qslots = g.d_q;      // left on T
-    aTz.H = T; aTz.Z = Z; aTz.qslots = zslots;  // right on T rows above W, Zacc Z_W
-    CK(hqr::launch_qz_chase(aH, T, zslots, P.max_kw, A));
-    st.launches_chase++;
-    int64_t items;
-    double fl, by;
-    CK(hqr::launch_left(aH, hw, g.num_sms, tmA, A, &items, &fl, &by));
-    st.launches_left += items > 0; st.flops_update += fl; st.bytes_update += by;
-    CK(hqr::launch_left(aT, hw, g.num_sms, tmB, A, &items, &fl, &by));
-    st.launches_left += items > 0; st.flops_update += fl; st.bytes_update += by;
-    aHz.right_mode = 1;
-    CK(hqr::launch_right(aHz, hw, g.num_sms, tmA, A, &items, &fl, &by));
-    st.launches_right += items > 0; st.flops_update += fl; st.bytes_update += by;
-    aTz.right_mode = 1;
-    CK(hqr::launch_right(aTz, hw, g.num_sms, tmB, A, &items, &fl, &by));
-    st.launches_right += items > 0; st.flops_update += fl; st.bytes_update += by;
-    if (Q) {
-      aH.right_mode = 2;
-      CK(hqr::launch_right(aH, hw, g.num_sms, tmA, A, &items, &fl, &by));
-      st.launches_right += items > 0; st.flops_update += fl; st.bytes_update += by;
+  // Stream A: chase -> left (H, T) -> right (H, T) per step (the next chase reads their results);
+  // stream B (low priority): Qacc Q_W and Zacc Z_W, which nothing reads, trailing A
+  // by up to kQSets - 1 steps (rotating slot sets).  Captured once per (plan, pointers) into a CUDA
+  // graph and replayed.
+  auto enqueue = [&](hqr_stats* sts) -> int {
+    cudaStream_t A = g.stream, Bs = g.zstream;
+    CK(cudaEventRecord(g.ev_fork, A));
+    CK(cudaStreamWaitEvent(Bs, g.ev_fork, 0));
+    for (int s = 0; s < P.nsteps; ++s) {
+      const int set = s % hqr::kQSets;
+      if (s >= hqr::kQSets) CK(cudaStreamWaitEvent(A, g.ev_z[set], 0));
+      StepArgs a{};
+      a.n = n; a.ilo = ilo; a.ihi = ihi; a.hcol0 = 0; a.lc0 = 0; a.lc1 = n; a.zrows = n; a.ldz = n;
+      a.wins = cp->d_wins; a.win_begin = P.step_begin[s]; a.win_count = P.step_begin[s + 1] - P.step_begin[s];
+      a.coef = g.d_coef; a.KP = KP; a.QLD = QLD; a.slot_offset = set * P.nchains; a.step = s;
+      const WindowDesc* hw = P.windows.data() + a.win_begin;
+      StepArgs aH = a, aHz = a, aT = a, aTz = a;
+      aH.H = H; aH.Z = Q; aH.qslots = g.d_q;             // left on H; Qacc Q_W
+      aHz.H = H; aHz.Z = nullptr; aHz.qslots = zslots;   // right on H rows above W with Z_W
+      aT.H = T; aT.Z = nullptr; aT.qslots = g.d_q;       // left on T
+      aTz.H = T; aTz.Z = Z; aTz.qslots = zslots;         // right on T rows above W; Zacc Z_W
+      CK(hqr::launch_qz_chase(aH, T, zslots, P.max_kw, A));
+      sts->launches_chase++;
+      int64_t items;
+      double fl, by;
+      auto acc = [&](int* l) { *l += items > 0; sts->flops_update += fl; sts->bytes_update += by; };
+      CK(hqr::launch_left(aH, hw, g.num_sms, tmA, A, &items, &fl, &by)); acc(&sts->launches_left);
+      CK(hqr::launch_left(aT, hw, g.num_sms, tmB, A, &items, &fl, &by)); acc(&sts->launches_left);
+      aHz.right_mode = 1;
+      CK(hqr::launch_right(aHz, hw, g.num_sms, tmA, A, &items, &fl, &by)); acc(&sts->launches_right);
+      aTz.right_mode = 1;
+      CK(hqr::launch_right(aTz, hw, g.num_sms, tmB, A, &items, &fl, &by)); acc(&sts->launches_right);
+      CK(cudaEventRecord(g.ev_q[set], A));
+      CK(cudaStreamWaitEvent(Bs, g.ev_q[set], 0));
+      if (Q) {
+        aH.right_mode = 2;
+        CK(hqr::launch_right(aH, hw, g.num_sms, tmA, Bs, &items, &fl, &by)); acc(&sts->launches_right);
+      }
+      if (Z) {
+        aTz.right_mode = 2;
+        CK(hqr::launch_right(aTz, hw, g.num_sms, tmB, Bs, &items, &fl, &by)); acc(&sts->launches_right);
+      }
+      CK(cudaEventRecord(g.ev_z[set], Bs));
     }
-    if (Z) {
-      aTz.right_mode = 2;
-      CK(hqr::launch_right(aTz, hw, g.num_sms, tmB, A, &items, &fl, &by));
-      st.launches_right += items > 0; st.flops_update += fl; st.bytes_update += by;
+    CK(cudaEventRecord(g.ev_join, Bs));
+    CK(cudaStreamWaitEvent(A, g.ev_join, 0));
+    sts->steps = P.nsteps;
+    sts->windows = (int64_t)P.windows.size();
+    sts->kernels_launched = sts->launches_chase + sts->launches_left + sts->launches_right;
+    return 0;
+  };
+  CK(cudaEventRecord(g.ev0, g.stream));
+  if (g.flags & (HQR_FLAG_NO_GRAPH | HQR_FLAG_PROFILE)) {
+    rc = enqueue(&st);
+    if (rc) return rc;
+  } else {
+    GraphKey gk{key, H, T};
+    gk.pk.push_back((int64_t)(uintptr_t)Q);
+    gk.pk.push_back((int64_t)(uintptr_t)Z);
+    auto git = g.graphs.find(gk);
+    if (git == g.graphs.end()) {
+      cudaGraph_t graph;
+      hqr_stats cap{};
+      CK(cudaStreamBeginCapture(g.stream, cudaStreamCaptureModeThreadLocal));
+      const int rc2 = enqueue(&cap);
+      const cudaError_t ec = cudaStreamEndCapture(g.stream, &graph);
+      if (rc2) return rc2;
+      CK(ec);
+      cudaGraphExec_t exec;
+      CK(cudaGraphInstantiate(&exec, graph, 0));
+      cudaGraphDestroy(graph);
+      git = g.graphs.emplace(gk, CachedGraph{exec, cap}).first;
     }
+    CK(cudaGraphLaunch(git->second.exec, g.stream));
+    const hqr_stats& c = git->second.stats;
+    st.flops_update = c.flops_update; st.bytes_update = c.bytes_update;
+    st.launches_chase = c.launches_chase; st.launches_left = c.launches_left; st.launches_right = c.launches_right;
+    st.steps = c.steps; st.windows = c.windows; st.kernels_launched = c.kernels_launched;
   }
-  CK(cudaEventRecord(g.ev1, A));
-  CK(cudaStreamSynchronize(A));
+  CK(cudaEventRecord(g.ev1, g.stream));
+  CK(cudaStreamSynchronize(g.stream));
   CK(cudaGetLastError());
-  cudaFree(d_wins);
   float ms = 0;
   CK(cudaEventElapsedTime(&ms, g.ev0, g.ev1));
   st.ms_total = ms;
-  st.steps = P.nsteps;
-  st.windows = (int64_t)P.windows.size();
-  st.kernels_launched = st.launches_chase + st.launches_left + st.launches_right;
   g.stats = st;
   g.wstats_plan = nullptr;  // flops_dmma is not tracked for the QZ sweep
   return 0;
