@@ -11,6 +11,7 @@
 //   (HQR_FLAG_NO_GRAPH launches directly; HQR_FLAG_PROFILE times each kernel with events).
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -80,10 +81,96 @@ struct FusedTasks {            // task queues of every step for the fused step k
   hqr::Task* d_tasks = nullptr;
   hqr::StepInfo* d_steps = nullptr;
   hqr::WinDeps* d_wdeps = nullptr;
-  int* d_ctr = nullptr;                  // [8 claim counters][4 per step][4 per window]
+  int* d_ctr = nullptr;                  // [8 claim counters][4 per step][kWinCtr per window][1 per task]
   size_t nctr = 0;
+  std::vector<int32_t> dep_begin;        // task t's dependencies: deps[dep_begin[t] .. dep_begin[t+1])
+  std::vector<int2> deps;                // (task index, completion count to wait for)
+  int32_t* d_dep_begin = nullptr;
+  int2* d_deps = nullptr;
   double flops = 0, bytes = 0;
 };
+
+// Precise task dependencies (DESIGN.md §6 "Task dependencies"): every update task and chase
+// reads and writes one rectangle of H or Z (a left task: the window's rows x its column tiles; a
+// right task: its row tiles x the window's columns; Z likewise; a chase: H(W, W)).  The task list is
+// a valid sequential order (steps in order; within a step LeftNear, RightNear, Left, chases, Right,
+// Z, far-right), so a task only has to wait for the last earlier task that touched each part of its
+// rectangle.  Parts = square cells of c x c elements; a shared cell without a shared element only
+// adds a wait (correct, but it can chain independent tasks: the windows of one wavefront step are
+// only lag*s - k rows / columns apart -- 16 at k = 96 -- so the cell side is the largest power of
+// two <= min(8, that gap)).  GEMM tasks also wait for their window's chase (the Q_W slot).
+int build_task_deps(const Plan& P, int KP, int64_t n, int64_t zrows, bool has_z, FusedTasks* f) {
+  int64_t gap = 8;
+  for (int g = 0; g < P.nsteps; ++g)
+    for (int i = P.step_begin[g] + 1; i < P.step_begin[g + 1]; ++i)
+      gap = std::min<int64_t>(gap, (int64_t)P.windows[i].w0 - P.windows[i - 1].w1 - 1);
+  int cell = 8;
+  while (cell > 1 && cell > gap) cell >>= 1;
+  const int kDepRows = cell, kDepCols = cell;
+  const int64_t rc = (n + kDepRows - 1) / kDepRows, cc = (n + kDepCols - 1) / kDepCols;
+  const int64_t zrc = (zrows + kDepRows - 1) / kDepRows;
+  std::vector<int32_t> lastH((size_t)(rc * cc), -1), lastZ(has_z ? (size_t)(zrc * cc) : 0, -1);
+  std::vector<int32_t> chase_task(P.windows.size(), -1);  // window -> its chase task
+  const int NT = hqr::left_cols(KP), MT = hqr::right_rows(KP);
+  f->dep_begin.assign(f->tasks.size() + 1, 0);
+  f->deps.clear();
+  std::vector<int32_t> seen;
+  StepArgs a{};
+  a.n = n; a.lc0 = 0; a.lc1 = n;
+  auto target = [&](int32_t d) {
+    const hqr::Task& D = f->tasks[d];
+    return D.type == hqr::kTaskChase ? 1 : 4 * D.ntiles;
+  };
+  for (int g = 0; g < P.nsteps; ++g) {
+    for (int32_t t = f->begin[g]; t < f->begin[g + 1]; ++t) {
+      const hqr::Task& T = f->tasks[t];
+      f->dep_begin[t] = (int32_t)f->deps.size();
+      seen.clear();
+      std::vector<int32_t>* grid = &lastH;
+      int64_t r0, r1, c0, c1;  // rectangle [r0, r1) x [c0, c1)
+      if (T.type == hqr::kTaskChase) {
+        const int wi = P.step_begin[g + 1] + T.win;
+        const WindowDesc& w = P.windows[wi];
+        chase_task[wi] = t;
+        r0 = c0 = w.w0;
+        r1 = c1 = (int64_t)w.w1 + 1;
+      } else {
+        const int wi = P.step_begin[g] + T.win;
+        const WindowDesc& w = P.windows[wi];
+        if (chase_task[wi] >= 0) seen.push_back(chase_task[wi]);  // the Q_W slot (step 0: own launch)
+        if (T.type == hqr::kTaskLeft || T.type == hqr::kTaskLeftNear) {
+          int64_t c, cnt;
+          hqr::left_range(a, w, c, cnt);
+          r0 = w.w0; r1 = (int64_t)w.w1 + 1;
+          c0 = c + (int64_t)NT * T.tile0;
+          c1 = std::min<int64_t>(c + (int64_t)NT * (T.tile0 + T.ntiles), n);
+        } else if (T.type == hqr::kTaskZ) {
+          grid = &lastZ;
+          r0 = (int64_t)MT * T.tile0;
+          r1 = std::min<int64_t>((int64_t)MT * (T.tile0 + T.ntiles), zrows);
+          c0 = w.w0; c1 = (int64_t)w.w1 + 1;
+        } else {  // right (near / rest / far)
+          r0 = T.r_lo + (int64_t)MT * T.tile0;
+          r1 = std::min<int64_t>(T.r_lo + (int64_t)MT * (T.tile0 + T.ntiles), T.r_hi);
+          c0 = w.w0; c1 = (int64_t)w.w1 + 1;
+        }
+      }
+      if (r1 > r0 && c1 > c0) {
+        for (int64_t cj = c0 / kDepCols; cj <= (c1 - 1) / kDepCols; ++cj)
+          for (int64_t ri = r0 / kDepRows; ri <= (r1 - 1) / kDepRows; ++ri) {
+            int32_t& cell = (*grid)[(size_t)(cj * (grid == &lastZ ? zrc : rc) + ri)];
+            if (cell >= 0 && (seen.empty() || seen.back() != cell)) seen.push_back(cell);
+            cell = t;
+          }
+      }
+      std::sort(seen.begin(), seen.end());
+      seen.erase(std::unique(seen.begin(), seen.end()), seen.end());
+      for (int32_t d : seen) f->deps.push_back(make_int2(d, target(d)));
+    }
+  }
+  f->dep_begin[f->tasks.size()] = (int32_t)f->deps.size();
+  return 0;
+}
 
 struct CachedPlan {
   Plan plan;
@@ -489,13 +576,23 @@ int get_fused(CachedPlan& cp, bool has_z, int64_t n, FusedTasks** out) {
         f->steps[g2].up_need = (int32_t)(reach / hqr::kUploadChunk);
       }
     }
+    {
+      int rcd = build_task_deps(P, cp.KP, n, n, has_z, f.get());
+      if (rcd) return rcd;
+      CK(cudaMalloc(&f->d_dep_begin, f->dep_begin.size() * sizeof(int32_t)));
+      CK(cudaMemcpy(f->d_dep_begin, f->dep_begin.data(), f->dep_begin.size() * sizeof(int32_t),
+                    cudaMemcpyHostToDevice));
+      CK(cudaMalloc(&f->d_deps, std::max<size_t>(f->deps.size(), 1) * sizeof(int2)));
+      if (!f->deps.empty())
+        CK(cudaMemcpy(f->d_deps, f->deps.data(), f->deps.size() * sizeof(int2), cudaMemcpyHostToDevice));
+    }
     CK(cudaMalloc(&f->d_tasks, f->tasks.size() * sizeof(hqr::Task)));
     CK(cudaMemcpy(f->d_tasks, f->tasks.data(), f->tasks.size() * sizeof(hqr::Task), cudaMemcpyHostToDevice));
     CK(cudaMalloc(&f->d_steps, f->steps.size() * sizeof(hqr::StepInfo)));
     CK(cudaMemcpy(f->d_steps, f->steps.data(), f->steps.size() * sizeof(hqr::StepInfo), cudaMemcpyHostToDevice));
     CK(cudaMalloc(&f->d_wdeps, f->wdeps.size() * sizeof(hqr::WinDeps)));
     CK(cudaMemcpy(f->d_wdeps, f->wdeps.data(), f->wdeps.size() * sizeof(hqr::WinDeps), cudaMemcpyHostToDevice));
-    f->nctr = 8 + 4 * (size_t)P.nsteps + hqr::kWinCtr * (size_t)nwin_all;
+    f->nctr = 8 + 4 * (size_t)P.nsteps + hqr::kWinCtr * (size_t)nwin_all + f->tasks.size();  // + per task
     CK(cudaMalloc(&f->d_ctr, f->nctr * sizeof(int)));
     slot = std::move(f);
   }
@@ -670,6 +767,7 @@ int enqueue_fused(CachedPlan& cp, double* H, double* Z, int64_t n, const hqr::Te
   st->launches_chase++;
   int* step_ctr = f->d_ctr + 8;
   int* win_ctr = step_ctr + 4 * (size_t)P.nsteps;
+  int* task_ctr = win_ctr + hqr::kWinCtr * P.windows.size();  // per task: completion count
   // (step 0's chases ran in their own launch: step-0 tasks do not wait for them)
   const StepArgs base = args(0);
   static const bool per_step = hqr::tuning_env("HQR_PER_STEP") != nullptr;  // A/B knob (tuning builds): a launch per step
@@ -677,8 +775,9 @@ int enqueue_fused(CachedPlan& cp, double* H, double* Z, int64_t n, const hqr::Te
     // one persistent launch for the whole sweep: step g+1's work starts as soon as its own
     // dependencies are met (no launch boundary, no end-of-step tail)
     mark(3);
-    CK(hqr::launch_step(base, f->d_steps, P.nsteps, f->d_wdeps, f->d_tasks, (int)f->tasks.size(), f->d_ctr,
-                        step_ctr, win_ctr, io ? io->d_flags : nullptr, tm, P.max_kw, g.num_sms, A));
+    CK(hqr::launch_step(base, f->d_steps, P.nsteps, f->d_tasks, (int)f->tasks.size(), 0, f->d_dep_begin,
+                        f->d_deps, f->d_ctr, step_ctr, task_ctr, io ? io->d_flags : nullptr, tm, P.max_kw,
+                        g.num_sms, A));
     mark(-1);
     st->launches_left++;
     if (io) {
@@ -690,8 +789,8 @@ int enqueue_fused(CachedPlan& cp, double* H, double* Z, int64_t n, const hqr::Te
     for (int s = 0; s < P.nsteps; ++s) {
       const int nt = f->begin[s + 1] - f->begin[s];
       mark(3);
-      CK(hqr::launch_step(base, f->d_steps, P.nsteps, f->d_wdeps, f->d_tasks + f->begin[s], nt,
-                          step_ctr + 4 * s + 3, step_ctr, win_ctr, nullptr, tm, P.max_kw, g.num_sms, A));
+      CK(hqr::launch_step(base, f->d_steps, P.nsteps, f->d_tasks + f->begin[s], nt, f->begin[s], f->d_dep_begin,
+                          f->d_deps, step_ctr + 4 * s + 3, step_ctr, task_ctr, nullptr, tm, P.max_kw, g.num_sms, A));
       mark(-1);
       st->launches_left++;  // one fused launch per step (counted once)
     }
@@ -802,6 +901,8 @@ int hqr_teardown(void) {
         if (f->d_ctr) cudaFree(f->d_ctr);
         if (f->d_steps) cudaFree(f->d_steps);
         if (f->d_wdeps) cudaFree(f->d_wdeps);
+        if (f->d_dep_begin) cudaFree(f->d_dep_begin);
+        if (f->d_deps) cudaFree(f->d_deps);
       }
   }
   g.plans.clear();

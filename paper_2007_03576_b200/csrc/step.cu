@@ -306,8 +306,9 @@ __device__ __forceinline__ StepArgs step_args(const StepArgs& base, const StepIn
 // (the left update of W and the near-right updates of step g-1 are ordered through W's chase).
 template <int KP>
 __global__ void __launch_bounds__(kStepThreads, 1)
-    step_kernel(StepArgs base, const StepInfo* __restrict__ steps, int nsteps, const WinDeps* __restrict__ wdeps,
-                const Task* __restrict__ tasks, int ntasks, int* next_ctr, int* step_ctr, int* win_ctr,
+    step_kernel(StepArgs base, const StepInfo* __restrict__ steps, int nsteps, const Task* __restrict__ tasks,
+                int ntasks, int task_base, const int32_t* __restrict__ dep_begin, const int2* __restrict__ deps,
+                int* next_ctr, int* step_ctr, int* task_ctr,
                 const int* __restrict__ up_flags, const __grid_constant__ CUtensorMap tmL, const __grid_constant__ CUtensorMap tmR,
                 const __grid_constant__ CUtensorMap tmZ) {
   constexpr int NS = stages_of(KP);
@@ -378,43 +379,42 @@ __global__ void __launch_bounds__(kStepThreads, 1)
       int* sc = step_ctr + 4 * g;
       const bool chase = T.type == kTaskChase;
       const int gw = chase ? -1 : S.win_begin + T.win;  // plan index of the task's window
-      const bool far_right = T.type == kTaskRightFar;
+      const int tg = task_base + t;                      // the task's index in the sweep
       if (lane == 0) {
         PROG(2000000 + t);
         if (up_flags) spin_until(up_flags + S.up_need, 1, 5);  // host-buffer sweep: rows / columns up
-        // (dependency rules: step.hpp)
-        if ((T.type == kTaskLeft || T.type == kTaskLeftNear || T.type == kTaskRightNear || chase) && g > 0) {
-          spin_until(sc - 4 + 0, 4 * steps[g - 1].nLt, 6);   // step g-1's left phase
-          spin_until(sc - 4 + 1, 4 * steps[g - 1].nRnt, 6);  // and near-right phase
-        }
-        if (!chase && g > 0) spin_until(win_ctr + kWinCtr * gw, 1, 0);
-        if (T.type == kTaskRight || far_right) spin_until(sc + 0, 4 * S.nLt, 1);
-        if (T.type == kTaskRightNear) {
-          const int k = wdeps[gw].rn_over;
-          if (k >= 0) spin_until(win_ctr + kWinCtr * k + 3, 4 * wdeps[k].lnear, 7);
-        }
-        if (chase) {
-          const WinDeps D = wdeps[steps[g + 1].win_begin + T.win];
-          if (D.c_pred >= 0) {
-            if (g > 0) spin_until(win_ctr + kWinCtr * D.c_pred, 1, 2);
-            spin_until(win_ctr + kWinCtr * D.c_pred + 3, 4 * wdeps[D.c_pred].lnear, 2);
-          }
-          if (D.c_below >= 0) {
-            if (g > 0) spin_until(win_ctr + kWinCtr * D.c_below, 1, 2);
-            spin_until(win_ctr + kWinCtr * D.c_below + 4, 4 * wdeps[D.c_below].rnear, 2);
-          }
+        if (chase) {  // the Q slot set is reused: every tile of step g+1-kQSets done
           const int g_old = g + 1 - kQSets;
           if (g_old >= 0) spin_until(step_ctr + 4 * g_old + 2, 4 * steps[g_old].ntiles, 3);
         }
-        if ((far_right || T.type == kTaskZ) && g > 0) {
-          const WinDeps D = wdeps[gw];
-          const int k = T.type == kTaskZ ? 1 : 2;
-          for (int i = 0; i < 3; ++i)
-            if (D.pred[i] >= 0)
-              spin_until(win_ctr + kWinCtr * D.pred[i] + k, 4 * (k == 1 ? wdeps[D.pred[i]].ztiles : wdeps[D.pred[i]].rftiles), 4);
-        }
-        fence_proxy_async_all();  // other SMs' generic stores before this SM's TMA reads
       }
+      {  // the last earlier task that touched each part of this task's rectangle, and (GEMM tasks)
+         // the chase that produced the window's factor (hqr_api.cu build_task_deps): 32 counters
+         // per round trip, one per lane
+#ifdef HQR_TIMING
+        const long long d0c = clock64();
+        bool waited = false;
+#endif
+        const int dend = dep_begin[tg + 1];
+        for (int d0 = dep_begin[tg]; d0 < dend; d0 += 32) {
+          const int d = d0 + lane;
+          int2 dp = make_int2(0, 0);
+          if (d < dend) dp = deps[d];
+          bool ok = d >= dend || ld_acquire(task_ctr + dp.x) >= dp.y;
+          while (!__all_sync(0xffffffffu, ok)) {
+#ifdef HQR_TIMING
+            waited = true;
+#endif
+            __nanosleep(64);
+            if (!ok) ok = ld_acquire(task_ctr + dp.x) >= dp.y;
+          }
+        }
+#ifdef HQR_TIMING
+        if (lane == 0 && waited) atomicAdd(&g_wait[1], (unsigned long long)(clock64() - d0c));
+#endif
+      }
+      __syncwarp();  // the lanes' acquires before lane 0's async-proxy fence and TMA reads
+      if (lane == 0) fence_proxy_async_all();  // other SMs' generic stores before this SM's TMA reads
       __syncwarp();
       if (chase) {
         marker(kDescChase);
@@ -436,7 +436,7 @@ __global__ void __launch_bounds__(kStepThreads, 1)
 #endif
         if (lane == 0) {
           TIM_MAX(g, 2);
-          red_release_add(win_ctr + kWinCtr * cwi, 1);  // the CTA's stores are ordered by the barrier
+          red_release_add(task_ctr + tg, 1);  // the CTA's stores are ordered by the barrier
         }
         q_win = -1;
         continue;
@@ -470,11 +470,9 @@ __global__ void __launch_bounds__(kStepThreads, 1)
                  chunk, &qfull);
       };
       const bool left = T.type == kTaskLeft || T.type == kTaskLeftNear;
-      // the counters the task's completion feeds (tiles x 4 warps)
-      int* const wc = win_ctr + kWinCtr * gw;
-      int* cnt = T.type == kTaskLeft ? sc + 0 : T.type == kTaskLeftNear ? wc + 3 : T.type == kTaskZ ? wc + 1
-               : far_right ? wc + 2 : T.type == kTaskRightNear ? wc + 4 : sc + 1;
-      int* cnt2 = T.type == kTaskLeftNear ? sc + 0 : T.type == kTaskRightNear ? sc + 1 : nullptr;
+      // the counters the task's completion feeds (tiles x 4 warps): its own, and the step's
+      int* cnt = task_ctr + tg;
+      int* cnt2 = nullptr;
       const int nq_pre = new_q ? min(T.ntiles, NS - 1) : 0;  // tiles issued before the Q_W load
       for (int i = 0; i < T.ntiles; ++i, ++j) {
         if (new_q && i == nq_pre) load_q();
@@ -620,9 +618,10 @@ size_t step_smem(int max_kw) {
 }
 
 template <int KP>
-cudaError_t launch_step_t(const StepArgs& base, const StepInfo* steps, int nsteps, const WinDeps* wdeps,
-                          const Task* tasks, int ntasks, int* next_ctr, int* step_ctr, int* win_ctr,
-                          const int* up_flags, const TensorMaps& tm, int max_kw, int num_sms, cudaStream_t st) {
+cudaError_t launch_step_t(const StepArgs& base, const StepInfo* steps, int nsteps, const Task* tasks, int ntasks,
+                          int task_base, const int32_t* dep_begin, const int2* deps, int* next_ctr, int* step_ctr,
+                          int* task_ctr, const int* up_flags, const TensorMaps& tm, int max_kw, int num_sms,
+                          cudaStream_t st) {
   static size_t configured = 0;
   const size_t smem = step_smem<KP>(max_kw);
   if (smem > configured) {
@@ -631,8 +630,9 @@ cudaError_t launch_step_t(const StepArgs& base, const StepInfo* steps, int nstep
     configured = smem;
   }
   const int grid = std::max(1, std::min(ntasks, num_sms));
-  step_kernel<KP><<<grid, kStepThreads, smem, st>>>(base, steps, nsteps, wdeps, tasks, ntasks, next_ctr,
-                                                     step_ctr, win_ctr, up_flags, tm.left_H, tm.right_H, tm.right_Z);
+  step_kernel<KP><<<grid, kStepThreads, smem, st>>>(base, steps, nsteps, tasks, ntasks, task_base, dep_begin, deps,
+                                                     next_ctr, step_ctr, task_ctr, up_flags, tm.left_H, tm.right_H,
+                                                     tm.right_Z);
   return cudaGetLastError();
 }
 
@@ -736,16 +736,20 @@ void debug_progress_init() {
 void debug_progress_init() {}
 #endif
 
-cudaError_t launch_step(const StepArgs& base, const StepInfo* steps, int nsteps, const WinDeps* wdeps,
-                        const Task* tasks, int ntasks, int* next_ctr, int* step_ctr, int* win_ctr,
-                        const int* up_flags, const TensorMaps& tm, int max_kw, int num_sms, cudaStream_t st) {
+cudaError_t launch_step(const StepArgs& base, const StepInfo* steps, int nsteps, const Task* tasks, int ntasks,
+                        int task_base, const int32_t* dep_begin, const int2* deps, int* next_ctr, int* step_ctr,
+                        int* task_ctr, const int* up_flags, const TensorMaps& tm, int max_kw, int num_sms,
+                        cudaStream_t st) {
   if (!tm.valid) return cudaErrorNotSupported;
+#define HQR_LS(K) return launch_step_t<K>(base, steps, nsteps, tasks, ntasks, task_base, dep_begin, deps, next_ctr, \
+                                          step_ctr, task_ctr, up_flags, tm, max_kw, num_sms, st)
   switch (base.KP) {
-    case 32: return launch_step_t<32>(base, steps, nsteps, wdeps, tasks, ntasks, next_ctr, step_ctr, win_ctr, up_flags, tm, max_kw, num_sms, st);
-    case 64: return launch_step_t<64>(base, steps, nsteps, wdeps, tasks, ntasks, next_ctr, step_ctr, win_ctr, up_flags, tm, max_kw, num_sms, st);
-    case 96: return launch_step_t<96>(base, steps, nsteps, wdeps, tasks, ntasks, next_ctr, step_ctr, win_ctr, up_flags, tm, max_kw, num_sms, st);
-    case 128: return launch_step_t<128>(base, steps, nsteps, wdeps, tasks, ntasks, next_ctr, step_ctr, win_ctr, up_flags, tm, max_kw, num_sms, st);
+    case 32: HQR_LS(32);
+    case 64: HQR_LS(64);
+    case 96: HQR_LS(96);
+    case 128: HQR_LS(128);
   }
+#undef HQR_LS
   return cudaErrorInvalidValue;
 }
 

@@ -75,11 +75,15 @@ void build_step_tasks(const StepArgs& a, const WindowDesc* wins, int nwin, const
 
 // One persistent launch (one CTA per SM) running `ntasks` tasks -- one step's queue, or the whole
 // sweep's -- claimed through *next_ctr.  base: the sweep's StepArgs (per-step fields come from
-// steps[]).  Needs the TMA path.
+// steps[]).  Task i of `tasks` is task task_base + i of the sweep; its dependencies are
+// deps[dep_begin[t] .. dep_begin[t+1]) (t the sweep index): (task, count) pairs, wait until
+// task_ctr[task] >= count (per-task completion counts: 4 per GEMM tile -- one per consumer warp --,
+// 1 per chase).  Needs the TMA path.
 // up_flags (nullable): per upload chunk, nonzero once on the device (host-buffer sweeps).
-cudaError_t launch_step(const StepArgs& base, const StepInfo* steps, int nsteps, const WinDeps* wdeps,
-                        const Task* tasks, int ntasks, int* next_ctr, int* step_ctr, int* win_ctr,
-                        const int* up_flags, const TensorMaps& tm, int max_kw, int num_sms, cudaStream_t st);
+cudaError_t launch_step(const StepArgs& base, const StepInfo* steps, int nsteps, const Task* tasks, int ntasks,
+                        int task_base, const int32_t* dep_begin, const int2* deps, int* next_ctr, int* step_ctr,
+                        int* task_ctr, const int* up_flags, const TensorMaps& tm, int max_kw, int num_sms,
+                        cudaStream_t st);
 
 // Debugging builds (-DHQR_PROGRESS): progress buffer in host-mapped memory, dumped after
 // HQR_PROGRESS_SECS seconds (then the process exits).  No-op otherwise.
