@@ -146,23 +146,31 @@ int hqr_qz_sweep(double* H, double* T, double* Q, double* Z, int64_t n, int64_t 
 #define HQR_MAX_WINDOW_QZ 80
 
 /*
- * QR iteration around the sweep (partial: shift generation and deflation
- * without the paper's AED window, R21):
- * repeatedly (a) take the bottom unreduced block [l, hi] of [ilo, ihi] (h(l, l-1) = 0); (b) if it has
- * at most nmin rows, compute its eigenvalues with the one-CTA Francis double-shift QR solver and
- * continue above it; (c) else sweep it (hqr_sweep's fused path, window `window`) with the
- * eigenvalues of its trailing nshifts x nshifts block as shifts (complex pairs first, then reals
- * paired), then set every subdiagonal entry with |h(k,k-1)| <= 2^-52 (|h(k-1,k-1)| + |h(k,k)|) to
- * zero (deflation).  H, Z (Z may be NULL) are n x n device matrices updated by every sweep, so on
+ * QR iteration around the sweep (PAPER.md P:270-297 AED and shifts, P:370-381,
+ * P:1142-1189 deflation; R21 / R22): repeatedly take the bottom unreduced block [l, hi] of
+ * [ilo, ihi] (h(l, l-1) = 0) and
+ *   (a) if it has at most nmin rows, compute its eigenvalues with the one-CTA Francis double-shift QR
+ *       solver and continue above it;
+ *   (b) aed_window > 0: aggressive early deflation on its trailing min(aed_window, N) window -- real
+ *       Schur form of the window (U accumulated), spike s U(0,:), deflation of the bottom blocks whose
+ *       spike entries are <= u ||H||_F (the paper's default norm-stable condition; without the
+ *       paper's reordering of failed blocks, R22), Hessenberg re-reduction, U propagated to the rest
+ *       of H and to Z by the DMMA update kernels; more than 14% deflated -> next round at once;
+ *   (c) sweep the block (hqr_sweep's fused path, window `window`) with up to nshifts shifts: the
+ *       bottom-most failed AED candidates (aed_window > 0) or the eigenvalues of the trailing
+ *       nshifts x nshifts block (aed_window == 0, R21), complex pairs first, reals paired; then set
+ *       every |h(k,k-1)| <= 2^-52 (|h(k-1,k-1)| + |h(k,k)|) to zero.
+ * H, Z (Z may be NULL) are n x n device matrices changed only by orthogonal similarities, so on
  * return Z^T H0 Z = H (Z0 = I) with H reduced to blocks of at most nmin rows.  wr, wi: host arrays of
  * n doubles receiving the eigenvalues of rows ilo..ihi (conjugate pairs adjacent).  *sweeps_out
- * (nullable): sweeps run.  Returns 0; > 0 = ihi' + 1 when max_sweeps was reached with rows
- * ilo..ihi' unfinished (LAPACK INFO style); -1 H NULL / host pointer / world > 1; -3 n; -4 ilo;
- * -5 ihi; -6 nshifts odd, < 2 or > 128; -7 window < 1; -8 nmin < 2 or > 128; -10 wr / wi NULL;
- * -100 not set up; 1000+cudaError_t.
+ * (nullable): sweeps run.  Returns 0; > 0 = ihi' + 1 when max_sweeps was reached with rows ilo..ihi'
+ * unfinished (LAPACK INFO style); -1 H NULL / host pointer / world > 1; -3 n; -4 ilo; -5 ihi; -6
+ * nshifts odd, < 2 or > 128; -7 window < 1; -8 nmin < 2 or > 128; -9 aed_window 1, < 0 or >
+ * HQR_MAX_WINDOW; -10 wr / wi NULL; -100 not set up; 1000+cudaError_t.  After the call hqr_get_stats
+ * reports launches_chase = AED steps and window_eff = eigenvalues deflated by AED.
  */
 int hqr_qr_iterate(double* H, double* Z, int64_t n, int64_t ilo, int64_t ihi, int nshifts, int window,
-                   int nmin, int max_sweeps, double* wr, double* wi, int* sweeps_out);
+                   int nmin, int aed_window, int max_sweeps, double* wr, double* wi, int* sweeps_out);
 
 /*
  * ---- Sharded sweep over several GPUs -------------------------------------------

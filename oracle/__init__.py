@@ -20,6 +20,9 @@ Functions and the passages they follow (PAPER.md line numbers, see hqr_oracle.c)
                               (the small Schur task's role; reading R21)
   qr_iterate(H, Z, ..)     -- repeated sweeps with shifts from the trailing block and deflation
                               (NEXT-2 without AED; reading R21)
+  schur(A) / aed(H, ..)    -- real Schur form with U; aggressive early deflation on a window
+                              (reading R22)
+  qr_iterate_aed(H, Z, ..) -- the QR iteration with AED (NEXT-2, R22)
 
 Parity pins for every function are in tests/test_oracle.py (none is "parity unpinned").
 """
@@ -83,6 +86,17 @@ def _load():
                                           ctypes.c_int64, ctypes.c_int, ctypes.c_int64, ctypes.c_int, dp, dp,
                                           ctypes.POINTER(ctypes.c_int)]
         lib.oracle_qr_iterate.restype = ctypes.c_int
+        ip = ctypes.POINTER(ctypes.c_int)
+        lib.oracle_schur.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p, ctypes.c_int64,
+                                     dp, dp]
+        lib.oracle_schur.restype = ctypes.c_int
+        lib.oracle_aed.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
+                                   ctypes.c_int, ctypes.c_double, dp, dp, dp, dp, ip]
+        lib.oracle_aed.restype = ctypes.c_int
+        lib.oracle_qr_iterate_aed.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64,
+                                              ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_int64, ctypes.c_int,
+                                              dp, dp, ip, ip, ip]
+        lib.oracle_qr_iterate_aed.restype = ctypes.c_int
         _lib = lib
     return _lib
 
@@ -209,3 +223,37 @@ def qr_iterate(H, Z, ilo, ihi, nshifts, nmin=64, max_sweeps=1000):
     rc = _load().oracle_qr_iterate(H.ctypes.data, None if Z is None else _as_colmajor(Z).ctypes.data, n, ilo,
                                    ihi, nshifts, nmin, max_sweeps, _dptr(wr), _dptr(wi), ctypes.byref(sw))
     return wr, wi, rc, sw.value
+
+
+def schur(A):
+    """(T, U, wr, wi, info): real Schur form T = U^T A U of the small Hessenberg matrix A."""
+    T = np.asfortranarray(np.array(A, dtype=np.float64))
+    m = T.shape[0]
+    U = np.asfortranarray(np.eye(m))
+    wr, wi = np.zeros(m), np.zeros(m)
+    info = _load().oracle_schur(T.ctypes.data, m, m, U.ctypes.data, m, _dptr(wr), _dptr(wi))
+    return T, U, wr, wi, info
+
+
+def aed(H, Z, ilo, k0, nw, thr):
+    """In place AED on the window [k0, k0+nw) of H (block from ilo): (nd, wr, wi, shift candidates)."""
+    H = _as_colmajor(H)
+    n = H.shape[0]
+    wr, wi = np.zeros(n), np.zeros(n)
+    swr, swi = np.zeros(nw), np.zeros(nw)
+    nund = ctypes.c_int()
+    nd = _load().oracle_aed(H.ctypes.data, None if Z is None else _as_colmajor(Z).ctypes.data, n, ilo, k0, nw, thr,
+                            _dptr(wr), _dptr(wi), _dptr(swr), _dptr(swi), ctypes.byref(nund))
+    return nd, wr, wi, swr[:nund.value] + 1j * swi[:nund.value]
+
+
+def qr_iterate_aed(H, Z, ilo, ihi, nshifts, nw=96, nmin=64, max_sweeps=1000):
+    """In place: the QR iteration with AED (R22).  Returns (wr, wi, rc, sweeps, aed_steps, aed_deflated)."""
+    H = _as_colmajor(H)
+    n = H.shape[0]
+    wr, wi = np.zeros(n), np.zeros(n)
+    sw, na, nd = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+    rc = _load().oracle_qr_iterate_aed(H.ctypes.data, None if Z is None else _as_colmajor(Z).ctypes.data, n, ilo,
+                                       ihi, nshifts, nw, nmin, max_sweeps, _dptr(wr), _dptr(wi), ctypes.byref(sw),
+                                       ctypes.byref(na), ctypes.byref(nd))
+    return wr, wi, rc, sw.value, na.value, nd.value

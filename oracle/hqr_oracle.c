@@ -486,3 +486,308 @@ int oracle_qr_iterate(double* H, double* Z, int64_t n, int64_t ilo, int64_t ihi,
   *sweeps_out = sweeps;
   return 0;
 }
+
+/* ===================================================================================================
+ * Aggressive early deflation (deflation conditions
+ * P:1142-1189; reading R22): on the trailing nw x nw window of an unreduced block,
+ *   (1) reduce the window to real Schur form T = U^T W U (Francis double-shift QR with deflation,
+ *       all window columns / rows updated, U accumulated);
+ *   (2) the spike v = s U(0, :) (s = the subdiagonal entry left of the window); from the bottom,
+ *       a 1x1 / 2x2 block of T is deflated when its spike entries are <= u ||H||_F (the paper's
+ *       default "norm-stable" condition) -- without the paper's reordering of failed blocks: the
+ *       first failure ends the check (R22);
+ *   (3) if anything deflated: zero the deflated spike entries, reflect the remaining spike v(0:m)
+ *       onto e1 (P = I - tau w w^T, applied to T(0:m,0:m) from both sides and to U(:, 0:m)) and
+ *       restore Hessenberg form of T(0:m, 0:m) by Householder reflectors (general length, R2
+ *       convention), accumulated into U;
+ *   (4) write T into H's window, the spike column (beta, 0, ...) left of it, and propagate U:
+ *       H(window, right) <- U^T H(window, right), H(above, window) <- H(above, window) U,
+ *       Z(:, window) <- Z(:, window) U.
+ * The eigenvalues of T(0:m, 0:m) -- the failed candidates -- are the next sweep's shifts.
+ * =================================================================================================== */
+
+/* R2 Householder reflector of general length m (x overwritten by v, v[0] = 1).  Returns tau, beta. */
+static void house_n(int m, double* x, double* tau, double* beta) {
+  double tail2 = 0.0;
+  for (int i = 1; i < m; ++i) tail2 += x[i] * x[i];
+  const double alpha = x[0];
+  if (tail2 == 0.0) {
+    *tau = 0.0;
+    *beta = alpha;
+    x[0] = 1.0;
+    for (int i = 1; i < m; ++i) x[i] = 0.0;
+    return;
+  }
+  const double norm = sqrt(alpha * alpha + tail2);
+  const double b = (alpha >= 0.0) ? -norm : norm;
+  *tau = (b - alpha) / b;
+  for (int i = 1; i < m; ++i) x[i] = x[i] / (alpha - b);
+  x[0] = 1.0;
+  *beta = b;
+}
+
+/* A(r0.., c0..c1) -= tau w (w^T A) for rows r0..r0+m-1 (ld lda) */
+static void refl_left(double* A, int64_t lda, int64_t r0, int m, int64_t c0, int64_t c1, const double* w, double tau) {
+  for (int64_t c = c0; c < c1; ++c) {
+    double s = 0.0;
+    for (int i = 0; i < m; ++i) s += w[i] * A[(r0 + i) + c * lda];
+    for (int i = 0; i < m; ++i) A[(r0 + i) + c * lda] -= tau * w[i] * s;
+  }
+}
+/* A(r0..r1-1, c0..c0+m-1) -= tau (A w) w^T */
+static void refl_right(double* A, int64_t lda, int64_t r0, int64_t r1, int64_t c0, int m, const double* w, double tau) {
+  for (int64_t r = r0; r < r1; ++r) {
+    double s = 0.0;
+    for (int i = 0; i < m; ++i) s += A[r + (c0 + i) * lda] * w[i];
+    for (int i = 0; i < m; ++i) A[r + (c0 + i) * lda] -= tau * s * w[i];
+  }
+}
+
+/* Real Schur form of the m x m Hessenberg matrix A (ld lda) with U (m x m, ld ldu) accumulated:
+ * oracle_small_eig's iteration with every reflector applied to all columns right of / rows above the
+ * active block (wantt) and to U (wantz).  Eigenvalues to wr / wi.  Returns 0 or the count not found. */
+int oracle_schur(double* A, int64_t m, int64_t lda, double* U, int64_t ldu, double* wr, double* wi) {
+#define A_(r, c) A[(size_t)(r) + (size_t)(c) * (size_t)lda]
+  int64_t i = m - 1;
+  int64_t total = 0;
+  while (i >= 0) {
+    int its = 0;
+    int64_t l = 0;
+    for (;;) {
+      for (l = i; l > 0; --l) {
+        const double s = fabs(A_(l - 1, l - 1)) + fabs(A_(l, l));
+        if (fabs(A_(l, l - 1)) <= 0x1p-52 * s) {
+          A_(l, l - 1) = 0.0;
+          break;
+        }
+      }
+      if (l >= i - 1) break;
+      if (++total > 30 * m) return (int)(i + 1);
+      ++its;
+      double sigma, pi;
+      if (its == 10 || its == 20) {
+        const double s = fabs(A_(i, i - 1)) + fabs(A_(i - 1, i - 2));
+        const double h11 = 0.75 * s + A_(i, i);
+        sigma = 2.0 * h11;
+        pi = h11 * h11 + 0.4375 * s * s;
+      } else {
+        const double a = A_(i - 1, i - 1), b = A_(i - 1, i), c = A_(i, i - 1), d = A_(i, i);
+        sigma = a + d;
+        pi = a * d - b * c;
+      }
+      for (int64_t p = l - 1; p <= i - 2; ++p) {
+        const int mm = (p <= i - 3) ? 3 : 2;
+        double x[3], v[3], tau, beta;
+        if (p == l - 1) {
+          const double h00 = A_(l, l), h01 = A_(l, l + 1), h10 = A_(l + 1, l), h11 = A_(l + 1, l + 1);
+          const double h21 = A_(l + 2, l + 1);
+          x[0] = h00 * (h00 - sigma) + h01 * h10 + pi;
+          x[1] = h10 * (h00 + h11 - sigma);
+          x[2] = h10 * h21;
+        } else {
+          for (int k = 0; k < mm; ++k) x[k] = A_(p + 1 + k, p);
+        }
+        oracle_house(mm, x, v, &tau, &beta);
+        refl_left(A, lda, p + 1, mm, (p == l - 1) ? l : p + 1, m, v, tau);   /* wantt: all columns */
+        if (p >= l) {
+          A_(p + 1, p) = beta;
+          for (int k = 1; k < mm; ++k) A_(p + 1 + k, p) = 0.0;
+        }
+        refl_right(A, lda, 0, ((p + mm + 1 < i) ? p + mm + 1 : i) + 1, p + 1, mm, v, tau);  /* rows 0.. */
+        refl_right(U, ldu, 0, m, p + 1, mm, v, tau);
+      }
+    }
+    if (l == i) {
+      wr[i] = A_(i, i);
+      wi[i] = 0.0;
+      i -= 1;
+    } else {
+      eig2(A_(i - 1, i - 1), A_(i - 1, i), A_(i, i - 1), A_(i, i), &wr[i - 1], &wi[i - 1], &wr[i], &wi[i]);
+      i -= 2;
+    }
+  }
+#undef A_
+  return 0;
+}
+
+/* AED on the window [k0, k0+nw) of H (n x n, column-major) inside the unreduced block [ilo, ihi]
+ * (k0 + nw - 1 == ihi).  thr: the deflation threshold (u ||H||_F).  Writes the eigenvalues of the
+ * deflated blocks to wr / wi at their rows and the window's undeflated eigenvalues (the shifts, top
+ * to bottom) to swr / swi (nw entries; count returned through *nund).  Returns the number of
+ * deflated eigenvalues nd (the rows k0+nw-nd .. ihi are then decoupled: H[ihi-nd+1, ihi-nd] = 0).
+ * H and Z change only when nd > 0. */
+int oracle_aed(double* H, double* Z, int64_t n, int64_t ilo, int64_t k0, int nw, double thr, double* wr,
+               double* wi, double* swr, double* swi, int* nund) {
+  double* T = (double*)malloc(sizeof(double) * (size_t)nw * nw * 2 + sizeof(double) * (size_t)(4 * nw + 8));
+  double* U = T + (size_t)nw * nw;
+  double* v = U + (size_t)nw * nw;
+  double* ew = v + nw;
+  double* ei = ew + nw;
+  double* w = ei + nw;
+  for (int c = 0; c < nw; ++c)
+    for (int r = 0; r < nw; ++r) {
+      T[r + c * nw] = EL(H, k0 + r, k0 + c, n);
+      U[r + c * nw] = (r == c) ? 1.0 : 0.0;
+    }
+  oracle_schur(T, nw, nw, U, nw, ew, ei);
+  const double s = (k0 > ilo) ? EL(H, k0, k0 - 1, n) : 0.0;
+  for (int j = 0; j < nw; ++j) v[j] = s * U[0 + j * nw];
+  /* deflation from the bottom (norm-stable condition, no reordering: R22) */
+  int m = nw;
+  while (m > 0) {
+    const int bs = (m >= 2 && T[(m - 1) + (m - 2) * nw] != 0.0) ? 2 : 1;
+    int ok = 1;
+    for (int j = m - bs; j < m; ++j) ok &= fabs(v[j]) <= thr;
+    if (!ok) break;
+    for (int j = m - bs; j < m; ++j) {
+      wr[k0 + j] = ew[j];
+      wi[k0 + j] = ei[j];
+      v[j] = 0.0;
+    }
+    m -= bs;
+  }
+  const int nd = nw - m;
+  *nund = m;
+  for (int j = 0; j < m; ++j) {
+    swr[j] = ew[j];
+    swi[j] = ei[j];
+  }
+  if (nd > 0) {
+    double beta = 0.0;
+    if (m > 1 && s != 0.0) { /* reflect the remaining spike onto e1 */
+      double tau;
+      for (int j = 0; j < m; ++j) w[j] = v[j];
+      house_n(m, w, &tau, &beta);
+      refl_left(T, nw, 0, m, 0, nw, w, tau);
+      refl_right(T, nw, 0, m, 0, m, w, tau);
+      refl_right(U, nw, 0, nw, 0, m, w, tau);
+      /* Hessenberg form of T(0:m, 0:m) */
+      for (int j = 0; j + 2 < m; ++j) {
+        const int len = m - j - 1;
+        for (int k = 0; k < len; ++k) w[k] = T[(j + 1 + k) + j * nw];
+        double tj, bj;
+        house_n(len, w, &tj, &bj);
+        refl_left(T, nw, j + 1, len, j + 1, nw, w, tj);
+        T[(j + 1) + j * nw] = bj;
+        for (int k = 1; k < len; ++k) T[(j + 1 + k) + j * nw] = 0.0;
+        refl_right(T, nw, 0, m, j + 1, len, w, tj);
+        refl_right(U, nw, 0, nw, j + 1, len, w, tj);
+      }
+    } else {
+      beta = v[0];
+    }
+    /* write back: the window, the spike column, then U into the rest of H and into Z */
+    for (int c = 0; c < nw; ++c)
+      for (int r = 0; r < nw; ++r) EL(H, k0 + r, k0 + c, n) = T[r + c * nw];
+    if (k0 > ilo) {
+      EL(H, k0, k0 - 1, n) = beta;
+      for (int r = 1; r < nw; ++r) EL(H, k0 + r, k0 - 1, n) = 0.0;
+    }
+    /* H(window, k0+nw : n) <- U^T H(window, ...) */
+    double* tmp = (double*)malloc(sizeof(double) * (size_t)nw);
+    for (int64_t c = k0 + nw; c < n; ++c) {
+      for (int i = 0; i < nw; ++i) {
+        double a = 0.0;
+        for (int k = 0; k < nw; ++k) a += U[k + i * nw] * EL(H, k0 + k, c, n);
+        tmp[i] = a;
+      }
+      for (int i = 0; i < nw; ++i) EL(H, k0 + i, c, n) = tmp[i];
+    }
+    /* H(0:k0, window) <- H(0:k0, window) U ; Z(:, window) <- Z(:, window) U */
+    for (int pass = 0; pass < 2; ++pass) {
+      double* M = pass == 0 ? H : Z;
+      const int64_t rows = pass == 0 ? k0 : n;
+      if (!M) continue;
+      for (int64_t r = 0; r < rows; ++r) {
+        for (int j = 0; j < nw; ++j) {
+          double a = 0.0;
+          for (int k = 0; k < nw; ++k) a += EL(M, r, k0 + k, n) * U[k + j * nw];
+          tmp[j] = a;
+        }
+        for (int j = 0; j < nw; ++j) EL(M, r, k0 + j, n) = tmp[j];
+      }
+    }
+    free(tmp);
+  }
+  free(T);
+  return nd;
+}
+
+/* The QR iteration with AED (R22): per round on the bottom unreduced block [l, hi] (N rows):
+ * N <= nmin -> oracle_small_eig; else AED on the trailing min(nw, N) window; if it deflated more than
+ * 14% of the window (LAPACK's nibble rule) the next round starts at once, else the block is swept with
+ * the bottom-most (up to nshifts) undeflated candidates as shifts, followed by the small-subdiagonal
+ * deflation (R16).  thr = 2^-53 ||H||_F (u = the unit roundoff, R10).  Returns 0, or -(sweeps) when
+ * max_sweeps was reached; *naed_out = AED steps, *ndefl_out = eigenvalues deflated by AED. */
+int oracle_qr_iterate_aed(double* H, double* Z, int64_t n, int64_t ilo, int64_t ihi, int nshifts, int nw,
+                          int64_t nmin, int max_sweeps, double* wr, double* wi, int* sweeps_out, int* naed_out,
+                          int* ndefl_out) {
+  double fro = 0.0;
+  for (size_t k = 0; k < (size_t)n * (size_t)n; ++k) fro += H[k] * H[k];
+  const double thr = 0x1p-53 * sqrt(fro);
+  int sweeps = 0, naed = 0, ndefl = 0;
+  int64_t hi = ihi;
+  double* B = (double*)malloc(sizeof(double) * (size_t)(nmin * nmin + 4 * nw + 4 * nshifts + 8));
+  double* swr = B + (size_t)nmin * nmin;
+  double* swi = swr + nw;
+  double* sr = swi + nw;
+  double* si = sr + nshifts;
+  int rc = 0;
+  while (hi >= ilo) {
+    int64_t l = hi;
+    while (l > ilo && EL(H, l, l - 1, n) != 0.0) --l;
+    const int64_t N = hi - l + 1;
+    if (N <= nmin) {
+      for (int64_t c = 0; c < N; ++c)
+        for (int64_t r = 0; r < N; ++r) B[r + c * N] = EL(H, l + r, l + c, n);
+      oracle_small_eig(B, N, N, wr + l, wi + l);
+      hi = l - 1;
+      continue;
+    }
+    if (sweeps >= max_sweeps) {
+      rc = -sweeps;
+      break;
+    }
+    const int nwin = (int)((N < nw) ? N : nw);
+    int nund = 0;
+    const int nd = oracle_aed(H, Z, n, l, hi - nwin + 1, nwin, thr, wr, wi, swr, swi, &nund);
+    ++naed;
+    ndefl += nd;
+    if (nd > 0) {
+      hi -= nd;
+      if (100 * nd > 14 * nwin) continue;
+      if (hi - l + 1 <= nmin) continue;
+    }
+    /* shifts: the bottom-most undeflated candidates, paired (make_shifts) */
+    const int ns_avail = nund;
+    const int want = (nshifts < ns_avail) ? nshifts : ns_avail;
+    int k = make_shifts(swr + (ns_avail - want), swi + (ns_avail - want), want, want, sr, si);
+    if (k > hi - l + 1) k = (int)((hi - l + 1) & ~(int64_t)1);
+    if (k < 2) { /* no usable candidates: the eigenvalues of the trailing block (R21) */
+      const int64_t Nb = hi - l + 1;
+      int ns = (int)((nshifts < ((Nb - 2) & ~(int64_t)1)) ? nshifts : ((Nb - 2) & ~(int64_t)1));
+      if (ns < 2) ns = 2;
+      double* Bt = (double*)malloc(sizeof(double) * (size_t)(ns * ns + 2 * ns));
+      for (int c = 0; c < ns; ++c)
+        for (int r = 0; r < ns; ++r) Bt[r + c * ns] = EL(H, hi - ns + 1 + r, hi - ns + 1 + c, n);
+      oracle_small_eig(Bt, ns, ns, Bt + ns * ns, Bt + ns * ns + ns);
+      k = make_shifts(Bt + ns * ns, Bt + ns * ns + ns, ns, ns, sr, si);
+      free(Bt);
+      if (k < 2) {
+        rc = -sweeps;
+        break;
+      }
+    }
+    oracle_sweep(H, Z, n, l, hi, sr, si, k, 0, 0, k / 2);
+    ++sweeps;
+    for (int64_t r = l + 1; r <= hi; ++r) {
+      const double sd = fabs(EL(H, r - 1, r - 1, n)) + fabs(EL(H, r, r, n));
+      if (fabs(EL(H, r, r - 1, n)) <= 0x1p-52 * sd) EL(H, r, r - 1, n) = 0.0;
+    }
+  }
+  free(B);
+  *sweeps_out = sweeps;
+  *naed_out = naed;
+  *ndefl_out = ndefl;
+  return rc;
+}

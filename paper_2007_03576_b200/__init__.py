@@ -134,7 +134,7 @@ def lib():
         L.hqr_qz_sweep.restype = ctypes.c_int
         L.hqr_qr_iterate.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64,
                                      ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
-                                     ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
+                                     ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
         L.hqr_qr_iterate.restype = ctypes.c_int
         for nm in ("hqr_sweep_dist_multi", "hqr_sweep_virtual_multi"):
             fn = getattr(L, nm)
@@ -293,15 +293,15 @@ def qz_sweep(H, T, Q, Z, ilo: int, ihi: int, shifts_re, shifts_im, window: int =
 
 
 def qr_iterate(H, Z, ilo: int, ihi: int, nshifts: int = 32, window: int = DEFAULT_WINDOW, nmin: int = 64,
-               max_sweeps: int = 10000):
+               max_sweeps: int = 10000, aed_window: int = 0):
     """QR iteration (include/hqr.h hqr_qr_iterate) on device H (and Z): returns (wr, wi, info,
-    sweeps) with the eigenvalues of rows ilo..ihi in wr / wi."""
+    sweeps) with the eigenvalues of rows ilo..ihi in wr / wi.  aed_window > 0: AED (R22)."""
     hp, n = _ptr_n(H)
     zp, _ = _ptr_n(Z)
     wr, wi = np.zeros(n), np.zeros(n)
     sw = ctypes.c_int()
-    rc = lib().hqr_qr_iterate(hp, zp, n, ilo, ihi, int(nshifts), int(window), int(nmin), int(max_sweeps),
-                              wr.ctypes.data, wi.ctypes.data, ctypes.byref(sw))
+    rc = lib().hqr_qr_iterate(hp, zp, n, ilo, ihi, int(nshifts), int(window), int(nmin), int(aed_window),
+                              int(max_sweeps), wr.ctypes.data, wi.ctypes.data, ctypes.byref(sw))
     if rc < 0:
         raise HQRError(rc, "hqr_qr_iterate")
     return wr, wi, rc, sw.value

@@ -1887,7 +1887,7 @@ int make_shifts_host(const double* wr, const double* wi, int m, int ns, double* 
 }  // namespace
 
 int hqr_qr_iterate(double* H, double* Z, int64_t n, int64_t ilo, int64_t ihi, int nshifts, int window,
-                   int nmin, int max_sweeps, double* wr, double* wi, int* sweeps_out) {
+                   int nmin, int aed_window, int max_sweeps, double* wr, double* wi, int* sweeps_out) {
   if (!H) return -1;
   if (n < 1) return -3;
   if (ilo < 0 || ilo > ihi) return -4;
@@ -1895,23 +1895,48 @@ int hqr_qr_iterate(double* H, double* Z, int64_t n, int64_t ilo, int64_t ihi, in
   if (nshifts < 2 || (nshifts & 1) || nshifts > hqr::small_eig_max()) return -6;
   if (window < 1) return -7;
   if (nmin < 2 || nmin > hqr::small_eig_max()) return -8;
+  if (aed_window < 0 || aed_window == 1 || aed_window > hqr::kMaxWindow) return -9;
   if (!wr || !wi) return -10;
   if (!g.ready) return -100;
   if (g.world > 1) return -1;
   CK(cudaSetDevice(g.device));
   if (!is_device_ptr(H) || (Z && !is_device_ptr(Z))) return -1;
-  double* d_w = nullptr;  // 2 * small_eig_max() eigenvalue scratch + info / counters
-  CK(cudaMalloc(&d_w, (2 * (size_t)hqr::small_eig_max() + 2) * sizeof(double)));
-  int* d_info = reinterpret_cast<int*>(d_w + 2 * hqr::small_eig_max());
-  std::vector<double> sub((size_t)std::max<int64_t>(n - 1, 1)), ewr(nshifts), ewi(nshifts), sr(nshifts), si(nshifts);
-  int sweeps = 0, rc = 0;
+  const int SM = hqr::small_eig_max();
+  const int KPa = hqr::padded_kp(std::max(aed_window, 2)), QLDa = hqr::pad_ld(KPa);
+  // scratch: eigenvalues (2 SM), AED eigenvalues (2 kMaxWindow), ||H||^2, ints, the AED factor slot,
+  // the AED window descriptor
+  const size_t nscr = 2 * (size_t)SM + 2 * (size_t)hqr::kMaxWindow + 8 + (size_t)KPa * QLDa + 16;
+  double* d_w = nullptr;
+  CK(cudaMalloc(&d_w, nscr * sizeof(double)));
+  double* d_ew = d_w + 2 * SM;
+  double* d_ei = d_ew + hqr::kMaxWindow;
+  double* d_fro = d_ei + hqr::kMaxWindow;
+  int* d_info = reinterpret_cast<int*>(d_fro + 1);   // [0] info, [1] deflate count, [2..3] AED res
+  double* d_uslot = d_fro + 8;
+  WindowDesc* d_wd = reinterpret_cast<WindowDesc*>(d_uslot + (size_t)KPa * QLDa);
+  std::vector<double> sub((size_t)std::max<int64_t>(n - 1, 1)), ewr(std::max(nshifts, hqr::kMaxWindow)),
+      ewi(ewr.size()), sr(nshifts), si(nshifts);
+  int sweeps = 0, rc = 0, naed = 0, ndefl = 0;
   int64_t hi = ihi;
-  double falg = 0.0;
+  double falg = 0.0, thr = 0.0;
   cudaEvent_t t0 = nullptr, t1 = nullptr;
   CK(cudaEventCreate(&t0));
   CK(cudaEventCreate(&t1));
   CK(cudaEventRecord(t0, g.stream));
   auto fail = [&](int code) { cudaFree(d_w); cudaEventDestroy(t0); cudaEventDestroy(t1); return code; };
+  if (aed_window > 0) {  // deflation threshold u ||H||_F (the paper's default norm-stable condition, R22)
+    double fro2 = 0.0;
+    cudaError_t e = hqr::launch_fro2(H, n * n, d_fro, g.num_sms, g.stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&fro2, d_fro, sizeof(double), cudaMemcpyDeviceToHost, g.stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(g.stream);
+    if (e != cudaSuccess) return fail(cuerr(e));
+    thr = 0x1p-53 * std::sqrt(fro2);
+  }
+  hqr::TensorMaps tma;
+  if (aed_window > 0) {
+    cudaError_t e = hqr::make_tensor_maps(&tma, H, n, Z, n, n, n, KPa);
+    if (e != cudaSuccess) return fail(cuerr(e));
+  }
   while (hi >= ilo) {
     // the bottom unreduced block [l, hi]: the subdiagonal h(k, k-1), k = ilo+1 .. hi (stride n+1)
     int64_t l = hi;
@@ -1924,10 +1949,9 @@ int hqr_qr_iterate(double* H, double* Z, int64_t n, int64_t ilo, int64_t ihi, in
     }
     const int64_t N = hi - l + 1;
     if (N <= nmin) {  // small block: its eigenvalues directly
-      cudaError_t e = hqr::launch_small_eig(H, n, l, (int)N, d_w, d_w + hqr::small_eig_max(), d_info, g.stream);
+      cudaError_t e = hqr::launch_small_eig(H, n, l, (int)N, d_w, d_w + SM, d_info, g.stream);
       if (e == cudaSuccess) e = cudaMemcpyAsync(wr + l, d_w, N * sizeof(double), cudaMemcpyDeviceToHost, g.stream);
-      if (e == cudaSuccess)
-        e = cudaMemcpyAsync(wi + l, d_w + hqr::small_eig_max(), N * sizeof(double), cudaMemcpyDeviceToHost, g.stream);
+      if (e == cudaSuccess) e = cudaMemcpyAsync(wi + l, d_w + SM, N * sizeof(double), cudaMemcpyDeviceToHost, g.stream);
       if (e == cudaSuccess) e = cudaStreamSynchronize(g.stream);
       if (e != cudaSuccess) return fail(cuerr(e));
       hi = l - 1;
@@ -1937,25 +1961,75 @@ int hqr_qr_iterate(double* H, double* Z, int64_t n, int64_t ilo, int64_t ihi, in
       rc = (int)(hi + 1);  // LAPACK-style: the eigenvalues of rows ilo..hi were not found
       break;
     }
-    int ns = (int)std::min<int64_t>(nshifts, (N - 2) & ~(int64_t)1);
-    if (ns < 2) ns = 2;
-    cudaError_t e = hqr::launch_small_eig(H, n, hi - ns + 1, ns, d_w, d_w + hqr::small_eig_max(), d_info, g.stream);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(ewr.data(), d_w, ns * sizeof(double), cudaMemcpyDeviceToHost, g.stream);
-    if (e == cudaSuccess)
-      e = cudaMemcpyAsync(ewi.data(), d_w + hqr::small_eig_max(), ns * sizeof(double), cudaMemcpyDeviceToHost, g.stream);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(g.stream);
-    if (e != cudaSuccess) return fail(cuerr(e));
-    const int k = make_shifts_host(ewr.data(), ewi.data(), ns, ns, sr.data(), si.data());
-    if (k < 2) {
-      rc = (int)(hi + 1);
-      break;
+    int k = 0;  // shifts found
+    if (aed_window > 0) {
+      // AED on the trailing window (R22): Schur form, spike, deflation, Hessenberg re-reduction,
+      // then the window's factor U propagated by the DMMA update kernels
+      const int nwin = (int)std::min<int64_t>(aed_window, N);
+      const int64_t k0 = hi - nwin + 1;
+      int res[2] = {0, 0};
+      cudaError_t e = hqr::launch_aed(H, n, l, k0, nwin, thr, d_uslot, KPa, QLDa, d_ew, d_ei, d_info + 2, g.stream);
+      if (e == cudaSuccess) e = cudaMemcpyAsync(res, d_info + 2, 2 * sizeof(int), cudaMemcpyDeviceToHost, g.stream);
+      if (e == cudaSuccess) e = cudaMemcpyAsync(ewr.data(), d_ew, nwin * sizeof(double), cudaMemcpyDeviceToHost, g.stream);
+      if (e == cudaSuccess) e = cudaMemcpyAsync(ewi.data(), d_ei, nwin * sizeof(double), cudaMemcpyDeviceToHost, g.stream);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(g.stream);
+      if (e != cudaSuccess) return fail(cuerr(e));
+      ++naed;
+      const int nd = res[0], m = res[1];
+      if (nd < 0) {  // the window's Schur iteration did not converge: plain shifts below
+        k = 0;
+      } else {
+        if (nd > 0) {
+          WindowDesc wd{};
+          wd.w0 = (int32_t)k0; wd.w1 = (int32_t)(k0 + nwin - 1); wd.slot = 0; wd.nbc = 0;
+          wd.ilo = (int32_t)l; wd.ihi = (int32_t)hi; wd.scan_lo = 0; wd.scan_hi = -1;
+          CK(cudaMemcpyAsync(d_wd, &wd, sizeof(wd), cudaMemcpyHostToDevice, g.stream));
+          StepArgs a{};
+          a.H = H; a.Z = Z; a.n = n; a.ilo = l; a.ihi = hi; a.hcol0 = 0; a.lc0 = 0; a.lc1 = n; a.zrows = n; a.ldz = n;
+          a.wins = d_wd; a.win_begin = 0; a.win_count = 1; a.qslots = d_uslot; a.KP = KPa; a.QLD = QLDa;
+          a.slot_offset = 0; a.right_mode = 0;
+          int64_t items;
+          double fl, by;
+          e = hqr::launch_left(a, &wd, g.num_sms, tma, g.stream, &items, &fl, &by);
+          if (e == cudaSuccess) e = hqr::launch_right(a, &wd, g.num_sms, tma, g.stream, &items, &fl, &by);
+          if (e != cudaSuccess) return fail(cuerr(e));
+          for (int j = m; j < nwin; ++j) {
+            wr[k0 + j] = ewr[j];
+            wi[k0 + j] = ewi[j];
+          }
+          ndefl += nd;
+          hi -= nd;
+          if (100 * nd > 14 * nwin) continue;  // many deflations: another AED before a sweep
+          if (hi - l + 1 <= nmin) continue;
+        }
+        // the bottom-most undeflated candidates (the failed ones) as shifts
+        const int want = std::min(nshifts, m);
+        k = make_shifts_host(ewr.data() + (m - want), ewi.data() + (m - want), want, want, sr.data(), si.data());
+        if (k > hi - l + 1) k = (int)((hi - l + 1) & ~(int64_t)1);
+      }
+    }
+    if (k < 2) {  // shifts: the eigenvalues of the trailing nshifts x nshifts block
+      const int64_t Nb = hi - l + 1;
+      int ns = (int)std::min<int64_t>(nshifts, (Nb - 2) & ~(int64_t)1);
+      if (ns < 2) ns = 2;
+      cudaError_t e = hqr::launch_small_eig(H, n, hi - ns + 1, ns, d_w, d_w + SM, d_info, g.stream);
+      if (e == cudaSuccess) e = cudaMemcpyAsync(ewr.data(), d_w, ns * sizeof(double), cudaMemcpyDeviceToHost, g.stream);
+      if (e == cudaSuccess)
+        e = cudaMemcpyAsync(ewi.data(), d_w + SM, ns * sizeof(double), cudaMemcpyDeviceToHost, g.stream);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(g.stream);
+      if (e != cudaSuccess) return fail(cuerr(e));
+      k = make_shifts_host(ewr.data(), ewi.data(), ns, ns, sr.data(), si.data());
+      if (k < 2) {
+        rc = (int)(hi + 1);
+        break;
+      }
     }
     const int src = sweep_impl(H, Z, n, make_blocks(1, &l, &hi, &k), sr.data(), si.data(), window);
     if (src) return fail(src);
     falg += g.stats.flops_alg;
     ++sweeps;
     CK(cudaMemsetAsync(d_info + 1, 0, sizeof(int), g.stream));
-    e = hqr::launch_deflate(H, n, l, hi, d_info + 1, g.stream);
+    cudaError_t e = hqr::launch_deflate(H, n, l, hi, d_info + 1, g.stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(g.stream);
     if (e != cudaSuccess) return fail(cuerr(e));
   }
@@ -1969,6 +2043,8 @@ int hqr_qr_iterate(double* H, double* Z, int64_t n, int64_t ilo, int64_t ihi, in
   g.stats.ms_total = ms;  // the whole iteration (device time of the library stream)
   g.stats.flops_alg = falg;
   g.stats.steps = sweeps;
+  g.stats.launches_chase = naed;    // (re-used: AED steps)
+  g.stats.window_eff = ndefl;       // (re-used: eigenvalues deflated by AED)
   if (sweeps_out) *sweeps_out = sweeps;
   return rc;
 }

@@ -76,6 +76,12 @@ int small_eig_max();
 cudaError_t launch_small_eig(const double* H, int64_t n, int64_t r0, int m, double* wr, double* wi, int* info,
                              cudaStream_t st);
 cudaError_t launch_deflate(double* H, int64_t n, int64_t lo, int64_t hi, int* count, cudaStream_t st);
+// out[0] <- sum of squares of H[0 .. count)
+cudaError_t launch_fro2(const double* H, int64_t count, double* out, int num_sms, cudaStream_t st);
+// AED on the window [k0, k0+nw) (nw <= kMaxWindow) of the block starting at ilo (qriter.cu); U to
+// uslot (KP x QLD Q slot), eigenvalues of the window to ew / ei, res = {nd, m}.
+cudaError_t launch_aed(double* H, int64_t n, int64_t ilo, int64_t k0, int nw, double thr, double* uslot, int KP,
+                       int QLD, double* ew, double* ei, int* res, cudaStream_t st);
 
 // 2-D TMA descriptors of H and Z (column-major, n x n) with the update kernels' SMEM boxes.
 // Valid only for even n (TMA global strides must be multiples of 16 bytes).

@@ -66,3 +66,30 @@ def test_qr_iteration_vs_oracle(n, ns, nmin, win, seed):
     assert max(b - a for a, b in zip(zeros, zeros[1:])) <= nmin
     # the sweep counts are of the same order (the trajectories differ by rounding)
     assert 0.5 * osw <= sweeps <= 2.0 * osw
+
+
+@pytest.mark.parametrize("n,ns,aed,nmin,win,seed", [(300, 16, 48, 32, 48, 0), (800, 32, 96, 64, 96, 1),
+                                                    (2000, 64, 96, 96, 96, 2)])
+def test_qr_iteration_with_aed_vs_oracle(n, ns, aed, nmin, win, seed):
+    """NEXT-2 with AED (reading R22) on hess_n matrices: the eigenvalue sets of the GPU
+    iteration and the oracle's agree; Z H Z^T = Z0 H0 Z0^T; most eigenvalues deflate in AED and the
+    iteration needs fewer sweeps than without AED."""
+    from hqr_inputs import make_hess
+    p = make_hess(n, 2, z0="orth")
+    Hd, Zd = hq.to_device(p.H), hq.to_device(p.Z)
+    wr, wi, rc, sweeps = hq.qr_iterate(Hd, Zd, 0, n - 1, nshifts=ns, window=win, nmin=nmin, aed_window=aed)
+    st = hq.stats()
+    assert rc == 0
+    H, Z = hq.from_device(Hd), hq.from_device(Zd)
+    Ho, Zo = p.H.copy(order="F"), p.Z.copy(order="F")
+    owr, owi, orc, osw, onaed, ondefl = oracle.qr_iterate_aed(Ho, Zo, 0, n - 1, ns, nw=aed, nmin=nmin)
+    assert orc == 0
+    assert _match(wr + 1j * wi, owr + 1j * owi) <= 1e-8
+    hn = np.linalg.norm(p.H)
+    assert np.linalg.norm(Z.T @ Z - np.eye(n)) <= 1e-13 * n
+    assert np.linalg.norm(Z @ H @ Z.T - p.Z @ p.H @ p.Z.T) <= 1e-13 * n * hn
+    assert np.all(np.tril(H, -2) == 0.0)
+    assert st["window_eff"] > n // 2                      # eigenvalues deflated by AED
+    Hd2 = hq.to_device(p.H)
+    _, _, _, sweeps_plain = hq.qr_iterate(Hd2, None, 0, n - 1, nshifts=ns, window=win, nmin=nmin)
+    assert sweeps < sweeps_plain

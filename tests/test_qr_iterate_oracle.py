@@ -85,3 +85,78 @@ def test_qr_iterate_eigenvalues_similarity(n, ns, nmin, seed):
     # H is reduced to unreduced blocks of at most nmin rows
     zeros = [0] + [k for k in range(1, n) if H[k, k - 1] == 0.0] + [n]
     assert max(b - a for a, b in zip(zeros, zeros[1:])) <= nmin
+
+
+# --------------------------------------------------------------------------------------------
+# AED (reading R22)
+# --------------------------------------------------------------------------------------------
+
+@pytest.mark.parametrize("seed,n", [(10, 6), (11, 8), (12, 40)])
+def test_schur_form(seed, n):
+    A, _, _, _ = random_case(seed, n, 2)
+    T, U, wr, wi, info = oracle.schur(A)
+    assert info == 0
+    assert np.linalg.norm(U.T @ U - np.eye(n)) <= 1e-13 * n
+    assert np.linalg.norm(U.T @ A @ U - T) <= 1e-13 * n * np.linalg.norm(A)
+    sub = np.diag(T, -1)
+    assert np.all(np.tril(T, -2) == 0.0) and not np.any((sub[:-1] != 0) & (sub[1:] != 0))  # quasi-triangular
+    if n <= 8:
+        assert _match(wr + 1j * wi, _charpoly_roots(A)) <= 1e-12
+
+
+def test_aed_deflates_below_a_tiny_spike():
+    """A window whose coupling entry s is tiny: every spike entry s U(0, j) is below u ||H||_F, so
+    the whole window deflates, its eigenvalues are those of the window, H stays similar."""
+    from hqr_inputs import make_hess
+    p = make_hess(60, 2)
+    H0 = p.H.copy(order="F")
+    k0, nw = 40, 20
+    H0[k0, k0 - 1] = 1e-30
+    W = H0[k0:, k0:].copy()
+    H, Z = H0.copy(order="F"), np.asfortranarray(np.eye(60))
+    thr = 2.0 ** -53 * np.linalg.norm(H0)
+    nd, wr, wi, cand = oracle.aed(H, Z, 0, k0, nw, thr)
+    assert nd == nw and len(cand) == 0
+    assert _match(wr[k0:] + 1j * wi[k0:], np.linalg.eigvals(W)) <= 1e-10
+    assert np.linalg.norm(Z @ H @ Z.T - H0) <= 1e-13 * 60 * np.linalg.norm(H0)
+    assert np.all(H[k0:, k0 - 1] == 0.0) and np.all(np.tril(H, -2)[:, :k0] == 0.0)
+
+
+@pytest.mark.parametrize("n,k0,nw,seed", [(80, 40, 40, 13), (120, 60, 60, 14)])
+def test_aed_structure_and_similarity(n, k0, nw, seed):
+    """After AED H is again upper Hessenberg, similar to H0 through Z, and the rows below
+    n - nd are decoupled with the deflated eigenvalues their eigenvalues."""
+    from hqr_inputs import make_hess
+    p = make_hess(n, 2, z0="orth")
+    H, Z = p.H.copy(order="F"), p.Z.copy(order="F")
+    # a converged-looking tail: shrink the subdiagonal entries inside the window's bottom part
+    for r in range(n - 6, n):
+        H[r, r - 1] *= 1e-9
+    H0, Z0 = H.copy(order="F"), Z.copy(order="F")
+    thr = 2.0 ** -53 * np.linalg.norm(H0)
+    nd, wr, wi, cand = oracle.aed(H, Z, 0, k0, nw, thr)
+    assert np.linalg.norm(Z @ H @ Z.T - Z0 @ H0 @ Z0.T) <= 1e-13 * n * np.linalg.norm(H0)
+    assert np.linalg.norm(Z.T @ Z - np.eye(n)) <= 1e-13 * n
+    assert np.all(np.tril(H, -2) == 0.0)
+    if nd > 0:
+        assert H[n - nd, n - nd - 1] == 0.0
+        tail = np.linalg.eigvals(H[n - nd:, n - nd:])
+        assert _match(wr[n - nd:] + 1j * wi[n - nd:], tail) <= 1e-8
+
+
+@pytest.mark.parametrize("n,ns,nw,nmin,seed", [(10, 2, 6, 2, 15), (300, 16, 48, 32, 16)])
+def test_qr_iterate_aed(n, ns, nw, nmin, seed):
+    from hqr_inputs import make_hess
+    p = make_hess(n, 2, z0="orth")
+    H, Z = p.H.copy(order="F"), p.Z.copy(order="F")
+    wr, wi, rc, sweeps, naed, ndefl = oracle.qr_iterate_aed(H, Z, 0, n - 1, ns, nw=nw, nmin=nmin)
+    assert rc == 0
+    if n <= 10:
+        assert _match(wr + 1j * wi, _charpoly_roots(p.H)) <= 1e-10
+    hn = np.linalg.norm(p.H)
+    assert np.linalg.norm(Z @ H @ Z.T - p.Z @ p.H @ p.Z.T) <= 1e-13 * n * hn
+    assert abs(np.sum(wr) - np.trace(p.H)) <= 1e-10 * n * hn
+    if n >= 100:  # AED pays: fewer sweeps than the iteration without it, most eigenvalues by AED
+        H2 = p.H.copy(order="F")
+        _, _, _, sweeps_plain = oracle.qr_iterate(H2, None, 0, n - 1, ns, nmin=nmin)
+        assert sweeps < sweeps_plain and ndefl > n // 2
