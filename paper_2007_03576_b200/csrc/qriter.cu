@@ -1,8 +1,11 @@
-// qriter.cu -- pieces of the QR iteration around the sweep (partial; reading
-// R21): the eigenvalues of a small Hessenberg block (the shifts of the next sweep, and the
-// eigenvalues of the small blocks left at the end -- the role of the paper's small Schur task,
-// P:367-372, here a Francis double-shift QR iteration in one CTA), and the deflation step that sets
-// negligible subdiagonal entries to zero after a sweep (criterion R16).
+// qriter.cu -- the QR iteration around the sweep (readings R21, R22):
+// aggressive early deflation on the trailing window of a block (Schur form of the window
+// with its factor U, spike, the norm-stable deflation condition of P:1142-1189, Hessenberg
+// re-reduction -- one CTA; U then goes through the DMMA update kernels), the eigenvalues of a small
+// Hessenberg block (shifts when AED has none, and the small blocks left at the end -- the role of the
+// paper's small Schur task: a Francis double-shift QR iteration in one CTA), the deflation
+// step that sets negligible subdiagonal entries to zero after a sweep (criterion R16), and
+// ||H||_F for the deflation threshold.
 #include <cuda_runtime.h>
 
 #include <algorithm>
