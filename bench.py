@@ -316,7 +316,9 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", type=int, default=3)
-    ap.add_argument("--window", type=int, default=96)
+    ap.add_argument("--window", type=int, default=None,
+                    help="window side (default: the config's window when BASELINE.json gives one -- configs[0] 24, "
+                         "configs[1] 151 -- else 96); the library's effective side is min(window, N, 112)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-bulges", type=int, default=32, help="oracle sample size (shift pairs)")
     ap.add_argument("--ref-bulges", type=int, default=16)
@@ -342,10 +344,13 @@ def main():
     import paper_2007_03576_b200 as hq
     from hqr_inputs import make
 
+    window_requested = args.window
     if args.workload == "qz":
+        args.window = args.window or 80
         run_qz(args)
         return
     if args.workload == "qriter":
+        args.window = args.window or 96
         run_qriter(args)
         return
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -368,6 +373,8 @@ def main():
     n = prob.H.shape[0]
     gen_s = time.time() - t0
     nshifts = len(prob.shifts_re)
+    if args.window is None:  # the config's window (configs[1]: 3 nshifts/2 + 1 = 151), else the default 96
+        args.window = prob.window if prob.window else 96
     shift_sets = None
     if args.sweeps > 1:  # NEXT-1: further shift sets from the same distribution (stream offsets)
         from hqr_inputs import CONFIGS, shifts as draw_shifts
@@ -569,7 +576,7 @@ def main():
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, BASELINE.json configs)",
             "config": {"workload": workload, "n": n, "nshifts": nshifts,
                        "sweeps_per_step": args.sweeps,
-                       "window": st["window_eff"],
+                       "window": st["window_eff"], "window_requested": window_requested or args.window,
                        "z": "random orthogonal" if (args.config in (1, 3) or args.workload == "hess") else "identity",
                        "parallelism": (f"{world} GPUs: H block-column (sqrt-balanced), Z block-row, "
                                        "per-window Q ncclBroadcast, lent slabs") if world > 1 else "1 GPU",
