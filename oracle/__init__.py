@@ -21,7 +21,10 @@ Functions and the passages they follow (PAPER.md line numbers, see hqr_oracle.c)
   qr_iterate(H, Z, ..)     -- repeated sweeps with shifts from the trailing block and deflation
                               (NEXT-2 without AED; reading R21)
   schur(A) / aed(H, ..)    -- real Schur form with U; aggressive early deflation on a window
-                              (reading R22)
+                              (reading R22) with the failed blocks
+                              reordered to the top (reading R23)
+  swap(T, U, i, p, q)      -- swap of two adjacent diagonal blocks of a quasi-triangular T
+                              (the reordering kernel; reading R23)
   qr_iterate_aed(H, Z, ..) -- the QR iteration with AED (NEXT-2, R22)
 
 Parity pins for every function are in tests/test_oracle.py (none is "parity unpinned").
@@ -90,6 +93,9 @@ def _load():
         lib.oracle_schur.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p, ctypes.c_int64,
                                      dp, dp]
         lib.oracle_schur.restype = ctypes.c_int
+        lib.oracle_swap.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p,
+                                    ctypes.c_int64, ctypes.c_int64, ctypes.c_int, ctypes.c_int]
+        lib.oracle_swap.restype = ctypes.c_int
         lib.oracle_aed.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
                                    ctypes.c_int, ctypes.c_double, dp, dp, dp, dp, ip]
         lib.oracle_aed.restype = ctypes.c_int
@@ -233,6 +239,15 @@ def schur(A):
     wr, wi = np.zeros(m), np.zeros(m)
     info = _load().oracle_schur(T.ctypes.data, m, m, U.ctypes.data, m, _dptr(wr), _dptr(wi))
     return T, U, wr, wi, info
+
+
+def swap(T, U, i, p, q):
+    """In place: swap the diagonal blocks T(i:i+p) and T(i+p:i+p+q) (p, q in {1, 2}), U <- U Q.
+    Returns 0, or 1 when the swap was rejected (T, U unchanged)."""
+    T = _as_colmajor(T)
+    U = _as_colmajor(U)
+    nw = T.shape[0]
+    return _load().oracle_swap(T.ctypes.data, nw, nw, U.ctypes.data, nw, i, p, q)
 
 
 def aed(H, Z, ilo, k0, nw, thr):

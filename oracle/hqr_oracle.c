@@ -494,8 +494,10 @@ int oracle_qr_iterate(double* H, double* Z, int64_t n, int64_t ilo, int64_t ihi,
  *       all window columns / rows updated, U accumulated);
  *   (2) the spike v = s U(0, :) (s = the subdiagonal entry left of the window); from the bottom,
  *       a 1x1 / 2x2 block of T is deflated when its spike entries are <= u ||H||_F (the paper's
- *       default "norm-stable" condition) -- without the paper's reordering of failed blocks: the
- *       first failure ends the check (R22);
+ *       default "norm-stable" condition); a block that fails is moved above the remaining
+ *       unevaluated blocks by swaps of adjacent diagonal blocks (oracle_swap, R23), which
+ *       pushes those down; a rejected swap halts the reordering and the blocks not yet
+ *       evaluated stay undeflated;
  *   (3) if anything deflated: zero the deflated spike entries, reflect the remaining spike v(0:m)
  *       onto e1 (P = I - tau w w^T, applied to T(0:m,0:m) from both sides and to U(:, 0:m)) and
  *       restore Hessenberg form of T(0:m, 0:m) by Householder reflectors (general length, R2
@@ -541,6 +543,111 @@ static void refl_right(double* A, int64_t lda, int64_t r0, int64_t r1, int64_t c
     for (int i = 0; i < m; ++i) s += A[r + (c0 + i) * lda] * w[i];
     for (int i = 0; i < m; ++i) A[r + (c0 + i) * lda] -= tau * s * w[i];
   }
+}
+
+/* Swap of the adjacent diagonal blocks A = T(i:i+p, i:i+p) and B = T(i+p:i+p+q, i+p:i+p+q) of the
+ * quasi-triangular T (nw x nw, ld ldt; p, q in {1, 2}) by an orthogonal similarity accumulated into U
+ * (nw x nw, ld ldu) -- the eigenvalue reordering of P:289-290 (LAPACK's DTREXC), reading R23:
+ *   X solves the Sylvester equation A X - X B = C, C = T(i:i+p, i+p:i+p+q), so that
+ *   T [-X; I_q] = [-X; I_q] B: the columns of [-X; I_q] span B's invariant subspace;
+ *   Q = P1 (P2) = the Householder (R2) QR factor of [-X; I_q]; T <- Q^T T Q puts B's eigenvalues in
+ *   the leading q x q block; U <- U Q; the new lower-left p x q block is set to exact zeros.
+ * The Sylvester equation is solved as its pq x pq Kronecker system (I_q (x) A - B^T (x) I_p) vec X =
+ * vec C by Gaussian elimination with complete pivoting, a pivot below 2^-52 max|K| replaced by that
+ * value (A and B sharing an eigenvalue).  The swap is rejected -- returns 1, T and U unchanged -- when
+ * the lower-left block of Q^T D Q (D = the (p+q)^2 diagonal block) exceeds 10 * 2^-52 * max|D| (too
+ * ill-conditioned).  Returns 0 on success. */
+int oracle_swap(double* T, int64_t ldt, int64_t nw, double* U, int64_t ldu, int64_t i, int p, int q) {
+  const int k = p + q;
+  double D[16], K[16], x[4], w1[4], w2[4];
+  double dnorm = 0.0;
+  for (int c = 0; c < k; ++c)
+    for (int r = 0; r < k; ++r) {
+      D[r + 4 * c] = T[(i + r) + (i + c) * ldt];
+      if (fabs(D[r + 4 * c]) > dnorm) dnorm = fabs(D[r + 4 * c]);
+    }
+  /* Kronecker system, unknown X(r, c) at index r + c p, equation (r, c) at row r + c p */
+  const int nk = p * q;
+  double kmax = 0.0;
+  for (int e = 0; e < nk * nk; ++e) K[e] = 0.0;
+  for (int c = 0; c < q; ++c)
+    for (int r = 0; r < p; ++r) {
+      const int row = r + c * p;
+      for (int t = 0; t < p; ++t) K[row + nk * (t + c * p)] += D[r + 4 * t];            /* A(r,t) X(t,c) */
+      for (int t = 0; t < q; ++t) K[row + nk * (r + t * p)] -= D[(p + t) + 4 * (p + c)]; /* X(r,t) B(t,c) */
+      x[row] = D[r + 4 * (p + c)];                                                       /* C(r,c) */
+    }
+  for (int e = 0; e < nk * nk; ++e)
+    if (fabs(K[e]) > kmax) kmax = fabs(K[e]);
+  const double smin = (kmax > 0.0 ? kmax : 1.0) * 0x1p-52;
+  int perm[4] = {0, 1, 2, 3}; /* column permutation (complete pivoting) */
+  for (int j = 0; j < nk; ++j) {
+    int pr = j, pc = j;
+    for (int c = j; c < nk; ++c)
+      for (int r = j; r < nk; ++r)
+        if (fabs(K[r + nk * c]) > fabs(K[pr + nk * pc])) { pr = r; pc = c; }
+    for (int c = 0; c < nk; ++c) { /* row swap */
+      const double t = K[j + nk * c]; K[j + nk * c] = K[pr + nk * c]; K[pr + nk * c] = t;
+    }
+    { const double t = x[j]; x[j] = x[pr]; x[pr] = t; }
+    for (int r = 0; r < nk; ++r) { /* column swap */
+      const double t = K[r + nk * j]; K[r + nk * j] = K[r + nk * pc]; K[r + nk * pc] = t;
+    }
+    { const int t = perm[j]; perm[j] = perm[pc]; perm[pc] = t; }
+    if (fabs(K[j + nk * j]) < smin) K[j + nk * j] = smin;
+    for (int r = j + 1; r < nk; ++r) {
+      const double f = K[r + nk * j] / K[j + nk * j];
+      for (int c = j; c < nk; ++c) K[r + nk * c] -= f * K[j + nk * c];
+      x[r] -= f * x[j];
+    }
+  }
+  double y[4];
+  for (int j = nk - 1; j >= 0; --j) {
+    double a = x[j];
+    for (int c = j + 1; c < nk; ++c) a -= K[j + nk * c] * y[c];
+    y[j] = a / K[j + nk * j];
+  }
+  double X[4];
+  for (int j = 0; j < nk; ++j) X[perm[j]] = y[j];
+  /* Householder QR of M = [-X; I_q] (k x q) */
+  double M[8];
+  for (int c = 0; c < q; ++c)
+    for (int r = 0; r < k; ++r) M[r + 4 * c] = (r < p) ? -X[r + c * p] : ((r - p == c) ? 1.0 : 0.0);
+  double tau1, tau2 = 0.0, beta;
+  for (int r = 0; r < k; ++r) w1[r] = M[r];
+  house_n(k, w1, &tau1, &beta);
+  if (q == 2) {
+    double s = 0.0;
+    for (int r = 0; r < k; ++r) s += w1[r] * M[r + 4];
+    for (int r = 0; r < k; ++r) M[r + 4] -= tau1 * w1[r] * s;
+    for (int r = 0; r < k - 1; ++r) w2[r] = M[1 + r + 4];
+    house_n(k - 1, w2, &tau2, &beta);
+  }
+  /* the check on D: D' = Q^T D Q */
+  refl_left(D, 4, 0, k, 0, k, w1, tau1);
+  refl_right(D, 4, 0, k, 0, k, w1, tau1);
+  if (q == 2) {
+    refl_left(D, 4, 1, k - 1, 0, k, w2, tau2);
+    refl_right(D, 4, 0, k, 1, k - 1, w2, tau2);
+  }
+  double low = 0.0;
+  for (int c = 0; c < q; ++c)
+    for (int r = q; r < k; ++r)
+      if (fabs(D[r + 4 * c]) > low) low = fabs(D[r + 4 * c]);
+  if (!(low <= 10.0 * 0x1p-52 * dnorm)) return 1;
+  /* accepted: T <- Q^T T Q (rows i..i+k-1 from column i on; columns i..i+k-1 for rows 0..i+k-1),
+   * U <- U Q, exact zeros below the new leading q x q block */
+  refl_left(T, ldt, i, k, i, nw, w1, tau1);
+  refl_right(T, ldt, 0, i + k, i, k, w1, tau1);
+  refl_right(U, ldu, 0, nw, i, k, w1, tau1);
+  if (q == 2) {
+    refl_left(T, ldt, i + 1, k - 1, i, nw, w2, tau2);
+    refl_right(T, ldt, 0, i + k, i + 1, k - 1, w2, tau2);
+    refl_right(U, ldu, 0, nw, i + 1, k - 1, w2, tau2);
+  }
+  for (int c = 0; c < q; ++c)
+    for (int r = q; r < k; ++r) T[(i + r) + (i + c) * ldt] = 0.0;
+  return 0;
 }
 
 /* Real Schur form of the m x m Hessenberg matrix A (ld lda) with U (m x m, ld ldu) accumulated:
@@ -632,19 +739,45 @@ int oracle_aed(double* H, double* Z, int64_t n, int64_t ilo, int64_t k0, int nw,
   oracle_schur(T, nw, nw, U, nw, ew, ei);
   const double s = (k0 > ilo) ? EL(H, k0, k0 - 1, n) : 0.0;
   for (int j = 0; j < nw; ++j) v[j] = s * U[0 + j * nw];
-  /* deflation from the bottom (norm-stable condition, no reordering: R22) */
-  int m = nw;
-  while (m > 0) {
-    const int bs = (m >= 2 && T[(m - 1) + (m - 2) * nw] != 0.0) ? 2 : 1;
+  /* deflation from the bottom (norm-stable condition, R22) with the failed blocks reordered to the
+   * top (R23): [0, ntop) the failed blocks, [ntop, m) not yet evaluated, [m, nw) deflated */
+  int m = nw, ntop = 0;
+  while (m > ntop) {
+    const int bs = (m - 2 >= ntop && T[(m - 1) + (m - 2) * nw] != 0.0) ? 2 : 1;
     int ok = 1;
-    for (int j = m - bs; j < m; ++j) ok &= fabs(v[j]) <= thr;
-    if (!ok) break;
-    for (int j = m - bs; j < m; ++j) {
-      wr[k0 + j] = ew[j];
-      wi[k0 + j] = ei[j];
-      v[j] = 0.0;
+    for (int j = m - bs; j < m; ++j) ok &= fabs(s * U[0 + j * nw]) <= thr;
+    if (ok) {
+      m -= bs;
+      continue;
     }
-    m -= bs;
+    int cur = m - bs, moved = 1;
+    while (cur > ntop) { /* move the failed block up past each block above it */
+      const int p = (cur - 2 >= ntop && T[(cur - 1) + (cur - 2) * nw] != 0.0) ? 2 : 1;
+      if (oracle_swap(T, nw, nw, U, nw, cur - p, p, bs) != 0) {
+        moved = 0;
+        break;
+      }
+      cur -= p;
+    }
+    if (!moved) break; /* a rejected swap halts the reordering */
+    ntop += bs;
+  }
+  /* the eigenvalues of the final blocks (the reordered T), the spike of the undeflated part */
+  for (int j = 0; j < nw;) {
+    if (j + 1 < nw && T[(j + 1) + j * nw] != 0.0) {
+      eig2(T[j + j * nw], T[j + (j + 1) * nw], T[(j + 1) + j * nw], T[(j + 1) + (j + 1) * nw], &ew[j], &ei[j],
+           &ew[j + 1], &ei[j + 1]);
+      j += 2;
+    } else {
+      ew[j] = T[j + j * nw];
+      ei[j] = 0.0;
+      j += 1;
+    }
+  }
+  for (int j = 0; j < nw; ++j) v[j] = (j < m) ? s * U[0 + j * nw] : 0.0;
+  for (int j = m; j < nw; ++j) {
+    wr[k0 + j] = ew[j];
+    wi[k0 + j] = ei[j];
   }
   const int nd = nw - m;
   *nund = m;

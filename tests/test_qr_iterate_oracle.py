@@ -160,3 +160,108 @@ def test_qr_iterate_aed(n, ns, nw, nmin, seed):
         H2 = p.H.copy(order="F")
         _, _, _, sweeps_plain = oracle.qr_iterate(H2, None, 0, n - 1, ns, nmin=nmin)
         assert sweeps < sweeps_plain and ndefl > n // 2
+
+
+# --------------------------------------------------------------------------------------------
+# Eigenvalue reordering inside AED (reading R23)
+# --------------------------------------------------------------------------------------------
+
+def _quasi(rng, nw, blocks):
+    """Quasi-triangular nw x nw T with the given diagonal block sizes (2x2 blocks complex)."""
+    T = np.triu(rng.standard_normal((nw, nw)))
+    j = 0
+    for b in blocks:
+        if b == 2:
+            a = rng.standard_normal()
+            T[j, j], T[j + 1, j + 1] = a, a
+            T[j, j + 1] = abs(rng.standard_normal()) + 0.5
+            T[j + 1, j] = -(abs(rng.standard_normal()) + 0.5)
+        j += b
+    return T
+
+
+@pytest.mark.parametrize("p,q", [(1, 1), (2, 1), (1, 2), (2, 2)])
+def test_swap_blocks(p, q):
+    """The swap moves B's eigenvalues into the leading q x q block and A's into the next p x p block
+    (eigenvalues from np.linalg.eigvals of the blocks), by an orthogonal similarity (U^T T0 U = T),
+    leaving exact zeros below them and touching nothing outside rows / columns i..i+p+q-1 beyond U."""
+    rng = np.random.default_rng(100 + 10 * p + q)
+    i = 2
+    layout = [1, 1, p, q, 1, 2]
+    nw = sum(layout)
+    T0 = np.asfortranarray(_quasi(rng, nw, layout))
+    T, U = T0.copy(order="F"), np.asfortranarray(np.eye(nw))
+    assert oracle.swap(T, U, i, p, q) == 0
+    k = p + q
+    assert np.linalg.norm(U.T @ U - np.eye(nw)) <= 1e-14 * nw
+    assert np.linalg.norm(U @ T @ U.T - T0) <= 1e-14 * nw * np.linalg.norm(T0)
+    ev = lambda M: np.sort_complex(np.linalg.eigvals(M))  # noqa: E731
+    assert np.abs(ev(T[i:i + q, i:i + q]) - ev(T0[i + p:i + k, i + p:i + k])).max() <= 1e-13
+    assert np.abs(ev(T[i + q:i + k, i + q:i + k]) - ev(T0[i:i + p, i:i + p])).max() <= 1e-13
+    assert np.all(T[i + q:i + k, i:i + q] == 0.0)
+    assert np.all(np.tril(T, -2) == 0.0)
+    # outside the swapped rows / columns T is unchanged; U differs from I only in those columns
+    rest = [r for r in range(nw) if not i <= r < i + k]
+    assert np.array_equal(T[np.ix_(rest, rest)], T0[np.ix_(rest, rest)])
+    assert np.array_equal(U[:, rest], np.eye(nw)[:, rest])
+
+
+def test_swap_two_1x1_closed_form():
+    """Two 1x1 blocks [[a, c], [0, b]]: the swap gives [[b, +-c], [0, a]] (a rotation keeps the
+    Frobenius norm and the trace / determinant, so the off-diagonal entry keeps its modulus)."""
+    for a, b, c in [(1.0, 2.0, 3.0), (-0.5, 4.0, 1e-3), (2.0, -2.0, 7.0)]:
+        T = np.asfortranarray([[a, c], [0.0, b]])
+        U = np.asfortranarray(np.eye(2))
+        assert oracle.swap(T, U, 0, 1, 1) == 0
+        assert abs(T[0, 0] - b) <= 1e-15 * 8 and abs(T[1, 1] - a) <= 1e-15 * 8 and T[1, 0] == 0.0
+        assert abs(abs(T[0, 1]) - abs(c)) <= 1e-14 * 8
+        # the first column of U is the eigenvector of b: (c, b - a) normalised
+        x = np.array([c, b - a]) / np.hypot(c, b - a)
+        assert abs(abs(U[:, 0] @ x) - 1.0) <= 1e-14
+
+
+def test_swap_rejected_leaves_state_unchanged():
+    """Badly scaled blocks (entries 1e-8 .. 1e8): a rejected swap returns 1 and leaves
+    T and U bit-identical; an accepted one is an orthogonal similarity to working accuracy."""
+    rng = np.random.default_rng(2)
+    rejected = 0
+    for _ in range(400):
+        p, q = int(rng.integers(1, 3)), int(rng.integers(1, 3))
+        k = p + q
+        T0 = np.triu(rng.standard_normal((k, k)) * 10.0 ** rng.uniform(-8, 8, (k, k)))
+        T0 = np.asfortranarray(T0)
+        T, U = T0.copy(order="F"), np.asfortranarray(np.eye(k))
+        rc = oracle.swap(T, U, 0, p, q)
+        if rc:
+            rejected += 1
+            assert np.array_equal(T, T0) and np.array_equal(U, np.eye(k))
+        else:
+            assert np.linalg.norm(U @ T @ U.T - T0) <= 1e-13 * np.abs(T0).max()
+    assert rejected >= 1
+
+
+def test_aed_reordering_matches_the_predicted_deflations():
+    """Windows whose bottom block fails the deflation check while blocks above it pass (no
+    reordering would deflate nothing): the oracle's AED deflates exactly the eigenvalues predicted
+    from the invariant subspaces of W (tests/aed_predict.py, LAPACK's ordered Schur form), H stays
+    similar and Hessenberg."""
+    from aed_predict import reorder_cases
+    cases = list(reorder_cases(oracle.schur))
+    assert len(cases) == 3
+    above = 6
+    rng = np.random.default_rng(3)
+    for W, s, thr, defl, dec in cases:
+        nw = W.shape[0]
+        n = above + nw
+        H0 = np.asfortranarray(np.triu(rng.standard_normal((n, n)), -1))
+        H0[above:, above:] = W
+        H0[above, above - 1] = s
+        H, Z = H0.copy(order="F"), np.asfortranarray(np.eye(n))
+        nd, wr, wi, cand = oracle.aed(H, Z, 0, above, nw, thr)
+        assert nd == len(defl) and nd > 0 and not dec[0]
+        got = wr[n - nd:] + 1j * wi[n - nd:]
+        assert _match(got, defl) <= 1e-10 and _match(defl, got) <= 1e-10
+        assert _match(cand, [l for l in np.linalg.eigvals(W) if min(abs(l - np.array(defl))) > 1e-8]) <= 1e-10
+        # similar up to the zeroed spike entries (each <= thr: the deflation's backward error)
+        assert np.linalg.norm(Z @ H @ Z.T - H0) <= np.sqrt(nd) * thr + 1e-13 * n * np.linalg.norm(H0)
+        assert np.all(np.tril(H, -2) == 0.0) and H[n - nd, n - nd - 1] == 0.0
