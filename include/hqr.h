@@ -152,10 +152,11 @@ int hqr_qz_sweep(double* H, double* T, double* Q, double* Z, int64_t n, int64_t 
  *   (a) if it has at most nmin rows, compute its eigenvalues with the one-CTA Francis double-shift QR
  *       solver and continue above it;
  *   (b) aed_window > 0: aggressive early deflation on its trailing min(aed_window, N) window -- real
- *       Schur form of the window (U accumulated), spike s U(0,:), deflation of the bottom blocks whose
- *       spike entries are <= u ||H||_F (the paper's default norm-stable condition; without the
- *       paper's reordering of failed blocks, R22), Hessenberg re-reduction, U propagated to the rest
- *       of H and to Z by the DMMA update kernels; more than 14% deflated -> next round at once;
+ *       Schur form of the window (U accumulated), spike s U(0,:), deflation from the bottom of the
+ *       blocks whose spike entries are <= u ||H||_F (the paper's default norm-stable condition, R22),
+ *       each failed block moved above the blocks not yet evaluated (R23), Hessenberg re-reduction,
+ *       U propagated to the rest of H and to Z by the DMMA update kernels (hqr_aed); more than 14%
+ *       deflated -> next round at once;
  *   (c) sweep the block (hqr_sweep's fused path, window `window`) with up to nshifts shifts: the
  *       bottom-most failed AED candidates (aed_window > 0) or the eigenvalues of the trailing
  *       nshifts x nshifts block (aed_window == 0, R21), complex pairs first, reals paired; then set
@@ -171,6 +172,32 @@ int hqr_qz_sweep(double* H, double* T, double* Q, double* Z, int64_t n, int64_t 
  */
 int hqr_qr_iterate(double* H, double* Z, int64_t n, int64_t ilo, int64_t ihi, int nshifts, int window,
                    int nmin, int aed_window, int max_sweeps, double* wr, double* wi, int* sweeps_out);
+
+/*
+ * One aggressive-early-deflation step (the AED window, its Schur form, the spike,
+ * the deflation check, the reordering of failed candidates "above the remaining unevaluated diagonal
+ * blocks" P:289-290, the Hessenberg reduction of the remaining spike P:292; the norm-stable deflation
+ * condition P:1142-1189; failed swaps halt the reordering P:893-894; R22 / R23) on
+ * the window W = H(k0 : k0+nw, k0 : k0+nw) of the n x n device matrix H (column-major, ld n), where
+ * rows k0 .. k0+nw-1 are the trailing rows of an unreduced block starting at row ilo (the caller
+ * guarantees h(k0+nw, k0+nw-1) = 0 or k0 + nw = n; s = h(k0, k0-1), 0 when k0 = ilo):
+ *   T = U^T W U real Schur form (Francis double-shift QR in one CTA); from the bottom, a 1x1 / 2x2
+ *   block of T deflates when every spike entry s U(0, j) of its rows is <= thr (thr is the caller's
+ *   threshold, e.g. 2^-53 ||H||_F); a failed block is moved to the top of the not-yet-evaluated
+ *   blocks by swaps of adjacent diagonal blocks (Sylvester equation + QR, rejected when too
+ *   ill-conditioned, which ends the check); when nd > 0 blocks deflated: the remaining spike is
+ *   reflected onto e1, T(0:m, 0:m) reduced to Hessenberg form, T and the spike column (beta, 0, ..)
+ *   written into H, H(window, k0+nw:) <- U^T H(..), H(0:k0, window) <- H(..) U, Z(:, window) <- Z U.
+ *   When nd = 0, H and Z are unchanged.
+ * Z may be NULL.  ew, ei: host arrays of nw doubles receiving the eigenvalues of the final blocks in
+ * window order -- [0, m) the undeflated candidates (the next sweep's shifts), [m, nw) the deflated
+ * eigenvalues of rows k0+m .. k0+nw-1.  *nd_out = nw - m deflated (-1: the Schur iteration did not
+ * converge, nothing changed), *nund_out = m.  Returns 0; -1 H NULL / host pointer / world > 1; -3 n;
+ * -4 ilo / k0 / nw outside H; -9 nw < 2 or > HQR_MAX_WINDOW; -10 an output pointer NULL; -100 not set
+ * up; 1000+cudaError_t.  Synchronous on return.
+ */
+int hqr_aed(double* H, double* Z, int64_t n, int64_t ilo, int64_t k0, int nw, double thr, double* ew,
+            double* ei, int* nd_out, int* nund_out);
 
 /*
  * ---- Sharded sweep over several GPUs -------------------------------------------

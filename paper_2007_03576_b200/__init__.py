@@ -72,7 +72,7 @@ SYMBOLS = ["hqr_setup", "hqr_sweep", "hqr_sweep_multi", "hqr_teardown", "hqr_pla
            "hqr_plan_query_multi", "hqr_get_stats", "hqr_error_string", "hqr_dist_layout",
            "hqr_dist_query", "hqr_nccl_unique_id", "hqr_sweep_dist", "hqr_sweep_virtual",
            "hqr_get_aftermath", "hqr_sweeps", "hqr_plan_query_sweeps", "hqr_qz_sweep", "hqr_qr_iterate",
-           "hqr_sweep_dist_multi", "hqr_sweep_virtual_multi"]
+           "hqr_sweep_dist_multi", "hqr_sweep_virtual_multi", "hqr_aed"]
 
 
 def lib():
@@ -136,6 +136,10 @@ def lib():
                                      ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                      ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
         L.hqr_qr_iterate.restype = ctypes.c_int
+        L.hqr_aed.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
+                              ctypes.c_int, ctypes.c_double, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                              ctypes.c_void_p]
+        L.hqr_aed.restype = ctypes.c_int
         for nm in ("hqr_sweep_dist_multi", "hqr_sweep_virtual_multi"):
             fn = getattr(L, nm)
             fn.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_void_p,
@@ -305,6 +309,21 @@ def qr_iterate(H, Z, ilo: int, ihi: int, nshifts: int = 32, window: int = DEFAUL
     if rc < 0:
         raise HQRError(rc, "hqr_qr_iterate")
     return wr, wi, rc, sw.value
+
+
+def aed(H, Z, ilo: int, k0: int, nw: int, thr: float):
+    """One AED step (include/hqr.h hqr_aed, R22 / R23) on the window [k0, k0+nw) of device H (and Z):
+    returns (nd, eigenvalues of the final window blocks as complex, nw entries in window order; the
+    first nw - nd are the undeflated candidates)."""
+    hp, n = _ptr_n(H)
+    zp, _ = _ptr_n(Z)
+    ew, ei = np.zeros(nw), np.zeros(nw)
+    nd, m = ctypes.c_int(), ctypes.c_int()
+    rc = lib().hqr_aed(hp, zp, n, int(ilo), int(k0), int(nw), ctypes.c_double(thr), ew.ctypes.data,
+                       ei.ctypes.data, ctypes.byref(nd), ctypes.byref(m))
+    if rc:
+        raise HQRError(rc, "hqr_aed")
+    return nd.value, ew + 1j * ei
 
 
 def dist_layout(n: int, world: int):

@@ -1884,6 +1884,42 @@ int make_shifts_host(const double* wr, const double* wi, int m, int ns, double* 
     }
   return k;
 }
+
+// One AED step on the window [k0, k0+nwin) (the trailing rows of the unreduced block [l, hi]):
+// the one-CTA kernel (Schur form, spike, deflation with reordering, Hessenberg re-reduction), then,
+// when something deflated, the window factor U applied to the rest of H and to Z by the DMMA update
+// kernels (left: H(window, right of it); right: H(above, window), Z(:, window)).  ewr / ewi (host,
+// nwin) receive the eigenvalues of the final window blocks in window order; *nd / *m the deflated /
+// undeflated counts (*nd < 0: the window's Schur iteration did not converge, nothing changed).
+cudaError_t aed_step(double* H, double* Z, int64_t n, int64_t l, int64_t hi, int nwin, double thr,
+                     double* d_uslot, int KPa, int QLDa, double* d_ew, double* d_ei, int* d_res, WindowDesc* d_wd,
+                     const hqr::TensorMaps& tma, double* ewr, double* ewi, int* nd, int* m) {
+  const int64_t k0 = hi - nwin + 1;
+  int res[2] = {0, 0};
+  cudaError_t e = hqr::launch_aed(H, n, l, k0, nwin, thr, d_uslot, KPa, QLDa, d_ew, d_ei, d_res, g.stream);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(res, d_res, 2 * sizeof(int), cudaMemcpyDeviceToHost, g.stream);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(ewr, d_ew, nwin * sizeof(double), cudaMemcpyDeviceToHost, g.stream);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(ewi, d_ei, nwin * sizeof(double), cudaMemcpyDeviceToHost, g.stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(g.stream);
+  if (e != cudaSuccess) return e;
+  *nd = res[0];
+  *m = res[1];
+  if (res[0] <= 0) return cudaSuccess;
+  WindowDesc wd{};
+  wd.w0 = (int32_t)k0; wd.w1 = (int32_t)(k0 + nwin - 1); wd.slot = 0; wd.nbc = 0;
+  wd.ilo = (int32_t)l; wd.ihi = (int32_t)hi; wd.scan_lo = 0; wd.scan_hi = -1;
+  e = cudaMemcpyAsync(d_wd, &wd, sizeof(wd), cudaMemcpyHostToDevice, g.stream);
+  if (e != cudaSuccess) return e;
+  StepArgs a{};
+  a.H = H; a.Z = Z; a.n = n; a.ilo = l; a.ihi = hi; a.hcol0 = 0; a.lc0 = 0; a.lc1 = n; a.zrows = n; a.ldz = n;
+  a.wins = d_wd; a.win_begin = 0; a.win_count = 1; a.qslots = d_uslot; a.KP = KPa; a.QLD = QLDa;
+  a.slot_offset = 0; a.right_mode = 0;
+  int64_t items;
+  double fl, by;
+  e = hqr::launch_left(a, &wd, g.num_sms, tma, g.stream, &items, &fl, &by);
+  if (e == cudaSuccess) e = hqr::launch_right(a, &wd, g.num_sms, tma, g.stream, &items, &fl, &by);
+  return e;
+}
 }  // namespace
 
 int hqr_qr_iterate(double* H, double* Z, int64_t n, int64_t ilo, int64_t ihi, int nshifts, int window,
@@ -1967,32 +2003,15 @@ int hqr_qr_iterate(double* H, double* Z, int64_t n, int64_t ilo, int64_t ihi, in
       // then the window's factor U propagated by the DMMA update kernels
       const int nwin = (int)std::min<int64_t>(aed_window, N);
       const int64_t k0 = hi - nwin + 1;
-      int res[2] = {0, 0};
-      cudaError_t e = hqr::launch_aed(H, n, l, k0, nwin, thr, d_uslot, KPa, QLDa, d_ew, d_ei, d_info + 2, g.stream);
-      if (e == cudaSuccess) e = cudaMemcpyAsync(res, d_info + 2, 2 * sizeof(int), cudaMemcpyDeviceToHost, g.stream);
-      if (e == cudaSuccess) e = cudaMemcpyAsync(ewr.data(), d_ew, nwin * sizeof(double), cudaMemcpyDeviceToHost, g.stream);
-      if (e == cudaSuccess) e = cudaMemcpyAsync(ewi.data(), d_ei, nwin * sizeof(double), cudaMemcpyDeviceToHost, g.stream);
-      if (e == cudaSuccess) e = cudaStreamSynchronize(g.stream);
+      int nd = 0, m = 0;
+      cudaError_t e = aed_step(H, Z, n, l, hi, nwin, thr, d_uslot, KPa, QLDa, d_ew, d_ei, d_info + 2, d_wd, tma,
+                               ewr.data(), ewi.data(), &nd, &m);
       if (e != cudaSuccess) return fail(cuerr(e));
       ++naed;
-      const int nd = res[0], m = res[1];
       if (nd < 0) {  // the window's Schur iteration did not converge: plain shifts below
         k = 0;
       } else {
         if (nd > 0) {
-          WindowDesc wd{};
-          wd.w0 = (int32_t)k0; wd.w1 = (int32_t)(k0 + nwin - 1); wd.slot = 0; wd.nbc = 0;
-          wd.ilo = (int32_t)l; wd.ihi = (int32_t)hi; wd.scan_lo = 0; wd.scan_hi = -1;
-          CK(cudaMemcpyAsync(d_wd, &wd, sizeof(wd), cudaMemcpyHostToDevice, g.stream));
-          StepArgs a{};
-          a.H = H; a.Z = Z; a.n = n; a.ilo = l; a.ihi = hi; a.hcol0 = 0; a.lc0 = 0; a.lc1 = n; a.zrows = n; a.ldz = n;
-          a.wins = d_wd; a.win_begin = 0; a.win_count = 1; a.qslots = d_uslot; a.KP = KPa; a.QLD = QLDa;
-          a.slot_offset = 0; a.right_mode = 0;
-          int64_t items;
-          double fl, by;
-          e = hqr::launch_left(a, &wd, g.num_sms, tma, g.stream, &items, &fl, &by);
-          if (e == cudaSuccess) e = hqr::launch_right(a, &wd, g.num_sms, tma, g.stream, &items, &fl, &by);
-          if (e != cudaSuccess) return fail(cuerr(e));
           for (int j = m; j < nwin; ++j) {
             wr[k0 + j] = ewr[j];
             wi[k0 + j] = ewi[j];
@@ -2047,6 +2066,39 @@ int hqr_qr_iterate(double* H, double* Z, int64_t n, int64_t ilo, int64_t ihi, in
   g.stats.window_eff = ndefl;       // (re-used: eigenvalues deflated by AED)
   if (sweeps_out) *sweeps_out = sweeps;
   return rc;
+}
+
+int hqr_aed(double* H, double* Z, int64_t n, int64_t ilo, int64_t k0, int nw, double thr, double* ew, double* ei,
+            int* nd_out, int* nund_out) {
+  if (!H) return -1;
+  if (n < 1) return -3;
+  if (ilo < 0 || k0 < ilo || k0 + nw > n) return -4;
+  if (nw < 2 || nw > hqr::kMaxWindow) return -9;
+  if (!ew || !ei || !nd_out || !nund_out) return -10;
+  if (!g.ready) return -100;
+  if (g.world > 1) return -1;
+  CK(cudaSetDevice(g.device));
+  if (!is_device_ptr(H) || (Z && !is_device_ptr(Z))) return -1;
+  const int KPa = hqr::padded_kp(nw), QLDa = hqr::pad_ld(KPa);
+  const size_t nscr = 2 * (size_t)hqr::kMaxWindow + 8 + (size_t)KPa * QLDa + 16;
+  double* d_w = nullptr;
+  CK(cudaMalloc(&d_w, nscr * sizeof(double)));
+  double* d_ew = d_w;
+  double* d_ei = d_ew + hqr::kMaxWindow;
+  int* d_res = reinterpret_cast<int*>(d_ei + hqr::kMaxWindow);
+  double* d_uslot = d_ei + hqr::kMaxWindow + 8;
+  WindowDesc* d_wd = reinterpret_cast<WindowDesc*>(d_uslot + (size_t)KPa * QLDa);
+  hqr::TensorMaps tma;
+  cudaError_t e = hqr::make_tensor_maps(&tma, H, n, Z, n, n, n, KPa);
+  int nd = 0, m = 0;
+  if (e == cudaSuccess)
+    e = aed_step(H, Z, n, ilo, k0 + nw - 1, nw, thr, d_uslot, KPa, QLDa, d_ew, d_ei, d_res, d_wd, tma, ew, ei, &nd, &m);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(g.stream);
+  cudaFree(d_w);
+  if (e != cudaSuccess) return cuerr(e);
+  *nd_out = nd;
+  *nund_out = m;
+  return 0;
 }
 
 int hqr_get_aftermath(signed char* flags, int64_t n) {

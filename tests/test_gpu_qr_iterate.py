@@ -93,3 +93,80 @@ def test_qr_iteration_with_aed_vs_oracle(n, ns, aed, nmin, win, seed):
     Hd2 = hq.to_device(p.H)
     _, _, _, sweeps_plain = hq.qr_iterate(Hd2, None, 0, n - 1, nshifts=ns, window=win, nmin=nmin)
     assert sweeps < sweeps_plain
+
+
+def _aed_problem(W, s, above, rng):
+    nw = W.shape[0]
+    n = above + nw
+    H0 = np.asfortranarray(np.triu(rng.standard_normal((n, n)), -1))
+    H0[above:, above:] = W
+    H0[above, above - 1] = s
+    return H0
+
+
+def test_aed_step_reordering_vs_oracle():
+    """One AED step through the C ABI (hqr_aed, reading R23) on windows that need the reordering
+    (the bottom block fails, blocks above it pass; decisions determined with a margin,
+    tests/aed_predict.py): the GPU deflates the predicted eigenvalues, like the oracle; its
+    candidates are the other eigenvalues of W; H stays Hessenberg and similar to H0 through Z up to
+    the zeroed spike entries (the window's 2x2 blocks, hence H itself, are unique only up to an
+    orthogonal basis of each block, so H is not compared entry by entry)."""
+    from aed_predict import reorder_cases
+    above = 6
+    rng = np.random.default_rng(3)
+    for W, s, thr, defl, dec in reorder_cases(oracle.schur):
+        H0 = _aed_problem(W, s, above, rng)
+        n, nw = H0.shape[0], W.shape[0]
+        Zo = np.asfortranarray(np.eye(n))
+        Ho = H0.copy(order="F")
+        ndo, owr, owi, _ = oracle.aed(Ho, Zo, 0, above, nw, thr)
+        Hd, Zd = hq.to_device(H0), hq.to_device(np.eye(n))
+        nd, ev = hq.aed(Hd, Zd, 0, above, nw, thr)
+        H, Z = hq.from_device(Hd), hq.from_device(Zd)
+        assert nd == ndo == len(defl)
+        assert _match(ev[nw - nd:], defl) <= 1e-10
+        assert _match(ev[:nw - nd], [l for l in np.linalg.eigvals(W) if min(abs(l - np.array(defl))) > 1e-8]) <= 1e-10
+        hn = np.linalg.norm(H0)
+        assert np.linalg.norm(Z.T @ Z - np.eye(n)) <= 1e-13 * n
+        assert np.linalg.norm(Z @ H @ Z.T - H0) <= np.sqrt(nd) * thr + 1e-13 * n * hn
+        assert np.all(np.tril(H, -2) == 0.0) and H[n - nd, n - nd - 1] == 0.0
+        assert _match(np.linalg.eigvals(H[n - nd:, n - nd:]), defl) <= 1e-9
+
+
+@pytest.mark.parametrize("n,nw,seed", [(300, 96, 0), (200, 64, 1)])
+def test_aed_step_converging_tail_vs_oracle(n, nw, seed):
+    """A hess_n matrix after a QR iteration ran to the point where its trailing part is close to
+    converged (subdiagonal entries of the window shrunk): the GPU AED step deflates as many
+    eigenvalues as the oracle's, the same ones; H stays Hessenberg and similar to H0 through Z;
+    thr = 2^-53 ||H||_F (the paper's norm-stable condition)."""
+    from hqr_inputs import make_hess
+    p = make_hess(n, 2, z0="orth")
+    H0 = p.H.copy(order="F")
+    k0 = n - nw
+    g = np.random.default_rng(seed)
+    for r in range(k0 + 1, n):  # graded subdiagonal: blocks near the bottom converge, some fail
+        H0[r, r - 1] *= 10.0 ** (-12.0 * g.uniform(0.0, 1.0))
+    thr = 2.0 ** -53 * np.linalg.norm(H0)
+    Ho, Zo = H0.copy(order="F"), p.Z.copy(order="F")
+    ndo, owr, owi, ocand = oracle.aed(Ho, Zo, 0, k0, nw, thr)
+    Hd, Zd = hq.to_device(H0), hq.to_device(p.Z)
+    nd, ev = hq.aed(Hd, Zd, 0, k0, nw, thr)
+    H, Z = hq.from_device(Hd), hq.from_device(Zd)
+    assert nd == ndo
+    if nd:
+        assert _match(ev[nw - nd:], owr[n - nd:] + 1j * owi[n - nd:]) <= 1e-9
+        assert H[n - nd, n - nd - 1] == 0.0
+    hn = np.linalg.norm(H0)
+    assert np.linalg.norm(Z.T @ Z - np.eye(n)) <= 1e-13 * n
+    assert np.linalg.norm(Z @ H @ Z.T - p.Z @ H0 @ p.Z.T) <= 1e-13 * n * hn
+    assert np.all(np.tril(H, -2) == 0.0)
+
+
+def test_aed_argument_errors():
+    Hd = hq.to_device(np.eye(10))
+    with pytest.raises(hq.HQRError):
+        hq.aed(Hd, None, 0, 5, 1, 1e-16)      # nw < 2
+    with pytest.raises(hq.HQRError):
+        hq.aed(Hd, None, 0, 5, 6, 1e-16)      # window outside H
+    with pytest.raises(hq.HQRError):
+        hq.aed(Hd, None, 6, 5, 4, 1e-16)      # k0 < ilo
