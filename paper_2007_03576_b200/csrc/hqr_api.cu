@@ -87,6 +87,12 @@ struct FusedTasks {            // task queues of every step for the fused step k
   std::vector<int2> deps;                // (task index, completion count to wait for)
   int32_t* d_dep_begin = nullptr;
   int2* d_deps = nullptr;
+  // two claim queues (DESIGN.md §6 "Critical SMs"): the chases and the near tasks the next chases
+  // read (LeftNear, RightNear) in list order, then every other task in list order
+  std::vector<int32_t> qidx;
+  int32_t ncrit = 0;
+  int32_t* d_qidx = nullptr;
+  double chase_path_us = 0.0;            // estimated chase critical path of one chain (us)
   double flops = 0, bytes = 0;
 };
 
@@ -457,6 +463,7 @@ hqr::ChunkSizes chunk_sizes() {
       cs.left = v[0]; cs.near = v[1]; cs.bulk = v[2]; cs.tail = v[3]; cs.tail_chunk = v[4];
     }
   }
+  if (const char* e = hqr::tuning_env("HQR_NEAR_TASK")) cs.near_task = std::max(1, atoi(e));  // tuning builds
   if (const char* e = hqr::tuning_env("HQR_PHASE_TAIL")) {  // tuning builds: "ltail,ntail,chunk"
     int v[3];
     if (sscanf(e, "%d,%d,%d", &v[0], &v[1], &v[2]) == 3 && v[0] >= 0 && v[1] >= 0 && v[2] > 0) {
@@ -579,6 +586,18 @@ int get_fused(CachedPlan& cp, bool has_z, int64_t n, FusedTasks** out) {
     {
       int rcd = build_task_deps(P, cp.KP, n, n, has_z, f.get());
       if (rcd) return rcd;
+      if (const char* path = hqr::tuning_env("HQR_DUMP_DEPS")) {  // tuning builds: the task graph for tools/
+        if (FILE* fd = fopen(path, "w")) {
+          fprintf(fd, "task,type,step,win,ntiles,deps\n");
+          for (size_t t = 0; t < f->tasks.size(); ++t) {
+            const hqr::Task& T = f->tasks[t];
+            fprintf(fd, "%zu,%d,%d,%d,%d,", t, T.type, T.step, T.win, T.ntiles);
+            for (int d = f->dep_begin[t]; d < f->dep_begin[t + 1]; ++d) fprintf(fd, "%d:%d ", f->deps[d].x, f->deps[d].y);
+            fprintf(fd, "\n");
+          }
+          fclose(fd);
+        }
+      }
       CK(cudaMalloc(&f->d_dep_begin, f->dep_begin.size() * sizeof(int32_t)));
       CK(cudaMemcpy(f->d_dep_begin, f->dep_begin.data(), f->dep_begin.size() * sizeof(int32_t),
                     cudaMemcpyHostToDevice));
@@ -588,6 +607,22 @@ int get_fused(CachedPlan& cp, bool has_z, int64_t n, FusedTasks** out) {
     }
     CK(cudaMalloc(&f->d_tasks, f->tasks.size() * sizeof(hqr::Task)));
     CK(cudaMemcpy(f->d_tasks, f->tasks.data(), f->tasks.size() * sizeof(hqr::Task), cudaMemcpyHostToDevice));
+    {  // the critical queue (chases, LeftNear, RightNear) and the bulk queue, each in list order
+      f->qidx.clear();
+      for (int pass = 0; pass < 2; ++pass)
+        for (int32_t i = 0; i < (int32_t)f->tasks.size(); ++i) {
+          const int ty = f->tasks[i].type;
+          const bool crit = ty == hqr::kTaskChase || ty == hqr::kTaskLeftNear || ty == hqr::kTaskRightNear;
+          if (crit == (pass == 0)) f->qidx.push_back(i);
+          if (pass == 0 && crit) ++f->ncrit;
+        }
+      CK(cudaMalloc(&f->d_qidx, f->qidx.size() * sizeof(int32_t)));
+      CK(cudaMemcpy(f->d_qidx, f->qidx.data(), f->qidx.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+      // one chain's chase path: its windows' steps back to back (~2700 cycles per step)
+      double steps = 0.0;
+      for (const WindowDesc& w : P.windows) steps += (double)(w.t1 - w.t0 + 1);
+      f->chase_path_us = steps / std::max(1, P.nchains) * 1.4;
+    }
     CK(cudaMalloc(&f->d_steps, f->steps.size() * sizeof(hqr::StepInfo)));
     CK(cudaMemcpy(f->d_steps, f->steps.data(), f->steps.size() * sizeof(hqr::StepInfo), cudaMemcpyHostToDevice));
     CK(cudaMalloc(&f->d_wdeps, f->wdeps.size() * sizeof(hqr::WinDeps)));
@@ -725,6 +760,19 @@ struct IoPlan {
   }
 };
 
+// Critical SMs: when one chain's chase path (its windows' chases back to back) is
+// comparable to the sweep's GEMM time, `2 nchains + 2` CTAs serve only the critical queue (chases and
+// the near tasks the next chases read), so a chase is claimed as soon as its inputs are ready instead
+// of behind the previous step's bulk tiles, and runs on an SM whose ring holds no bulk tiles to drain.
+// GEMM-bound sweeps (the chase path well below the GEMM time) keep one queue (0).
+int crit_sms(const Plan& P, const FusedTasks& f) {
+  if (const char* e = hqr::tuning_env("HQR_CRIT_SMS")) return std::max(0, atoi(e));  // tuning builds
+  const double gemm_us = f.flops / (g.num_sms * 0.19e12) * 1e6;  // ~0.75 of the per-SM DMMA peak
+  if (f.chase_path_us < 0.5 * gemm_us) return 0;
+  const int c = 2 * P.nchains + 2;  // a chase and its near tiles per chain at once, plus two
+  return c <= g.num_sms / 4 ? c : 0;
+}
+
 int enqueue_fused(CachedPlan& cp, double* H, double* Z, int64_t n, const hqr::TensorMaps& tm,
                   hqr_stats* st, bool prof = false, std::vector<int>* classes = nullptr,
                   IoPlan* io = nullptr) {
@@ -777,7 +825,7 @@ int enqueue_fused(CachedPlan& cp, double* H, double* Z, int64_t n, const hqr::Te
     mark(3);
     CK(hqr::launch_step(base, f->d_steps, P.nsteps, f->d_tasks, (int)f->tasks.size(), 0, f->d_dep_begin,
                         f->d_deps, f->d_ctr, step_ctr, task_ctr, io ? io->d_flags : nullptr, tm, P.max_kw,
-                        g.num_sms, A));
+                        g.num_sms, A, f->d_qidx, f->ncrit, crit_sms(P, *f)));
     mark(-1);
     st->launches_left++;
     if (io) {
@@ -790,7 +838,8 @@ int enqueue_fused(CachedPlan& cp, double* H, double* Z, int64_t n, const hqr::Te
       const int nt = f->begin[s + 1] - f->begin[s];
       mark(3);
       CK(hqr::launch_step(base, f->d_steps, P.nsteps, f->d_tasks + f->begin[s], nt, f->begin[s], f->d_dep_begin,
-                          f->d_deps, step_ctr + 4 * s + 3, step_ctr, task_ctr, nullptr, tm, P.max_kw, g.num_sms, A));
+                          f->d_deps, step_ctr + 4 * s + 3, step_ctr, task_ctr, nullptr, tm, P.max_kw, g.num_sms, A,
+                          nullptr, 0, 0));
       mark(-1);
       st->launches_left++;  // one fused launch per step (counted once)
     }
@@ -903,6 +952,7 @@ int hqr_teardown(void) {
         if (f->d_wdeps) cudaFree(f->d_wdeps);
         if (f->d_dep_begin) cudaFree(f->d_dep_begin);
         if (f->d_deps) cudaFree(f->d_deps);
+        if (f->d_qidx) cudaFree(f->d_qidx);
       }
   }
   g.plans.clear();

@@ -310,7 +310,10 @@ __device__ __noinline__ void swap_factor(const double* T, int ld, int i, double*
 // ---- the AED kernel: one CTA of kAedThreads threads (all phases are latency-bound chains of small
 // reflector applications; with 256 threads every application over the window's <= 112 rows or
 // columns is one pass, and T and U updates of a step run side by side) -------------------------
-constexpr int kAedThreads = 256;
+#ifndef HQR_AED_THREADS
+#define HQR_AED_THREADS 256
+#endif
+constexpr int kAedThreads = HQR_AED_THREADS;
 
 // A(r0 .. r0+m-1, c) -= tau w (w^T A(.., c)) for the columns c handled by thread t (stride nthr)
 __device__ __forceinline__ void refl_left_col(double* A, int lda, int r0, int m, int c, const double* w, double tau) {

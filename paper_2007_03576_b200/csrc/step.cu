@@ -19,6 +19,8 @@
 // two-phase step of chase.cu with all of the CTA's warps.
 #include <cuda_runtime.h>
 
+#include <string>
+
 #include <algorithm>
 #ifdef HQR_PROGRESS  // debugging build only: per-warp progress in host-mapped memory, dumped on a hang
 #include <chrono>
@@ -71,6 +73,8 @@ __device__ __forceinline__ unsigned long long gtime() {
   return t;
 }
 __device__ unsigned long long g_ctim[8];
+__device__ unsigned long long g_wrec[8192][6];
+__device__ unsigned long long g_trec[262144][8];  // per task: claim, deps met, tiles issued, done (max flush), type | win << 8, step  // per chased window: start, end (globaltimer ns), b0, step, claim, deps met
 __device__ unsigned long long g_wait[12];  // [0..7] producer dependency spins per tag; [8] chase, [9] CTA, [10] consumer waits, [11] consumer K+epilogue  // chase: summed cycles per phase (all warps), windows
 #define TIM_MIN(s, k) atomicMin(&g_tim[(s) & 4095][k], gtime())
 #define TIM_MAX(s, k) atomicMax(&g_tim[(s) & 4095][k], gtime())
@@ -249,6 +253,9 @@ struct StageDesc {
   int* ctr2;   // ... a second one (near tasks: their phase's step counter) or nullptr ...
   int* ctr_all;  // ... and the step's all-tiles counter
   TileRef t;
+#ifdef HQR_TIMING
+  int task;    // timing builds: the sweep task index
+#endif
 };
 
 // One release fence, then relaxed adds: the release pattern for several counters at the cost of one
@@ -310,7 +317,7 @@ __global__ void __launch_bounds__(kStepThreads, 1)
                 int ntasks, int task_base, const int32_t* __restrict__ dep_begin, const int2* __restrict__ deps,
                 int* next_ctr, int* step_ctr, int* task_ctr,
                 const int* __restrict__ up_flags, const __grid_constant__ CUtensorMap tmL, const __grid_constant__ CUtensorMap tmR,
-                const __grid_constant__ CUtensorMap tmZ) {
+                const __grid_constant__ CUtensorMap tmZ, const int32_t* __restrict__ qidx, int ncrit, int crit_sms) {
   constexpr int NS = stages_of(KP);
   constexpr int QLD = pad_ld(KP);
   constexpr int SS = Geom<KP, true>::STAGE > Geom<KP, false>::STAGE ? Geom<KP, true>::STAGE
@@ -366,7 +373,17 @@ __global__ void __launch_bounds__(kStepThreads, 1)
     for (;;) {
       int t = 0;
       PROG(1000000 + j);
-      if (lane == 0) t = atomicAdd(next_ctr, 1);
+      if (lane == 0) {
+        if (crit_sms == 0) {
+          t = atomicAdd(next_ctr, 1);
+        } else if ((int)blockIdx.x < crit_sms) {  // the critical queue
+          const int i = atomicAdd(next_ctr, 1);
+          t = i < ncrit ? qidx[i] : ntasks;
+        } else {                                  // the bulk queue
+          const int i = atomicAdd(next_ctr + 1, 1);
+          t = i < ntasks - ncrit ? qidx[ncrit + i] : ntasks;
+        }
+      }
       t = __shfl_sync(0xffffffffu, t, 0);
       if (t >= ntasks) {
         marker(kDescExit);
@@ -380,6 +397,9 @@ __global__ void __launch_bounds__(kStepThreads, 1)
       const bool chase = T.type == kTaskChase;
       const int gw = chase ? -1 : S.win_begin + T.win;  // plan index of the task's window
       const int tg = task_base + t;                      // the task's index in the sweep
+#ifdef HQR_TIMING
+      const unsigned long long w_claim = gtime();
+#endif
       if (lane == 0) {
         PROG(2000000 + t);
         if (up_flags) spin_until(up_flags + S.up_need, 1, 5);  // host-buffer sweep: rows / columns up
@@ -416,7 +436,18 @@ __global__ void __launch_bounds__(kStepThreads, 1)
       __syncwarp();  // the lanes' acquires before lane 0's async-proxy fence and TMA reads
       if (lane == 0) fence_proxy_async_all();  // other SMs' generic stores before this SM's TMA reads
       __syncwarp();
+#ifdef HQR_TIMING
+      if (lane == 0 && tg < 262144) {
+        g_trec[tg][0] = w_claim;
+        g_trec[tg][1] = gtime();
+        g_trec[tg][4] = (unsigned long long)(T.type | (T.win << 8));
+        g_trec[tg][5] = (unsigned long long)T.step | ((unsigned long long)T.ntiles << 32);
+      }
+#endif
       if (chase) {
+#ifdef HQR_TIMING
+        const unsigned long long w_depok = gtime();
+#endif
         marker(kDescChase);
         PROG(7000000 + j);
         if (lane == 0) {
@@ -429,14 +460,28 @@ __global__ void __launch_bounds__(kStepThreads, 1)
 #ifdef HQR_TIMING
         const long long c_start = clock64();
 #endif
+#ifdef HQR_TIMING
+        const unsigned long long w_start = gtime();
+#endif
         chase_window_9w(cargs, cw, cwi, sm, R);
         __syncthreads();
 #ifdef HQR_TIMING
         if (lane == 0) atomicAdd(&g_wait[8], (unsigned long long)(clock64() - c_start));
+        if (lane == 0 && cwi < 8192) {
+          g_wrec[cwi][0] = w_start;
+          g_wrec[cwi][1] = gtime();
+          g_wrec[cwi][2] = (unsigned long long)cw.b0;
+          g_wrec[cwi][3] = (unsigned long long)(g + 1);
+          g_wrec[cwi][4] = w_claim;
+          g_wrec[cwi][5] = w_depok;
+        }
 #endif
         if (lane == 0) {
           TIM_MAX(g, 2);
           red_release_add(task_ctr + tg, 1);  // the CTA's stores are ordered by the barrier
+#ifdef HQR_TIMING
+          if (tg < 262144) g_trec[tg][3] = gtime();
+#endif
         }
         q_win = -1;
         continue;
@@ -480,6 +525,9 @@ __global__ void __launch_bounds__(kStepThreads, 1)
         if (lane == 0) {
           StageDesc& d = desc[j % NS];
           d.pos = j; d.kind = kDescTile; d.left = left; d.qe = qe;
+#ifdef HQR_TIMING
+          d.task = tg;
+#endif
           // completion counts: on each group's last tile of the task, that group's tile count
           // (the group of tile i takes the task's tiles i, i-G, ..., i.e. i/G + 1 of them)
           const bool last = i + kGroups >= T.ntiles;
@@ -498,6 +546,9 @@ __global__ void __launch_bounds__(kStepThreads, 1)
         __syncwarp();
       }
       if (new_q && nq_pre == T.ntiles) load_q();  // short task: the Q_W load after its tiles
+#ifdef HQR_TIMING
+      if (lane == 0 && tg < 262144) g_trec[tg][2] = gtime();
+#endif
     }
   } else {
     // ================================ consumers ================================
@@ -516,6 +567,9 @@ __global__ void __launch_bounds__(kStepThreads, 1)
       if (lane == 0) {
         fence_release_gpu();  // the warp's stores (ordered by __syncwarp) before the three counts
         red_relaxed_add(pend_p, pend_n);
+#ifdef HQR_TIMING
+        if (pend_p - task_ctr >= 0 && pend_p - task_ctr < 262144) atomicMax(&g_trec[pend_p - task_ctr][3], gtime());
+#endif
         if (pend_p2) red_relaxed_add(pend_p2, pend_n);
         red_relaxed_add(pend_all, pend_n);
       }
@@ -589,11 +643,14 @@ __global__ void __launch_bounds__(kStepThreads, 1)
       const int qq = kGroups == 2 ? (i4 + 2 * q) & 3 : (i4 + j) & 3;
 #ifdef HQR_TIMING
       const long long ck0 = clock64();
+      const int ttask = desc[s].task;
+      if (lane == 0 && ttask < 262144) atomicMin(&g_trec[ttask][6], gtime());
 #endif
       if (left) consume_tile<KP, true>(Qs, Ps + s * SS, &empty[s], t, qq, lane, mid);
       else consume_tile<KP, false>(Qs, Ps + s * SS, &empty[s], t, qq, lane, mid);
 #ifdef HQR_TIMING
       if (lane == 0) atomicAdd(&g_wait[11], (unsigned long long)(clock64() - ck0));
+      if (lane == 0 && ttask < 262144) atomicMax(&g_trec[ttask][7], gtime());
 #endif
       if (cp) {
         pend_p = cp;
@@ -621,7 +678,7 @@ template <int KP>
 cudaError_t launch_step_t(const StepArgs& base, const StepInfo* steps, int nsteps, const Task* tasks, int ntasks,
                           int task_base, const int32_t* dep_begin, const int2* deps, int* next_ctr, int* step_ctr,
                           int* task_ctr, const int* up_flags, const TensorMaps& tm, int max_kw, int num_sms,
-                          cudaStream_t st) {
+                          cudaStream_t st, const int32_t* qidx, int ncrit, int crit_sms) {
   static size_t configured = 0;
   const size_t smem = step_smem<KP>(max_kw);
   if (smem > configured) {
@@ -630,9 +687,10 @@ cudaError_t launch_step_t(const StepArgs& base, const StepInfo* steps, int nstep
     configured = smem;
   }
   const int grid = std::max(1, std::min(ntasks, num_sms));
+  if (crit_sms >= grid || ncrit <= 0 || ncrit >= ntasks) crit_sms = 0;  // both queues need CTAs and tasks
   step_kernel<KP><<<grid, kStepThreads, smem, st>>>(base, steps, nsteps, tasks, ntasks, task_base, dep_begin, deps,
                                                      next_ctr, step_ctr, task_ctr, up_flags, tm.left_H, tm.right_H,
-                                                     tm.right_Z);
+                                                     tm.right_Z, qidx, ncrit, crit_sms);
   return cudaGetLastError();
 }
 
@@ -647,6 +705,17 @@ void debug_timing(int nsteps, bool reset) {
     unsigned long long z[12] = {0};
     cudaMemcpyToSymbol(g_ctim, z, 8 * sizeof(unsigned long long));
     cudaMemcpyToSymbol(g_wait, z, sizeof(z));
+    static unsigned long long wz[8192][6];
+    cudaMemcpyToSymbol(g_wrec, wz, sizeof(wz));
+    void* tz = nullptr;
+    if (cudaGetSymbolAddress(&tz, g_trec) == cudaSuccess) {
+      static unsigned long long tinit[262144][8];
+      for (int i = 0; i < 262144; ++i) {
+        for (int k = 0; k < 8; ++k) tinit[i][k] = 0;
+        tinit[i][6] = ~0ull;
+      }
+      cudaMemcpy(tz, tinit, sizeof(tinit), cudaMemcpyHostToDevice);
+    }
     return;
   }
   cudaDeviceSynchronize();
@@ -685,6 +754,28 @@ void debug_timing(int nsteps, bool reset) {
   fprintf(stderr, "hqr timing: %d steps, mean launch %.1f us, chase start %.1f us, chase end %.1f us "
           "(%d steps with chases), mean gap between launches %.2f us\n", nsteps, e / nsteps,
           cs / std::max(nc, 1), ce / std::max(nc, 1), nc, gap / std::max(nsteps - 1, 1));
+  if (const char* path = tuning_env("HQR_TIMING_WREC")) {  // per-window chase records for tools/
+    static unsigned long long wr[8192][6];
+    cudaMemcpyFromSymbol(wr, g_wrec, sizeof(wr));
+    if (FILE* f = fopen(path, "w")) {
+      fprintf(f, "window,start_ns,end_ns,b0,step,claim_ns,depok_ns\n");
+      for (int i = 0; i < 8192; ++i)
+        if (wr[i][1])
+          fprintf(f, "%d,%llu,%llu,%llu,%llu,%llu,%llu\n", i, wr[i][0], wr[i][1], wr[i][2], wr[i][3], wr[i][4], wr[i][5]);
+      fclose(f);
+    }
+    static unsigned long long tr[262144][8];
+    cudaMemcpyFromSymbol(tr, g_trec, sizeof(tr));
+    std::string tp = std::string(path) + ".tasks";
+    if (FILE* f = fopen(tp.c_str(), "w")) {
+      fprintf(f, "task,claim_ns,depok_ns,issued_ns,done_ns,type,win,step,cstart_ns,cend_ns,ntiles\n");
+      for (int i = 0; i < 262144; ++i)
+        if (tr[i][0])
+          fprintf(f, "%d,%llu,%llu,%llu,%llu,%llu,%llu,%llu,%llu,%llu,%llu\n", i, tr[i][0], tr[i][1], tr[i][2], tr[i][3],
+                  tr[i][4] & 255, tr[i][4] >> 8, tr[i][5] & 0xffffffffull, tr[i][6], tr[i][7], tr[i][5] >> 32);
+      fclose(f);
+    }
+  }
   for (int s = 0; s < nsteps && s < 4096; s += std::max(1, nsteps / 12)) {
     const double t0 = (double)h[s][0];
     fprintf(stderr, "  step %4d: launch %.1f us, chase %.1f .. %.1f us\n", s, (h[s][3] - t0) * 1e-3,
@@ -739,10 +830,11 @@ void debug_progress_init() {}
 cudaError_t launch_step(const StepArgs& base, const StepInfo* steps, int nsteps, const Task* tasks, int ntasks,
                         int task_base, const int32_t* dep_begin, const int2* deps, int* next_ctr, int* step_ctr,
                         int* task_ctr, const int* up_flags, const TensorMaps& tm, int max_kw, int num_sms,
-                        cudaStream_t st) {
+                        cudaStream_t st, const int32_t* qidx, int ncrit, int crit_sms) {
   if (!tm.valid) return cudaErrorNotSupported;
+  if (!qidx) crit_sms = 0;
 #define HQR_LS(K) return launch_step_t<K>(base, steps, nsteps, tasks, ntasks, task_base, dep_begin, deps, next_ctr, \
-                                          step_ctr, task_ctr, up_flags, tm, max_kw, num_sms, st)
+                                          step_ctr, task_ctr, up_flags, tm, max_kw, num_sms, st, qidx, ncrit, crit_sms)
   switch (base.KP) {
     case 32: HQR_LS(32);
     case 64: HQR_LS(64);
@@ -788,10 +880,10 @@ void build_step_tasks(const StepArgs& a, const WindowDesc* wins, int nwin, const
   };
   const size_t base = out->size();
   // what the next step's chases read first: LeftNear, RightNear, then the chases themselves
-  for (int i = 0; i < nwin; ++i) add(kTaskLeftNear, i, 0, lnear[i], 0, 0, cs.left);
+  for (int i = 0; i < nwin; ++i) add(kTaskLeftNear, i, 0, lnear[i], 0, 0, cs.near_task);
   for (int i = 0; i < nwin; ++i) {
     const int64_t w0 = wins[i].w0;
-    if (rnear[i] < w0) add(kTaskRightNear, i, 0, (w0 - rnear[i] + MT - 1) / MT, rnear[i], w0, cs.near);
+    if (rnear[i] < w0) add(kTaskRightNear, i, 0, (w0 - rnear[i] + MT - 1) / MT, rnear[i], w0, cs.near_task);
   }
   auto chases = [&]() {
     for (int i = 0; i < nnext; ++i) {

@@ -65,6 +65,8 @@ struct ChunkSizes {   // tiles per task, per phase
   int left = 24, near = 48, bulk = 48;  // tuned for the persistent sweep (configs[3], tools/tune_chunks.sh)
   int tail = 0, tail_chunk = 8;  // the queue's last `tail` tiles in chunks of `tail_chunk`
   int ltail = 300, ntail = 0, phase_chunk = 2;  // the left phase's last tiles in small chunks (tools/tune_phase_tail.sh)
+  int near_task = 1;  // tiles per LeftNear / RightNear task: the next chase waits for these (one tile
+                      // each: the tiles of one window run on several SMs at once)
 };
 
 // Tasks of one step in queue order (LeftNear, RightNear, C, L, Rn, Z, Rf).
@@ -80,10 +82,13 @@ void build_step_tasks(const StepArgs& a, const WindowDesc* wins, int nwin, const
 // task_ctr[task] >= count (per-task completion counts: 4 per GEMM tile -- one per consumer warp --,
 // 1 per chase).  Needs the TMA path.
 // up_flags (nullable): per upload chunk, nonzero once on the device (host-buffer sweeps).
+// crit_sms > 0: CTAs 0 .. crit_sms-1 claim tasks qidx[0 .. ncrit) through next_ctr[0], the others
+// qidx[ncrit .. ntasks) through next_ctr[1] (two queues, each in list order); 0: one queue in list
+// order through next_ctr[0] (qidx unused).
 cudaError_t launch_step(const StepArgs& base, const StepInfo* steps, int nsteps, const Task* tasks, int ntasks,
                         int task_base, const int32_t* dep_begin, const int2* deps, int* next_ctr, int* step_ctr,
                         int* task_ctr, const int* up_flags, const TensorMaps& tm, int max_kw, int num_sms,
-                        cudaStream_t st);
+                        cudaStream_t st, const int32_t* qidx, int ncrit, int crit_sms);
 
 // Debugging builds (-DHQR_PROGRESS): progress buffer in host-mapped memory, dumped after
 // HQR_PROGRESS_SECS seconds (then the process exits).  No-op otherwise.
