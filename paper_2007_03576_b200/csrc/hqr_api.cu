@@ -196,6 +196,8 @@ struct State {
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   cudaEvent_t ev_q[hqr::kQSets] = {}, ev_z[hqr::kQSets] = {};
   cudaStream_t cstream = nullptr;  // sharded sweep: NCCL broadcasts (comm stream)
+  cudaStream_t qzs[3] = {};        // QZ sweep: the step's four update launches side by side
+  cudaEvent_t qz_fork = nullptr, qz_join[3] = {};
   cudaEvent_t dev_chase[kQSetsDist] = {}, dev_bc[kQSetsDist] = {}, dev_bulk[kQSetsDist] = {};
   double* d_coef = nullptr;
   size_t coef_cap = 0;
@@ -913,6 +915,11 @@ int hqr_setup(const hqr_config* cfg) {
   CK(cudaEventCreateWithFlags(&g.ev_fork, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&g.ev_join, cudaEventDisableTiming));
   CK(cudaStreamCreateWithPriority(&g.cstream, cudaStreamNonBlocking, prio_hi));
+  CK(cudaEventCreateWithFlags(&g.qz_fork, cudaEventDisableTiming));
+  for (int i = 0; i < 3; ++i) {
+    CK(cudaStreamCreateWithPriority(&g.qzs[i], cudaStreamNonBlocking, prio_hi));
+    CK(cudaEventCreateWithFlags(&g.qz_join[i], cudaEventDisableTiming));
+  }
   for (int i = 0; i < kQSetsDist; ++i) {
     CK(cudaEventCreateWithFlags(&g.dev_chase[i], cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&g.dev_bc[i], cudaEventDisableTiming));
@@ -987,6 +994,14 @@ int hqr_teardown(void) {
   }
   if (g.cstream) cudaStreamDestroy(g.cstream);
   g.cstream = nullptr;
+  if (g.qz_fork) cudaEventDestroy(g.qz_fork);
+  g.qz_fork = nullptr;
+  for (int i = 0; i < 3; ++i) {
+    if (g.qzs[i]) cudaStreamDestroy(g.qzs[i]);
+    if (g.qz_join[i]) cudaEventDestroy(g.qz_join[i]);
+    g.qzs[i] = nullptr;
+    g.qz_join[i] = nullptr;
+  }
   for (int i = 0; i < hqr::kQSets; ++i) {
     cudaEventDestroy(g.ev_q[i]);
     cudaEventDestroy(g.ev_z[i]);
@@ -1842,12 +1857,18 @@ int hqr_qz_sweep(double* H, double* T, double* Q, double* Z, int64_t n, int64_t 
       int64_t items;
       double fl, by;
       auto acc = [&](int* l) { *l += items > 0; sts->flops_update += fl; sts->bytes_update += by; };
+      // H's and T's updates side by side (two streams, joined before the next chase); on one matrix
+      // the left update precedes the right one (a step's windows share blocks H(W1 rows, W2 cols))
+      CK(cudaEventRecord(g.qz_fork, A));
+      CK(cudaStreamWaitEvent(g.qzs[0], g.qz_fork, 0));
       CK(hqr::launch_left(aH, hw, g.num_sms, tmA, A, &items, &fl, &by)); acc(&sts->launches_left);
-      CK(hqr::launch_left(aT, hw, g.num_sms, tmB, A, &items, &fl, &by)); acc(&sts->launches_left);
+      CK(hqr::launch_left(aT, hw, g.num_sms, tmB, g.qzs[0], &items, &fl, &by)); acc(&sts->launches_left);
       aHz.right_mode = 1;
       CK(hqr::launch_right(aHz, hw, g.num_sms, tmA, A, &items, &fl, &by)); acc(&sts->launches_right);
       aTz.right_mode = 1;
-      CK(hqr::launch_right(aTz, hw, g.num_sms, tmB, A, &items, &fl, &by)); acc(&sts->launches_right);
+      CK(hqr::launch_right(aTz, hw, g.num_sms, tmB, g.qzs[0], &items, &fl, &by)); acc(&sts->launches_right);
+      CK(cudaEventRecord(g.qz_join[0], g.qzs[0]));
+      CK(cudaStreamWaitEvent(A, g.qz_join[0], 0));
       CK(cudaEventRecord(g.ev_q[set], A));
       CK(cudaStreamWaitEvent(Bs, g.ev_q[set], 0));
       if (Q) {
