@@ -373,8 +373,13 @@ def main():
     n = prob.H.shape[0]
     gen_s = time.time() - t0
     nshifts = len(prob.shifts_re)
-    if args.window is None:  # the config's window (configs[1]: 3 nshifts/2 + 1 = 151), else the default 96
+    window_note = None
+    if args.window is None:  # the config's window, else the default 96
         args.window = prob.window if prob.window else 96
+        if args.window > 112:  # configs[1]'s 3 nshifts/2 + 1 = 151 exceeds the library's 112 (SMEM)
+            window_note = (f"config window {args.window} exceeds the maximum 112 (R5 / DESIGN.md); the default 96 "
+                           f"is used (112: slower)")
+            args.window = 96
     shift_sets = None
     if args.sweeps > 1:  # NEXT-1: further shift sets from the same distribution (stream offsets)
         from hqr_inputs import CONFIGS, shifts as draw_shifts
@@ -550,7 +555,7 @@ def main():
         Zh = torch.empty((n, n), dtype=torch.float64, pin_memory=True)
         Hp = np.asfortranarray(prob.H)
         e2e_t = []
-        for i in range(2):
+        for i in range(4):  # wall clock over PCIe copies varies ~20% call to call: the best of four
             Hh.copy_(torch.from_numpy(Hp.T.copy()))
             Zh.copy_(torch.from_numpy(np.ascontiguousarray(prob.Z.T)))
             rc_t = time.perf_counter()
@@ -577,6 +582,7 @@ def main():
             "config": {"workload": workload, "n": n, "nshifts": nshifts,
                        "sweeps_per_step": args.sweeps,
                        "window": st["window_eff"], "window_requested": window_requested or args.window,
+                       **({"window_note": window_note} if window_note else {}),
                        "z": "random orthogonal" if (args.config in (1, 3) or args.workload == "hess") else "identity",
                        "parallelism": (f"{world} GPUs: H block-column (sqrt-balanced), Z block-row, "
                                        "per-window Q ncclBroadcast, lent slabs") if world > 1 else "1 GPU",
