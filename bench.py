@@ -284,6 +284,41 @@ def run_qriter(args):
     print(json.dumps(line), flush=True)
 
 
+def chase_line(hq, n, prob, nshifts, args, ms_chase, clocks, sweep_ms):
+    """The chase kernel's own figures (north_star: its achieved HBM GB/s): step 0's windows run in a
+    standalone chase launch (timed with CUDA events under FLAG_PROFILE); every later window is chased
+    inside the persistent kernel with the same code.  Algorithmic bytes per window: H(W,W) in and out
+    plus Q_W out, 3 k^2 doubles."""
+    if args.sweeps > 1 or ms_chase <= 0:
+        return None
+    try:
+        info, wins = hq.plan_query(n, prob.ilo, prob.ihi, nshifts, args.window)
+    except Exception:  # multi-block configs: no single plan
+        return None
+    first = wins[wins[:, 0] == 0]
+    if len(first) == 0:
+        return None
+    kw_all = (wins[:, 3] - wins[:, 2] + 1).astype(np.float64)
+    sweep_bytes = float(np.sum(3.0 * kw_all * kw_all * 8.0))
+    kw = (first[:, 3] - first[:, 2] + 1).astype(np.float64)
+    steps = (first[:, 5] - first[:, 4] + 1).astype(np.float64)
+    nbytes = float(np.sum(3.0 * kw * kw * 8.0))
+    peaks = json.load(open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "MEASURED_PEAKS.json")))
+    gbs = nbytes / (ms_chase * 1e-3) / 1e9
+    mhz = (clocks or {}).get("sm_mhz") or peaks.get("sm_max_mhz", 1965.0)
+    return {"kernel": "chase kernel, step 0's windows (one standalone launch; later windows inside the "
+                      "persistent kernel, same code)",
+            "windows": int(len(first)), "ms": ms_chase, "us_per_window": ms_chase * 1e3 / len(first),
+            "bulge_steps_per_window": float(steps.mean()),
+            "cycles_per_bulge_step": ms_chase * 1e-3 * mhz * 1e6 / float(steps.max()),
+            "algorithmic_bytes": nbytes, "achieved_gbs": gbs, "peak_gbs": peaks["hbm_gbs"],
+            "frac_hbm": gbs / peaks["hbm_gbs"],
+            "sweep_windows": int(len(wins)), "sweep_chase_bytes": sweep_bytes,
+            "sweep_chase_gbs_over_sweep_time": sweep_bytes / (sweep_ms * 1e-3) / 1e9,
+            "bound": "latency: the reflector chain and SMEM traffic of the in-window chase (DESIGN.md §6), "
+                     "not HBM; the windows of a step run concurrently, one CTA each"}
+
+
 def run_reference(args, cfg_idx):
     """--impl reference: the oracle timed as it stands on the host cores."""
     rank = int(os.environ.get("RANK", "0"))
@@ -495,6 +530,7 @@ def main():
     peak_sus, peak_burst = fp64_peak()
     gflops_exec = (st["flops_update"] + st["flops_chase"]) / (ms * 1e-3) / 1e9
 
+    chase = None
     if world == 1:
         # per-kernel CUDA-event times: the same sweep in profiling mode (events around every launch)
         hq.teardown()
@@ -538,6 +574,7 @@ def main():
                     "avg_launch_ms": upd_ms / max(1, upd_launches),
                     "share_of_step": upd_ms / max(1e-9, ps["ms_chase"] + upd_ms),
                     "ms_chase_only_launches": ps["ms_chase"], "ms_kernel_total": upd_ms}
+        chase = chase_line(hq, n, prob, nshifts, args, ps["ms_chase"], clocks, ms)
     else:
         # per-rank GEMM flops over the whole sweep time (lower bound of the kernels' own rate)
         fl = torch.tensor([st["flops_update"]], device=dev, dtype=torch.float64)
@@ -595,7 +632,7 @@ def main():
             "gflops_dmma": st["flops_dmma"] / (ms * 1e-3) / 1e9 if world == 1 else None,
             "frac_fp64_peak_dmma": st["flops_dmma"] / (ms * 1e-3) / 1e12 / peak_sus if world == 1 else None,
             "flops_dense_over_alg": (st["flops_update"] + st["flops_chase"]) / fa,
-            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
+            "roofline": roofline, "chase": chase, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
             "gpu_launches": launches, "steps_per_sweep": st["steps"], "windows_per_sweep": st["windows"],
             "input_gen_s": gen_s,
             "sequential_sweeps_ms": sequential_ms,
