@@ -313,6 +313,9 @@ typedef struct hqr_stats {
   double flops_alg;           /* design-independent F_alg (every reflector applied directly, SURVEY
                                  Appendix B) of the last call's sweeps; hqr_qr_iterate: summed over
                                  its sweeps                                                          */
+  int crit_sms;               /* CTAs of the persistent launch that served only the critical queue
+                                 (chases and their near tiles; 0: one queue) -- DESIGN.md §6        */
+  int pad_;
 } hqr_stats;
 
 int hqr_get_stats(hqr_stats* out);

@@ -62,7 +62,8 @@ class Stats(ctypes.Structure):
                 ("h2d_bytes", ctypes.c_int64), ("d2h_bytes", ctypes.c_int64),
                 ("launches_left", ctypes.c_int), ("launches_right", ctypes.c_int),
                 ("launches_chase", ctypes.c_int), ("window_eff", ctypes.c_int),
-                ("flops_dmma", ctypes.c_double), ("flops_alg", ctypes.c_double)]
+                ("flops_dmma", ctypes.c_double), ("flops_alg", ctypes.c_double),
+                ("crit_sms", ctypes.c_int), ("pad_", ctypes.c_int)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

@@ -825,9 +825,14 @@ int enqueue_fused(CachedPlan& cp, double* H, double* Z, int64_t n, const hqr::Te
     // one persistent launch for the whole sweep: step g+1's work starts as soon as its own
     // dependencies are met (no launch boundary, no end-of-step tail)
     mark(3);
+    int csms = crit_sms(P, *f);
+    if (csms >= std::max(1, std::min((int)f->tasks.size(), g.num_sms)) || f->ncrit <= 0 ||
+        f->ncrit >= (int)f->tasks.size())
+      csms = 0;  // (launch_step's own rule: both queues need CTAs and tasks)
+    st->crit_sms = csms;
     CK(hqr::launch_step(base, f->d_steps, P.nsteps, f->d_tasks, (int)f->tasks.size(), 0, f->d_dep_begin,
                         f->d_deps, f->d_ctr, step_ctr, task_ctr, io ? io->d_flags : nullptr, tm, P.max_kw,
-                        g.num_sms, A, f->d_qidx, f->ncrit, crit_sms(P, *f)));
+                        g.num_sms, A, f->d_qidx, f->ncrit, csms));
     mark(-1);
     st->launches_left++;
     if (io) {
@@ -1188,6 +1193,7 @@ int sweep_impl(double* H, double* Z, int64_t n, const Blocks& blocks, const doub
     st.steps = c.steps;
     st.windows = c.windows;
     st.kernels_launched = c.kernels_launched;
+    st.crit_sms = c.crit_sms;
   } else if (fused) {
     rc = enqueue_fused(*cp, dH, dZ, n, tmf, &st, prof, &classes);
     if (rc) return rc;

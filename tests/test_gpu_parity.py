@@ -590,3 +590,18 @@ def test_overlapped_sweeps_parity(n, ilo, ihi, sweeps, win):
         oracle.sweep(Ho, Zo, ilo, ihi, re_, im_)
     check(Hg, Zg, Ho, Zo, H0, ilo, ihi)
     assert np.array_equal(hq.aftermath(n), oracle.subdiag_scan(Hg, [(ilo, ihi)]))
+
+
+@pytest.mark.parametrize("n,ns,crit", [(1500, 64, True), (2000, 600, False)])
+def test_critical_queue_and_single_queue_parity(n, ns, crit):
+    """The persistent launch's two task-claiming modes (DESIGN.md §6 "Critical SMs"): a chase-bound
+    sweep serves chases and their near tiles from a dedicated critical queue on 2*nchains+2 CTAs
+    (hqr_stats.crit_sms > 0), a GEMM-bound one keeps one queue (0); both match the oracle.  (Shifts
+    from a small disk: many shifts near the spectrum converge subdiagonals during the sweep and put
+    the oracle's own floor above 1e-10, reading R14.)"""
+    H0, Z0, re_, im_ = random_case(93, n, ns, z0="orth", shift_kind="disk2")
+    Hg, Zg = gpu_sweep(H0, Z0, 0, n - 1, re_, im_, 96)
+    st = hq.stats()
+    assert (st["crit_sms"] > 0) == crit, st["crit_sms"]
+    Ho, Zo = oracle_sweep(H0, Z0, 0, n - 1, re_, im_)
+    check(Hg, Zg, Ho, Zo, H0, 0, n - 1)
