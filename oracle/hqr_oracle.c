@@ -439,8 +439,35 @@ static int make_shifts(const double* wr, const double* wi, int64_t m, int ns, do
 /* The QR iteration on H (n x n, active block [ilo, ihi]) with Z: until every unreduced block is at
  * most nmin long, sweep the bottom unreduced block [l, hi] with the eigenvalues of its trailing
  * nshifts x nshifts block as shifts (oracle_sweep), then set negligible subdiagonals (R16) to zero;
- * the eigenvalues of the remaining small blocks by oracle_small_eig.  wr / wi: n entries (rows
- * outside [ilo, ihi] untouched).  Returns 0, or -(sweeps) when max_sweeps was reached. */
+ * the remaining small blocks in real Schur form (small_block_schur, R24), so H ends quasi-triangular.
+ * wr / wi: n entries (rows outside [ilo, ihi] untouched).  Returns 0, or -(sweeps) when max_sweeps
+ * was reached. */
+int oracle_aed(double* H, double* Z, int64_t n, int64_t ilo, int64_t k0, int nw, double thr, double* wr,
+               double* wi, double* swr, double* swi, int* nund);
+
+/* A small unreduced block [l, hi] (N = hi-l+1 rows, h(l, l-1) = 0) at the end of the QR iteration, in
+ * real Schur form (reading R24: LAPACK's wantt / wantz): N = 1 is its own eigenvalue; 2 <= N <= 112
+ * (the GPU's one-CTA window) goes through oracle_aed on the window [l, hi] with l as the block start,
+ * so the spike is zero and every block deflates -- T (real Schur form) written back, its factor
+ * applied to the rest of H and to Z; larger blocks: the eigenvalues only (oracle_small_eig). */
+static void small_block_schur(double* H, double* Z, int64_t n, int64_t l, int64_t hi, double* B, double* wr,
+                              double* wi) {
+  const int64_t N = hi - l + 1;
+  if (N == 1) {
+    wr[l] = EL(H, l, l, n);
+    wi[l] = 0.0;
+  } else if (N <= 112) {
+    double* sw = (double*)malloc(sizeof(double) * 2 * (size_t)N);
+    int nund = 0;
+    oracle_aed(H, Z, n, l, l, (int)N, 0.0, wr, wi, sw, sw + N, &nund);
+    free(sw);
+  } else {
+    for (int64_t c = 0; c < N; ++c)
+      for (int64_t r = 0; r < N; ++r) B[r + c * N] = EL(H, l + r, l + c, n);
+    oracle_small_eig(B, N, N, wr + l, wi + l);
+  }
+}
+
 int oracle_qr_iterate(double* H, double* Z, int64_t n, int64_t ilo, int64_t ihi, int nshifts, int64_t nmin,
                       int max_sweeps, double* wr, double* wi, int* sweeps_out) {
   int sweeps = 0;
@@ -451,10 +478,7 @@ int oracle_qr_iterate(double* H, double* Z, int64_t n, int64_t ilo, int64_t ihi,
     while (l > ilo && EL(H, l, l - 1, n) != 0.0) --l;
     const int64_t N = hi - l + 1;
     if (N <= nmin) {
-      double* B = work;
-      for (int64_t c = 0; c < N; ++c)
-        for (int64_t r = 0; r < N; ++r) B[r + c * N] = EL(H, l + r, l + c, n);
-      oracle_small_eig(B, N, N, wr + l, wi + l);
+      small_block_schur(H, Z, n, l, hi, work, wr, wi);
       hi = l - 1;
       continue;
     }
@@ -871,9 +895,7 @@ int oracle_qr_iterate_aed(double* H, double* Z, int64_t n, int64_t ilo, int64_t 
     while (l > ilo && EL(H, l, l - 1, n) != 0.0) --l;
     const int64_t N = hi - l + 1;
     if (N <= nmin) {
-      for (int64_t c = 0; c < N; ++c)
-        for (int64_t r = 0; r < N; ++r) B[r + c * N] = EL(H, l + r, l + c, n);
-      oracle_small_eig(B, N, N, wr + l, wi + l);
+      small_block_schur(H, Z, n, l, hi, B, wr, wi);
       hi = l - 1;
       continue;
     }

@@ -69,6 +69,23 @@ def test_small_eig_deflated_and_2x2_blocks():
     assert info == 0 and _match(wr + 1j * wi, [1 + 2j, 1 - 2j, 7, 3, -1]) <= 1e-14
 
 
+def _assert_real_schur(H, wr, wi):
+    n = H.shape[0]
+    sub = np.diag(H, -1)
+    assert np.all(np.tril(H, -2) == 0.0)
+    assert not np.any((sub[:-1] != 0.0) & (sub[1:] != 0.0))  # no 3x3 or larger blocks
+    lam = []
+    j = 0
+    while j < n:
+        if j + 1 < n and H[j + 1, j] != 0.0:
+            lam += list(np.linalg.eigvals(H[j:j + 2, j:j + 2]))
+            j += 2
+        else:
+            lam.append(H[j, j])
+            j += 1
+    assert _match(np.array(lam), wr + 1j * wi) <= 1e-9
+
+
 @pytest.mark.parametrize("n,ns,nmin,seed", [(10, 2, 2, 5), (60, 8, 8, 6), (300, 16, 32, 7)])
 def test_qr_iterate_eigenvalues_similarity(n, ns, nmin, seed):
     H0, Z0, _, _ = random_case(seed, n, 2, z0="orth")
@@ -82,9 +99,9 @@ def test_qr_iterate_eigenvalues_similarity(n, ns, nmin, seed):
     assert abs(np.sum(wr) - np.trace(H0)) <= 1e-10 * n * np.linalg.norm(H0)
     assert np.linalg.norm(Z.T @ Z - np.eye(n)) <= 1e-13 * n
     assert np.linalg.norm(Z @ H @ Z.T - Z0 @ H0 @ Z0.T) <= 1e-13 * n * np.linalg.norm(H0)
-    # H is reduced to unreduced blocks of at most nmin rows
-    zeros = [0] + [k for k in range(1, n) if H[k, k - 1] == 0.0] + [n]
-    assert max(b - a for a, b in zip(zeros, zeros[1:])) <= nmin
+    # H ends in real Schur form (R24): quasi-triangular, and the reported eigenvalues are those of
+    # its 1x1 / 2x2 diagonal blocks
+    _assert_real_schur(H, wr, wi)
 
 
 # --------------------------------------------------------------------------------------------
@@ -156,6 +173,7 @@ def test_qr_iterate_aed(n, ns, nw, nmin, seed):
     hn = np.linalg.norm(p.H)
     assert np.linalg.norm(Z @ H @ Z.T - p.Z @ p.H @ p.Z.T) <= 1e-13 * n * hn
     assert abs(np.sum(wr) - np.trace(p.H)) <= 1e-10 * n * hn
+    _assert_real_schur(H, wr, wi)
     if n >= 100:  # AED pays: fewer sweeps than the iteration without it, most eigenvalues by AED
         H2 = p.H.copy(order="F")
         _, _, _, sweeps_plain = oracle.qr_iterate(H2, None, 0, n - 1, ns, nmin=nmin)
