@@ -2015,7 +2015,9 @@ int hqr_qr_iterate(double* H, double* Z, int64_t n, int64_t ilo, int64_t ihi, in
   CK(cudaSetDevice(g.device));
   if (!is_device_ptr(H) || (Z && !is_device_ptr(Z))) return -1;
   const int SM = hqr::small_eig_max();
-  const int KPa = hqr::padded_kp(std::max(aed_window, 2)), QLDa = hqr::pad_ld(KPa);
+  // the AED factor slot also serves the small blocks left at the end (R24: up to kMaxWindow rows)
+  const int KPa = hqr::padded_kp(std::max({aed_window, std::min(nmin, hqr::kMaxWindow), 2})),
+            QLDa = hqr::pad_ld(KPa);
   // scratch: eigenvalues (2 SM), AED eigenvalues (2 kMaxWindow), ||H||^2, ints, the AED factor slot,
   // the AED window descriptor
   const size_t nscr = 2 * (size_t)SM + 2 * (size_t)hqr::kMaxWindow + 8 + (size_t)KPa * QLDa + 16;
@@ -2046,7 +2048,7 @@ int hqr_qr_iterate(double* H, double* Z, int64_t n, int64_t ilo, int64_t ihi, in
     thr = 0x1p-53 * std::sqrt(fro2);
   }
   hqr::TensorMaps tma;
-  if (aed_window > 0) {
+  {
     cudaError_t e = hqr::make_tensor_maps(&tma, H, n, Z, n, n, n, KPa);
     if (e != cudaSuccess) return fail(cuerr(e));
   }
@@ -2061,7 +2063,31 @@ int hqr_qr_iterate(double* H, double* Z, int64_t n, int64_t ilo, int64_t ihi, in
       while (l > ilo && sub[(size_t)(l - 1 - ilo)] != 0.0) --l;
     }
     const int64_t N = hi - l + 1;
-    if (N <= nmin) {  // small block: its eigenvalues directly
+    if (N <= nmin) {  // small block: real Schur form (R24), its eigenvalues from the diagonal blocks
+      if (N == 1) {
+        cudaError_t e = cudaMemcpy(wr + l, H + l + l * n, sizeof(double), cudaMemcpyDeviceToHost);
+        if (e != cudaSuccess) return fail(cuerr(e));
+        wi[l] = 0.0;
+        hi = l - 1;
+        continue;
+      }
+      if (N <= hqr::kMaxWindow) {
+        // the AED window machinery with the block's first row as the window start: the spike is
+        // zero, every block deflates (threshold 0), T and U are applied to the rest of H and to Z
+        int nd = 0, m = 0;
+        cudaError_t e = aed_step(H, Z, n, l, hi, (int)N, 0.0, d_uslot, KPa, QLDa, d_ew, d_ei, d_info + 2, d_wd, tma,
+                                 ewr.data(), ewi.data(), &nd, &m);
+        if (e != cudaSuccess) return fail(cuerr(e));
+        if (nd == N) {
+          for (int j = 0; j < N; ++j) {
+            wr[l + j] = ewr[j];
+            wi[l + j] = ewi[j];
+          }
+          hi = l - 1;
+          continue;
+        }
+        // (not converged: H unchanged, the eigenvalue-only solver below)
+      }
       cudaError_t e = hqr::launch_small_eig(H, n, l, (int)N, d_w, d_w + SM, d_info, g.stream);
       if (e == cudaSuccess) e = cudaMemcpyAsync(wr + l, d_w, N * sizeof(double), cudaMemcpyDeviceToHost, g.stream);
       if (e == cudaSuccess) e = cudaMemcpyAsync(wi + l, d_w + SM, N * sizeof(double), cudaMemcpyDeviceToHost, g.stream);

@@ -35,13 +35,16 @@ def _match(a, b):
 
 @pytest.mark.parametrize("n,seed", [(3, 0), (8, 1), (40, 2), (127, 3), (128, 4)])
 def test_small_block_solver(n, seed):
-    """A block of at most nmin rows goes straight to the one-CTA Francis QR solver."""
+    """A block of at most nmin rows goes straight to the small-block path: real Schur form through the
+    AED window machinery up to 112 rows (R24), the one-CTA Francis QR eigenvalue solver above."""
     H0, _, _, _ = random_case(seed, n, 2)
     Hd = hq.to_device(H0)
     wr, wi, rc, sweeps = hq.qr_iterate(Hd, None, 0, n - 1, nshifts=2, nmin=128)
     assert rc == 0 and sweeps == 0
     owr, owi, info = oracle.small_eig(H0)
     assert info == 0 and _match(wr + 1j * wi, owr + 1j * owi) <= 1e-10
+    if n <= 112:
+        _assert_real_schur(hq.from_device(Hd), wr, wi)
     for k in range(n):
         if wi[k] > 0:
             assert wr[k + 1] == wr[k] and wi[k + 1] == -wi[k]
@@ -62,8 +65,7 @@ def test_qr_iteration_vs_oracle(n, ns, nmin, win, seed):
     assert np.linalg.norm(Z.T @ Z - np.eye(n)) <= 1e-13 * n
     assert np.linalg.norm(Z @ H @ Z.T - Z0 @ H0 @ Z0.T) <= 1e-13 * n * hn
     assert np.all(np.tril(H, -2) == 0.0)
-    zeros = [0] + [k for k in range(1, n) if H[k, k - 1] == 0.0] + [n]
-    assert max(b - a for a, b in zip(zeros, zeros[1:])) <= nmin
+    _assert_real_schur(H, wr, wi)  # R24: the small blocks end in real Schur form
     # the sweep counts are of the same order (the trajectories differ by rounding)
     assert 0.5 * osw <= sweeps <= 2.0 * osw
 
@@ -88,11 +90,29 @@ def test_qr_iteration_with_aed_vs_oracle(n, ns, aed, nmin, win, seed):
     hn = np.linalg.norm(p.H)
     assert np.linalg.norm(Z.T @ Z - np.eye(n)) <= 1e-13 * n
     assert np.linalg.norm(Z @ H @ Z.T - p.Z @ p.H @ p.Z.T) <= 1e-13 * n * hn
-    assert np.all(np.tril(H, -2) == 0.0)
+    _assert_real_schur(H, wr, wi)
     assert st["window_eff"] > n // 2                      # eigenvalues deflated by AED
     Hd2 = hq.to_device(p.H)
     _, _, _, sweeps_plain = hq.qr_iterate(Hd2, None, 0, n - 1, nshifts=ns, window=win, nmin=nmin)
     assert sweeps < sweeps_plain
+
+
+def _assert_real_schur(H, wr, wi):
+    """Quasi-triangular H (no two consecutive nonzero subdiagonals) whose 1x1 / 2x2 diagonal blocks
+    carry the reported eigenvalues (R24)."""
+    n = H.shape[0]
+    sub = np.diag(H, -1)
+    assert np.all(np.tril(H, -2) == 0.0)
+    assert not np.any((sub[:-1] != 0.0) & (sub[1:] != 0.0))
+    lam, j = [], 0
+    while j < n:
+        if j + 1 < n and H[j + 1, j] != 0.0:
+            lam += list(np.linalg.eigvals(H[j:j + 2, j:j + 2]))
+            j += 2
+        else:
+            lam.append(H[j, j])
+            j += 1
+    assert _match(np.array(lam), wr + 1j * wi) <= 1e-9
 
 
 def _aed_problem(W, s, above, rng):
