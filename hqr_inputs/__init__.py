@@ -185,6 +185,21 @@ def make(cfg_idx: int, z_device: str = "cpu", n_override: int | None = None,
     return Problem(H, Z, 0, n - 1, np.concatenate(res), np.concatenate(ims), c.window, blocks)
 
 
+def config4_block(b: int, H: np.ndarray | None = None, shift_kind: str | None = None):
+    """Diagonal block b of BASELINE configs[4] as a problem of its own: (H_bb copy, shifts_re,
+    shifts_im, (lo, hi)).  The blocks are decoupled, so one sweep of the whole matrix acts on H_bb
+    exactly as a sweep of H_bb alone with Z = I (Z(:, block) = its factor).  H: the full configs[4]
+    matrix if already materialised (else it is generated); shift_kind: another shift distribution
+    (e.g. "ring68") for every block."""
+    c = CONFIGS[4]
+    if H is None:
+        H = hessenberg(c.n, c.upper, c.idx, blocks=c.blocks)
+    bs = c.n // c.blocks
+    lo, hi = b * bs, b * bs + bs - 1
+    re, im = shifts(shift_kind or c.shifts, c.nshifts, c.idx, stream_offset=b)
+    return np.asfortranarray(H[lo:hi + 1, lo:hi + 1]), re, im, (lo, hi)
+
+
 HESS_CFG = 5  # seed-space id of the hess_n workload (SURVEY §8(f) NEXT-3)
 
 

@@ -13,7 +13,14 @@ from hqr_inputs import make  # noqa: E402
 
 
 def main(cfg, shift_kind=None):
-    p = make(cfg, shift_kind=shift_kind)
+    if cfg == 4:  # "4:b<k>": diagonal block k of configs[4] alone, Z = I (the blocks are decoupled)
+        from types import SimpleNamespace
+        from hqr_inputs import config4_block
+        Hb, re_, im_, _ = config4_block(int(shift_kind[1:]))
+        nb = Hb.shape[0]
+        p = SimpleNamespace(H=Hb, Z=np.asfortranarray(np.eye(nb)), ilo=0, ihi=nb - 1, shifts_re=re_, shifts_im=im_)
+    else:
+        p = make(cfg, shift_kind=shift_kind)
     n = p.H.shape[0]
     t0 = time.time()
     Hs, Zs = p.H.copy(order="F"), p.Z.copy(order="F")
@@ -35,7 +42,8 @@ def main(cfg, shift_kind=None):
 
 
 if __name__ == "__main__":
-    # arguments: "3" (configs[3] as specified) or "3:ring68" (configs[3] with another shift set)
+    # arguments: "3" (configs[3] as specified), "3:ring68" (configs[3] with another shift set) or
+    # "4:b2" (diagonal block 2 of configs[4], swept alone with Z = I)
     for c in sys.argv[1:]:
         cfg, _, kind = c.partition(":")
         main(int(cfg), kind or None)
