@@ -59,7 +59,7 @@ __device__ __forceinline__ void produce_tile(double* dst, uint64_t* full, const 
 
 // K steps [ks, ke) of one warp, multiplying only the Q_W column blocks F..L of its quarter (LEFT:
 // fragment rows i, RIGHT: fragment columns jn); software-pipelined: the fragments of k-step k+4 are
-// loaded before the DMMAs of step k.
+// loaded before the DMMAs of step k.  The extents are multiples of 4 (store_q_slot).
 template <int FM, int FN, bool LEFT, int F, int L>
 __device__ __forceinline__ void kseg(double (&acc)[FN][FM][2], const double* A, int a_i, int a_k,
                                      const double* B, int b_j, int b_k, int ks, int ke) {
@@ -80,17 +80,26 @@ __device__ __forceinline__ void kseg(double (&acc)[FN][FM][2], const double* A, 
     for (int jn = J0; jn <= J1; ++jn) fb[h][jn] = B[jn * b_j + k * b_k];
   };
   load(0, ks);
-  for (int kk = ks; kk < ke; kk += 8) {
+  // an odd k-step count peels one step; then branch-free pairs (a data-dependent exit inside the
+  // pair made every pair a WARPSYNC + branch: tools/tile_ceiling.cu, in-tile executed DMMA rate
+  // 31.9 -> 34.4 TF/s)
+  auto mul = [&](int h) {
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int k = kk + 4 * h;
-      if (k >= ke) break;
-      if (k + 4 < ke) load(h ^ 1, k + 4);
+    for (int jn = J0; jn <= J1; ++jn)
 #pragma unroll
-      for (int jn = J0; jn <= J1; ++jn)
-#pragma unroll
-        for (int i = I0; i <= I1; ++i) dmma(acc[jn][i], fb[h][jn], fa[h][i]);
-    }
+      for (int i = I0; i <= I1; ++i) dmma(acc[jn][i], fb[h][jn], fa[h][i]);
+  };
+  int kk = ks;
+  if ((ke - ks) & 4) {
+    mul(0);
+    kk += 4;
+    if (kk < ke) load(0, kk);
+  }
+  for (; kk < ke; kk += 8) {
+    load(1, kk + 4);
+    mul(0);
+    if (kk + 8 < ke) load(0, kk + 8);
+    mul(1);
   }
 }
 
