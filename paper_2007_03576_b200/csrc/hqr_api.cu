@@ -1837,10 +1837,21 @@ int hqr_qz_sweep(double* H, double* T, double* Q, double* Z, int64_t n, int64_t 
   CK(hqr::make_tensor_maps(&tmB, T, n, Z, n, n, n, KP));
   hqr_stats st{};
   st.window_eff = P.k;
-  // Stream A: chase -> left (H, T) -> right (H, T) per step (the next chase reads their results);
-  // stream B (low priority): Qacc Q_W and Zacc Z_W, which nothing reads, trailing A
-  // by up to kQSets - 1 steps (rotating slot sets).  Captured once per (plan, pointers) into a CUDA
-  // graph and replayed.
+  // Stream A: chase -> left (H, T) -> near-right (H, T: rows [sp, w0)) per step (the next chase
+  // reads their results); stream B (low priority): the far-right rows [0, sp) of H and T, Qacc Q_W
+  // and Zacc Z_W, which no later chase, left or near-right update reads,
+  // started after the step's left updates (a far-right block of W meets the left update of a window
+  // above it in the same step) and trailing A by up to kQSets - 1 steps (rotating slot sets).
+  // sp(s) = the smallest first row of any later window, even (as the fused QR kernel's split).
+  // Captured once per (plan, pointers) into a CUDA graph and replayed.
+  std::vector<int64_t> sp(P.nsteps, 0);
+  {
+    int64_t run = n;
+    for (int s = P.nsteps - 1; s >= 0; --s) {
+      sp[s] = run & ~(int64_t)1;
+      for (int i = P.step_begin[s]; i < P.step_begin[s + 1]; ++i) run = std::min<int64_t>(run, P.windows[i].w0);
+    }
+  }
   auto enqueue = [&](hqr_stats* sts) -> int {
     cudaStream_t A = g.stream, Bs = g.zstream;
     CK(cudaEventRecord(g.ev_fork, A));
@@ -1869,14 +1880,24 @@ int hqr_qz_sweep(double* H, double* T, double* Q, double* Z, int64_t n, int64_t 
       CK(cudaStreamWaitEvent(g.qzs[0], g.qz_fork, 0));
       CK(hqr::launch_left(aH, hw, g.num_sms, tmA, A, &items, &fl, &by)); acc(&sts->launches_left);
       CK(hqr::launch_left(aT, hw, g.num_sms, tmB, g.qzs[0], &items, &fl, &by)); acc(&sts->launches_left);
-      aHz.right_mode = 1;
-      CK(hqr::launch_right(aHz, hw, g.num_sms, tmA, A, &items, &fl, &by)); acc(&sts->launches_right);
-      aTz.right_mode = 1;
-      CK(hqr::launch_right(aTz, hw, g.num_sms, tmB, g.qzs[0], &items, &fl, &by)); acc(&sts->launches_right);
+      CK(cudaEventRecord(g.qz_join[1], g.qzs[0]));  // the step's left updates, for B
+      CK(cudaEventRecord(g.ev_q[set], A));
+      StepArgs aHn = aHz, aTn = aTz;
+      aHn.right_mode = 1; aHn.rrow_lo = sp[s]; aHn.rrow_hi = n;  // rows [sp, w0)
+      CK(hqr::launch_right(aHn, hw, g.num_sms, tmA, A, &items, &fl, &by)); acc(&sts->launches_right);
+      aTn.right_mode = 1; aTn.rrow_lo = sp[s]; aTn.rrow_hi = n;
+      CK(hqr::launch_right(aTn, hw, g.num_sms, tmB, g.qzs[0], &items, &fl, &by)); acc(&sts->launches_right);
       CK(cudaEventRecord(g.qz_join[0], g.qzs[0]));
       CK(cudaStreamWaitEvent(A, g.qz_join[0], 0));
-      CK(cudaEventRecord(g.ev_q[set], A));
       CK(cudaStreamWaitEvent(Bs, g.ev_q[set], 0));
+      CK(cudaStreamWaitEvent(Bs, g.qz_join[1], 0));
+      if (sp[s] > 0) {  // far-right rows [0, sp) (rrow_hi = 0 would mean all rows)
+        aHz.right_mode = 1; aHz.rrow_lo = 0; aHz.rrow_hi = sp[s];
+        CK(hqr::launch_right(aHz, hw, g.num_sms, tmA, Bs, &items, &fl, &by)); acc(&sts->launches_right);
+        StepArgs aTf = aTz;
+        aTf.Z = nullptr; aTf.right_mode = 1; aTf.rrow_lo = 0; aTf.rrow_hi = sp[s];
+        CK(hqr::launch_right(aTf, hw, g.num_sms, tmB, Bs, &items, &fl, &by)); acc(&sts->launches_right);
+      }
       if (Q) {
         aH.right_mode = 2;
         CK(hqr::launch_right(aH, hw, g.num_sms, tmA, Bs, &items, &fl, &by)); acc(&sts->launches_right);

@@ -38,6 +38,7 @@ __global__ void __launch_bounds__(416) ceil_k(const double* qsrc, const double* 
   for (int r = 0; r < reps; ++r) {
     const int qq = rotate ? (i4 + r + q) & 3 : i4;
     consume_tile<KP, LEFT>(Qs, Ps + q * SS, &empty[q], t, qq, lane);
+    if (rotate == 2) named_sync(1 + q, 128);  // a group's warps in lock step (the ring's coupling, tight)
   }
 }
 
@@ -76,9 +77,9 @@ int main(int argc, char** argv) {
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
-  for (int mode = 0; mode < 4; ++mode) {
-    const bool left = mode < 2;
-    const int rot = mode & 1;
+  for (int mode = 0; mode < 6; ++mode) {
+    const bool left = mode % 2 == 0;
+    const int rot = mode / 2 == 0 ? 0 : mode / 2 == 1 ? 1 : 2;
     auto launch = [&]() {
       if (left) ceil_k<true><<<sms, 416, smem>>>(dq, dp, dout, reps, rot);
       else ceil_k<false><<<sms, 416, smem>>>(dq, dp, dout, reps, rot);
@@ -95,7 +96,7 @@ int main(int argc, char** argv) {
     const double tile_fl = units * 8.0 * 32.0 * 2.0;
     const double fl = (double)sms * 3 * reps * tile_fl;
     printf("{\"tile\": \"%s\", \"quarters\": \"%s\", \"nbc\": %d, \"exec_frac\": %.3f, \"ms\": %.3f, "
-           "\"exec_tflops\": %.2f, \"err\": \"%s\"}\n", left ? "left" : "right", rot ? "rotating" : "fixed",
+           "\"exec_tflops\": %.2f, \"err\": \"%s\"}\n", left ? "left" : "right", rot == 0 ? "fixed" : rot == 1 ? "rotating" : "rotating, group lock step",
            nbc, units * 8.0 / (KP * KP), ms, fl / (ms * 1e-3) / 1e12, cudaGetErrorString(cudaGetLastError()));
   }
   return 0;
