@@ -76,8 +76,10 @@ int hqr_setup(const hqr_config* cfg);
  * One multishift QR sweep, in place.  Synchronous: returns after the device has finished.
  *   H         [in,out] n x n column-major; device pointer, or host pointer (pinned or pageable, in
  *                      which case the library stages it through its own device memory and the
- *                      host<->device copies are part of the call).  Must be upper Hessenberg on
- *                      [ilo, ihi] with H[ilo, ilo-1] == 0 (ilo > 0) and H[ihi+1, ihi] == 0 (ihi < n-1).
+ *                      host<->device copies are part of the call).  Must be upper Hessenberg (zero
+ *                      below the first subdiagonal; a host H is uploaded by row chunks from the
+ *                      subdiagonal on, and entries below it may come back as zeros) with
+ *                      H[ilo, ilo-1] == 0 (ilo > 0) and H[ihi+1, ihi] == 0 (ihi < n-1).
  *   Z         [in,out] n x n column-major (device or host), or NULL to skip Z <- Z Q.
  *   n         matrix order, n >= 1
  *   ilo, ihi  active block [ilo, ihi], 0 <= ilo <= ihi < n, N = ihi - ilo + 1 >= 3

@@ -219,6 +219,7 @@ struct State {
   double* d_hstage = nullptr;
   double* d_zstage = nullptr;
   size_t stage_cap = 0;
+  int64_t hstage_zero_n = -1;  // d_hstage is zero below the subdiagonal of the n x n layout (overlapped uploads)
   std::map<PlanKey, std::unique_ptr<CachedPlan>> plans;
   std::map<GraphKey, CachedGraph> graphs;
   std::vector<cudaEvent_t> prof_events;
@@ -679,7 +680,9 @@ int stream_value_fns(StreamValueFn* wr, StreamValueFn* wt) {
 // (StepInfo::up_need).  Column c of H and Z is final once every step that touches it is done (every
 // later window starts below c), so a second copy stream waits for the steps' completion counters
 // (cuStreamWaitValue32) and copies finished column chunks down during the sweep; of H only the
-// rows [0, c + 2) of column c come back (below them the matrix is Hessenberg: zero in and out).
+// rows [0, c1 + 1) of a column chunk [c0, c1) come back, and of a row chunk [r, r + 512) only the
+// columns [r - 1, n) go up (below the subdiagonal H is zero in and out: those entries are zeroed on
+// the device, never read from the caller's buffer).
 struct IoPlan {
   double* Hh = nullptr;  // caller's host H (nullptr: H is device-resident)
   double* Zh = nullptr;  // caller's host Z (nullptr: device-resident or absent)
@@ -707,12 +710,29 @@ struct IoPlan {
     const size_t col = (size_t)n * sizeof(double);
     CK(cudaStreamWaitEvent(g.cin, g.ev0, 0));
     CK(cudaMemsetAsync(d_flags, 0, (size_t)nchunks() * sizeof(int), g.cin));
+    h2d = 0;
+    // zeros below the subdiagonal of the staging buffer: set once per (buffer, n) and kept (the sweep
+    // writes exact zeros there), all before the first copy -- a memset is a kernel, and a kernel
+    // queued behind the copies the running sweep waits for could not find an SM
+    if (Hh && g.hstage_zero_n != n) {
+      for (int64_t k = 1; k < nchunks(); ++k) {
+        const int64_t c = k * chunk, w = std::min(chunk, n - c);
+        CK(cudaMemset2DAsync(dH + c, col, 0, (size_t)w * sizeof(double), (size_t)(c - 1), g.cin));
+      }
+      g.hstage_zero_n = n;
+    }
     for (int64_t k = 0; k < nchunks(); ++k) {
       const int64_t c = k * chunk, w = std::min(chunk, n - c);
-      if (Hh)  // rows [c, c + w) of every column
-        CK(cudaMemcpy2DAsync(dH + c, col, Hh + c, col, (size_t)w * sizeof(double), (size_t)n,
-                             cudaMemcpyHostToDevice, g.cin));
-      if (Zh) CK(cudaMemcpyAsync(dZ + c * n, Zh + c * n, col * w, cudaMemcpyHostToDevice, g.cin));
+      if (Hh) {  // rows [c, c + w): columns [c - 1, n) up (below them: the zeros above)
+        const int64_t j0 = std::max<int64_t>(c - 1, 0);
+        CK(cudaMemcpy2DAsync(dH + c + j0 * n, col, Hh + c + j0 * n, col, (size_t)w * sizeof(double),
+                             (size_t)(n - j0), cudaMemcpyHostToDevice, g.cin));
+        h2d += w * (n - j0) * (int64_t)sizeof(double);
+      }
+      if (Zh) {
+        CK(cudaMemcpyAsync(dZ + c * n, Zh + c * n, col * w, cudaMemcpyHostToDevice, g.cin));
+        h2d += (int64_t)(col * w);
+      }
       CU(write_value((CUstream)g.cin, (CUdeviceptr)(d_flags + k), 1, 0));
       if (c <= first_rows && first_rows < c + w) {  // chase(0) is a separate launch: an event
         cudaEvent_t e = io_event(0);
@@ -720,7 +740,6 @@ struct IoPlan {
         CK(cudaStreamWaitEvent(A, e, 0));
       }
     }
-    h2d = (int64_t)(col * n) * ((Hh ? 1 : 0) + (Zh ? 1 : 0));
     return 0;
   }
   int down(int64_t c0, int64_t c1) {  // finished columns [c0, c1) to the host (on cout)
@@ -987,6 +1006,7 @@ int hqr_teardown(void) {
   if (g.d_zstage) cudaFree(g.d_zstage);
   g.d_coef = g.d_q = g.d_hstage = g.d_zstage = nullptr;
   g.coef_cap = g.q_cap = g.stage_cap = 0;
+  g.hstage_zero_n = -1;
   cudaEventDestroy(g.ev0);
   cudaEventDestroy(g.ev1);
   cudaEventDestroy(g.ev_in);
@@ -1112,6 +1132,7 @@ int sweep_impl(double* H, double* Z, int64_t n, const Blocks& blocks, const doub
       if (g.d_zstage) CK(cudaFree(g.d_zstage));
       g.d_hstage = g.d_zstage = nullptr;
       g.stage_cap = 0;
+      g.hstage_zero_n = -1;
       CK(cudaMalloc(&g.d_hstage, need * sizeof(double)));
       CK(cudaMalloc(&g.d_zstage, need * sizeof(double)));
       g.stage_cap = need;
@@ -1140,6 +1161,7 @@ int sweep_impl(double* H, double* Z, int64_t n, const Blocks& blocks, const doub
     if (!h_dev) {
       CK(cudaMemcpyAsync(dH, H, nn * sizeof(double), cudaMemcpyHostToDevice, g.stream));
       st.h2d_bytes += nn * sizeof(double);
+      g.hstage_zero_n = -1;  // the caller's entries below the subdiagonal are in the buffer now
     }
     if (Z && !z_dev) {
       CK(cudaMemcpyAsync(dZ, Z, nn * sizeof(double), cudaMemcpyHostToDevice, g.stream));
