@@ -40,6 +40,7 @@ struct TileRef {
   int w0, kw, nbc;
   double* M;
   int64_t c0, lc1;   // LEFT
+  int64_t lcs;       // LEFT: first column stored (columns [c0, lcs) are multiplied, not stored)
   int64_t r0, r1;    // RIGHT
   int64_t ld, cb;    // M's leading dimension and column base (LEFT: n, hcol0)
   bool isZ;
@@ -201,7 +202,7 @@ __device__ __forceinline__ void consume_tile(const double* Qs, const double* P, 
 #pragma unroll
     for (int jn = 0; jn < FN; ++jn) {
       const int64_t col = t.c0 + 8 * jn + lr;
-      if (col >= t.lc1) continue;
+      if (col < t.lcs || col >= t.lc1) continue;
       double* cp = t.M + (col - t.cb) * t.ld + t.w0;
 #pragma unroll
       for (int i = 0; i < FM; ++i) {

@@ -145,11 +145,11 @@ int build_task_deps(const Plan& P, int KP, int64_t n, int64_t zrows, bool has_z,
         const WindowDesc& w = P.windows[wi];
         if (chase_task[wi] >= 0) seen.push_back(chase_task[wi]);  // the Q_W slot (step 0: own launch)
         if (T.type == hqr::kTaskLeft || T.type == hqr::kTaskLeftNear) {
-          int64_t c, cnt;
-          hqr::left_range(a, w, c, cnt);
+          int64_t c, c_al, cnt;  // (the columns the tiles store: from c on)
+          hqr::left_range_al(a, w, c, c_al, cnt);
           r0 = w.w0; r1 = (int64_t)w.w1 + 1;
-          c0 = c + (int64_t)NT * T.tile0;
-          c1 = std::min<int64_t>(c + (int64_t)NT * (T.tile0 + T.ntiles), n);
+          c0 = std::max<int64_t>(c, c_al + (int64_t)NT * T.tile0);
+          c1 = std::min<int64_t>(c_al + (int64_t)NT * (T.tile0 + T.ntiles), n);
         } else if (T.type == hqr::kTaskZ) {
           grid = &lastZ;
           r0 = (int64_t)MT * T.tile0;
@@ -481,11 +481,13 @@ int get_fused(CachedPlan& cp, bool has_z, int64_t n, FusedTasks** out) {
   if (!slot) {
     auto f = std::make_unique<FusedTasks>();
     const Plan& P = cp.plan;
-    // sp(g): smallest first row of any window of a later step (suffix minimum), rounded to even
+    // sp(g): smallest first row of any window of a later step (suffix minimum), rounded down to a
+    // multiple of 8 like the RightNear rows below: the right tiles (MT rows from these starts) then
+    // keep to the 8-row cells of the dependency grid (see left_range_al)
     std::vector<int64_t> sp(P.nsteps, INT64_MAX);
     int64_t run = INT64_MAX;
     for (int g = P.nsteps - 1; g >= 0; --g) {
-      sp[g] = (run == INT64_MAX) ? run : (run & ~(int64_t)1);
+      sp[g] = (run == INT64_MAX) ? run : (run & ~(int64_t)7);
       for (int i = P.step_begin[g]; i < P.step_begin[g + 1]; ++i) run = std::min<int64_t>(run, P.windows[i].w0);
     }
     StepArgs a{};
@@ -517,7 +519,7 @@ int get_fused(CachedPlan& cp, bool has_z, int64_t n, FusedTasks** out) {
           } else {
             if (D2.c_below >= 0) return -103;
             D2.c_below = b0 + i;
-            rnear[i] = std::min<int64_t>(rnear[i], std::max<int64_t>((int64_t)W2.w0 & ~(int64_t)1, sp[g]));
+            rnear[i] = std::min<int64_t>(rnear[i], std::max<int64_t>((int64_t)W2.w0 & ~(int64_t)7, sp[g]));
           }
         }
       }
@@ -531,10 +533,10 @@ int get_fused(CachedPlan& cp, bool has_z, int64_t n, FusedTasks** out) {
           }
       }
       for (int i = 0; i < nw; ++i) {
-        int64_t c, cnt;
-        hqr::left_range(a, w[i], c, cnt);
+        int64_t c, c_al, cnt;
+        hqr::left_range_al(a, w[i], c, c_al, cnt);
         const int64_t tiles = (cnt + NT - 1) / NT;
-        lnear[i] = (int)std::min<int64_t>(tiles, (xcol[i] - w[i].w1 + NT - 1) / NT);
+        lnear[i] = (int)std::min<int64_t>(tiles, (xcol[i] + 1 - c_al + NT - 1) / NT);
       }
       int nl, nrn;
       a.step = g;

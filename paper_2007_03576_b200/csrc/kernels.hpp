@@ -113,6 +113,20 @@ __host__ __device__ inline void left_range(const StepArgs& a, const WindowDesc& 
   if (cnt < 0) cnt = 0;
 }
 
+// The fused kernel's left tiles start at the multiple of 8 at or below c (c_al): their boundaries then
+// fall on the 8-column cells of the task dependency grid (hqr_api.cu build_task_deps), so two tiles of
+// one window never share a cell -- with c itself as the origin, every window whose w1 + 1 is not a
+// multiple of 8 (strides s = k - 3 nbc - 1 other than 56, or ilo not a multiple of 8) chained all its
+// left tiles one after another.  The columns [c_al, c) are multiplied but not stored (TileRef::lcs).
+// cnt counts from c_al (0 when the window has no columns right of it).
+__host__ __device__ inline void left_range_al(const StepArgs& a, const WindowDesc& w, int64_t& c,
+                                              int64_t& c_al, int64_t& cnt) {
+  left_range(a, w, c, cnt);
+  c_al = c & ~(int64_t)7;
+  if (c_al < a.lc0) c_al = c;
+  if (cnt > 0) cnt = a.lc1 - c_al;
+}
+
 // Q slot sets in flight: the Z update of step g may trail the chase of step g + kQSets - 1
 constexpr int kQSets = 4;
 

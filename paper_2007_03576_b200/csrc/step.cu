@@ -274,16 +274,16 @@ __device__ __forceinline__ TileRef make_tile_ref(const StepArgs& a, const Window
   TileRef t;
   t.w0 = w.w0; t.kw = w.w1 - w.w0 + 1; t.nbc = w.nbc;
   if (LEFT) {
-    int64_t c, cnt;
-    left_range(a, w, c, cnt);
-    t.M = a.H; t.c0 = c + (int64_t)(T.tile0 + i) * G::NT; t.lc1 = a.lc1; t.ld = a.n; t.cb = a.hcol0;
-    t.isZ = false; t.r0 = t.r1 = 0;
+    int64_t c, c_al, cnt;
+    left_range_al(a, w, c, c_al, cnt);
+    t.M = a.H; t.c0 = c_al + (int64_t)(T.tile0 + i) * G::NT; t.lc1 = a.lc1; t.ld = a.n; t.cb = a.hcol0;
+    t.isZ = false; t.r0 = t.r1 = 0; t.lcs = c;
   } else if (T.type == kTaskZ) {
     t.M = a.Z; t.r0 = (int64_t)(T.tile0 + i) * G::MT; t.r1 = a.zrows; t.ld = a.ldz; t.cb = 0;
-    t.isZ = true; t.c0 = t.lc1 = 0;
+    t.isZ = true; t.c0 = t.lc1 = t.lcs = 0;
   } else {
     t.M = a.H; t.r0 = T.r_lo + (int64_t)(T.tile0 + i) * G::MT; t.r1 = T.r_hi; t.ld = a.n;
-    t.cb = a.hcol0; t.isZ = false; t.c0 = t.lc1 = 0;
+    t.cb = a.hcol0; t.isZ = false; t.c0 = t.lc1 = t.lcs = 0;
   }
   return t;
 }
@@ -899,8 +899,8 @@ void build_step_tasks(const StepArgs& a, const WindowDesc* wins, int nwin, const
   if (chase_pos == 0) chases();
   const size_t l0 = out->size();
   for (int i = 0; i < nwin; ++i) {
-    int64_t c, cnt;
-    left_range(a, wins[i], c, cnt);
+    int64_t c, c_al, cnt;
+    left_range_al(a, wins[i], c, c_al, cnt);
     add(kTaskLeft, i, lnear[i], (cnt + NT - 1) / NT, 0, 0, cs.left);
   }
   if (cs.ltail > 0) resplit(l0, cs.ltail, cs.phase_chunk);

@@ -134,7 +134,7 @@ __global__ void __launch_bounds__(kThreadsBulk, 1)
     t.w0 = w.w0; t.kw = w.w1 - w.w0 + 1; t.nbc = w.nbc;
     if (LEFT) {
       t.M = a.H; t.c0 = si.rt[wi] + tile * NT; t.lc1 = a.lc1; t.ld = n; t.cb = a.hcol0; t.isZ = false;
-      t.r0 = t.r1 = 0;
+      t.r0 = t.r1 = 0; t.lcs = si.rt[wi];
     } else if (tile < si.rt[wi]) {
       int64_t lo, hi;
       right_row_range(a, w, lo, hi);
