@@ -1362,6 +1362,26 @@ int run_dist(const CachedPlan& cp, const hqr::DistLayout& L, std::vector<RankCtx
   // it lends or borrows columns (B may still be updating the lent ones; the borrower's whole right
   // update of the straddling window must follow its earlier deferred far-right rows).
   cudaStream_t A = g.stream, B = g.zstream, C = nccl ? g.cstream : g.stream;
+  // Per-rank busy time (tuning builds, virtual ranks: HQR_DIST_PROFILE=file): every launch on one
+  // stream, bracketed by events, written as (step, rank, class, ms) -- each rank's kernels as they
+  // would run on its own GPU, for tools/dist_balance_measured.py.  Classes: 0 chase, 1 left,
+  // 2 near-right, 3 far-right, 4 Z, 5 slab copies.
+  const char* prof_path = nccl ? nullptr : hqr::tuning_env("HQR_DIST_PROFILE");
+  struct ProfRec { int step, rank, cls; cudaEvent_t e0, e1; };
+  std::vector<ProfRec> prof;
+  if (prof_path) B = A;
+  auto pbeg = [&](int s, int r, int cls) -> int {
+    if (!prof_path) return -1;
+    ProfRec pr{s, r, cls, nullptr, nullptr};
+    cudaEventCreate(&pr.e0);
+    cudaEventCreate(&pr.e1);
+    cudaEventRecord(pr.e0, A);
+    prof.push_back(pr);
+    return (int)prof.size() - 1;
+  };
+  auto pend = [&](int i) {
+    if (i >= 0) cudaEventRecord(prof[i].e1, A);
+  };
   for (auto& rc : ranks) {
     CK(hqr::make_tensor_maps(&rc.tm, rc.H, rc.hcols, rc.Z, rc.zrows, rc.zrows, n, cp.KP));
   }
@@ -1418,9 +1438,12 @@ int run_dist(const CachedPlan& cp, const hqr::DistLayout& L, std::vector<RankCtx
     } else {
       for (size_t r = 0; r + 1 < ranks.size(); ++r) {
         const int64_t cnt = ranks[r].steps[s].lend_in;
-        if (cnt)
+        if (cnt) {
+          const int pi = pbeg(s, (int)r, 5);
           CK(cudaMemcpyAsync(ranks[r].H + (L.cb[r + 1] - L.cb[r]) * n, ranks[r + 1].H,
                              (size_t)cnt * n * sizeof(double), cudaMemcpyDeviceToDevice, A));
+          pend(pi);
+        }
       }
     }
     // (2) chase owned windows
@@ -1429,7 +1452,9 @@ int run_dist(const CachedPlan& cp, const hqr::DistLayout& L, std::vector<RankCtx
       if (!nown) continue;
       StepArgs a = args(rc, s, so);
       a.wins = rc.d_owned; a.win_begin = rc.owned_begin[s]; a.win_count = nown;
+      const int pi = pbeg(s, rc.rank, 0);
       CK(hqr::launch_chase(a, P.max_kw, P.max_nbc, A));
+      pend(pi);
       st->launches_chase++;
     }
     CK(cudaEventRecord(g.dev_chase[set], A));
@@ -1455,7 +1480,9 @@ int run_dist(const CachedPlan& cp, const hqr::DistLayout& L, std::vector<RankCtx
       const WindowDesc* hw = P.windows.data() + a.win_begin;
       int64_t items;
       double fl, by;
+      const int pi = pbeg(s, rc.rank, 1);
       CK(hqr::launch_left(a, hw, g.num_sms, rc.tm, A, &items, &fl, &by));
+      pend(pi);
       account(items, fl, by, &st->launches_left);
     }
     // B starts the step's deferred work only after the step's left updates: the far-right rows
@@ -1478,20 +1505,26 @@ int run_dist(const CachedPlan& cp, const hqr::DistLayout& L, std::vector<RankCtx
         const bool straddle = rc.steps[s].lend_in > 0;
         ar.rrow_lo = straddle ? 0 : sp[s];
         ar.rrow_hi = n;  // rows [rrow_lo, w0)
+        int pi = pbeg(s, rc.rank, 2);
         CK(hqr::launch_right(ar, rc.owned.data() + rc.owned_begin[s], g.num_sms, rc.tm, A, &items, &fl, &by));
+        pend(pi);
         account(items, fl, by, &st->launches_right);
         if (!straddle && sp[s] > 0) {
           StepArgs af = ar;
           af.rrow_lo = 0;
           af.rrow_hi = sp[s];
+          pi = pbeg(s, rc.rank, 3);
           CK(hqr::launch_right(af, rc.owned.data() + rc.owned_begin[s], g.num_sms, rc.tm, B, &items, &fl, &by));
+          pend(pi);
           account(items, fl, by, &st->launches_right);
         }
       }
       if (rc.Z) {
         StepArgs az = a;
         az.right_mode = 2;
+        const int pi = pbeg(s, rc.rank, 4);
         CK(hqr::launch_right(az, hw, g.num_sms, rc.tm, B, &items, &fl, &by));
+        pend(pi);
         account(items, fl, by, &st->launches_right);
       }
     }
@@ -1511,9 +1544,12 @@ int run_dist(const CachedPlan& cp, const hqr::DistLayout& L, std::vector<RankCtx
     } else {
       for (size_t r = 0; r + 1 < ranks.size(); ++r) {
         const int64_t cnt = ranks[r].steps[s].lend_in;
-        if (cnt)
+        if (cnt) {
+          const int pi = pbeg(s, (int)r, 5);
           CK(cudaMemcpyAsync(ranks[r + 1].H, ranks[r].H + (L.cb[r + 1] - L.cb[r]) * n,
                              (size_t)cnt * n * sizeof(double), cudaMemcpyDeviceToDevice, A));
+          pend(pi);
+        }
       }
     }
   }
@@ -1522,6 +1558,22 @@ int run_dist(const CachedPlan& cp, const hqr::DistLayout& L, std::vector<RankCtx
   if (nccl) {
     CK(cudaEventRecord(g.ev_join, C));
     CK(cudaStreamWaitEvent(A, g.ev_join, 0));
+  }
+  if (prof_path) {
+    CK(cudaStreamSynchronize(A));
+    if (FILE* fp = fopen(prof_path, "w")) {
+      fprintf(fp, "step,rank,cls,ms\n");
+      for (auto& pr : prof) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, pr.e0, pr.e1);
+        fprintf(fp, "%d,%d,%d,%.6f\n", pr.step, pr.rank, pr.cls, ms);
+      }
+      fclose(fp);
+    }
+    for (auto& pr : prof) {
+      cudaEventDestroy(pr.e0);
+      cudaEventDestroy(pr.e1);
+    }
   }
   st->steps = P.nsteps;
   st->windows = (int64_t)P.windows.size();
