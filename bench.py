@@ -272,7 +272,7 @@ def run_qriter(args):
     line = {"metric": METRIC, "value": float(np.mean(falg)) / (ms * 1e-3) / 1e9, "unit": "GFLOP/s", "n_gpus": 1,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (seeded N(0,1) upper Hessenberg, U[0.5,1.5] subdiagonal)",
+            "data": "synthetic (seeded hess_n, PAPER.md P:1061-1068: N(0,1) upper entries, sqrt(chi^2(n-i)) subdiagonal)",
             "config": {"workload": f"QR iteration with AED (NEXT-2, window {aed}) to all eigenvalues, n={n}, up to "
                                    f"{ns} shifts per sweep, blocks <= {nmin} by the one-CTA solver", "n": n,
                        "nshifts": ns, "aed_window": aed, "window": args.window, "parallelism": "1 GPU"},
