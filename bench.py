@@ -33,9 +33,11 @@ FP64_PEAK_FILE = os.path.join(ROOT, "profiles", "fp64_peaks_r01.json")
 METRIC = "seconds/sweep & fp64 GFLOP/s (frac of FP64 TC peak), n=10k/20k, 1/2/4/8 B200"
 
 
-def ncu_traffic(persistent):
+def ncu_traffic(persistent, workload, sweeps):
     """DRAM bytes per fused-kernel launch from the committed ncu captures (profiles/): the
-    persistent launch (one per sweep) from the launch list, or one step's launch."""
+    persistent launch (one per sweep) from the launch list, or one step's launch. Only the workload
+    the capture was taken on (its "workload" key, one sweep per launch) gets a number; every other
+    workload reports traffic null (no capture of it)."""
     path = os.path.join(ROOT, "profiles", "ncu_step_summary.json")
     if not os.path.exists(path):
         return None
@@ -45,6 +47,8 @@ def ncu_traffic(persistent):
         if "persistent_launch" not in d:
             return None
         d = d["persistent_launch"]
+    if d.get("workload") != workload or sweeps != 1:
+        return None
     return {"bytes_per_launch": d["dram_bytes_read"] + d["dram_bytes_write"], "source": d["source"]}
 
 
@@ -576,13 +580,14 @@ def main():
         # actually multiply (hqr_stats.flops_dmma, recorded per window by the chase); the dense
         # 2*m*n*k count of the same GEMMs is reported beside it
         achieved = ps["flops_dmma"] / (upd_ms * 1e-3) / 1e12
-        traffic = ncu_traffic(ps["launches_left"] == 1)
+        traffic = ncu_traffic(ps["launches_left"] == 1, workload, args.sweeps)
         dg = dgemm_peak()
         roofline = {"bound": "tensor", "kernel": kern,
                     "achieved": achieved, "peak": peak_sus, "unit": "TFLOP/s", "frac": achieved / peak_sus,
                     "frac_of_cublas_dgemm": achieved / dg if dg else None, "cublas_dgemm_tflops": dg,
                     "traffic": traffic["bytes_per_launch"] if traffic else None,
-                    "traffic_source": traffic["source"] if traffic else None,
+                    "traffic_source": traffic["source"] if traffic else
+                        "no ncu capture of this workload (the committed one is configs[3], one sweep)",
                     "achieved_what": "executed FP64 DMMA flops (band-trimmed update GEMMs) per launch / "
                                      "mean CUDA-event launch time",
                     "peak_source": "measured FP64 DMMA sustained, profiles/fp64_peaks_r01.json "
