@@ -84,9 +84,42 @@ def dgemm_peak():
 
 
 class Clocks:
-    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+    """SM clock and throttle-reason sampling during the timed region (B200_PROFILING.md clocks
+    line): an NVML thread polling every 10 ms (enough samples in a sub-second region), else
+    `nvidia-smi -lms 200`."""
+
+    _REASON_BITS = {"sw_power_cap": 0x4, "hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20,
+                    "hw_thermal_slowdown": 0x40}
 
     def __init__(self, index=0):
+        self.p = None
+        self.thread = None
+        self.sm, self.smax, self.reasons = [], None, set()
+        try:
+            import threading
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.smax = float(pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM))
+            get_reasons = getattr(pynvml, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                pynvml.nvmlDeviceGetCurrentClocksThrottleReasons
+            self.stop_evt = threading.Event()
+
+            def poll():
+                while True:
+                    self.sm.append(float(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)))
+                    bits = get_reasons(h)
+                    for nm, b in self._REASON_BITS.items():
+                        if bits & b:
+                            self.reasons.add(nm)
+                    if self.stop_evt.wait(0.01):
+                        return
+
+            self.thread = threading.Thread(target=poll, daemon=True)
+            self.thread.start()
+            return
+        except Exception:
+            self.thread = None
         self.path = f"/tmp/bench_clocks_{os.getpid()}.csv"
         q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
@@ -100,28 +133,33 @@ class Clocks:
             self.p = None
 
     def stop(self):
-        if self.p is None:
+        if self.thread is not None:
+            self.stop_evt.set()
+            self.thread.join()
+            sm, smax, reasons, how = self.sm, self.smax, self.reasons, "nvml 10 ms"
+        elif self.p is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        self.p.terminate()
-        self.p.wait()
-        self.f.close()
-        sm, smax, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in open(self.path):
-            parts = [x.strip() for x in line.split(",")]
-            if len(parts) < 9:
-                continue
-            try:
-                sm.append(float(parts[1]))
-                smax = float(parts[2])
-            except ValueError:
-                continue
-            for nm, v in zip(names, parts[5:9]):
-                if v.lower().startswith("active"):
-                    reasons.add(nm)
+        else:
+            self.p.terminate()
+            self.p.wait()
+            self.f.close()
+            sm, smax, reasons, how = [], None, set(), "nvidia-smi 200 ms"
+            names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+            for line in open(self.path):
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) < 9:
+                    continue
+                try:
+                    sm.append(float(parts[1]))
+                    smax = float(parts[2])
+                except ValueError:
+                    continue
+                for nm, v in zip(names, parts[5:9]):
+                    if v.lower().startswith("active"):
+                        reasons.add(nm)
         loaded = [s for s in sm if smax and s > 0.5 * smax] or sm
         return {"sm_mhz": float(np.median(loaded)) if loaded else None, "sm_max_mhz": smax,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm), "sampler": how}
 
 
 def host_info():
