@@ -39,6 +39,7 @@ for w in sw:
     alg += 16.0 * kw * ((n - 1 - w1) + w0 + n)
 out = {
     "source": f"ncu --set full of one fused step kernel launch (configs[3], step {step}); {tag}",
+    "workload": "configs[3]",  # bench.ncu_traffic gives traffic only to this workload's line
     "step": step,
     "duration_s": val("gpu__time_duration.sum"),
     "dram_bytes_read": val("dram__bytes_read.sum"),
