@@ -587,6 +587,9 @@ __global__ void __launch_bounds__(kStepThreads, 1)
       const long long cw0 = clock64();
 #endif
       while (*reinterpret_cast<volatile int*>(&desc[s].pos) != j) {
+#ifdef HQR_EXP_DESC_SLEEP  // experiment: back off the consumers' descriptor spin
+        __nanosleep(HQR_EXP_DESC_SLEEP);
+#endif
       }
 #ifdef HQR_TIMING
       const long long cw1 = clock64();
